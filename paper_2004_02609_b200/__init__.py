@@ -1,0 +1,322 @@
+"""voxcap-b200: ctypes binding of libvoxcap.so (include/voxcap.h).
+
+Argument marshalling only -- every step of the hot path (panel indexing, kernel generation,
+FFT matvec, preconditioner, GMRES, capacitance) runs in the library's CUDA kernels.  There is no
+CPU fallback: importing works without a GPU, but creating a :class:`VoxCap` context requires the
+built library and a CUDA device, and raises otherwise.
+
+Host arrays are numpy; device vectors may be passed as CUDA torch tensors (float64,
+contiguous), in which case work is ordered on the current torch stream of that device.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+__all__ = ["VoxCap", "VoxCapError", "lib_path", "load_library", "EXPORTS", "BuildOpts",
+           "SolveOpts", "SolveInfo", "Stats"]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_NAME = "libvoxcap.so"
+
+# every symbol include/voxcap.h declares
+EXPORTS = ("vc_create", "vc_set_geometry", "vc_get_sizes", "vc_get_panels", "vc_build_operator",
+           "vc_get_grid", "vc_matvec", "vc_precond", "vc_solve", "vc_solve_capacitance",
+           "vc_set_timing", "vc_get_stats", "vc_reset_stats", "vc_debug_kernel_entries",
+           "vc_debug_fft", "vc_last_error", "vc_version", "vc_destroy")
+
+STATUS = {0: "VC_OK", 1: "VC_ERR_INPUT", 2: "VC_ERR_STATE", 3: "VC_ERR_OOM", 4: "VC_ERR_CUDA",
+          5: "VC_ERR_NCCL", 6: "VC_NOT_CONVERGED", 7: "VC_ERR_UNSUPPORTED"}
+
+
+class VoxCapError(RuntimeError):
+    def __init__(self, status, msg):
+        self.status = status
+        self.code = STATUS.get(status, str(status))
+        super().__init__(f"{self.code}: {msg}")
+
+
+class BuildOpts(ctypes.Structure):
+    _fields_ = [("pad", ctypes.c_int32 * 3), ("box", ctypes.c_int32 * 3),
+                ("precond", ctypes.c_int32), ("reserved", ctypes.c_int32 * 9)]
+
+
+class SolveOpts(ctypes.Structure):
+    _fields_ = [("tol", ctypes.c_double), ("restart", ctypes.c_int32), ("maxit", ctypes.c_int32),
+                ("x0_is_guess", ctypes.c_int32), ("reserved", ctypes.c_int32 * 5)]
+
+
+class SolveInfo(ctypes.Structure):
+    _fields_ = [("iters", ctypes.c_int32), ("converged", ctypes.c_int32),
+                ("rre_prec", ctypes.c_double), ("rre_true", ctypes.c_double)]
+
+    def as_dict(self):
+        return {"iters": self.iters, "converged": bool(self.converged),
+                "rre_prec": self.rre_prec, "rre_true": self.rre_true}
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [("n_matvec", ctypes.c_int64), ("ms_matvec", ctypes.c_double),
+                ("n_pass", ctypes.c_int64 * 5), ("ms_pass", ctypes.c_double * 5),
+                ("bytes_pass", ctypes.c_double * 5), ("bytes_matvec", ctypes.c_double),
+                ("ms_setup", ctypes.c_double), ("ms_precond_build", ctypes.c_double),
+                ("gpu_launches", ctypes.c_int64), ("reserved", ctypes.c_int64 * 8)]
+
+    def as_dict(self):
+        return {"n_matvec": self.n_matvec, "ms_matvec": self.ms_matvec,
+                "n_pass": list(self.n_pass), "ms_pass": list(self.ms_pass),
+                "bytes_pass": list(self.bytes_pass), "bytes_matvec": self.bytes_matvec,
+                "ms_setup": self.ms_setup, "ms_precond_build": self.ms_precond_build,
+                "gpu_launches": self.gpu_launches}
+
+
+def lib_path():
+    return os.path.join(_HERE, _LIB_NAME)
+
+
+_lib = None
+
+
+def load_library(build_if_missing=False):
+    """Load libvoxcap.so (raises if absent; never falls back to anything else)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    p = lib_path()
+    if not os.path.exists(p):
+        if build_if_missing:
+            from .build import build
+            build()
+        else:
+            raise VoxCapError(4, f"{p} not built: run `python -m paper_2004_02609_b200.build`")
+    lib = ctypes.CDLL(p)
+    vp, i32, i64, dbl = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_double
+    P = ctypes.POINTER
+    sig = {
+        "vc_create": [P(vp), ctypes.c_int, vp],
+        "vc_set_geometry": [vp, i32, i32, i32, dbl, vp, vp, dbl, i32],
+        "vc_get_sizes": [vp, P(i64), P(i64), P(i64), P(i32)],
+        "vc_get_panels": [vp, vp, vp, vp, vp, vp, vp],
+        "vc_build_operator": [vp, P(BuildOpts)],
+        "vc_get_grid": [vp, vp],
+        "vc_matvec": [vp, vp, vp, i32],
+        "vc_precond": [vp, vp, vp, i32],
+        "vc_solve": [vp, vp, vp, P(SolveOpts), P(SolveInfo), i32],
+        "vc_solve_capacitance": [vp, vp, P(SolveOpts), vp],
+        "vc_set_timing": [vp, i32],
+        "vc_get_stats": [vp, P(Stats)],
+        "vc_reset_stats": [vp],
+        "vc_debug_kernel_entries": [vp, i32, vp, vp, vp, vp, vp],
+        "vc_debug_fft": [vp, i32, i32, vp, i32],
+    }
+    for name, args in sig.items():
+        f = getattr(lib, name)
+        f.argtypes = args
+        f.restype = ctypes.c_int
+    lib.vc_last_error.argtypes = [vp]
+    lib.vc_last_error.restype = ctypes.c_char_p
+    lib.vc_version.argtypes = []
+    lib.vc_version.restype = ctypes.c_char_p
+    lib.vc_destroy.argtypes = [vp]
+    lib.vc_destroy.restype = None
+    _lib = lib
+    return lib
+
+
+def _ptr(a):
+    return ctypes.c_void_p(a.ctypes.data) if isinstance(a, np.ndarray) else ctypes.c_void_p(a.data_ptr())
+
+
+def _is_cuda_tensor(a):
+    return hasattr(a, "is_cuda") and a.is_cuda
+
+
+class VoxCap:
+    """One context = one device (+ stream).  Methods mirror the C ABI one to one."""
+
+    def __init__(self, device=0, stream=None):
+        self._lib = load_library()
+        self._ctx = ctypes.c_void_p()
+        if stream is None:
+            try:
+                import torch
+                if torch.cuda.is_available():
+                    stream = torch.cuda.current_stream(device).cuda_stream
+            except ImportError:
+                stream = None
+        st = self._lib.vc_create(ctypes.byref(self._ctx), int(device),
+                                 ctypes.c_void_p(stream) if stream else None)
+        if st != 0:
+            raise VoxCapError(st, "vc_create failed (no CUDA device?)")
+        self.device = device
+        self.n = 0
+        self.m = 0
+
+    # -- plumbing ------------------------------------------------------------------------
+    def _check(self, st, allow=(0,)):
+        if st not in allow:
+            raise VoxCapError(st, self._lib.vc_last_error(self._ctx).decode())
+        return st
+
+    def close(self):
+        if getattr(self, "_ctx", None) and self._ctx.value:
+            self._lib.vc_destroy(self._ctx)
+            self._ctx = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    @staticmethod
+    def version():
+        return load_library().vc_version().decode()
+
+    # -- geometry ------------------------------------------------------------------------
+    def set_geometry(self, label, eps=None, eps_out=1.0, dv=1e-6):
+        """label (Nz, Ny, Nx) int32 (numpy, or CUDA torch tensor), eps same shape float64."""
+        on_dev = _is_cuda_tensor(label)
+        if on_dev:
+            lab = label.contiguous()
+            ep = None if eps is None else eps.contiguous()
+            assert str(lab.dtype) == "torch.int32"
+        else:
+            lab = np.ascontiguousarray(label, dtype=np.int32)
+            ep = None if eps is None else np.ascontiguousarray(eps, dtype=np.float64)
+        nz, ny, nx = lab.shape
+        self._keep = (lab, ep)
+        self._check(self._lib.vc_set_geometry(self._ctx, nx, ny, nz, float(dv), _ptr(lab),
+                                              None if ep is None else _ptr(ep), float(eps_out),
+                                              1 if on_dev else 0))
+        n, nc, nd, m = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int32()
+        self._check(self._lib.vc_get_sizes(self._ctx, ctypes.byref(n), ctypes.byref(nc),
+                                           ctypes.byref(nd), ctypes.byref(m)))
+        self.n, self.n_cond, self.n_diel, self.m = n.value, nc.value, nd.value, m.value
+        return self
+
+    def set_structure(self, st):
+        """Convenience: a voxgen.Structure-like object (label, eps, eps_out, dv)."""
+        return self.set_geometry(st.label, st.eps, st.eps_out, st.dv)
+
+    def panels(self):
+        n = self.n
+        out = {"axis": np.empty(n, np.int8), "slot": np.empty((n, 3), np.int32),
+               "sign": np.empty(n, np.int8), "cid": np.empty(n, np.int32),
+               "eps_d": np.empty(n, np.float64), "eps_b": np.empty(n, np.float64)}
+        self._check(self._lib.vc_get_panels(self._ctx, *[_ptr(out[k]) for k in
+                                                         ("axis", "slot", "sign", "cid",
+                                                          "eps_d", "eps_b")]))
+        return out
+
+    # -- operator ------------------------------------------------------------------------
+    def build_operator(self, pad=None, box=None, precond=3):
+        o = BuildOpts()
+        if pad is not None:
+            for a in range(3):
+                o.pad[a] = int(pad[a])
+        if box is not None:
+            for a in range(3):
+                o.box[a] = int(box[a])
+        o.precond = int(precond)
+        self._check(self._lib.vc_build_operator(self._ctx, ctypes.byref(o)))
+        return self
+
+    def grid(self):
+        m3 = (ctypes.c_int32 * 3)()
+        self._check(self._lib.vc_get_grid(self._ctx, m3))
+        return tuple(m3)
+
+    def _vec_call(self, fn, x, out=None):
+        if _is_cuda_tensor(x):
+            import torch
+            x = x.contiguous()
+            y = torch.empty_like(x) if out is None else out
+            self._check(fn(self._ctx, _ptr(x), _ptr(y), 1))
+            return y
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        y = np.empty_like(x) if out is None else out
+        self._check(fn(self._ctx, _ptr(x), _ptr(y), 0))
+        return y
+
+    def matvec(self, x, out=None):
+        """y = ([0; Ī] + [P; E]) x (Eq. 4)."""
+        return self._vec_call(self._lib.vc_matvec, x, out)
+
+    def precond(self, r, out=None):
+        return self._vec_call(self._lib.vc_precond, r, out)
+
+    @staticmethod
+    def _sopts(tol, restart, maxit, guess=False):
+        o = SolveOpts()
+        o.tol = float(tol or 0)
+        o.restart = int(restart or 0)
+        o.maxit = int(maxit or 0)
+        o.x0_is_guess = 1 if guess else 0
+        return o
+
+    def solve(self, b, tol=1e-4, restart=35, maxit=2000, x0=None):
+        o = self._sopts(tol, restart, maxit, x0 is not None)
+        info = SolveInfo()
+        on_dev = _is_cuda_tensor(b)
+        if on_dev:
+            import torch
+            x = torch.zeros_like(b) if x0 is None else x0.clone()
+            st = self._lib.vc_solve(self._ctx, _ptr(b.contiguous()), _ptr(x), ctypes.byref(o),
+                                    ctypes.byref(info), 1)
+        else:
+            b = np.ascontiguousarray(b, dtype=np.float64)
+            x = np.zeros_like(b) if x0 is None else np.array(x0, dtype=np.float64)
+            st = self._lib.vc_solve(self._ctx, _ptr(b), _ptr(x), ctypes.byref(o),
+                                    ctypes.byref(info), 0)
+        self._check(st, allow=(0, 6))
+        return x, info.as_dict()
+
+    def solve_capacitance(self, tol=1e-4, restart=35, maxit=2000):
+        """Maxwell capacitance matrix (m x m, farads) and per-column solve info."""
+        o = self._sopts(tol, restart, maxit)
+        C = np.zeros((self.m, self.m), np.float64)
+        infos = (SolveInfo * max(1, self.m))()
+        st = self._lib.vc_solve_capacitance(self._ctx, _ptr(C), ctypes.byref(o), infos)
+        self._check(st, allow=(0, 6))
+        return C, [infos[i].as_dict() for i in range(self.m)]
+
+    # -- instrumentation / test hooks -----------------------------------------------------
+    def set_timing(self, detail=True):
+        self._check(self._lib.vc_set_timing(self._ctx, 1 if detail else 0))
+
+    def stats(self):
+        s = Stats()
+        self._check(self._lib.vc_get_stats(self._ctx, ctypes.byref(s)))
+        return s.as_dict()
+
+    def reset_stats(self):
+        self._check(self._lib.vc_reset_stats(self._ctx))
+
+    def kernel_entries(self, kind, alpha, beta, d):
+        """Device kernel-entry generator in unit-voxel units (test hook)."""
+        d = np.ascontiguousarray(d, dtype=np.int32).reshape(-1, 3)
+        n = d.shape[0]
+        kind = np.ascontiguousarray(np.broadcast_to(kind, (n,)), dtype=np.int32)
+        alpha = np.ascontiguousarray(np.broadcast_to(alpha, (n,)), dtype=np.int32)
+        beta = np.ascontiguousarray(np.broadcast_to(beta, (n,)), dtype=np.int32)
+        out = np.empty(n, np.float64)
+        self._check(self._lib.vc_debug_kernel_entries(self._ctx, n, _ptr(kind), _ptr(alpha),
+                                                      _ptr(beta), _ptr(d), _ptr(out)))
+        return out
+
+    def fft(self, data, inverse=False):
+        """Device batched FFT along the last axis (test hook); complex128 in, complex128 out."""
+        a = np.ascontiguousarray(data, dtype=np.complex128).copy()
+        L = a.shape[-1]
+        nl = a.size // L
+        self._check(self._lib.vc_debug_fft(self._ctx, L, nl, _ptr(a), 1 if inverse else -1))
+        return a

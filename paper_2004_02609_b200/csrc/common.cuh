@@ -1,0 +1,48 @@
+// common.cuh -- shared device/host helpers of libvoxcap (sm_100a).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace vc {
+
+constexpr double kPi = 3.14159265358979323846264338327950288;
+constexpr double kEps0 = 8.8541878128e-12;  // F/m (reading O15)
+constexpr int kMaxL = 4096;                 // largest FFT length per axis
+constexpr int kTabN = 2 * kMaxL;            // twiddle table: exp(-2 pi i n / kTabN)
+
+// Half-integer centre offsets of the a-normal panel grids, doubled (c_x = (0,1/2,1/2) ...;
+// P:97 grids, Table VII P:331-341 in the S = c_beta - c_alpha form).
+__host__ __device__ constexpr int c2(int normal, int axis) { return normal == axis ? 0 : 1; }
+
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+    return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+// a * conj(b)
+__device__ __forceinline__ double2 cmulc(double2 a, double2 b) {
+    return make_double2(fma(a.x, b.x, a.y * b.y), fma(a.y, b.x, -a.x * b.y));
+}
+__device__ __forceinline__ double2 cconj(double2 a) { return make_double2(a.x, -a.y); }
+__device__ __forceinline__ double2 cscale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
+__device__ __forceinline__ double2 czero() { return make_double2(0.0, 0.0); }
+
+// exp(-2 pi i n / kTabN) for n in [0, kTabN); inverse direction uses the conjugate.
+template <bool INV>
+__device__ __forceinline__ double2 twiddle(const double2* __restrict__ tw, int n) {
+    double2 w = __ldg(tw + n);
+    return INV ? cconj(w) : w;
+}
+
+// Half-shift phase exp(sgn * i pi kt / M) for a signed frequency kt in [-M/2, M/2]
+// (sgn = -1: phi-bar, sgn = +1: phi; SURVEY App. B / DESIGN.md "spectra").
+__device__ __forceinline__ double2 half_phase(const double2* __restrict__ tw, int kt, int M, int sgn) {
+    // exp(-2 pi i |kt| / (2M)) = tw[|kt| * kTabN / (2M)]
+    int a = kt < 0 ? -kt : kt;
+    double2 w = __ldg(tw + a * (kTabN / (2 * M)));  // = exp(-i pi |kt| / M)
+    // want exp(sgn * i pi kt / M): if sgn*kt > 0 -> conj(w), else w
+    bool pos = (sgn > 0) == (kt > 0);
+    return (kt != 0 && pos) ? cconj(w) : w;
+}
+
+}  // namespace vc

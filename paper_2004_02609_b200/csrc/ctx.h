@@ -1,0 +1,141 @@
+// ctx.h -- host-side context of libvoxcap (one per device / stream).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/voxcap.h"
+
+namespace vc {
+
+// Owning device buffer (cudaMallocAsync on the context stream would tie lifetime to the
+// stream; plain cudaMalloc keeps it simple for setup-time allocations).
+template <class T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() { reset(); }
+    void reset() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    cudaError_t alloc(size_t count) {
+        reset();
+        if (count == 0) return cudaSuccess;
+        cudaError_t e = cudaMalloc(&p, count * sizeof(T));
+        if (e == cudaSuccess) n = count;
+        else p = nullptr;
+        return e;
+    }
+    T* get() const { return p; }
+    size_t bytes() const { return n * sizeof(T); }
+};
+
+struct PanelsDev {
+    DevBuf<int8_t> axis, sign, info;  // info bit0: dielectric row, bit1: sign < 0
+    DevBuf<int32_t> si, sj, sk, cid;
+    DevBuf<double> eps_d, eps_b, ibar, fc;
+    DevBuf<int32_t> slotmap[3];  // per orientation: slot -> panel index or -1
+};
+
+// Output field of the FFT matvec: C^alpha (kind 0, conductor rows) or D^alpha (kind 1).
+struct Field {
+    int kind, axis;
+    int ext[3];  // slot extent relative to the window origin, per axis
+};
+
+struct Precond;  // precond.cu
+
+struct Timing {
+    bool detail = false;
+    cudaEvent_t ev[12] = {};
+    bool ev_ok = false;
+};
+
+}  // namespace vc
+
+struct vc_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    std::string err;
+
+    // ---- geometry (vc_set_geometry) ----
+    bool has_geom = false;
+    int nx = 0, ny = 0, nz = 0;
+    double dv = 0, eps_out = 1;
+    int64_t N = 0, Nc = 0, Nd = 0;
+    int m = 0;
+    vc::PanelsDev pan;
+    // [kind][orientation][0 = min, 1 = max][axis]; min > max when no such panels
+    int ext[2][3][2][3];
+    // host mirror of the panel table (structure-only work: preconditioner boxes)
+    std::vector<int8_t> h_axis, h_sign;
+    std::vector<int32_t> h_si, h_sj, h_sk, h_cid;
+    std::vector<double> h_ibar;
+
+    // ---- operator (vc_build_operator) ----
+    bool has_op = false;
+    int M[3] = {0, 0, 0}, Kx = 0;
+    int lo[3] = {0, 0, 0};
+    int ext_in[3][3];  // per source orientation beta: slot extents (0 = no beta panels)
+    int nf = 0;
+    vc::Field f[6];
+    int blk[6][3];  // kernel spectrum index for (field, beta), -1 = none
+    int nblk = 0;
+    size_t blk_stride = 0;  // doubles per folded spectrum
+    vc::DevBuf<double> Rt;  // folded, phase-stripped, scaled kernel spectra
+    vc::DevBuf<double2> tw;  // twiddles exp(-2 pi i n / kTabN)
+    vc::DevBuf<double2> bufA, bufB, bufC;  // X1/X4, X2, X3
+    size_t offA_in[3], offB[3], offC[6], offA_out[6];
+    double bytes_pass[5] = {0, 0, 0, 0, 0};
+    int precond_kind = 3;
+    vc::Precond* pc = nullptr;
+
+    // ---- solver work ----
+    vc::DevBuf<double> work;  // Krylov basis + temporaries
+    size_t work_n = 0;
+    vc::DevBuf<double> partial;
+    vc::DevBuf<double> dvec;  // small device vector (dots)
+    double* h_pinned = nullptr;  // pinned host scratch (dots)
+
+    // ---- instrumentation ----
+    vc_stats stats{};
+    vc::Timing timing;
+};
+
+namespace vc {
+// error helpers
+inline vc_status set_err(vc_ctx* c, vc_status s, const std::string& msg) {
+    c->err = msg;
+    return s;
+}
+#define VC_CUDA(c, expr)                                                                    \
+    do {                                                                                    \
+        cudaError_t _e = (expr);                                                            \
+        if (_e != cudaSuccess)                                                              \
+            return vc::set_err((c), _e == cudaErrorMemoryAllocation ? VC_ERR_OOM : VC_ERR_CUDA, \
+                               std::string(#expr) + ": " + cudaGetErrorString(_e));        \
+    } while (0)
+
+// entry points implemented in the .cu files
+vc_status geometry_build(vc_ctx* c, const int32_t* d_label, const double* d_eps);
+vc_status operator_build(vc_ctx* c, const vc_build_opts* o);
+vc_status matvec_dev(vc_ctx* c, const double* d_x, double* d_y);
+vc_status precond_build(vc_ctx* c, const int32_t box[3], int kind);
+vc_status precond_apply_dev(vc_ctx* c, const double* d_r, double* d_z);
+void precond_free(vc_ctx* c);
+vc_status solve_dev(vc_ctx* c, const double* d_b, double* d_x, const vc_solve_opts* o,
+                    vc_solve_info* info);
+vc_status capacitance_dev(vc_ctx* c, double* h_C, const vc_solve_opts* o, vc_solve_info* info);
+vc_status debug_kernel_entries(vc_ctx* c, int n, const int32_t* kind, const int32_t* a,
+                               const int32_t* b, const int32_t* d, double* out);
+vc_status debug_fft(vc_ctx* c, int L, int nl, double* data, int dir);
+inline void count_launch(vc_ctx* c, int k = 1) { c->stats.gpu_launches += k; }
+}  // namespace vc

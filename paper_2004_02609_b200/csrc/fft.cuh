@@ -1,0 +1,174 @@
+// fft.cuh -- batched in-shared-memory fp64 FFT building blocks (sm_100a).
+//
+// A length-L (power of two, 8..4096) transform is done as NS = ceil(log2 L / 4) in-place
+// decimation-in-frequency radix-R stages (R = 2^bits, bits <= 4, spread evenly), each stage a
+// register-resident R-point DFT followed by the inter-stage twiddle.  T independent pencils are
+// transformed together; the caller supplies load/store functors, so the first stage can read
+// straight from global memory (zero-padded input, strided pencils) and the last stage can write
+// straight to global memory at the digit-reversed position -> frequency map, with shared memory
+// only between stages (layout [element][pencil], pencil fastest, so lanes of a warp hit
+// consecutive 16-byte words).
+#pragma once
+#include "common.cuh"
+
+namespace vc {
+
+constexpr int ilog2c(int n) { return n <= 1 ? 0 : 1 + ilog2c(n / 2); }
+
+template <int L>
+struct Plan {
+    static_assert(L >= 2 && (L & (L - 1)) == 0 && L <= kMaxL, "L must be a power of two");
+    static constexpr int B = ilog2c(L);
+    static constexpr int NS = (B + 3) / 4;
+    __host__ __device__ static constexpr int bits(int s) { return B / NS + (s < B % NS ? 1 : 0); }
+    __host__ __device__ static constexpr int radix(int s) { return 1 << bits(s); }
+    __host__ __device__ static constexpr int lc(int s) {
+        int r = L;
+        for (int i = 0; i < s; ++i) r >>= bits(i);
+        return r;
+    }
+    // storage position p (after all DIF stages) -> frequency k
+    __host__ __device__ static constexpr int freq(int p) {
+        int k = 0, mul = 1;
+        for (int s = 0; s < NS; ++s) {
+            int S = lc(s) / radix(s);
+            int m = (p / S) % radix(s);
+            k += m * mul;
+            mul *= radix(s);
+        }
+        return k;
+    }
+    // frequency k -> storage position p
+    __host__ __device__ static constexpr int pos(int k) {
+        int p = 0;
+        for (int s = 0; s < NS; ++s) {
+            int R = radix(s);
+            p += (k % R) * (lc(s) / R);
+            k /= R;
+        }
+        return p;
+    }
+};
+
+template <int R>
+__device__ __forceinline__ constexpr int bitrev(int i) {
+    int r = 0;
+    for (int b = 1; b < R; b <<= 1) {
+        r = (r << 1) | (i & 1);
+        i >>= 1;
+    }
+    return r;
+}
+
+// Multiply by w_16^k16 (forward: exp(-2 pi i k16/16)), k16 a compile-time constant after
+// unrolling; trivial angles become adds / swaps.
+template <bool INV>
+__device__ __forceinline__ double2 rot16(double2 v, int k16) {
+    constexpr double C1 = 0.92387953251128675613;  // cos(pi/8)
+    constexpr double S1 = 0.38268343236508977173;  // sin(pi/8)
+    constexpr double H = 0.70710678118654752440;   // sqrt(1/2)
+    double c, s;  // w = c - i s (forward)
+    switch (k16 & 15) {
+        case 0: return v;
+        case 4: return INV ? make_double2(-v.y, v.x) : make_double2(v.y, -v.x);
+        case 8: return make_double2(-v.x, -v.y);
+        case 12: return INV ? make_double2(v.y, -v.x) : make_double2(-v.y, v.x);
+        case 1: c = C1; s = S1; break;
+        case 2: c = H; s = H; break;
+        case 3: c = S1; s = C1; break;
+        case 5: c = -S1; s = C1; break;
+        case 6: c = -H; s = H; break;
+        case 7: c = -C1; s = S1; break;
+        case 9: c = -C1; s = -S1; break;
+        case 10: c = -H; s = -H; break;
+        case 11: c = -S1; s = -C1; break;
+        case 13: c = S1; s = -C1; break;
+        case 14: c = H; s = -H; break;
+        default: c = C1; s = -S1; break;  // 15
+    }
+    if (INV) s = -s;
+    // (vx + i vy)(c - i s)
+    return make_double2(fma(v.x, c, v.y * s), fma(v.y, c, -v.x * s));
+}
+
+// In-register R-point DFT (DIF radix-2 butterflies); on return register i holds frequency
+// bitrev_R(i).
+template <int R, bool INV>
+__device__ __forceinline__ void reg_dft(double2 (&v)[R]) {
+#pragma unroll
+    for (int half = R / 2; half >= 1; half /= 2) {
+#pragma unroll
+        for (int g = 0; g < R; g += 2 * half) {
+#pragma unroll
+            for (int j = 0; j < half; ++j) {
+                double2 a = v[g + j], b = v[g + j + half];
+                v[g + j] = cadd(a, b);
+                v[g + j + half] = rot16<INV>(csub(a, b), j * (16 / (2 * half)));
+            }
+        }
+    }
+}
+
+// One DIF stage s of the length-L transform over T pencils with NT threads.
+//   ld(t, p) -> double2 : element at storage position p of pencil t (stage input)
+//   st(t, p, v)         : write element at position p of pencil t (stage output)
+//   PF = true : consecutive lanes take consecutive pencils (strided-axis passes)
+//   PF = false: consecutive lanes take consecutive butterflies of one pencil (contiguous lines)
+template <int L, int T, int NT, bool INV, bool PF, int s, class LD, class ST>
+__device__ __forceinline__ void fft_stage(LD&& ld, ST&& st, const double2* __restrict__ tw) {
+    constexpr int R = Plan<L>::radix(s);
+    constexpr int Lc = Plan<L>::lc(s);
+    constexpr int S = Lc / R;
+    constexpr int NB = T * (L / R);
+    constexpr int TW = kTabN / Lc;
+#pragma unroll 1
+    for (int u = threadIdx.x; u < NB; u += NT) {
+        const int t = PF ? u % T : u / (L / R);
+        const int rest = PF ? u / T : u % (L / R);
+        const int b = rest % S;
+        const int g = rest / S;
+        const int base = g * Lc + b;
+        double2 v[R];
+#pragma unroll
+        for (int j = 0; j < R; ++j) v[j] = ld(t, base + j * S);
+        reg_dft<R, INV>(v);
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+            const int m = bitrev<R>(i);
+            double2 x = v[i];
+            if (S > 1 && m != 0) x = cmul(x, twiddle<INV>(tw, b * m * TW));
+            st(t, base + m * S, x);
+        }
+    }
+}
+
+// Shared-memory index of (pencil t, position p): PF -> [pos][pencil], else [pencil][pos].
+template <int L, int T, bool PF>
+__device__ __forceinline__ int smi(int t, int p) { return PF ? p * T + t : t * L + p; }
+
+// Full transform: stage 0 reads through `ld0`, the last stage writes through `stN`, and the
+// intermediate stages use shared memory `sm` (layout smi<L,T,PF>).  If NS == 1 the single
+// stage goes ld0 -> stN.  No trailing __syncthreads().
+template <int L, int T, int NT, bool INV, bool PF, class LD, class ST>
+__device__ __forceinline__ void fft_run(double2* sm, LD&& ld0, ST&& stN,
+                                        const double2* __restrict__ tw) {
+    constexpr int NS = Plan<L>::NS;
+    auto lds = [&](int t, int p) { return sm[smi<L, T, PF>(t, p)]; };
+    auto sts = [&](int t, int p, double2 v) { sm[smi<L, T, PF>(t, p)] = v; };
+    if constexpr (NS == 1) {
+        fft_stage<L, T, NT, INV, PF, 0>(ld0, stN, tw);
+    } else if constexpr (NS == 2) {
+        fft_stage<L, T, NT, INV, PF, 0>(ld0, sts, tw);
+        __syncthreads();
+        fft_stage<L, T, NT, INV, PF, 1>(lds, stN, tw);
+    } else {
+        static_assert(NS == 3, "L <= 4096");
+        fft_stage<L, T, NT, INV, PF, 0>(ld0, sts, tw);
+        __syncthreads();
+        fft_stage<L, T, NT, INV, PF, 1>(lds, sts, tw);
+        __syncthreads();
+        fft_stage<L, T, NT, INV, PF, 2>(lds, stN, tw);
+    }
+}
+
+}  // namespace vc

@@ -1,0 +1,330 @@
+// krylov.cu -- restarted GMRES with left preconditioning (Eq. 14) and the capacitance
+// extraction of Eq. (8).  DESIGN.md a11 / a12.
+//
+// Orthogonalisation is classical Gram-Schmidt applied twice (CGS2) so each Arnoldi step is two
+// fused multi-dot passes + two multi-axpy passes over the basis; all reductions are two-level
+// and fixed-order (deterministic).  The (restart+1) x restart Hessenberg least-squares problem
+// is tiny and is updated with Givens rotations on the host, one 3*(restart+1)-double device ->
+// host copy per iteration.
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "ctx.h"
+
+namespace vc {
+
+namespace {
+
+constexpr int kMaxBasis = 64;  // restart + 1 <= 64
+constexpr int kRedBlocks = 296;
+constexpr int kRedNT = 256;
+
+// partial[b * nv + i] = sum_{n in block b} V[i][n] * w[n]
+__global__ void __launch_bounds__(kRedNT) k_multidot(const double* __restrict__ V, int64_t ldv, int nv,
+                                                     const double* __restrict__ w, int64_t n,
+                                                     double* __restrict__ partial) {
+    double acc[kMaxBasis];
+#pragma unroll
+    for (int i = 0; i < kMaxBasis; ++i) acc[i] = 0.0;
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        const double wk = w[k];
+#pragma unroll
+        for (int i = 0; i < kMaxBasis; ++i)
+            if (i < nv) acc[i] = fma(V[i * ldv + k], wk, acc[i]);
+    }
+    __shared__ double s[kRedNT / 32][kMaxBasis];
+    const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+#pragma unroll
+    for (int i = 0; i < kMaxBasis; ++i) {
+        if (i >= nv) break;
+        double v = acc[i];
+        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) s[wp][i] = v;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < nv; i += blockDim.x) {
+        double v = 0.0;
+        for (int q = 0; q < kRedNT / 32; ++q) v += s[q][i];
+        partial[(int64_t)blockIdx.x * nv + i] = v;
+    }
+}
+
+__global__ void k_reduce_partials(const double* __restrict__ partial, int nblk, int nv,
+                                  double* __restrict__ out) {
+    const int i = threadIdx.x;
+    if (i >= nv) return;
+    double v = 0.0;
+    for (int b = 0; b < nblk; ++b) v += partial[(int64_t)b * nv + i];
+    out[i] = v;
+}
+
+// w -= sum_i h[i] V[i]   (h on the device)
+__global__ void k_multiaxpy(double* __restrict__ w, const double* __restrict__ V, int64_t ldv,
+                            int nv, const double* __restrict__ h, int64_t n, double sgn) {
+    __shared__ double hs[kMaxBasis];
+    if (threadIdx.x < nv) hs[threadIdx.x] = h[threadIdx.x];
+    __syncthreads();
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        double acc = 0.0;
+        for (int i = 0; i < nv; ++i) acc = fma(hs[i], V[i * ldv + k], acc);
+        w[k] = fma(sgn, acc, w[k]);
+    }
+}
+
+// dst = src / sqrt(*nrm2)
+__global__ void k_scale_by_norm(double* __restrict__ dst, const double* __restrict__ src,
+                                const double* __restrict__ nrm2, int64_t n) {
+    const double s = 1.0 / sqrt(*nrm2);
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+         k += (int64_t)gridDim.x * blockDim.x)
+        dst[k] = src[k] * s;
+}
+
+// y = a*x + b*y
+__global__ void k_axpby(double* __restrict__ y, const double* __restrict__ x, double a, double b,
+                        int64_t n) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+         k += (int64_t)gridDim.x * blockDim.x)
+        y[k] = fma(a, x[k], b * y[k]);
+}
+
+// b_k = dv^2 on the panels of conductor j (V_k = A_k Phi_k)
+__global__ void k_rhs(double* __restrict__ b, const int32_t* __restrict__ cid, int j, double area,
+                      int64_t n) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+         k += (int64_t)gridDim.x * blockDim.x)
+        b[k] = cid[k] == j ? area : 0.0;
+}
+
+// partial[i * nb + blk] = sum over conductor-i panels in block blk of A fc rho  (Eq. 8)
+__global__ void k_cap_partial(const double* __restrict__ rho, const int32_t* __restrict__ cid,
+                              const double* __restrict__ fc, double area, int64_t n, int m,
+                              double* __restrict__ partial) {
+    // one pass per conductor i = blockIdx.y + 1
+    const int i = blockIdx.y + 1;
+    double acc = 0.0;
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+         k += (int64_t)gridDim.x * blockDim.x)
+        if (cid[k] == i) acc = fma(area * fc[k], rho[k], acc);
+    __shared__ double s[kRedNT / 32];
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double v = 0.0;
+        for (int q = 0; q < kRedNT / 32; ++q) v += s[q];
+        partial[(int64_t)blockIdx.y * gridDim.x + blockIdx.x] = v;
+    }
+}
+
+__global__ void k_cap_final(const double* __restrict__ partial, int nb, int m,
+                            double* __restrict__ out) {
+    const int i = threadIdx.x;
+    if (i >= m) return;
+    double v = 0.0;
+    for (int q = 0; q < nb; ++q) v += partial[(int64_t)i * nb + q];
+    out[i] = v;
+}
+
+inline unsigned grid_for(int64_t n) {
+    return (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 8));
+}
+
+}  // namespace
+
+struct Krylov {
+    vc_ctx* c;
+    int64_t n;
+    double *V, *w, *t, *r, *b, *x;  // V: (m+1) x n
+    int m;
+    vc_status ensure(int restart) {
+        m = restart;
+        const size_t need = (size_t)(m + 1 + 5) * n;
+        if (c->work_n < need) {
+            VC_CUDA(c, c->work.alloc(need));
+            c->work_n = need;
+        }
+        if (c->partial.n < (size_t)kRedBlocks * kMaxBasis) VC_CUDA(c, c->partial.alloc((size_t)kRedBlocks * kMaxBasis));
+        if (c->dvec.n < 4 * kMaxBasis) VC_CUDA(c, c->dvec.alloc(4 * kMaxBasis));
+        if (!c->h_pinned) VC_CUDA(c, cudaMallocHost(&c->h_pinned, 8 * 4 * kMaxBasis));
+        V = c->work.p;
+        w = V + (size_t)(m + 1) * n;
+        t = w + n;
+        r = t + n;
+        b = r + n;
+        x = b + n;
+        return VC_OK;
+    }
+    // out[0..nv) = V[0..nv) . vec
+    void dots(const double* Vb, int nv, const double* vec, double* out) {
+        k_multidot<<<kRedBlocks, kRedNT, 0, c->stream>>>(Vb, n, nv, vec, n, c->partial.p);
+        k_reduce_partials<<<1, kMaxBasis, 0, c->stream>>>(c->partial.p, kRedBlocks, nv, out);
+        count_launch(c, 2);
+    }
+    vc_status norm2_host(const double* vec, double* out) {
+        dots(vec, 1, vec, c->dvec.p);
+        VC_CUDA(c, cudaMemcpyAsync(c->h_pinned, c->dvec.p, 8, cudaMemcpyDeviceToHost, c->stream));
+        VC_CUDA(c, cudaStreamSynchronize(c->stream));
+        *out = std::sqrt(c->h_pinned[0]);
+        return VC_OK;
+    }
+    // dst = R A src
+    vc_status op(const double* src, double* dst, double* tmp) {
+        vc_status s = matvec_dev(c, src, tmp);
+        if (s) return s;
+        return precond_apply_dev(c, tmp, dst);
+    }
+};
+
+vc_status solve_dev(vc_ctx* c, const double* d_b, double* d_x, const vc_solve_opts* o,
+                    vc_solve_info* info) {
+    const double tol = (o && o->tol > 0) ? o->tol : 1e-4;
+    const int restart = (o && o->restart > 0) ? std::min(o->restart, kMaxBasis - 1) : 35;
+    const int maxit = (o && o->maxit > 0) ? o->maxit : 2000;
+    const bool guess = o && o->x0_is_guess;
+    Krylov K{c, c->N};
+    vc_status s = K.ensure(restart);
+    if (s) return s;
+    cudaStream_t st = c->stream;
+    const int64_t n = c->N;
+    const unsigned gn = grid_for(n);
+    VC_CUDA(c, cudaMemcpyAsync(K.b, d_b, 8 * n, cudaMemcpyDeviceToDevice, st));
+    if (guess) VC_CUDA(c, cudaMemcpyAsync(K.x, d_x, 8 * n, cudaMemcpyDeviceToDevice, st));
+    else VC_CUDA(c, cudaMemsetAsync(K.x, 0, 8 * n, st));
+    // ||R b||
+    if ((s = precond_apply_dev(c, K.b, K.r))) return s;
+    double nrb = 0, nb = 0;
+    if ((s = K.norm2_host(K.r, &nrb))) return s;
+    if ((s = K.norm2_host(K.b, &nb))) return s;
+    int iters = 0;
+    double rre = 1.0;
+    bool converged = false;
+    std::vector<double> H((size_t)(restart + 1) * restart), cs(restart), sn(restart), g(restart + 1), y(restart);
+    if (nrb == 0.0) {
+        converged = true;
+        rre = 0.0;
+    }
+    while (!converged && iters < maxit) {
+        // r = R (b - A x)
+        if (iters == 0 && !guess) {
+            // x = 0: r = R b (already in K.r)
+        } else {
+            if ((s = matvec_dev(c, K.x, K.w))) return s;
+            k_axpby<<<gn, 256, 0, st>>>(K.w, K.b, 1.0, -1.0, n);  // w = b - A x
+            count_launch(c);
+            if ((s = precond_apply_dev(c, K.w, K.r))) return s;
+        }
+        double beta = 0;
+        if ((s = K.norm2_host(K.r, &beta))) return s;
+        rre = beta / nrb;
+        if (rre <= tol) {
+            converged = true;
+            break;
+        }
+        k_axpby<<<gn, 256, 0, st>>>(K.V, K.r, 1.0 / beta, 0.0, n);  // V0 = r / beta
+        count_launch(c);
+        std::fill(g.begin(), g.end(), 0.0);
+        g[0] = beta;
+        int jend = 0;
+        for (int j = 0; j < restart && iters < maxit; ++j) {
+            double* vj = K.V + (size_t)j * n;
+            double* vn = K.V + (size_t)(j + 1) * n;
+            if ((s = K.op(vj, K.t, K.w))) return s;
+            ++iters;
+            double* dh = c->dvec.p;
+            // CGS2: h = V^T t; t -= V h; h2 = V^T t; t -= V h2; ||t||^2
+            K.dots(K.V, j + 1, K.t, dh);
+            k_multiaxpy<<<gn, 256, 0, st>>>(K.t, K.V, n, j + 1, dh, n, -1.0);
+            K.dots(K.V, j + 1, K.t, dh + kMaxBasis);
+            k_multiaxpy<<<gn, 256, 0, st>>>(K.t, K.V, n, j + 1, dh + kMaxBasis, n, -1.0);
+            K.dots(K.t, 1, K.t, dh + 2 * kMaxBasis);
+            k_scale_by_norm<<<gn, 256, 0, st>>>(vn, K.t, dh + 2 * kMaxBasis, n);
+            count_launch(c, 3);
+            VC_CUDA(c, cudaMemcpyAsync(c->h_pinned, dh, 8 * 3 * kMaxBasis, cudaMemcpyDeviceToHost, st));
+            VC_CUDA(c, cudaStreamSynchronize(st));
+            const double* hh = c->h_pinned;
+            double* Hj = H.data() + (size_t)j * (restart + 1);  // column j
+            for (int i = 0; i <= j; ++i) Hj[i] = hh[i] + hh[kMaxBasis + i];
+            Hj[j + 1] = std::sqrt(hh[2 * kMaxBasis]);
+            for (int i = 0; i < j; ++i) {
+                const double a = Hj[i], bb = Hj[i + 1];
+                Hj[i] = cs[i] * a + sn[i] * bb;
+                Hj[i + 1] = -sn[i] * a + cs[i] * bb;
+            }
+            const double a = Hj[j], bb = Hj[j + 1];
+            const double den = std::hypot(a, bb);
+            cs[j] = den > 0 ? a / den : 1.0;
+            sn[j] = den > 0 ? bb / den : 0.0;
+            Hj[j] = den;
+            Hj[j + 1] = 0.0;
+            g[j + 1] = -sn[j] * g[j];
+            g[j] = cs[j] * g[j];
+            rre = std::fabs(g[j + 1]) / nrb;
+            jend = j + 1;
+            if (rre <= tol || !(rre == rre)) break;
+        }
+        // y = H^{-1} g (upper triangular), x += V y
+        for (int i = jend - 1; i >= 0; --i) {
+            double v = g[i];
+            for (int k = i + 1; k < jend; ++k) v -= H[(size_t)k * (restart + 1) + i] * y[k];
+            y[i] = v / H[(size_t)i * (restart + 1) + i];
+        }
+        VC_CUDA(c, cudaMemcpyAsync(c->dvec.p + 3 * kMaxBasis, y.data(), 8 * jend, cudaMemcpyHostToDevice, st));
+        k_multiaxpy<<<gn, 256, 0, st>>>(K.x, K.V, n, jend, c->dvec.p + 3 * kMaxBasis, n, 1.0);
+        count_launch(c);
+        if (rre <= tol) converged = true;
+        if (!(rre == rre)) break;
+    }
+    // true residual ||b - A x|| / ||b||
+    if ((s = matvec_dev(c, K.x, K.w))) return s;
+    k_axpby<<<gn, 256, 0, st>>>(K.w, K.b, 1.0, -1.0, n);
+    count_launch(c);
+    double nr = 0;
+    if ((s = K.norm2_host(K.w, &nr))) return s;
+    VC_CUDA(c, cudaMemcpyAsync(d_x, K.x, 8 * n, cudaMemcpyDeviceToDevice, st));
+    VC_CUDA(c, cudaStreamSynchronize(st));
+    if (info) {
+        info->iters = iters;
+        info->converged = converged ? 1 : 0;
+        info->rre_prec = rre;
+        info->rre_true = nb > 0 ? nr / nb : 0.0;
+    }
+    return converged ? VC_OK : set_err(c, VC_NOT_CONVERGED, "GMRES did not reach tol within maxit");
+}
+
+vc_status capacitance_dev(vc_ctx* c, double* h_C, const vc_solve_opts* o, vc_solve_info* info) {
+    cudaStream_t st = c->stream;
+    const int64_t n = c->N;
+    const int m = c->m;
+    DevBuf<double> b, rho, part, col;
+    VC_CUDA(c, b.alloc(n));
+    VC_CUDA(c, rho.alloc(n));
+    const unsigned nb = 148;
+    VC_CUDA(c, part.alloc((size_t)nb * m));
+    VC_CUDA(c, col.alloc(m));
+    std::vector<double> hp(m);
+    const double area = c->dv * c->dv;
+    vc_status worst = VC_OK;
+    for (int j = 1; j <= m; ++j) {
+        k_rhs<<<grid_for(n), 256, 0, st>>>(b.p, c->pan.cid.p, j, area, n);
+        count_launch(c);
+        vc_solve_info inf{};
+        vc_status s = solve_dev(c, b.p, rho.p, o, &inf);
+        if (s != VC_OK && s != VC_NOT_CONVERGED) return s;
+        if (s == VC_NOT_CONVERGED) worst = s;
+        if (info) info[j - 1] = inf;
+        dim3 g(nb, m);
+        k_cap_partial<<<g, kRedNT, 0, st>>>(rho.p, c->pan.cid.p, c->pan.fc.p, area, n, m, part.p);
+        k_cap_final<<<1, std::max(32, ((m + 31) / 32) * 32), 0, st>>>(part.p, nb, m, col.p);
+        count_launch(c, 2);
+        VC_CUDA(c, cudaMemcpyAsync(hp.data(), col.p, 8 * (size_t)m, cudaMemcpyDeviceToHost, st));
+        VC_CUDA(c, cudaStreamSynchronize(st));
+        for (int i = 0; i < m; ++i) h_C[(size_t)i * m + (j - 1)] = hp[i];
+    }
+    return worst == VC_OK ? VC_OK : set_err(c, worst, "some capacitance columns did not converge");
+}
+
+}  // namespace vc

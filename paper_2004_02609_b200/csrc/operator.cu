@@ -1,0 +1,824 @@
+// operator.cu -- FFT-accelerated Galerkin matvec (DESIGN.md a2-a8; Eqs. 9-12).
+//
+// Data flow of one matvec (all complex128, kx fastest, window origin lo = min panel slot):
+//   P1  x  --scatter + R2C along x (two real lines per complex FFT)-->  X1[b][z<ez][y<ey][kx]
+//   P2  X1 --C2C along y, zero-padded to My, times phi-bar_b,y-->        X2[b][z<ez][ky][kx]
+//   P3  X2 --C2C along z, times phi-bar_b,z; MAC with the folded real spectra R^{f,b};
+//           times i (E blocks) and phi_f,z; inverse C2C along z, pruned-->  X3[f][z<ez_f][ky][kx]
+//   P4  X3 --times phi_f,y; inverse C2C along y, pruned-->             X4[f][z][y<ey_f][kx]
+//   P5  X4 --times phi_f,x; C2R along x (two lines per complex FFT); gather at the f-panels:
+//           y_k = C^a[slot_k] (conductor rows) or s_k D^a[slot_k] + Ī_k x_k (dielectric rows)
+// K^{ab}(k) = phi_a(k) R^{ab}(k) conj(phi_b(k)), phi_g(k) = exp(2 pi i sum_c kt_c cg_c / M_c),
+// R real for P blocks and i*real for E blocks, even / odd (E along a) in each kt_c, so only the
+// octant 0 <= kt_c <= M_c/2 is stored; R^{yx} = R^{xy} (Eq. 12 after phase stripping).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "ctx.h"
+#include "fft.cuh"
+#include "kgen.cuh"
+
+namespace vc {
+
+struct MV {
+    int Mx, My, Mz, Kx;
+    int lo[3];
+    int G[3][3];       // slot-grid dims [orientation][axis]
+    int ext_in[3][3];  // [beta][axis]
+    int nf;
+    int fkind[6], faxis[6];
+    int ext_out[6][3];
+    const int32_t* slotmap[3];
+    const double* x;
+    double* y;
+    const int8_t* info;
+    const double* ibar;
+    double2* X1[3];
+    double2* X2[3];
+    double2* X3[6];
+    double2* X4[6];
+    const double* Rt;
+    size_t blk_stride;
+    int blk[6][3];
+    const double2* tw;
+};
+
+// ---- tile-size choices (compile-time functions of the FFT length) -----------------------
+constexpr int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
+template <int L> struct TX { static constexpr int T = clampi(4096 / L, 1, 64); };   // x passes
+template <int L> struct TY { static constexpr int T = clampi(4096 / L, 1, 32); };   // y passes
+template <int L> struct TZ { static constexpr int T = clampi(1024 / L, 1, 32); };   // z + MAC
+constexpr int kNT = 256;
+
+__device__ __forceinline__ int ktil(int k, int M) { return k <= M / 2 ? k : k - M; }
+
+// ---------------------------------------------------------------------------------------
+// P1: scatter + forward R2C along x
+// ---------------------------------------------------------------------------------------
+template <int L>
+__global__ void __launch_bounds__(kNT) k_p1(MV mv) {
+    constexpr int T = TX<L>::T;
+    extern __shared__ double2 sm[];
+    const int beta = blockIdx.y;
+    const int ex = mv.ext_in[beta][0], ey = mv.ext_in[beta][1], ez = mv.ext_in[beta][2];
+    if (ex == 0) return;
+    const int nyp = (ey + 1) >> 1;
+    const int nch = (nyp + T - 1) / T;
+    const int z = blockIdx.x / nch, ch = blockIdx.x % nch;
+    if (z >= ez) return;
+    const int32_t* __restrict__ smap = mv.slotmap[beta];
+    const int Gx = mv.G[beta][0], Gy = mv.G[beta][1];
+    const int64_t zrow = ((int64_t)(z + mv.lo[2]) * Gy + mv.lo[1]) * Gx + mv.lo[0];
+    const double* __restrict__ x = mv.x;
+    auto ld0 = [&](int t, int n) -> double2 {
+        const int q = ch * T + t;
+        double re = 0.0, im = 0.0;
+        if (q < nyp && n < ex) {
+            const int64_t r0 = zrow + (int64_t)(2 * q) * Gx + n;
+            const int p0 = smap[r0];
+            if (p0 >= 0) re = x[p0];
+            if (2 * q + 1 < ey) {
+                const int p1 = smap[r0 + Gx];
+                if (p1 >= 0) im = x[p1];
+            }
+        }
+        return make_double2(re, im);
+    };
+    auto sts = [&](int t, int p, double2 v) { sm[smi<L, T, false>(t, p)] = v; };
+    fft_run<L, T, kNT, false, false>(sm, ld0, sts, mv.tw);
+    __syncthreads();
+    constexpr int K = L / 2 + 1;
+    const bool ph = beta != 0;  // c_beta,x = 1/2 for y- and z-normal panels
+    double2* __restrict__ out = mv.X1[beta] + (int64_t)z * ey * mv.Kx;
+    for (int u = threadIdx.x; u < T * K; u += kNT) {
+        const int t = u / K, k = u % K;
+        const int q = ch * T + t;
+        if (q >= nyp) continue;
+        const double2 zk = sm[smi<L, T, false>(t, Plan<L>::pos(k))];
+        const double2 zm = sm[smi<L, T, false>(t, Plan<L>::pos((L - k) & (L - 1)))];
+        double2 A = make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y));
+        double2 B = make_double2(0.5 * (zk.y + zm.y), -0.5 * (zk.x - zm.x));
+        if (ph) {
+            const double2 w = half_phase(mv.tw, k, L, -1);
+            A = cmul(A, w);
+            B = cmul(B, w);
+        }
+        out[(int64_t)(2 * q) * mv.Kx + k] = A;
+        if (2 * q + 1 < ey) out[(int64_t)(2 * q + 1) * mv.Kx + k] = B;
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// P2: forward C2C along y (zero-padded input), times conj(phi_beta,y)
+// ---------------------------------------------------------------------------------------
+template <int L>
+__global__ void __launch_bounds__(kNT) k_p2(MV mv) {
+    constexpr int T = TY<L>::T;
+    extern __shared__ double2 sm[];
+    const int beta = blockIdx.y;
+    const int ex = mv.ext_in[beta][0], ey = mv.ext_in[beta][1], ez = mv.ext_in[beta][2];
+    if (ex == 0) return;
+    const int Kx = mv.Kx;
+    const int ntile = (Kx + T - 1) / T;
+    const int z = blockIdx.x / ntile, tile = blockIdx.x % ntile;
+    if (z >= ez) return;
+    const double2* __restrict__ in = mv.X1[beta] + (int64_t)z * ey * Kx;
+    double2* __restrict__ out = mv.X2[beta] + (int64_t)z * L * Kx;
+    const bool ph = beta != 1;  // c_beta,y = 1/2 for x- and z-normal panels
+    auto ld0 = [&](int t, int n) -> double2 {
+        const int kx = tile * T + t;
+        return (n < ey && kx < Kx) ? in[(int64_t)n * Kx + kx] : czero();
+    };
+    auto stN = [&](int t, int p, double2 v) {
+        const int kx = tile * T + t;
+        if (kx >= Kx) return;
+        const int k = Plan<L>::freq(p);
+        if (ph) v = cmul(v, half_phase(mv.tw, ktil(k, L), L, -1));
+        out[(int64_t)k * Kx + kx] = v;
+    };
+    fft_run<L, T, kNT, false, true>(sm, ld0, stN, mv.tw);
+}
+
+// ---------------------------------------------------------------------------------------
+// P3: forward z FFT of the three source fields, orientation-block MAC (Eqs. 10-12), inverse z
+// ---------------------------------------------------------------------------------------
+template <int L>
+__global__ void __launch_bounds__(kNT) k_p3(MV mv) {
+    constexpr int T = TZ<L>::T;
+    constexpr int TI = 6 * T, TO = 2 * T;
+    constexpr int KZ = L / 2 + 1;
+    extern __shared__ double2 sm[];
+    double2* smin = sm;
+    double2* smout = sm + L * TI;
+    const int Kx = mv.Kx, My = mv.My;
+    const int ntile = (Kx + T - 1) / T;
+    const int q = blockIdx.x / ntile, tile = blockIdx.x % ntile;
+    const int nside = (q == 0 || 2 * q == My) ? 1 : 2;
+    const int ky[2] = {q, My - q};
+    auto ld0 = [&](int pp, int n) -> double2 {
+        const int t = pp % T, grp = pp / T, beta = grp >> 1, side = grp & 1;
+        const int kx = tile * T + t;
+        if (side >= nside || kx >= Kx || n >= mv.ext_in[beta][2]) return czero();
+        return mv.X2[beta][((int64_t)n * My + ky[side]) * Kx + kx];
+    };
+    auto sti = [&](int pp, int p, double2 v) { smin[p * TI + pp] = v; };
+    fft_run<L, TI, kNT, false, true>(smin, ld0, sti, mv.tw);
+    __syncthreads();
+    for (int f = 0; f < mv.nf; ++f) {
+        const int kind = mv.fkind[f], alpha = mv.faxis[f];
+        const int ezo = mv.ext_out[f][2];
+        const bool phz_out = alpha != 2;  // c_alpha,z = 1/2 for x- and y-normal fields
+        for (int u = threadIdx.x; u < L * TO; u += kNT) {
+            const int t = u % T, side = (u / T) & 1, k = u / TO;
+            const int kx = tile * T + t;
+            double2 acc = czero();
+            if (side < nside && kx < Kx) {
+                const int p = Plan<L>::pos(k);
+                const int kt = ktil(k, L);
+                const int kzp = kt < 0 ? -kt : kt;
+                const double2 phin = half_phase(mv.tw, kt, L, -1);
+#pragma unroll
+                for (int beta = 0; beta < 3; ++beta) {
+                    const int b = mv.blk[f][beta];
+                    if (b < 0) continue;
+                    double2 qv = smin[p * TI + (beta * 2 + side) * T + t];
+                    if (beta != 2) qv = cmul(qv, phin);
+                    double r = __ldg(mv.Rt + (size_t)b * mv.blk_stride +
+                                     ((size_t)q * KZ + kzp) * Kx + kx);
+                    if (kind == 1) {
+                        if (alpha == 1 && side == 1) r = -r;
+                        if (alpha == 2 && kt < 0) r = -r;
+                    }
+                    acc.x = fma(r, qv.x, acc.x);
+                    acc.y = fma(r, qv.y, acc.y);
+                }
+                if (kind == 1) acc = make_double2(-acc.y, acc.x);
+                if (phz_out) acc = cmul(acc, half_phase(mv.tw, kt, L, +1));
+            }
+            smout[k * TO + side * T + t] = acc;
+        }
+        __syncthreads();
+        double2* __restrict__ X3 = mv.X3[f];
+        auto ldo = [&](int pp, int n) { return smout[n * TO + pp]; };
+        auto sto = [&](int pp, int p, double2 v) {
+            const int t = pp % T, side = pp / T;
+            const int kx = tile * T + t;
+            const int zz = Plan<L>::freq(p);
+            if (side < nside && kx < Kx && zz < ezo)
+                X3[((int64_t)zz * My + ky[side]) * Kx + kx] = v;
+        };
+        fft_run<L, TO, kNT, true, true>(smout, ldo, sto, mv.tw);
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// P4: times phi_f,y, inverse C2C along y, pruned to y < ey_f
+// ---------------------------------------------------------------------------------------
+template <int L>
+__global__ void __launch_bounds__(kNT) k_p4(MV mv) {
+    constexpr int T = TY<L>::T;
+    extern __shared__ double2 sm[];
+    const int f = blockIdx.y;
+    if (f >= mv.nf) return;
+    const int alpha = mv.faxis[f];
+    const int eyo = mv.ext_out[f][1], ezo = mv.ext_out[f][2];
+    const int Kx = mv.Kx;
+    const int ntile = (Kx + T - 1) / T;
+    const int z = blockIdx.x / ntile, tile = blockIdx.x % ntile;
+    if (z >= ezo) return;
+    const double2* __restrict__ in = mv.X3[f] + (int64_t)z * L * Kx;
+    double2* __restrict__ out = mv.X4[f] + (int64_t)z * eyo * Kx;
+    const bool ph = alpha != 1;
+    auto ld0 = [&](int t, int n) -> double2 {
+        const int kx = tile * T + t;
+        if (kx >= Kx) return czero();
+        double2 v = in[(int64_t)n * Kx + kx];
+        if (ph) v = cmul(v, half_phase(mv.tw, ktil(n, L), L, +1));
+        return v;
+    };
+    auto stN = [&](int t, int p, double2 v) {
+        const int kx = tile * T + t;
+        const int yy = Plan<L>::freq(p);
+        if (kx < Kx && yy < eyo) out[(int64_t)yy * Kx + kx] = v;
+    };
+    fft_run<L, T, kNT, true, true>(sm, ld0, stN, mv.tw);
+}
+
+// ---------------------------------------------------------------------------------------
+// P5: times phi_f,x, C2R along x (two lines per complex FFT), gather + dielectric terms
+// ---------------------------------------------------------------------------------------
+template <int L>
+__global__ void __launch_bounds__(kNT) k_p5(MV mv) {
+    constexpr int T = TX<L>::T;
+    extern __shared__ double2 sm[];
+    const int f = blockIdx.y;
+    if (f >= mv.nf) return;
+    const int kind = mv.fkind[f], alpha = mv.faxis[f];
+    const int exo = mv.ext_out[f][0], eyo = mv.ext_out[f][1], ezo = mv.ext_out[f][2];
+    const int nyp = (eyo + 1) >> 1;
+    const int nch = (nyp + T - 1) / T;
+    const int z = blockIdx.x / nch, ch = blockIdx.x % nch;
+    if (z >= ezo) return;
+    const int Kx = mv.Kx;
+    const double2* __restrict__ in = mv.X4[f] + (int64_t)z * eyo * Kx;
+    const bool ph = alpha != 0;
+    auto At = [&](int yrow, int k) -> double2 {
+        double2 v = in[(int64_t)yrow * Kx + k];
+        if (ph) v = cmul(v, half_phase(mv.tw, k, L, +1));
+        if (k == 0 || 2 * k == L) v.y = 0.0;
+        return v;
+    };
+    auto ld0 = [&](int t, int n) -> double2 {
+        const int q = ch * T + t;
+        if (q >= nyp) return czero();
+        const bool has1 = 2 * q + 1 < eyo;
+        double2 A, B = czero();
+        if (2 * n <= L) {
+            A = At(2 * q, n);
+            if (has1) B = At(2 * q + 1, n);
+        } else {
+            A = cconj(At(2 * q, L - n));
+            if (has1) B = cconj(At(2 * q + 1, L - n));
+        }
+        return make_double2(A.x - B.y, A.y + B.x);
+    };
+    const int32_t* __restrict__ smap = mv.slotmap[alpha];
+    const int Gx = mv.G[alpha][0], Gy = mv.G[alpha][1];
+    const int64_t zrow = ((int64_t)(z + mv.lo[2]) * Gy + mv.lo[1]) * Gx + mv.lo[0];
+    auto put = [&](int p, double val) {
+        const int inf = mv.info[p];
+        if ((inf & 1) != kind) return;
+        if (kind == 0) mv.y[p] = val;
+        else mv.y[p] = ((inf & 2) ? -val : val) + mv.ibar[p] * mv.x[p];
+    };
+    auto stN = [&](int t, int p, double2 v) {
+        const int q = ch * T + t;
+        const int n = Plan<L>::freq(p);
+        if (q >= nyp || n >= exo) return;
+        const int64_t r0 = zrow + (int64_t)(2 * q) * Gx + n;
+        const int p0 = smap[r0];
+        if (p0 >= 0) put(p0, v.x);
+        if (2 * q + 1 < eyo) {
+            const int p1 = smap[r0 + Gx];
+            if (p1 >= 0) put(p1, v.y);
+        }
+    };
+    fft_run<L, T, kNT, true, false>(sm, ld0, stN, mv.tw);
+}
+
+// ---------------------------------------------------------------------------------------
+// setup kernels: kernel-entry grid (a2), in-place 3-D C2C FFT, spectrum extraction (a3)
+// ---------------------------------------------------------------------------------------
+__global__ void k_twiddles(double2* tw) {
+    const int n = blockIdx.x * blockDim.x + threadIdx.x;
+    if (n >= kTabN) return;
+    double s, c;
+    sincospi(-2.0 * n / (double)kTabN, &s, &c);
+    tw[n] = make_double2(c, s);
+}
+
+// representative slot offset of cyclic index n for doubled half-shift s2
+__device__ __forceinline__ int rep_offset(int n, int M, int s2) {
+    if (s2 > 0) return n < M / 2 ? n : n - M;   // minimise |delta + 1/2|
+    if (s2 < 0) return n <= M / 2 ? n : n - M;  // minimise |delta - 1/2|
+    return n <= M / 2 ? n : n - M;              // tie at M/2 -> +M/2
+}
+
+__global__ void k_kgen(double2* G, int Mx, int My, int Mz, int kind, int alpha, int beta) {
+    const int64_t tot = (int64_t)Mx * My * Mz;
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < tot;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int nx = (int)(idx % Mx);
+        const int ny = (int)((idx / Mx) % My);
+        const int nz = (int)(idx / ((int64_t)Mx * My));
+        const int n[3] = {nx, ny, nz};
+        const int M[3] = {Mx, My, Mz};
+        int d[3];
+        bool zero = false;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            const int s2 = c2(alpha, a) - c2(beta, a);
+            d[a] = rep_offset(n[a], M[a], s2);
+            // odd kernel (E^{aa} along a) at the unresolvable tie n = M/2 -> 0
+            if (kind == 1 && alpha == beta && a == alpha && 2 * n[a] == M[a]) zero = true;
+        }
+        const double v = zero ? 0.0 : kappa(kind, alpha, beta, d[0], d[1], d[2]);
+        G[idx] = make_double2(v, 0.0);
+    }
+}
+
+// in-place C2C FFT of contiguous lines: data[line][L]
+template <int L, bool INV>
+__global__ void __launch_bounds__(kNT) k_fft_lines(double2* data, int64_t nlines,
+                                                   const double2* __restrict__ tw) {
+    constexpr int T = TX<L>::T;
+    extern __shared__ double2 sm[];
+    const int64_t l0 = (int64_t)blockIdx.x * T;
+    auto ld0 = [&](int t, int n) -> double2 {
+        return l0 + t < nlines ? data[(l0 + t) * L + n] : czero();
+    };
+    auto stN = [&](int t, int p, double2 v) {
+        if (l0 + t < nlines) data[(l0 + t) * L + Plan<L>::freq(p)] = v;
+    };
+    fft_run<L, T, kNT, INV, false>(sm, ld0, stN, tw);
+}
+
+// in-place C2C FFT along a strided axis: element n of column c in batch b at
+// data[b*bs + n*es + c], columns c in [0, ncols) contiguous.
+template <int L>
+__global__ void __launch_bounds__(kNT) k_fft_strided(double2* data, int64_t es, int64_t ncols,
+                                                     int64_t bs, const double2* __restrict__ tw) {
+    constexpr int T = TY<L>::T;
+    extern __shared__ double2 sm[];
+    const int64_t ntile = (ncols + T - 1) / T;
+    const int64_t b = blockIdx.x / ntile, c0 = (blockIdx.x % ntile) * T;
+    double2* base = data + b * bs + c0;
+    auto ld0 = [&](int t, int n) -> double2 {
+        return c0 + t < ncols ? base[n * es + t] : czero();
+    };
+    auto stN = [&](int t, int p, double2 v) {
+        if (c0 + t < ncols) base[(int64_t)Plan<L>::freq(p) * es + t] = v;
+    };
+    fft_run<L, T, kNT, false, true>(sm, ld0, stN, tw);
+}
+
+// R[ky'][kz'][kx] = {Re | Im}(K^(kx,ky',kz') exp(-2 pi i k.(c_a - c_b)/M)) * scale
+__global__ void k_extract(const double2* __restrict__ G, double* __restrict__ R, int Mx, int My,
+                          int Mz, int Kx, int kind, int alpha, int beta, double scale,
+                          const double2* __restrict__ tw) {
+    const int KY = My / 2 + 1, KZ = Mz / 2 + 1;
+    const int64_t tot = (int64_t)Kx * KY * KZ;
+    const int s2x = c2(alpha, 0) - c2(beta, 0), s2y = c2(alpha, 1) - c2(beta, 1),
+              s2z = c2(alpha, 2) - c2(beta, 2);
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < tot;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int kx = (int)(idx % Kx);
+        const int kz = (int)((idx / Kx) % KZ);
+        const int ky = (int)(idx / ((int64_t)Kx * KZ));
+        double2 v = G[((int64_t)kz * My + ky) * Mx + kx];
+        v = cmul(v, half_phase(tw, kx * s2x, Mx, -1));
+        v = cmul(v, half_phase(tw, ky * s2y, My, -1));
+        v = cmul(v, half_phase(tw, kz * s2z, Mz, -1));
+        R[idx] = (kind == 0 ? v.x : v.y) * scale;
+    }
+}
+
+__global__ void k_zero(double* y, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        y[i] = 0.0;
+}
+
+__global__ void k_debug_kappa(int n, const int32_t* kind, const int32_t* a, const int32_t* b,
+                              const int32_t* d, double* out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = kappa(kind[i], a[i], b[i], d[3 * i], d[3 * i + 1], d[3 * i + 2]);
+}
+
+// ---------------------------------------------------------------------------------------
+// launchers (compile-time FFT length dispatch)
+// ---------------------------------------------------------------------------------------
+template <class K>
+static cudaError_t prep(K kern, size_t smem) {
+    if (smem > 48 * 1024) return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    return cudaSuccess;
+}
+
+#define VC_DISPATCH_L(L, ...)                                       \
+    switch (L) {                                                    \
+        case 8: { constexpr int LL = 8; __VA_ARGS__; } break;       \
+        case 16: { constexpr int LL = 16; __VA_ARGS__; } break;     \
+        case 32: { constexpr int LL = 32; __VA_ARGS__; } break;     \
+        case 64: { constexpr int LL = 64; __VA_ARGS__; } break;     \
+        case 128: { constexpr int LL = 128; __VA_ARGS__; } break;   \
+        case 256: { constexpr int LL = 256; __VA_ARGS__; } break;   \
+        case 512: { constexpr int LL = 512; __VA_ARGS__; } break;   \
+        case 1024: { constexpr int LL = 1024; __VA_ARGS__; } break; \
+        case 2048: { constexpr int LL = 2048; __VA_ARGS__; } break; \
+        case 4096: { constexpr int LL = 4096; __VA_ARGS__; } break; \
+        default: return cudaErrorInvalidValue;                      \
+    }
+
+static cudaError_t launch_p1(const MV& mv, cudaStream_t st) {
+    int maxch = 0, maxz = 0;
+    for (int b = 0; b < 3; ++b) { maxz = std::max(maxz, mv.ext_in[b][2]); }
+    VC_DISPATCH_L(mv.Mx, {
+        constexpr int T = TX<LL>::T;
+        for (int b = 0; b < 3; ++b) maxch = std::max(maxch, ((mv.ext_in[b][1] + 1) / 2 + T - 1) / T);
+        const size_t smem = sizeof(double2) * LL * T;
+        cudaError_t e = prep(k_p1<LL>, smem);
+        if (e) return e;
+        dim3 grid(std::max(1, maxch * maxz), 3);
+        k_p1<LL><<<grid, kNT, smem, st>>>(mv);
+    });
+    return cudaGetLastError();
+}
+static cudaError_t launch_p2(const MV& mv, cudaStream_t st) {
+    int maxz = 0;
+    for (int b = 0; b < 3; ++b) maxz = std::max(maxz, mv.ext_in[b][2]);
+    VC_DISPATCH_L(mv.My, {
+        constexpr int T = TY<LL>::T;
+        const size_t smem = sizeof(double2) * LL * T;
+        cudaError_t e = prep(k_p2<LL>, smem);
+        if (e) return e;
+        dim3 grid(std::max(1, ((mv.Kx + T - 1) / T) * maxz), 3);
+        k_p2<LL><<<grid, kNT, smem, st>>>(mv);
+    });
+    return cudaGetLastError();
+}
+static cudaError_t launch_p3(const MV& mv, cudaStream_t st) {
+    VC_DISPATCH_L(mv.Mz, {
+        constexpr int T = TZ<LL>::T;
+        const size_t smem = sizeof(double2) * LL * 8 * T;
+        cudaError_t e = prep(k_p3<LL>, smem);
+        if (e) return e;
+        dim3 grid(((mv.Kx + T - 1) / T) * (mv.My / 2 + 1));
+        k_p3<LL><<<grid, kNT, smem, st>>>(mv);
+    });
+    return cudaGetLastError();
+}
+static cudaError_t launch_p4(const MV& mv, cudaStream_t st) {
+    int maxz = 0;
+    for (int f = 0; f < mv.nf; ++f) maxz = std::max(maxz, mv.ext_out[f][2]);
+    VC_DISPATCH_L(mv.My, {
+        constexpr int T = TY<LL>::T;
+        const size_t smem = sizeof(double2) * LL * T;
+        cudaError_t e = prep(k_p4<LL>, smem);
+        if (e) return e;
+        dim3 grid(std::max(1, ((mv.Kx + T - 1) / T) * maxz), mv.nf);
+        k_p4<LL><<<grid, kNT, smem, st>>>(mv);
+    });
+    return cudaGetLastError();
+}
+static cudaError_t launch_p5(const MV& mv, cudaStream_t st) {
+    int maxz = 0, maxch = 0;
+    for (int f = 0; f < mv.nf; ++f) maxz = std::max(maxz, mv.ext_out[f][2]);
+    VC_DISPATCH_L(mv.Mx, {
+        constexpr int T = TX<LL>::T;
+        for (int f = 0; f < mv.nf; ++f) maxch = std::max(maxch, ((mv.ext_out[f][1] + 1) / 2 + T - 1) / T);
+        const size_t smem = sizeof(double2) * LL * T;
+        cudaError_t e = prep(k_p5<LL>, smem);
+        if (e) return e;
+        dim3 grid(std::max(1, maxch * maxz), mv.nf);
+        k_p5<LL><<<grid, kNT, smem, st>>>(mv);
+    });
+    return cudaGetLastError();
+}
+static cudaError_t launch_fft_lines(double2* d, int L, int64_t nlines, bool inv,
+                                    const double2* tw, cudaStream_t st) {
+    VC_DISPATCH_L(L, {
+        constexpr int T = TX<LL>::T;
+        const size_t smem = sizeof(double2) * LL * T;
+        const unsigned grid = (unsigned)((nlines + T - 1) / T);
+        if (inv) {
+            cudaError_t e = prep(k_fft_lines<LL, true>, smem);
+            if (e) return e;
+            k_fft_lines<LL, true><<<grid, kNT, smem, st>>>(d, nlines, tw);
+        } else {
+            cudaError_t e = prep(k_fft_lines<LL, false>, smem);
+            if (e) return e;
+            k_fft_lines<LL, false><<<grid, kNT, smem, st>>>(d, nlines, tw);
+        }
+    });
+    return cudaGetLastError();
+}
+static cudaError_t launch_fft_strided(double2* d, int L, int64_t es, int64_t ncols,
+                                      int64_t nbatch, int64_t bs, const double2* tw,
+                                      cudaStream_t st) {
+    VC_DISPATCH_L(L, {
+        constexpr int T = TY<LL>::T;
+        const size_t smem = sizeof(double2) * LL * T;
+        cudaError_t e = prep(k_fft_strided<LL>, smem);
+        if (e) return e;
+        const unsigned grid = (unsigned)(((ncols + T - 1) / T) * nbatch);
+        k_fft_strided<LL><<<grid, kNT, smem, st>>>(d, es, ncols, bs, tw);
+    });
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------------------
+// planning and build (vc_build_operator)
+// ---------------------------------------------------------------------------------------
+static int next_pow2(int v) {
+    int p = 8;
+    while (p < v) p *= 2;
+    return p;
+}
+
+vc_status operator_build(vc_ctx* c, const vc_build_opts* o) {
+    cudaStream_t st = c->stream;
+    // window origin and per-orientation extents
+    int lo[3] = {INT32_MAX, INT32_MAX, INT32_MAX};
+    bool has[2][3] = {{false, false, false}, {false, false, false}};
+    for (int kind = 0; kind < 2; ++kind)
+        for (int a = 0; a < 3; ++a) {
+            if (c->ext[kind][a][0][0] > c->ext[kind][a][1][0]) continue;
+            has[kind][a] = true;
+            for (int t = 0; t < 3; ++t) lo[t] = std::min(lo[t], c->ext[kind][a][0][t]);
+        }
+    // centre extents (doubled) of each (kind, orientation) class along each axis
+    auto cmin2 = [&](int kind, int a, int t) { return 2 * c->ext[kind][a][0][t] + c2(a, t); };
+    auto cmax2 = [&](int kind, int a, int t) { return 2 * c->ext[kind][a][1][t] + c2(a, t); };
+    int req[3] = {8, 8, 8};
+    for (int t = 0; t < 3; ++t) {
+        for (int kr = 0; kr < 2; ++kr)
+            for (int al = 0; al < 3; ++al) {
+                if (!has[kr][al]) continue;
+                for (int ks = 0; ks < 2; ++ks)
+                    for (int be = 0; be < 3; ++be) {
+                        if (!has[ks][be]) continue;
+                        // largest |centre offset| (doubled) between rows (kr,al) and cols (ks,be)
+                        const int L2 = std::max(cmax2(kr, al, t) - cmin2(ks, be, t),
+                                                cmax2(ks, be, t) - cmin2(kr, al, t));
+                        const int s2 = c2(al, t) - c2(be, t);
+                        int r;
+                        if (s2 != 0) r = L2 + 1;            // half-integer offsets: M >= 2L + 1
+                        else r = L2 + ((kr == 1 && al == t) ? 1 : 0);  // integer: 2L (+1 if odd)
+                        req[t] = std::max(req[t], r);
+                    }
+            }
+        int extmax = 0;
+        for (int kind = 0; kind < 2; ++kind)
+            for (int a = 0; a < 3; ++a)
+                if (has[kind][a]) extmax = std::max(extmax, c->ext[kind][a][1][t] - lo[t] + 1);
+        req[t] = std::max(req[t], extmax);
+    }
+    int M[3];
+    for (int t = 0; t < 3; ++t) {
+        M[t] = next_pow2(req[t]);
+        if (o && o->pad[t]) {
+            if (o->pad[t] < req[t] || (o->pad[t] & (o->pad[t] - 1)) || o->pad[t] < 8)
+                return set_err(c, VC_ERR_INPUT, "pad must be a power of two >= 8 and >= the exactness bound " + std::to_string(req[t]));
+            M[t] = o->pad[t];
+        }
+        if (M[t] > kMaxL) return set_err(c, VC_ERR_UNSUPPORTED, "padded FFT size > 4096 along an axis");
+    }
+    for (int t = 0; t < 3; ++t) {
+        c->M[t] = M[t];
+        c->lo[t] = lo[t];
+    }
+    c->Kx = M[0] / 2 + 1;
+    const int Kx = c->Kx, My = M[1], Mz = M[2];
+    // source orientations (any panel kind) and output fields
+    for (int b = 0; b < 3; ++b) {
+        int hi[3] = {-1, -1, -1};
+        for (int kind = 0; kind < 2; ++kind)
+            if (has[kind][b])
+                for (int t = 0; t < 3; ++t) hi[t] = std::max(hi[t], c->ext[kind][b][1][t]);
+        for (int t = 0; t < 3; ++t) c->ext_in[b][t] = hi[t] < 0 ? 0 : hi[t] - lo[t] + 1;
+    }
+    c->nf = 0;
+    for (int kind = 0; kind < 2; ++kind)
+        for (int a = 0; a < 3; ++a) {
+            if (!has[kind][a]) continue;
+            Field& F = c->f[c->nf++];
+            F.kind = kind;
+            F.axis = a;
+            for (int t = 0; t < 3; ++t) F.ext[t] = c->ext[kind][a][1][t] - lo[t] + 1;
+        }
+    // kernel blocks: (field, beta); P^{ab} and P^{ba} share one spectrum (Eq. 12)
+    int pblk[3][3];
+    for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) pblk[a][b] = -1;
+    struct BlkDef { int kind, alpha, beta; };
+    std::vector<BlkDef> defs;
+    for (int f = 0; f < c->nf; ++f)
+        for (int b = 0; b < 3; ++b) {
+            c->blk[f][b] = -1;
+            if (c->ext_in[b][0] == 0) continue;
+            const int kind = c->f[f].kind, a = c->f[f].axis;
+            if (kind == 0) {
+                const int lo_ = std::min(a, b), hi_ = std::max(a, b);
+                if (pblk[lo_][hi_] < 0) {
+                    pblk[lo_][hi_] = (int)defs.size();
+                    defs.push_back({0, lo_, hi_});
+                }
+                c->blk[f][b] = pblk[lo_][hi_];
+            } else {
+                c->blk[f][b] = (int)defs.size();
+                defs.push_back({1, a, b});
+            }
+        }
+    for (int f = c->nf; f < 6; ++f)
+        for (int b = 0; b < 3; ++b) c->blk[f][b] = -1;
+    c->nblk = (int)defs.size();
+    c->blk_stride = (size_t)Kx * (My / 2 + 1) * (Mz / 2 + 1);
+    VC_CUDA(c, c->tw.alloc(kTabN));
+    k_twiddles<<<(kTabN + 255) / 256, 256, 0, st>>>(c->tw.p);
+    count_launch(c);
+    VC_CUDA(c, c->Rt.alloc(c->blk_stride * std::max(1, c->nblk)));
+    // spectra
+    {
+        DevBuf<double2> G;
+        const int64_t tot = (int64_t)M[0] * M[1] * M[2];
+        VC_CUDA(c, G.alloc(tot));
+        const double fpe = 4.0 * kPi * kEps0;
+        for (int i = 0; i < c->nblk; ++i) {
+            const BlkDef& d = defs[i];
+            const int gblocks = (int)std::min<int64_t>((tot + 255) / 256, 148 * 64);
+            k_kgen<<<gblocks, 256, 0, st>>>(G.p, M[0], M[1], M[2], d.kind, d.alpha, d.beta);
+            VC_CUDA(c, launch_fft_lines(G.p, M[0], (int64_t)M[1] * M[2], false, c->tw.p, st));
+            VC_CUDA(c, launch_fft_strided(G.p, M[1], M[0], M[0], M[2], (int64_t)M[0] * M[1], c->tw.p, st));
+            VC_CUDA(c, launch_fft_strided(G.p, M[2], (int64_t)M[0] * M[1], (int64_t)M[0] * M[1], 1, 0, c->tw.p, st));
+            const double scale = (d.kind == 0 ? c->dv * c->dv * c->dv : c->dv * c->dv) / fpe /
+                                 ((double)M[0] * M[1] * M[2]);
+            const int eblocks = (int)std::min<int64_t>((c->blk_stride + 255) / 256, 148 * 32);
+            k_extract<<<eblocks, 256, 0, st>>>(G.p, c->Rt.p + c->blk_stride * i, M[0], M[1], M[2],
+                                               Kx, d.kind, d.alpha, d.beta, scale, c->tw.p);
+            count_launch(c, 5);
+        }
+        VC_CUDA(c, cudaStreamSynchronize(st));
+        VC_CUDA(c, cudaGetLastError());
+    }
+    // pass buffers: A holds X1 (P1->P2) and later X4 (P4->P5); B holds X2; C holds X3
+    size_t nA_in = 0, nA_out = 0, nB = 0, nC = 0;
+    for (int b = 0; b < 3; ++b) {
+        c->offA_in[b] = nA_in;
+        c->offB[b] = nB;
+        nA_in += (size_t)c->ext_in[b][2] * c->ext_in[b][1] * Kx;
+        nB += (size_t)c->ext_in[b][2] * My * Kx;
+    }
+    for (int f = 0; f < c->nf; ++f) {
+        c->offC[f] = nC;
+        c->offA_out[f] = nA_out;
+        nC += (size_t)c->f[f].ext[2] * My * Kx;
+        nA_out += (size_t)c->f[f].ext[2] * c->f[f].ext[1] * Kx;
+    }
+    VC_CUDA(c, c->bufA.alloc(std::max<size_t>(1, std::max(nA_in, nA_out))));
+    VC_CUDA(c, c->bufB.alloc(std::max<size_t>(1, nB)));
+    VC_CUDA(c, c->bufC.alloc(std::max<size_t>(1, nC)));
+    // algorithmic bytes per pass: complex128 reads + writes of the pass
+    // arrays, kernel spectra read once, panel vectors and slot maps once.
+    const double cb = 16.0;
+    double slots = 0;
+    for (int b = 0; b < 3; ++b) slots += (double)c->ext_in[b][0] * c->ext_in[b][1] * c->ext_in[b][2];
+    double slots_out = 0;
+    for (int f = 0; f < c->nf; ++f) slots_out += (double)c->f[f].ext[0] * c->f[f].ext[1] * c->f[f].ext[2];
+    c->bytes_pass[0] = cb * nA_in + 4.0 * slots + 8.0 * c->N;
+    c->bytes_pass[1] = cb * (nA_in + nB);
+    c->bytes_pass[2] = cb * (nB + nC) + 8.0 * c->blk_stride * c->nblk;
+    c->bytes_pass[3] = cb * (nC + nA_out);
+    c->bytes_pass[4] = cb * nA_out + 4.0 * slots_out + 8.0 * c->N + (8.0 + 8.0 + 1.0) * c->Nd + 1.0 * c->N;
+    double tot = 0;
+    for (int p = 0; p < 5; ++p) {
+        c->stats.bytes_pass[p] = c->bytes_pass[p];
+        tot += c->bytes_pass[p];
+    }
+    c->stats.bytes_matvec = tot;
+    return VC_OK;
+}
+
+static MV make_mv(vc_ctx* c, const double* x, double* y) {
+    MV mv;
+    memset(&mv, 0, sizeof(mv));
+    mv.Mx = c->M[0];
+    mv.My = c->M[1];
+    mv.Mz = c->M[2];
+    mv.Kx = c->Kx;
+    for (int t = 0; t < 3; ++t) mv.lo[t] = c->lo[t];
+    for (int a = 0; a < 3; ++a) {
+        mv.G[a][0] = c->nx + (a == 0);
+        mv.G[a][1] = c->ny + (a == 1);
+        mv.G[a][2] = c->nz + (a == 2);
+        for (int t = 0; t < 3; ++t) mv.ext_in[a][t] = c->ext_in[a][t];
+        mv.slotmap[a] = c->pan.slotmap[a].p;
+        mv.X1[a] = c->bufA.p + c->offA_in[a];
+        mv.X2[a] = c->bufB.p + c->offB[a];
+    }
+    mv.nf = c->nf;
+    for (int f = 0; f < 6; ++f) {
+        for (int b = 0; b < 3; ++b) mv.blk[f][b] = c->blk[f][b];
+        if (f < c->nf) {
+            mv.fkind[f] = c->f[f].kind;
+            mv.faxis[f] = c->f[f].axis;
+            for (int t = 0; t < 3; ++t) mv.ext_out[f][t] = c->f[f].ext[t];
+            mv.X3[f] = c->bufC.p + c->offC[f];
+            mv.X4[f] = c->bufA.p + c->offA_out[f];
+        }
+    }
+    mv.x = x;
+    mv.y = y;
+    mv.info = c->pan.info.p;
+    mv.ibar = c->pan.ibar.p;
+    mv.Rt = c->Rt.p;
+    mv.blk_stride = c->blk_stride;
+    mv.tw = c->tw.p;
+    return mv;
+}
+
+vc_status matvec_dev(vc_ctx* c, const double* d_x, double* d_y) {
+    cudaStream_t st = c->stream;
+    const MV mv = make_mv(c, d_x, d_y);
+    Timing& T = c->timing;
+    const bool det = T.detail && T.ev_ok;
+    if (T.ev_ok) VC_CUDA(c, cudaEventRecord(T.ev[0], st));
+    k_zero<<<std::max<int64_t>(1, std::min<int64_t>((c->N + 255) / 256, 1184)), 256, 0, st>>>(d_y, c->N);
+    cudaError_t (*launch[5])(const MV&, cudaStream_t) = {launch_p1, launch_p2, launch_p3,
+                                                         launch_p4, launch_p5};
+    for (int p = 0; p < 5; ++p) {
+        if (det) VC_CUDA(c, cudaEventRecord(T.ev[1 + p], st));
+        VC_CUDA(c, launch[p](mv, st));
+        if (det) VC_CUDA(c, cudaEventRecord(T.ev[6 + p], st));
+    }
+    if (T.ev_ok) VC_CUDA(c, cudaEventRecord(T.ev[11], st));
+    count_launch(c, 6);
+    c->stats.n_matvec += 1;
+    for (int p = 0; p < 5; ++p) c->stats.n_pass[p] += 1;
+    if (T.ev_ok) {
+        // accumulate device times (waits for this matvec; used only with timing on)
+        VC_CUDA(c, cudaEventSynchronize(T.ev[11]));
+        float ms = 0;
+        VC_CUDA(c, cudaEventElapsedTime(&ms, T.ev[0], T.ev[11]));
+        c->stats.ms_matvec += ms;
+        if (det)
+            for (int p = 0; p < 5; ++p) {
+                VC_CUDA(c, cudaEventElapsedTime(&ms, T.ev[1 + p], T.ev[6 + p]));
+                c->stats.ms_pass[p] += ms;
+            }
+    }
+    return VC_OK;
+}
+
+vc_status debug_kernel_entries(vc_ctx* c, int n, const int32_t* kind, const int32_t* a,
+                               const int32_t* b, const int32_t* d, double* out) {
+    DevBuf<int32_t> dk, da, db, dd;
+    DevBuf<double> dout;
+    VC_CUDA(c, dk.alloc(n));
+    VC_CUDA(c, da.alloc(n));
+    VC_CUDA(c, db.alloc(n));
+    VC_CUDA(c, dd.alloc(3 * (size_t)n));
+    VC_CUDA(c, dout.alloc(n));
+    cudaStream_t st = c->stream;
+    VC_CUDA(c, cudaMemcpyAsync(dk.p, kind, 4 * (size_t)n, cudaMemcpyHostToDevice, st));
+    VC_CUDA(c, cudaMemcpyAsync(da.p, a, 4 * (size_t)n, cudaMemcpyHostToDevice, st));
+    VC_CUDA(c, cudaMemcpyAsync(db.p, b, 4 * (size_t)n, cudaMemcpyHostToDevice, st));
+    VC_CUDA(c, cudaMemcpyAsync(dd.p, d, 12 * (size_t)n, cudaMemcpyHostToDevice, st));
+    k_debug_kappa<<<(n + 127) / 128, 128, 0, st>>>(n, dk.p, da.p, db.p, dd.p, dout.p);
+    count_launch(c);
+    VC_CUDA(c, cudaMemcpyAsync(out, dout.p, 8 * (size_t)n, cudaMemcpyDeviceToHost, st));
+    VC_CUDA(c, cudaStreamSynchronize(st));
+    VC_CUDA(c, cudaGetLastError());
+    return VC_OK;
+}
+
+vc_status debug_fft(vc_ctx* c, int L, int nl, double* data, int dir) {
+    if (L < 8 || L > kMaxL || (L & (L - 1))) return set_err(c, VC_ERR_INPUT, "L must be a power of two in [8, 4096]");
+    cudaStream_t st = c->stream;
+    if (!c->tw.p) {
+        VC_CUDA(c, c->tw.alloc(kTabN));
+        k_twiddles<<<(kTabN + 255) / 256, 256, 0, st>>>(c->tw.p);
+        count_launch(c);
+    }
+    DevBuf<double2> d;
+    VC_CUDA(c, d.alloc((size_t)L * nl));
+    VC_CUDA(c, cudaMemcpyAsync(d.p, data, 16 * (size_t)L * nl, cudaMemcpyHostToDevice, st));
+    VC_CUDA(c, launch_fft_lines(d.p, L, nl, dir > 0, c->tw.p, st));
+    count_launch(c);
+    VC_CUDA(c, cudaMemcpyAsync(data, d.p, 16 * (size_t)L * nl, cudaMemcpyDeviceToHost, st));
+    VC_CUDA(c, cudaStreamSynchronize(st));
+    return VC_OK;
+}
+
+}  // namespace vc

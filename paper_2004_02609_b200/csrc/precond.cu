@@ -1,0 +1,286 @@
+// precond.cu -- block-diagonal-diagonal preconditioner (Eq. 14; DESIGN.md a9/a10).
+//
+// R_BD: the bounding box is split into boxes of Nvx x Nvy x Nvz voxels; every box's
+// conductor panels (reading O9; a panel belongs to box min(slot_a / Nv_a, nbox_a - 1)) form a
+// dense block of Eq. (5) interactions, which is inverted.  Boxes whose panel configurations are
+// identical up to translation share one inverted block ("only unique blocks are
+// stored").  R_D = Ī^{-1} on dielectric rows.
+// Structure (box assignment, signatures, dedup) is host C++; block entries, inversion and the
+// apply are CUDA kernels.
+#include <algorithm>
+#include <cstring>
+#include <unordered_map>
+
+#include "ctx.h"
+#include "kgen.cuh"
+
+namespace vc {
+
+struct Precond {
+    int kind = 3;
+    int nbox = 0, nuniq = 0;
+    int max_n = 0;
+    DevBuf<int32_t> box_start, box_n, box_uid;  // per non-empty box
+    DevBuf<int32_t> panel_ids;                   // conductor panels sorted by box
+    DevBuf<int64_t> uniq_off;                    // offset of each unique block (doubles)
+    DevBuf<int32_t> uniq_n, uniq_list_off;
+    DevBuf<int32_t> uniq_axis, uniq_slot;        // local panel descriptors (3 ints per slot)
+    DevBuf<double> blocks;                       // inverted blocks, row-major
+    DevBuf<double> diag_inv;                     // per panel: 1/Ī (diel), 1/P_kk (diag-only)
+    int64_t block_doubles = 0;
+};
+
+namespace {
+
+__global__ void k_pc_fill(const int32_t* __restrict__ un, const int64_t* __restrict__ uoff,
+                          const int32_t* __restrict__ ulist, const int32_t* __restrict__ uaxis,
+                          const int32_t* __restrict__ uslot, double* __restrict__ blocks,
+                          double scale) {
+    const int u = blockIdx.y;
+    const int n = un[u];
+    const int64_t nn = (int64_t)n * n;
+    double* B = blocks + uoff[u];
+    const int l0 = ulist[u];
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nn;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int i = (int)(e / n), j = (int)(e % n);
+        const int ai = uaxis[l0 + i], aj = uaxis[l0 + j];
+        const int dx = uslot[3 * (l0 + i)] - uslot[3 * (l0 + j)];
+        const int dy = uslot[3 * (l0 + i) + 1] - uslot[3 * (l0 + j) + 1];
+        const int dz = uslot[3 * (l0 + i) + 2] - uslot[3 * (l0 + j) + 2];
+        B[e] = scale * kappa(0, ai, aj, dx, dy, dz);
+    }
+}
+
+// in-place Gauss-Jordan inverse of an SPD block (no pivoting needed), one CTA per block
+__global__ void k_pc_invert(const int32_t* __restrict__ un, const int64_t* __restrict__ uoff,
+                            double* __restrict__ blocks) {
+    extern __shared__ double sh[];
+    const int u = blockIdx.x;
+    const int n = un[u];
+    double* A = blocks + uoff[u];
+    double* rowk = sh;
+    double* colk = sh + n;
+    for (int k = 0; k < n; ++k) {
+        __syncthreads();
+        const double piv = A[(int64_t)k * n + k];
+        const double ip = 1.0 / piv;
+        for (int j = threadIdx.x; j < n; j += blockDim.x) {
+            rowk[j] = j == k ? ip : A[(int64_t)k * n + j] * ip;
+            colk[j] = A[(int64_t)j * n + k];
+        }
+        __syncthreads();
+        for (int64_t e = threadIdx.x; e < (int64_t)n * n; e += blockDim.x) {
+            const int i = (int)(e / n), j = (int)(e % n);
+            if (i == k) A[e] = rowk[j];
+            else if (j == k) A[e] = -colk[i] * ip;
+            else A[e] -= colk[i] * rowk[j];
+        }
+    }
+}
+
+// z = R_D r on all rows (dielectric: r/Ī; conductor: r * diag_inv (diag-only) or 0)
+__global__ void k_pc_diag(int64_t N, const double* __restrict__ r, const double* __restrict__ dinv,
+                          double* __restrict__ z) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N;
+         i += (int64_t)gridDim.x * blockDim.x)
+        z[i] = r[i] * dinv[i];
+}
+
+// z_b = R_b r_b for every box (warp per row)
+__global__ void k_pc_apply(const int32_t* __restrict__ bstart, const int32_t* __restrict__ bn,
+                           const int32_t* __restrict__ buid, const int32_t* __restrict__ pids,
+                           const int64_t* __restrict__ uoff, const double* __restrict__ blocks,
+                           const double* __restrict__ r, double* __restrict__ z) {
+    extern __shared__ double rb[];
+    const int b = blockIdx.x;
+    const int n = bn[b], s0 = bstart[b];
+    const double* R = blocks + uoff[buid[b]];
+    for (int j = threadIdx.x; j < n; j += blockDim.x) rb[j] = r[pids[s0 + j]];
+    __syncthreads();
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int i = w; i < n; i += nw) {
+        const double* Ri = R + (int64_t)i * n;
+        double acc = 0.0;
+        for (int j = lane; j < n; j += 32) acc = fma(__ldg(Ri + j), rb[j], acc);
+        for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) z[pids[s0 + i]] = acc;
+    }
+}
+
+struct SigHash {
+    size_t operator()(const std::vector<int32_t>& v) const {
+        uint64_t h = 1469598103934665603ull;
+        for (int32_t x : v) {
+            h ^= (uint32_t)x;
+            h *= 1099511628211ull;
+        }
+        return (size_t)h;
+    }
+};
+
+}  // namespace
+
+void precond_free(vc_ctx* c) {
+    delete c->pc;
+    c->pc = nullptr;
+}
+
+vc_status precond_build(vc_ctx* c, const int32_t box_in[3], int kind) {
+    precond_free(c);
+    Precond* pc = new Precond();
+    c->pc = pc;
+    pc->kind = kind;
+    cudaStream_t st = c->stream;
+    const int64_t N = c->N;
+    const double fpe = 4.0 * kPi * kEps0;
+    const double pscale = c->dv * c->dv * c->dv / fpe;
+    // diagonal part
+    std::vector<double> dinv(N, 0.0);
+    // self term of a unit square (textbook), used only for the diagonal-only option
+    const double pself = pscale * ((4.0 / 3.0) * (1.0 - std::sqrt(2.0)) + 4.0 * std::log(1.0 + std::sqrt(2.0)));
+    for (int64_t p = 0; p < N; ++p) {
+        if (c->h_cid[p] == 0) dinv[p] = kind == 1 ? 1.0 : 1.0 / c->h_ibar[p];
+        else dinv[p] = kind == 1 ? 1.0 : (kind == 2 ? 1.0 / pself : 0.0);
+    }
+    VC_CUDA(c, pc->diag_inv.alloc(N));
+    VC_CUDA(c, cudaMemcpyAsync(pc->diag_inv.p, dinv.data(), 8 * N, cudaMemcpyHostToDevice, st));
+    if (kind != 3) {
+        VC_CUDA(c, cudaStreamSynchronize(st));
+        return VC_OK;
+    }
+    int nv[3], nb[3];
+    const int dims[3] = {c->nx, c->ny, c->nz};
+    for (int a = 0; a < 3; ++a) {
+        nv[a] = box_in[a] > 0 ? box_in[a] : 10;
+        nb[a] = std::max(1, (dims[a] + nv[a] - 1) / nv[a]);
+    }
+    // box of every conductor panel; stable counting sort by box
+    std::vector<int64_t> pbox;
+    std::vector<int32_t> cond;
+    cond.reserve(c->Nc);
+    for (int64_t p = 0; p < N; ++p)
+        if (c->h_cid[p] > 0) cond.push_back((int32_t)p);
+    std::unordered_map<int64_t, int32_t> box_index;
+    std::vector<int64_t> box_keys;
+    std::vector<int32_t> pb(cond.size());
+    for (size_t q = 0; q < cond.size(); ++q) {
+        const int64_t p = cond[q];
+        const int s[3] = {c->h_si[p], c->h_sj[p], c->h_sk[p]};
+        int64_t bx[3];
+        for (int a = 0; a < 3; ++a) bx[a] = std::min<int64_t>(s[a] / nv[a], nb[a] - 1);
+        const int64_t key = (bx[2] * nb[1] + bx[1]) * nb[0] + bx[0];
+        auto it = box_index.find(key);
+        if (it == box_index.end()) {
+            it = box_index.emplace(key, (int32_t)box_keys.size()).first;
+            box_keys.push_back(key);
+        }
+        pb[q] = it->second;
+    }
+    const int nbox = (int)box_keys.size();
+    std::vector<int32_t> bcount(nbox, 0), bstart(nbox + 1, 0);
+    for (int32_t b : pb) bcount[b]++;
+    for (int b = 0; b < nbox; ++b) bstart[b + 1] = bstart[b] + bcount[b];
+    std::vector<int32_t> sorted(cond.size()), fillp(bstart.begin(), bstart.end() - 1);
+    for (size_t q = 0; q < cond.size(); ++q) sorted[fillp[pb[q]]++] = cond[q];
+    // signatures (axis + slot relative to the box origin, canonical order) -> unique blocks
+    std::unordered_map<std::vector<int32_t>, int32_t, SigHash> uniq;
+    std::vector<int32_t> buid(nbox), un, ulist_off, uaxis, uslot;
+    std::vector<int64_t> uoff;
+    int64_t total = 0;
+    int maxn = 0;
+    for (int b = 0; b < nbox; ++b) {
+        const int64_t key = box_keys[b];
+        const int64_t bx = key % nb[0], by = (key / nb[0]) % nb[1], bz = key / ((int64_t)nb[0] * nb[1]);
+        const int org[3] = {(int)(bx * nv[0]), (int)(by * nv[1]), (int)(bz * nv[2])};
+        std::vector<int32_t> sig;
+        sig.reserve(4 * bcount[b]);
+        for (int q = bstart[b]; q < bstart[b + 1]; ++q) {
+            const int p = sorted[q];
+            sig.push_back(c->h_axis[p]);
+            sig.push_back(c->h_si[p] - org[0]);
+            sig.push_back(c->h_sj[p] - org[1]);
+            sig.push_back(c->h_sk[p] - org[2]);
+        }
+        auto it = uniq.find(sig);
+        if (it == uniq.end()) {
+            const int id = (int)un.size();
+            const int n = bcount[b];
+            un.push_back(n);
+            ulist_off.push_back((int32_t)uaxis.size());
+            uoff.push_back(total);
+            total += (int64_t)n * n;
+            maxn = std::max(maxn, n);
+            for (size_t t = 0; t < sig.size(); t += 4) {
+                uaxis.push_back(sig[t]);
+                uslot.push_back(sig[t + 1]);
+                uslot.push_back(sig[t + 2]);
+                uslot.push_back(sig[t + 3]);
+            }
+            it = uniq.emplace(std::move(sig), id).first;
+        }
+        buid[b] = it->second;
+    }
+    if ((size_t)maxn * 2 * sizeof(double) > 200 * 1024)
+        return set_err(c, VC_ERR_UNSUPPORTED, "preconditioner block too large (" + std::to_string(maxn) + " panels in one box); use smaller boxes");
+    pc->nbox = nbox;
+    pc->nuniq = (int)un.size();
+    pc->max_n = maxn;
+    pc->block_doubles = total;
+    VC_CUDA(c, pc->box_start.alloc(std::max(1, nbox)));
+    VC_CUDA(c, pc->box_n.alloc(std::max(1, nbox)));
+    VC_CUDA(c, pc->box_uid.alloc(std::max(1, nbox)));
+    VC_CUDA(c, pc->panel_ids.alloc(std::max<size_t>(1, sorted.size())));
+    VC_CUDA(c, pc->uniq_off.alloc(std::max<size_t>(1, uoff.size())));
+    VC_CUDA(c, pc->uniq_n.alloc(std::max<size_t>(1, un.size())));
+    VC_CUDA(c, pc->uniq_list_off.alloc(std::max<size_t>(1, un.size())));
+    VC_CUDA(c, pc->uniq_axis.alloc(std::max<size_t>(1, uaxis.size())));
+    VC_CUDA(c, pc->uniq_slot.alloc(std::max<size_t>(1, uslot.size())));
+    VC_CUDA(c, pc->blocks.alloc(std::max<int64_t>(1, total)));
+    auto up = [&](void* d, const void* h, size_t bytes) {
+        return bytes ? cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, st) : cudaSuccess;
+    };
+    VC_CUDA(c, up(pc->box_start.p, bstart.data(), 4 * nbox));
+    VC_CUDA(c, up(pc->box_n.p, bcount.data(), 4 * nbox));
+    VC_CUDA(c, up(pc->box_uid.p, buid.data(), 4 * nbox));
+    VC_CUDA(c, up(pc->panel_ids.p, sorted.data(), 4 * sorted.size()));
+    VC_CUDA(c, up(pc->uniq_off.p, uoff.data(), 8 * uoff.size()));
+    VC_CUDA(c, up(pc->uniq_n.p, un.data(), 4 * un.size()));
+    VC_CUDA(c, up(pc->uniq_list_off.p, ulist_off.data(), 4 * ulist_off.size()));
+    VC_CUDA(c, up(pc->uniq_axis.p, uaxis.data(), 4 * uaxis.size()));
+    VC_CUDA(c, up(pc->uniq_slot.p, uslot.data(), 4 * uslot.size()));
+    if (pc->nuniq > 0) {
+        dim3 g(std::max(1, std::min(64, (maxn * maxn + 255) / 256)), pc->nuniq);
+        k_pc_fill<<<g, 256, 0, st>>>(pc->uniq_n.p, pc->uniq_off.p, pc->uniq_list_off.p,
+                                     pc->uniq_axis.p, pc->uniq_slot.p, pc->blocks.p, pscale);
+        const size_t sh = 2 * sizeof(double) * maxn;
+        if (sh > 48 * 1024)
+            VC_CUDA(c, cudaFuncSetAttribute(k_pc_invert, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
+        k_pc_invert<<<pc->nuniq, 512, sh, st>>>(pc->uniq_n.p, pc->uniq_off.p, pc->blocks.p);
+        count_launch(c, 2);
+    }
+    VC_CUDA(c, cudaStreamSynchronize(st));
+    VC_CUDA(c, cudaGetLastError());
+    return VC_OK;
+}
+
+vc_status precond_apply_dev(vc_ctx* c, const double* d_r, double* d_z) {
+    Precond* pc = c->pc;
+    if (!pc) return set_err(c, VC_ERR_STATE, "no preconditioner");
+    cudaStream_t st = c->stream;
+    const int64_t N = c->N;
+    k_pc_diag<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((N + 255) / 256, 148 * 8)), 256, 0, st>>>(N, d_r, pc->diag_inv.p, d_z);
+    count_launch(c);
+    if (pc->kind == 3 && pc->nbox > 0) {
+        const size_t sh = sizeof(double) * pc->max_n;
+        if (sh > 48 * 1024)
+            VC_CUDA(c, cudaFuncSetAttribute(k_pc_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
+        k_pc_apply<<<pc->nbox, 128, sh, st>>>(pc->box_start.p, pc->box_n.p, pc->box_uid.p,
+                                              pc->panel_ids.p, pc->uniq_off.p, pc->blocks.p, d_r, d_z);
+        count_launch(c);
+    }
+    VC_CUDA(c, cudaGetLastError());
+    return VC_OK;
+}
+
+}  // namespace vc

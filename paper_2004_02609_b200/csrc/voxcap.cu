@@ -1,0 +1,338 @@
+// voxcap.cu -- the C ABI of libvoxcap.so (include/voxcap.h).  Argument checking, state
+// machine, host<->device marshalling; every step of the path runs in the kernels of
+// panels.cu / operator.cu / precond.cu / krylov.cu.
+#include <cmath>
+#include <cstring>
+#include <new>
+
+#include "ctx.h"
+
+using namespace vc;
+
+namespace {
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+#define VC_CHECK_CTX(c)                        \
+    do {                                       \
+        if (!(c)) return VC_ERR_INPUT;         \
+        (c)->err.clear();                      \
+    } while (0)
+
+void drop_operator(vc_ctx* c) {
+    c->has_op = false;
+    c->Rt.reset();
+    c->bufA.reset();
+    c->bufB.reset();
+    c->bufC.reset();
+    c->work.reset();
+    c->work_n = 0;
+    precond_free(c);
+}
+
+void drop_geometry(vc_ctx* c) {
+    drop_operator(c);
+    c->has_geom = false;
+    PanelsDev& P = c->pan;
+    P.axis.reset(); P.sign.reset(); P.info.reset();
+    P.si.reset(); P.sj.reset(); P.sk.reset(); P.cid.reset();
+    P.eps_d.reset(); P.eps_b.reset(); P.ibar.reset(); P.fc.reset();
+    for (auto& s : P.slotmap) s.reset();
+    c->N = c->Nc = c->Nd = 0;
+    c->m = 0;
+}
+
+// run f(d_in, d_out) with host or device vectors of length n
+template <class F>
+vc_status with_vectors(vc_ctx* c, const double* in, double* out, int on_device, bool copy_out_in,
+                       F&& f) {
+    if (on_device) return f(in, out);
+    const int64_t n = c->N;
+    DevBuf<double> din, dout;
+    VC_CUDA(c, din.alloc(n));
+    VC_CUDA(c, dout.alloc(n));
+    VC_CUDA(c, cudaMemcpyAsync(din.p, in, 8 * n, cudaMemcpyHostToDevice, c->stream));
+    if (copy_out_in) VC_CUDA(c, cudaMemcpyAsync(dout.p, out, 8 * n, cudaMemcpyHostToDevice, c->stream));
+    vc_status s = f(din.p, dout.p);
+    if (s != VC_OK && s != VC_NOT_CONVERGED) return s;
+    VC_CUDA(c, cudaMemcpyAsync(out, dout.p, 8 * n, cudaMemcpyDeviceToHost, c->stream));
+    VC_CUDA(c, cudaStreamSynchronize(c->stream));
+    return s;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* vc_version(void) { return "voxcap-b200 0.1 (sm_100a)"; }
+
+vc_status vc_create(vc_ctx** out, int cuda_device, void* cuda_stream) {
+    if (!out) return VC_ERR_INPUT;
+    *out = nullptr;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return VC_ERR_CUDA;
+    if (cuda_device < 0 || cuda_device >= ndev) return VC_ERR_INPUT;
+    vc_ctx* c = new (std::nothrow) vc_ctx();
+    if (!c) return VC_ERR_OOM;
+    c->device = cuda_device;
+    DeviceGuard g(cuda_device);
+    if (cuda_stream) {
+        c->stream = (cudaStream_t)cuda_stream;
+    } else {
+        if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
+            delete c;
+            return VC_ERR_CUDA;
+        }
+        c->own_stream = true;
+    }
+    memset(&c->stats, 0, sizeof(c->stats));
+    *out = c;
+    return VC_OK;
+}
+
+void vc_destroy(vc_ctx* c) {
+    if (!c) return;
+    {
+        DeviceGuard g(c->device);
+        cudaStreamSynchronize(c->stream);
+        drop_geometry(c);
+        c->tw.reset();
+        c->partial.reset();
+        c->dvec.reset();
+        if (c->h_pinned) cudaFreeHost(c->h_pinned);
+        if (c->timing.ev_ok)
+            for (auto& e : c->timing.ev) cudaEventDestroy(e);
+        if (c->own_stream) cudaStreamDestroy(c->stream);
+    }
+    delete c;
+}
+
+const char* vc_last_error(const vc_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+vc_status vc_set_geometry(vc_ctx* c, int32_t nx, int32_t ny, int32_t nz, double dv_m,
+                          const int32_t* label, const double* eps_r, double eps_r_outside,
+                          int32_t on_device) {
+    VC_CHECK_CTX(c);
+    DeviceGuard g(c->device);
+    drop_geometry(c);
+    if (nx <= 0 || ny <= 0 || nz <= 0) return set_err(c, VC_ERR_INPUT, "dims must be > 0");
+    if (!(dv_m > 0) || !std::isfinite(dv_m)) return set_err(c, VC_ERR_INPUT, "dv must be finite and > 0");
+    if (!(eps_r_outside > 0) || !std::isfinite(eps_r_outside)) return set_err(c, VC_ERR_INPUT, "eps_r_outside must be finite and > 0");
+    if (!label) return set_err(c, VC_ERR_INPUT, "label is NULL");
+    if ((int64_t)nx + 1 > 65536 || (int64_t)ny + 1 > 65536 || (int64_t)nz + 1 > 65536)
+        return set_err(c, VC_ERR_UNSUPPORTED, "grid too large");
+    c->nx = nx;
+    c->ny = ny;
+    c->nz = nz;
+    c->dv = dv_m;
+    c->eps_out = eps_r_outside;
+    const int64_t nvox = (int64_t)nx * ny * nz;
+    DevBuf<int32_t> dl;
+    DevBuf<double> de;
+    const int32_t* pl = label;
+    const double* pe = eps_r;
+    if (!on_device) {
+        VC_CUDA(c, dl.alloc(nvox));
+        VC_CUDA(c, cudaMemcpyAsync(dl.p, label, 4 * nvox, cudaMemcpyHostToDevice, c->stream));
+        pl = dl.p;
+        if (eps_r) {
+            VC_CUDA(c, de.alloc(nvox));
+            VC_CUDA(c, cudaMemcpyAsync(de.p, eps_r, 8 * nvox, cudaMemcpyHostToDevice, c->stream));
+            pe = de.p;
+        }
+    }
+    vc_status s = geometry_build(c, pl, pe);
+    if (s != VC_OK) {
+        std::string msg = c->err;
+        drop_geometry(c);
+        c->err = msg;
+        return s;
+    }
+    c->has_geom = true;
+    return VC_OK;
+}
+
+vc_status vc_get_sizes(const vc_ctx* c, int64_t* n_panels, int64_t* n_cond, int64_t* n_diel,
+                       int32_t* m_conductors) {
+    if (!c) return VC_ERR_INPUT;
+    if (!c->has_geom) return VC_ERR_STATE;
+    if (n_panels) *n_panels = c->N;
+    if (n_cond) *n_cond = c->Nc;
+    if (n_diel) *n_diel = c->Nd;
+    if (m_conductors) *m_conductors = c->m;
+    return VC_OK;
+}
+
+vc_status vc_get_panels(const vc_ctx* cc, int8_t* axis, int32_t* slot, int8_t* sign,
+                        int32_t* cid, double* eps_d, double* eps_b) {
+    vc_ctx* c = const_cast<vc_ctx*>(cc);
+    VC_CHECK_CTX(c);
+    if (!c->has_geom) return set_err(c, VC_ERR_STATE, "no geometry");
+    DeviceGuard g(c->device);
+    const int64_t n = c->N;
+    cudaStream_t st = c->stream;
+    if (axis) VC_CUDA(c, cudaMemcpyAsync(axis, c->pan.axis.p, n, cudaMemcpyDeviceToHost, st));
+    if (sign) VC_CUDA(c, cudaMemcpyAsync(sign, c->pan.sign.p, n, cudaMemcpyDeviceToHost, st));
+    if (cid) VC_CUDA(c, cudaMemcpyAsync(cid, c->pan.cid.p, 4 * n, cudaMemcpyDeviceToHost, st));
+    if (eps_d) VC_CUDA(c, cudaMemcpyAsync(eps_d, c->pan.eps_d.p, 8 * n, cudaMemcpyDeviceToHost, st));
+    if (eps_b) VC_CUDA(c, cudaMemcpyAsync(eps_b, c->pan.eps_b.p, 8 * n, cudaMemcpyDeviceToHost, st));
+    VC_CUDA(c, cudaStreamSynchronize(st));
+    if (slot)
+        for (int64_t p = 0; p < n; ++p) {
+            slot[3 * p] = c->h_si[p];
+            slot[3 * p + 1] = c->h_sj[p];
+            slot[3 * p + 2] = c->h_sk[p];
+        }
+    return VC_OK;
+}
+
+vc_status vc_build_operator(vc_ctx* c, const vc_build_opts* o) {
+    VC_CHECK_CTX(c);
+    if (!c->has_geom) return set_err(c, VC_ERR_STATE, "vc_build_operator before vc_set_geometry");
+    DeviceGuard g(c->device);
+    drop_operator(c);
+    int kind = (o && o->precond) ? o->precond : 3;
+    if (kind < 1 || kind > 3) return set_err(c, VC_ERR_INPUT, "precond must be 0..3");
+    int box[3] = {10, 10, 10};
+    if (o)
+        for (int a = 0; a < 3; ++a) {
+            if (o->box[a] < 0) return set_err(c, VC_ERR_INPUT, "box must be >= 0");
+            if (o->box[a] > 0) box[a] = o->box[a];
+        }
+    cudaEvent_t e0, e1, e2;
+    VC_CUDA(c, cudaEventCreate(&e0));
+    VC_CUDA(c, cudaEventCreate(&e1));
+    VC_CUDA(c, cudaEventCreate(&e2));
+    VC_CUDA(c, cudaEventRecord(e0, c->stream));
+    vc_status s = operator_build(c, o);
+    if (s == VC_OK) {
+        VC_CUDA(c, cudaEventRecord(e1, c->stream));
+        s = precond_build(c, box, kind);
+        VC_CUDA(c, cudaEventRecord(e2, c->stream));
+    }
+    if (s == VC_OK) {
+        VC_CUDA(c, cudaEventSynchronize(e2));
+        float a = 0, b = 0;
+        cudaEventElapsedTime(&a, e0, e1);
+        cudaEventElapsedTime(&b, e1, e2);
+        c->stats.ms_setup = a + b;
+        c->stats.ms_precond_build = b;
+        c->precond_kind = kind;
+        c->has_op = true;
+    } else {
+        std::string msg = c->err;
+        drop_operator(c);
+        c->err = msg;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaEventDestroy(e2);
+    return s;
+}
+
+vc_status vc_get_grid(const vc_ctx* c, int32_t* m3) {
+    if (!c || !m3) return VC_ERR_INPUT;
+    if (!c->has_op) return VC_ERR_STATE;
+    for (int a = 0; a < 3; ++a) m3[a] = c->M[a];
+    return VC_OK;
+}
+
+vc_status vc_matvec(vc_ctx* c, const double* x, double* y, int32_t on_device) {
+    VC_CHECK_CTX(c);
+    if (!c->has_op) return set_err(c, VC_ERR_STATE, "vc_matvec before vc_build_operator");
+    if (!x || !y) return set_err(c, VC_ERR_INPUT, "null vector");
+    DeviceGuard g(c->device);
+    return with_vectors(c, x, y, on_device, false,
+                        [&](const double* dx, double* dy) { return matvec_dev(c, dx, dy); });
+}
+
+vc_status vc_precond(vc_ctx* c, const double* r, double* z, int32_t on_device) {
+    VC_CHECK_CTX(c);
+    if (!c->has_op) return set_err(c, VC_ERR_STATE, "vc_precond before vc_build_operator");
+    if (!r || !z) return set_err(c, VC_ERR_INPUT, "null vector");
+    DeviceGuard g(c->device);
+    return with_vectors(c, r, z, on_device, false,
+                        [&](const double* dr, double* dz) { return precond_apply_dev(c, dr, dz); });
+}
+
+vc_status vc_solve(vc_ctx* c, const double* b, double* x, const vc_solve_opts* o,
+                   vc_solve_info* info, int32_t on_device) {
+    VC_CHECK_CTX(c);
+    if (!c->has_op) return set_err(c, VC_ERR_STATE, "vc_solve before vc_build_operator");
+    if (!b || !x) return set_err(c, VC_ERR_INPUT, "null vector");
+    if (o && (o->tol < 0 || o->restart < 0 || o->maxit < 0)) return set_err(c, VC_ERR_INPUT, "negative solve option");
+    DeviceGuard g(c->device);
+    const bool guess = o && o->x0_is_guess;
+    return with_vectors(c, b, x, on_device, guess, [&](const double* db, double* dx) {
+        return solve_dev(c, db, dx, o, info);
+    });
+}
+
+vc_status vc_solve_capacitance(vc_ctx* c, double* C, const vc_solve_opts* o,
+                               vc_solve_info* per_column) {
+    VC_CHECK_CTX(c);
+    if (!c->has_op) return set_err(c, VC_ERR_STATE, "vc_solve_capacitance before vc_build_operator");
+    if (!C) return set_err(c, VC_ERR_INPUT, "C is NULL");
+    if (o && (o->tol < 0 || o->restart < 0 || o->maxit < 0)) return set_err(c, VC_ERR_INPUT, "negative solve option");
+    DeviceGuard g(c->device);
+    return capacitance_dev(c, C, o, per_column);
+}
+
+vc_status vc_set_timing(vc_ctx* c, int32_t detail) {
+    VC_CHECK_CTX(c);
+    DeviceGuard g(c->device);
+    if (!c->timing.ev_ok) {
+        for (auto& e : c->timing.ev) VC_CUDA(c, cudaEventCreate(&e));
+        c->timing.ev_ok = true;
+    }
+    c->timing.detail = detail != 0;
+    return VC_OK;
+}
+
+vc_status vc_get_stats(const vc_ctx* c, vc_stats* out) {
+    if (!c || !out) return VC_ERR_INPUT;
+    *out = c->stats;
+    return VC_OK;
+}
+
+vc_status vc_reset_stats(vc_ctx* c) {
+    VC_CHECK_CTX(c);
+    const double bp[5] = {c->stats.bytes_pass[0], c->stats.bytes_pass[1], c->stats.bytes_pass[2],
+                          c->stats.bytes_pass[3], c->stats.bytes_pass[4]};
+    const double bm = c->stats.bytes_matvec, ms = c->stats.ms_setup, mp = c->stats.ms_precond_build;
+    memset(&c->stats, 0, sizeof(c->stats));
+    for (int p = 0; p < 5; ++p) c->stats.bytes_pass[p] = bp[p];
+    c->stats.bytes_matvec = bm;
+    c->stats.ms_setup = ms;
+    c->stats.ms_precond_build = mp;
+    return VC_OK;
+}
+
+vc_status vc_debug_kernel_entries(vc_ctx* c, int32_t n, const int32_t* kind, const int32_t* alpha,
+                                  const int32_t* beta, const int32_t* d, double* out) {
+    VC_CHECK_CTX(c);
+    if (n < 0 || (n > 0 && (!kind || !alpha || !beta || !d || !out))) return set_err(c, VC_ERR_INPUT, "bad arguments");
+    if (n == 0) return VC_OK;
+    DeviceGuard g(c->device);
+    return debug_kernel_entries(c, n, kind, alpha, beta, d, out);
+}
+
+vc_status vc_debug_fft(vc_ctx* c, int32_t L, int32_t n_lines, double* data, int32_t dir) {
+    VC_CHECK_CTX(c);
+    if (n_lines <= 0 || !data || (dir != 1 && dir != -1)) return set_err(c, VC_ERR_INPUT, "bad arguments");
+    DeviceGuard g(c->device);
+    return debug_fft(c, L, n_lines, data, dir);
+}
+
+}  // extern "C"

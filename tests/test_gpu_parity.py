@@ -1,0 +1,208 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on seeded inputs.
+
+Tolerances: panel indexing bit-exact; kernel entries <= 1e-12 relative;
+matvec relative L2 <= 1e-10 (BASELINE north_star); capacitance entries <= 1e-6 relative.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+import voxgen
+
+pytestmark = pytest.mark.gpu
+
+try:
+    import paper_2004_02609_b200 as vc
+except Exception:  # pragma: no cover
+    vc = None
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    c = vc.VoxCap(0)
+    yield c
+    c.close()
+
+
+def _setup(ctx, st, **kw):
+    ctx.set_structure(st)
+    ctx.build_operator(**kw)
+    return O.enumerate_panels(st.label, st.eps, st.eps_out, st.dv)
+
+
+# ------------------------------------------------------------------------------ building blocks
+@pytest.mark.parametrize("L", [8, 16, 32, 64, 128, 256, 512, 1024, 2048, 4096])
+def test_fft_vs_numpy(ctx, L):
+    rng = np.random.default_rng(L)
+    a = rng.standard_normal((5, L)) + 1j * rng.standard_normal((5, L))
+    f = ctx.fft(a)
+    ref = np.fft.fft(a, axis=-1)
+    assert np.abs(f - ref).max() <= 1e-14 * np.abs(ref).max() * np.log2(L)
+    b = ctx.fft(a, inverse=True)
+    refb = np.fft.ifft(a, axis=-1) * L
+    assert np.abs(b - refb).max() <= 1e-14 * np.abs(refb).max() * np.log2(L)
+
+
+def _offsets():
+    rng = np.random.default_rng(11)
+    near = np.array(np.meshgrid(*[np.arange(-5, 6)] * 3, indexing="ij")).reshape(3, -1).T
+    far = rng.integers(-300, 301, (600, 3))
+    mid = rng.integers(-25, 26, (600, 3))
+    return np.concatenate([near, mid, far])
+
+
+@pytest.mark.parametrize("kind", [0, 1])
+def test_kernel_entries_vs_oracle(ctx, kind):
+    D = _offsets()
+    worst = 0.0
+    for a in range(3):
+        for b in range(3):
+            g = ctx.kernel_entries(kind, a, b, D)
+            r = O.kappa_batch(kind, a, b, D)
+            cen = D + 0.5 * ((np.arange(3) != a).astype(float) - (np.arange(3) != b).astype(float))
+            dist = np.maximum(np.linalg.norm(cen, axis=1), 1.0)
+            scale = 1.0 / dist if kind == 0 else 1.0 / dist ** 2  # magnitude of the kernel
+            err = np.abs(g - r) / scale
+            worst = max(worst, err.max())
+            assert err.max() < 2e-12, (a, b, D[err.argmax()], g[err.argmax()], r[err.argmax()])
+    print("worst scaled entry error", worst)
+
+
+# ------------------------------------------------------------------------------ a1 indexing
+@pytest.mark.parametrize("name", ["C1", "C2", "R1", "R2", "R3", "R4", "R5", "sphere16", "C4"])
+def test_panels_bit_exact(ctx, name):
+    st = voxgen.sphere(16) if name == "sphere16" else voxgen.config(name)
+    ctx.set_structure(st)
+    p = O.enumerate_panels(st.label, st.eps, st.eps_out, st.dv)
+    g = ctx.panels()
+    assert ctx.n == p.n and ctx.n_cond == p.n_cond and ctx.m == p.m
+    assert np.array_equal(g["axis"], p.axis)
+    assert np.array_equal(g["slot"], p.slot)
+    assert np.array_equal(g["sign"], p.sign)
+    assert np.array_equal(g["cid"], p.cid)
+    assert np.array_equal(g["eps_d"], p.eps_d)
+    assert np.array_equal(g["eps_b"], p.eps_b)
+
+
+@pytest.mark.parametrize("case", ["neg", "gap_ids", "empty", "clash", "eps0"])
+def test_geometry_errors(ctx, case):
+    lab = np.zeros((3, 3, 3), np.int32)
+    eps = np.ones((3, 3, 3))
+    if case == "neg":
+        lab[0, 0, 0] = -1
+    elif case == "gap_ids":
+        lab[0, 0, 0] = 2
+    elif case == "clash":
+        lab[0, 0, 0] = 1
+        lab[0, 0, 1] = 2
+    elif case == "eps0":
+        lab[1, 1, 1] = 1
+        eps[0, 0, 0] = 0.0
+    with pytest.raises(vc.VoxCapError) as e:
+        ctx.set_geometry(lab, eps)
+    assert e.value.code == "VC_ERR_INPUT"
+    with pytest.raises(vc.VoxCapError) as e:
+        ctx.matvec(np.zeros(4))
+    assert e.value.code == "VC_ERR_STATE"
+
+
+# ------------------------------------------------------------------------------ a2-a8 matvec
+def _rel(a, b):
+    return np.linalg.norm(a - b) / np.linalg.norm(b)
+
+
+@pytest.mark.parametrize("name", ["R1", "R2", "R3", "R4", "R5", "C1", "C2"])
+def test_matvec_dense_parity(ctx, name):
+    st = voxgen.config(name)
+    p = _setup(ctx, st)
+    A = O.assemble(p)
+    for seed in range(2):
+        x = voxgen.seeded_vector(p.n, seed)
+        y = ctx.matvec(x)
+        assert _rel(y, A @ x) <= 1e-10, (name, ctx.grid(), _rel(y, A @ x))
+
+
+def test_matvec_padding_invariance(ctx):
+    st = voxgen.config("R2")
+    _setup(ctx, st)
+    x = voxgen.seeded_vector(ctx.n, 3)
+    y0 = ctx.matvec(x)
+    M = ctx.grid()
+    ctx.build_operator(pad=[2 * v for v in M])
+    y1 = ctx.matvec(x)
+    assert _rel(y1, y0) < 1e-13
+
+
+def test_matvec_device_tensors(ctx):
+    import torch
+    st = voxgen.config("R5")
+    _setup(ctx, st)
+    x = voxgen.seeded_vector(ctx.n, 4)
+    y_host = ctx.matvec(x)
+    y_dev = ctx.matvec(torch.from_numpy(x).cuda()).cpu().numpy()
+    assert np.array_equal(y_host, y_dev)
+
+
+@pytest.mark.parametrize("name,nrows", [("C3", 6), ("C4", 4)])
+def test_matvec_row_sampled_full_size(ctx, name, nrows):
+    """BASELINE full sizes, the launch configuration bench.py times: sampled rows vs oracle."""
+    st = voxgen.config(name)
+    ctx.set_structure(st)
+    ctx.build_operator()
+    p = O.enumerate_panels(st.label, st.eps, st.eps_out, st.dv)
+    x = voxgen.seeded_vector(p.n, 0)
+    y = ctx.matvec(x)
+    rng = np.random.default_rng(5)
+    rows = rng.choice(p.n, nrows, replace=False)
+    if p.n_diel:
+        rows[-1] = rng.choice(np.nonzero(~p.is_cond)[0])
+        rows[0] = rng.choice(np.nonzero(p.is_cond)[0])
+    ref = O.matvec_rows(p, x, rows)
+    scale = np.sqrt(np.mean(y ** 2))
+    err = np.abs(y[rows] - ref) / scale
+    assert err.max() <= 1e-10, (rows, y[rows], ref)
+
+
+# ------------------------------------------------------------------------------ a9/a10 precond
+@pytest.mark.parametrize("name,box", [("R1", (3, 3, 3)), ("R5", (4, 4, 4)), ("C1", (10, 10, 10)),
+                                      ("C1", (3, 3, 3)), ("R2", (2, 5, 3))])
+def test_precond_parity(ctx, name, box):
+    st = voxgen.config(name)
+    p = _setup(ctx, st, box=box)
+    r = voxgen.seeded_vector(p.n, 7)
+    z = ctx.precond(r)
+    ref = O.precond_apply(p, r, nv=box)
+    assert _rel(z, ref) <= 1e-12
+
+
+# ------------------------------------------------------------------------------ a11/a12 solve
+@pytest.mark.parametrize("name", ["C1", "R1", "R2", "R3", "R4", "R5"])
+def test_capacitance_parity(ctx, name):
+    st = voxgen.config(name)
+    p = _setup(ctx, st)
+    C, info = ctx.solve_capacitance(tol=1e-12, maxit=3000)
+    Cref = O.solve_capacitance(p)
+    assert all(i["converged"] for i in info)
+    err = np.abs(C - Cref).max() / np.abs(Cref).max()
+    assert err <= 1e-6, (C, Cref)
+
+
+def test_capacitance_c2(ctx):
+    st = voxgen.config("C2")
+    p = _setup(ctx, st)
+    C, info = ctx.solve_capacitance(tol=1e-12, maxit=5000)
+    Cref = O.solve_capacitance(p)
+    assert np.abs(C - Cref).max() <= 1e-6 * np.abs(Cref).max(), (C, Cref)
+
+
+@pytest.mark.parametrize("precond", [1, 2, 3])
+def test_solve_matches_direct(ctx, precond):
+    st = voxgen.config("R5")
+    p = _setup(ctx, st, precond=precond, box=(4, 4, 4))
+    A = O.assemble(p)
+    b = voxgen.seeded_vector(p.n, 9)
+    x, info = ctx.solve(b, tol=1e-12, maxit=2000)
+    assert info["converged"]
+    xref = np.linalg.solve(A, b)
+    assert _rel(x, xref) < 1e-9
+    assert info["rre_true"] < 1e-10

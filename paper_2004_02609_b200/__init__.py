@@ -139,11 +139,15 @@ class VoxCap:
     def __init__(self, device=0, stream=None):
         self._lib = load_library()
         self._ctx = ctypes.c_void_p()
+        self._tstream = None
         if stream is None:
             try:
                 import torch
                 if torch.cuda.is_available():
-                    stream = torch.cuda.current_stream(device).cuda_stream
+                    # the context's own stream, known to torch so device-tensor calls can be
+                    # fenced against torch's current stream (see _fence_in / _fence_out)
+                    self._tstream = torch.cuda.Stream(device)
+                    stream = self._tstream.cuda_stream
             except ImportError:
                 stream = None
         st = self._lib.vc_create(ctypes.byref(self._ctx), int(device),
@@ -189,6 +193,7 @@ class VoxCap:
             lab = label.contiguous()
             ep = None if eps is None else eps.contiguous()
             assert str(lab.dtype) == "torch.int32"
+            self._fence_in(*[t for t in (lab, ep) if t is not None])
         else:
             lab = np.ascontiguousarray(label, dtype=np.int32)
             ep = None if eps is None else np.ascontiguousarray(eps, dtype=np.float64)
@@ -235,12 +240,28 @@ class VoxCap:
         self._check(self._lib.vc_get_grid(self._ctx, m3))
         return tuple(m3)
 
+    def _fence_in(self, *tensors):
+        """Order the context stream after torch's current stream (inputs are ready)."""
+        if self._tstream is not None:
+            import torch
+            self._tstream.wait_stream(torch.cuda.current_stream(self.device))
+            for t in tensors:
+                t.record_stream(self._tstream)
+
+    def _fence_out(self):
+        """Order torch's current stream after the context stream (outputs are ready)."""
+        if self._tstream is not None:
+            import torch
+            torch.cuda.current_stream(self.device).wait_stream(self._tstream)
+
     def _vec_call(self, fn, x, out=None):
         if _is_cuda_tensor(x):
             import torch
             x = x.contiguous()
             y = torch.empty_like(x) if out is None else out
+            self._fence_in(x, y)
             self._check(fn(self._ctx, _ptr(x), _ptr(y), 1))
+            self._fence_out()
             return y
         x = np.ascontiguousarray(x, dtype=np.float64)
         y = np.empty_like(x) if out is None else out
@@ -269,9 +290,12 @@ class VoxCap:
         on_dev = _is_cuda_tensor(b)
         if on_dev:
             import torch
+            b = b.contiguous()
             x = torch.zeros_like(b) if x0 is None else x0.clone()
-            st = self._lib.vc_solve(self._ctx, _ptr(b.contiguous()), _ptr(x), ctypes.byref(o),
+            self._fence_in(b, x)
+            st = self._lib.vc_solve(self._ctx, _ptr(b), _ptr(x), ctypes.byref(o),
                                     ctypes.byref(info), 1)
+            self._fence_out()
         else:
             b = np.ascontiguousarray(b, dtype=np.float64)
             x = np.zeros_like(b) if x0 is None else np.array(x0, dtype=np.float64)

@@ -83,12 +83,12 @@ __global__ void k_scale_by_norm(double* __restrict__ dst, const double* __restri
         dst[k] = src[k] * s;
 }
 
-// y = a*x + b*y
+// y = a*x + b*y  (y is not read when b == 0: it may hold stale non-finite data)
 __global__ void k_axpby(double* __restrict__ y, const double* __restrict__ x, double a, double b,
                         int64_t n) {
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
          k += (int64_t)gridDim.x * blockDim.x)
-        y[k] = fma(a, x[k], b * y[k]);
+        y[k] = b == 0.0 ? a * x[k] : fma(a, x[k], b * y[k]);
 }
 
 // b_k = dv^2 on the panels of conductor j (V_k = A_k Phi_k)

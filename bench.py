@@ -295,7 +295,12 @@ def main():
             "matvec_bytes": stats["bytes_matvec"],
             "gmres_iters_per_column": iters,
             "setup_ms": stats["ms_setup"],
+            "setup_breakdown_ms": {"geometry": stats["ms_geometry"], "kgen": stats["ms_kgen"],
+                                   "kernel_fft": stats["ms_kfft"],
+                                   "precond_build": stats["ms_precond_build"]},
             "pass_ms_mean": [msp[i] / max(1, stats["n_pass"][i]) for i in range(5)],
+            "pass_gbs": [stats["bytes_pass"][i] / (msp[i] / max(1, stats["n_pass"][i]) * 1e-3) / 1e9
+                         if msp[i] > 0 else None for i in range(5)],
             "roofline": {"bound": "hbm", "kernel": f"P{dom + 1}", "achieved": achieved,
                          "peak": pk["hbm_gbs"], "peak_kind": pk_kind, "unit": "GB/s",
                          "frac": achieved / pk["hbm_gbs"], "traffic": traffic,

@@ -95,7 +95,10 @@ typedef struct {
     double  ms_setup;       /* device time of the last build_operator                        */
     double  ms_precond_build;
     int64_t gpu_launches;   /* kernels launched by the library since the last reset          */
-    int64_t reserved[8];
+    double  ms_kgen;        /* last build: kernel-entry generation (octant + fill)           */
+    double  ms_kfft;        /* last build: 3-D FFT of the kernels + phase strip / fold        */
+    double  ms_geometry;    /* last vc_set_geometry (panel indexing), device time            */
+    int64_t reserved[5];
 } vc_stats;
 
 /* Create a context on CUDA device `cuda_device`.  `cuda_stream` is a cudaStream_t to order

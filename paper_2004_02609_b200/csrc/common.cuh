@@ -45,4 +45,13 @@ __device__ __forceinline__ double2 half_phase(const double2* __restrict__ tw, in
     return (kt != 0 && pos) ? cconj(w) : w;
 }
 
+// 8-byte global -> shared asynchronous copy (LDGSTS) and completion wait
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
+
 }  // namespace vc

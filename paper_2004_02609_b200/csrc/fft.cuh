@@ -50,6 +50,12 @@ struct Plan {
     }
 };
 
+__host__ __device__ constexpr int hipow2(int m) {
+    int h = 1;
+    while (h * 2 <= m) h *= 2;
+    return h;
+}
+
 template <int R>
 __device__ __forceinline__ constexpr int bitrev(int i) {
     int r = 0;
@@ -132,12 +138,24 @@ __device__ __forceinline__ void fft_stage(LD&& ld, ST&& st, const double2* __res
 #pragma unroll
         for (int j = 0; j < R; ++j) v[j] = ld(t, base + j * S);
         reg_dft<R, INV>(v);
+        if (S > 1) {
+            // inter-stage twiddles w_Lc^{b m}: one table load, powers by squaring/products
+            double2 wp[R];
+            wp[0] = make_double2(1.0, 0.0);
+            wp[1] = twiddle<INV>(tw, b * TW);
 #pragma unroll
-        for (int i = 0; i < R; ++i) {
-            const int m = bitrev<R>(i);
-            double2 x = v[i];
-            if (S > 1 && m != 0) x = cmul(x, twiddle<INV>(tw, b * m * TW));
-            st(t, base + m * S, x);
+            for (int m = 2; m < R; ++m) {
+                const int hb = hipow2(m);  // highest power of two <= m
+                wp[m] = (m == hb) ? cmul(wp[m / 2], wp[m / 2]) : cmul(wp[hb], wp[m - hb]);
+            }
+#pragma unroll
+            for (int i = 0; i < R; ++i) {
+                const int m = bitrev<R>(i);
+                st(t, base + m * S, m == 0 ? v[i] : cmul(v[i], wp[m]));
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < R; ++i) st(t, base + bitrev<R>(i) * S, v[i]);
         }
     }
 }

@@ -13,7 +13,7 @@
 //                a b ln(a+r) + (a^2-c^2)/2 ln(b+r) - a c atan(ab/(c r)) - b r/2
 //   exact zeros on touching orthogonal pairs take the one-sided limit (reading O5): a -> +eta,
 //   b -> sign(sibling b) eta, c -> sign(sibling c) eta.
-// Far pairs: tensor Gauss-Legendre over both panels, q per axis from the distance band
+// Far pairs: Gauss-Legendre (triangle rule on shared axes), q per axis from the distance band
 //   (reading O6): P q = 6 (d < 5), 5 (< 15), 4 (< 50), 3; E q = 7 (< 5), 6 (< 10),
 //   5 (< 20), 4.
 // These formulas are written independently of the CPU oracle (which follows Eqs. 15/16
@@ -147,37 +147,64 @@ static __device__ double kappa_orth_cf(int kind, int Dg, int Db, int Da) {
     return s;
 }
 
-// ---- far field: tensor Gauss-Legendre over both panels ------------------------------------
+// ---- far field: Gauss-Legendre with the triangle rule on shared axes --------------------
+// Along an axis both unit panels span, the double integral over [x0,x0+1] x [0,1] of g(x - x')
+// equals \int_{-1}^{1} (1 - |s|) g(D + s) ds; split at the kink, each half gets q GL points with
+// weights w (1 - x).  Parallel pairs share both in-plane axes ((2q)^2 points instead of q^4);
+// orthogonal pairs share the third axis and keep one GL axis on each panel (2q^3 points).
 template <int A, int B, int Q, int KIND>
 __device__ double kappa_gl(double d0x, double d0y, double d0z) {
-    constexpr int U1 = A == 0 ? 1 : 0, V1 = A == 2 ? 1 : 2;  // observer in-plane axes
-    constexpr int U2 = B == 0 ? 1 : 0, V2 = B == 2 ? 1 : 2;  // source in-plane axes
-    const double* X = kGLx[Q - 3];
+    const double* X = kGLx[Q - 3];  // offsets from 1/2 of the [0,1] nodes
     const double* W = kGLw[Q - 3];
     double acc = 0.0;
+    if constexpr (A == B) {
+        constexpr int U = A == 0 ? 1 : 0, V = A == 2 ? 1 : 2;
 #pragma unroll 1
-    for (int i = 0; i < Q; ++i)
-#pragma unroll 1
-        for (int j = 0; j < Q; ++j) {
+        for (int i = 0; i < 2 * Q; ++i) {
+            const int ki = i % Q;
+            const double xi = (i < Q ? 1.0 : -1.0) * (0.5 + X[ki]);
+            const double wi = W[ki] * (0.5 - X[ki]);
             double e[3] = {d0x, d0y, d0z};
-            e[U1] += X[i];
-            e[V1] += X[j];
-            const double wij = W[i] * W[j];
-            double accij = 0.0;
+            e[U] += xi;
+            double accj = 0.0;
 #pragma unroll
-            for (int k = 0; k < Q; ++k)
+            for (int j = 0; j < 2 * Q; ++j) {
+                const int kj = j % Q;
+                double f[3] = {e[0], e[1], e[2]};
+                f[V] += (j < Q ? 1.0 : -1.0) * (0.5 + X[kj]);
+                const double r2 = f[0] * f[0] + f[1] * f[1] + f[2] * f[2];
+                const double ri = rsqrt(r2);
+                const double v = KIND == 0 ? ri : -f[A] * ri * ri * ri;
+                accj = fma(W[kj] * (0.5 - X[kj]), v, accj);
+            }
+            acc = fma(wi, accj, acc);
+        }
+    } else {
+        constexpr int G = 3 - A - B;
+#pragma unroll 1
+        for (int i = 0; i < 2 * Q; ++i) {
+            const int ki = i % Q;
+            const double wi = W[ki] * (0.5 - X[ki]);
+            double e[3] = {d0x, d0y, d0z};
+            e[G] += (i < Q ? 1.0 : -1.0) * (0.5 + X[ki]);
+#pragma unroll 1
+            for (int j = 0; j < Q; ++j) {
+                double f0[3] = {e[0], e[1], e[2]};
+                f0[B] += X[j];  // observer extent along beta
+                double acck = 0.0;
 #pragma unroll
-                for (int l = 0; l < Q; ++l) {
-                    double f[3] = {e[0], e[1], e[2]};
-                    f[U2] -= X[k];
-                    f[V2] -= X[l];
+                for (int k = 0; k < Q; ++k) {
+                    double f[3] = {f0[0], f0[1], f0[2]};
+                    f[A] -= X[k];  // source extent along alpha
                     const double r2 = f[0] * f[0] + f[1] * f[1] + f[2] * f[2];
                     const double ri = rsqrt(r2);
                     const double v = KIND == 0 ? ri : -f[A] * ri * ri * ri;
-                    accij = fma(W[k] * W[l], v, accij);
+                    acck = fma(W[k], v, acck);
                 }
-            acc = fma(wij, accij, acc);
+                acc = fma(wi * W[j], acck, acc);
+            }
         }
+    }
     return acc;
 }
 

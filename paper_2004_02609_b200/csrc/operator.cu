@@ -41,6 +41,7 @@ struct MV {
     const double* Rt;
     size_t blk_stride;
     int blk[6][3];
+    int nblk;
     const double2* tw;
 };
 
@@ -48,8 +49,9 @@ struct MV {
 constexpr int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
 template <int L> struct TX { static constexpr int T = clampi(4096 / L, 1, 64); };   // x passes
 template <int L> struct TY { static constexpr int T = clampi(4096 / L, 1, 32); };   // y passes
-template <int L> struct TZ { static constexpr int T = clampi(1024 / L, 1, 32); };   // z + MAC
+template <int L> struct TZ { static constexpr int T = clampi(256 / L, 2, 16); };    // z + MAC
 constexpr int kNT = 256;
+constexpr int kNT3 = 128;  // P3 threads per CTA
 
 __device__ __forceinline__ int ktil(int k, int M) { return k <= M / 2 ? k : k - M; }
 
@@ -142,20 +144,39 @@ __global__ void __launch_bounds__(kNT) k_p2(MV mv) {
 
 // ---------------------------------------------------------------------------------------
 // P3: forward z FFT of the three source fields, orientation-block MAC (Eqs. 10-12), inverse z
+//   One CTA = T adjacent kx x the ky pair {q, My - q} (the two share every folded spectrum
+//   row, so each R element is read from HBM once).  The CTA's R tile (all blocks, kz' in
+//   [0, Mz/2], T kx) and the z half-shift phases are staged in shared memory with cp.async
+//   while the forward FFT's first stage streams X2 in.
 // ---------------------------------------------------------------------------------------
 template <int L>
-__global__ void __launch_bounds__(kNT) k_p3(MV mv) {
+__global__ void __launch_bounds__(kNT3) k_p3(MV mv) {
     constexpr int T = TZ<L>::T;
     constexpr int TI = 6 * T, TO = 2 * T;
     constexpr int KZ = L / 2 + 1;
     extern __shared__ double2 sm[];
-    double2* smin = sm;
-    double2* smout = sm + L * TI;
+    double2* smin = sm;              // [L][TI]
+    double2* smout = smin + L * TI;  // [L][TO]
+    double2* ph = smout + L * TO;    // [L] exp(-i pi kt / L)
+    double* rs = reinterpret_cast<double*>(ph + L);  // [nblk][KZ][T]
     const int Kx = mv.Kx, My = mv.My;
     const int ntile = (Kx + T - 1) / T;
     const int q = blockIdx.x / ntile, tile = blockIdx.x % ntile;
     const int nside = (q == 0 || 2 * q == My) ? 1 : 2;
     const int ky[2] = {q, My - q};
+    // stage the R tile (async) and the phase table
+    {
+        const int nr = mv.nblk * KZ * T;
+        for (int e = threadIdx.x; e < nr; e += kNT3) {
+            const int t = e % T, kzp = (e / T) % KZ, b = e / (T * KZ);
+            const int kx = tile * T + t;
+            if (kx < Kx)
+                cp_async8(rs + e, mv.Rt + (size_t)b * mv.blk_stride + ((size_t)q * KZ + kzp) * Kx + kx);
+            else
+                rs[e] = 0.0;
+        }
+        for (int k = threadIdx.x; k < L; k += kNT3) ph[k] = half_phase(mv.tw, ktil(k, L), L, -1);
+    }
     auto ld0 = [&](int pp, int n) -> double2 {
         const int t = pp % T, grp = pp / T, beta = grp >> 1, side = grp & 1;
         const int kx = tile * T + t;
@@ -163,38 +184,45 @@ __global__ void __launch_bounds__(kNT) k_p3(MV mv) {
         return mv.X2[beta][((int64_t)n * My + ky[side]) * Kx + kx];
     };
     auto sti = [&](int pp, int p, double2 v) { smin[p * TI + pp] = v; };
-    fft_run<L, TI, kNT, false, true>(smin, ld0, sti, mv.tw);
+    fft_run<L, TI, kNT3, false, true>(smin, ld0, sti, mv.tw);
+    cp_async_wait_all();
     __syncthreads();
     for (int f = 0; f < mv.nf; ++f) {
         const int kind = mv.fkind[f], alpha = mv.faxis[f];
         const int ezo = mv.ext_out[f][2];
         const bool phz_out = alpha != 2;  // c_alpha,z = 1/2 for x- and y-normal fields
-        for (int u = threadIdx.x; u < L * TO; u += kNT) {
+        const int b0 = mv.blk[f][0], b1 = mv.blk[f][1], b2 = mv.blk[f][2];
+        for (int u = threadIdx.x; u < L * TO; u += kNT3) {
             const int t = u % T, side = (u / T) & 1, k = u / TO;
-            const int kx = tile * T + t;
             double2 acc = czero();
-            if (side < nside && kx < Kx) {
+            if (side < nside) {
                 const int p = Plan<L>::pos(k);
                 const int kt = ktil(k, L);
                 const int kzp = kt < 0 ? -kt : kt;
-                const double2 phin = half_phase(mv.tw, kt, L, -1);
-#pragma unroll
-                for (int beta = 0; beta < 3; ++beta) {
-                    const int b = mv.blk[f][beta];
-                    if (b < 0) continue;
-                    double2 qv = smin[p * TI + (beta * 2 + side) * T + t];
-                    if (beta != 2) qv = cmul(qv, phin);
-                    double r = __ldg(mv.Rt + (size_t)b * mv.blk_stride +
-                                     ((size_t)q * KZ + kzp) * Kx + kx);
-                    if (kind == 1) {
-                        if (alpha == 1 && side == 1) r = -r;
-                        if (alpha == 2 && kt < 0) r = -r;
-                    }
+                const double2 phin = ph[k];
+                const double2* qin = smin + p * TI + side * T + t;
+                double sg = 1.0;
+                if (kind == 1 && ((alpha == 1 && side == 1) || (alpha == 2 && kt < 0))) sg = -1.0;
+                if (b0 >= 0) {  // beta = x: phi-bar_x,z applies
+                    const double r = sg * rs[(b0 * KZ + kzp) * T + t];
+                    const double2 qv = cmul(qin[0], phin);
+                    acc.x = fma(r, qv.x, acc.x);
+                    acc.y = fma(r, qv.y, acc.y);
+                }
+                if (b1 >= 0) {  // beta = y
+                    const double r = sg * rs[(b1 * KZ + kzp) * T + t];
+                    const double2 qv = cmul(qin[2 * T], phin);
+                    acc.x = fma(r, qv.x, acc.x);
+                    acc.y = fma(r, qv.y, acc.y);
+                }
+                if (b2 >= 0) {  // beta = z: no z half-shift
+                    const double r = sg * rs[(b2 * KZ + kzp) * T + t];
+                    const double2 qv = qin[4 * T];
                     acc.x = fma(r, qv.x, acc.x);
                     acc.y = fma(r, qv.y, acc.y);
                 }
                 if (kind == 1) acc = make_double2(-acc.y, acc.x);
-                if (phz_out) acc = cmul(acc, half_phase(mv.tw, kt, L, +1));
+                if (phz_out) acc = cmulc(acc, phin);  // times exp(+i pi kt / L)
             }
             smout[k * TO + side * T + t] = acc;
         }
@@ -208,7 +236,7 @@ __global__ void __launch_bounds__(kNT) k_p3(MV mv) {
             if (side < nside && kx < Kx && zz < ezo)
                 X3[((int64_t)zz * My + ky[side]) * Kx + kx] = v;
         };
-        fft_run<L, TO, kNT, true, true>(smout, ldo, sto, mv.tw);
+        fft_run<L, TO, kNT3, true, true>(smout, ldo, sto, mv.tw);
         __syncthreads();
     }
 }
@@ -319,32 +347,63 @@ __global__ void k_twiddles(double2* tw) {
     tw[n] = make_double2(c, s);
 }
 
-// representative slot offset of cyclic index n for doubled half-shift s2
-__device__ __forceinline__ int rep_offset(int n, int M, int s2) {
-    if (s2 > 0) return n < M / 2 ? n : n - M;   // minimise |delta + 1/2|
-    if (s2 < 0) return n <= M / 2 ? n : n - M;  // minimise |delta - 1/2|
-    return n <= M / 2 ? n : n - M;              // tie at M/2 -> +M/2
+// Cyclic index n on an M-grid -> signed geometric offset t (doubled, 2t) of the representative
+// slot difference minimising |delta + s|, s2 = 2 s in {-1, 0, 1}.  The tie of
+// s = 0 at n = M/2 is taken as +M/2 (odd kernels are zeroed there by the caller).
+__device__ __forceinline__ int rep_t2(int n, int M, int s2) {
+    int d;
+    if (s2 > 0) d = n < M / 2 ? n : n - M;
+    else if (s2 < 0) d = n <= M / 2 ? n : n - M;
+    else d = n <= M / 2 ? n : n - M;
+    return 2 * d + s2;
 }
 
-__global__ void k_kgen(double2* G, int Mx, int My, int Mz, int kind, int alpha, int beta) {
+// a2 on the parity octant: Ko[iz][iy][ix] = kappa at the non-negative geometric offset
+// |t| = i (s = 0) or i + 1/2 (s = +-1/2) per axis.  P blocks are even in every component of t,
+// E^{a.} blocks odd along a and even otherwise (Table VIII), so the
+// full cyclic grid follows from this octant with signs.
+__global__ void k_kgen_oct(double* Ko, int Ox, int Oy, int Oz, int kind, int alpha, int beta,
+                           double scale) {
+    const int64_t tot = (int64_t)Ox * Oy * Oz;
+    const int O[3] = {Ox, Oy, Oz};
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < tot;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int i[3] = {(int)(idx % Ox), (int)((idx / Ox) % Oy), (int)(idx / ((int64_t)Ox * Oy))};
+        int D[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            const int s2 = c2(alpha, a) - c2(beta, a);
+            // |t| = i (s2 = 0) or i + 1/2; slot offset D = t - s
+            D[a] = s2 == 0 ? i[a] : (s2 > 0 ? i[a] : i[a] + 1);
+        }
+        (void)O;
+        Ko[idx] = scale * kappa(kind, alpha, beta, D[0], D[1], D[2]);
+    }
+}
+
+// full cyclic grid (real part of G) from the octant table, with the parity signs
+__global__ void k_kfill(double2* G, const double* __restrict__ Ko, int Mx, int My, int Mz, int Ox,
+                        int Oy, int kind, int alpha, int beta) {
     const int64_t tot = (int64_t)Mx * My * Mz;
     for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < tot;
          idx += (int64_t)gridDim.x * blockDim.x) {
-        const int nx = (int)(idx % Mx);
-        const int ny = (int)((idx / Mx) % My);
-        const int nz = (int)(idx / ((int64_t)Mx * My));
-        const int n[3] = {nx, ny, nz};
+        const int n[3] = {(int)(idx % Mx), (int)((idx / Mx) % My), (int)(idx / ((int64_t)Mx * My))};
         const int M[3] = {Mx, My, Mz};
-        int d[3];
+        int o[3];
+        double sg = 1.0;
         bool zero = false;
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
             const int s2 = c2(alpha, a) - c2(beta, a);
-            d[a] = rep_offset(n[a], M[a], s2);
-            // odd kernel (E^{aa} along a) at the unresolvable tie n = M/2 -> 0
-            if (kind == 1 && alpha == beta && a == alpha && 2 * n[a] == M[a]) zero = true;
+            const int t2 = rep_t2(n[a], M[a], s2);
+            const int at2 = t2 < 0 ? -t2 : t2;
+            o[a] = s2 == 0 ? at2 / 2 : (at2 - 1) / 2;
+            if (kind == 1 && a == alpha) {
+                if (t2 < 0) sg = -sg;
+                if (s2 == 0 && 2 * n[a] == M[a]) zero = true;  // unresolvable odd tie
+            }
         }
-        const double v = zero ? 0.0 : kappa(kind, alpha, beta, d[0], d[1], d[2]);
+        const double v = zero ? 0.0 : sg * Ko[((int64_t)o[2] * Oy + o[1]) * Ox + o[0]];
         G[idx] = make_double2(v, 0.0);
     }
 }
@@ -471,11 +530,12 @@ static cudaError_t launch_p2(const MV& mv, cudaStream_t st) {
 static cudaError_t launch_p3(const MV& mv, cudaStream_t st) {
     VC_DISPATCH_L(mv.Mz, {
         constexpr int T = TZ<LL>::T;
-        const size_t smem = sizeof(double2) * LL * 8 * T;
+        const size_t smem = sizeof(double2) * (LL * 8 * T + LL) +
+                            sizeof(double) * (size_t)mv.nblk * (LL / 2 + 1) * T;
         cudaError_t e = prep(k_p3<LL>, smem);
         if (e) return e;
         dim3 grid(((mv.Kx + T - 1) / T) * (mv.My / 2 + 1));
-        k_p3<LL><<<grid, kNT, smem, st>>>(mv);
+        k_p3<LL><<<grid, kNT3, smem, st>>>(mv);
     });
     return cudaGetLastError();
 }
@@ -649,27 +709,49 @@ vc_status operator_build(vc_ctx* c, const vc_build_opts* o) {
     k_twiddles<<<(kTabN + 255) / 256, 256, 0, st>>>(c->tw.p);
     count_launch(c);
     VC_CUDA(c, c->Rt.alloc(c->blk_stride * std::max(1, c->nblk)));
-    // spectra
+    // spectra (a2 on the parity octant -> full cyclic grid -> 3-D FFT -> phase strip + fold)
     {
+        cudaEvent_t ev[4];
+        for (auto& e : ev) VC_CUDA(c, cudaEventCreate(&e));
+        float t_kgen = 0, t_fft = 0, t_ext = 0, ms;
         DevBuf<double2> G;
+        DevBuf<double> Ko;
         const int64_t tot = (int64_t)M[0] * M[1] * M[2];
+        const int Ox = M[0] / 2 + 1, Oy = M[1] / 2 + 1, Oz = M[2] / 2 + 1;
+        const int64_t otot = (int64_t)Ox * Oy * Oz;
         VC_CUDA(c, G.alloc(tot));
+        VC_CUDA(c, Ko.alloc(otot));
         const double fpe = 4.0 * kPi * kEps0;
         for (int i = 0; i < c->nblk; ++i) {
             const BlkDef& d = defs[i];
+            const double scale = (d.kind == 0 ? c->dv * c->dv * c->dv : c->dv * c->dv) / fpe /
+                                 ((double)M[0] * M[1] * M[2]);
+            VC_CUDA(c, cudaEventRecord(ev[0], st));
+            const int oblocks = (int)std::min<int64_t>((otot + 127) / 128, 148 * 64);
+            k_kgen_oct<<<oblocks, 128, 0, st>>>(Ko.p, Ox, Oy, Oz, d.kind, d.alpha, d.beta, scale);
             const int gblocks = (int)std::min<int64_t>((tot + 255) / 256, 148 * 64);
-            k_kgen<<<gblocks, 256, 0, st>>>(G.p, M[0], M[1], M[2], d.kind, d.alpha, d.beta);
+            k_kfill<<<gblocks, 256, 0, st>>>(G.p, Ko.p, M[0], M[1], M[2], Ox, Oy, d.kind, d.alpha, d.beta);
+            VC_CUDA(c, cudaEventRecord(ev[1], st));
             VC_CUDA(c, launch_fft_lines(G.p, M[0], (int64_t)M[1] * M[2], false, c->tw.p, st));
             VC_CUDA(c, launch_fft_strided(G.p, M[1], M[0], M[0], M[2], (int64_t)M[0] * M[1], c->tw.p, st));
             VC_CUDA(c, launch_fft_strided(G.p, M[2], (int64_t)M[0] * M[1], (int64_t)M[0] * M[1], 1, 0, c->tw.p, st));
-            const double scale = (d.kind == 0 ? c->dv * c->dv * c->dv : c->dv * c->dv) / fpe /
-                                 ((double)M[0] * M[1] * M[2]);
+            VC_CUDA(c, cudaEventRecord(ev[2], st));
             const int eblocks = (int)std::min<int64_t>((c->blk_stride + 255) / 256, 148 * 32);
             k_extract<<<eblocks, 256, 0, st>>>(G.p, c->Rt.p + c->blk_stride * i, M[0], M[1], M[2],
-                                               Kx, d.kind, d.alpha, d.beta, scale, c->tw.p);
-            count_launch(c, 5);
+                                               Kx, d.kind, d.alpha, d.beta, 1.0, c->tw.p);
+            VC_CUDA(c, cudaEventRecord(ev[3], st));
+            count_launch(c, 6);
+            VC_CUDA(c, cudaEventSynchronize(ev[3]));
+            cudaEventElapsedTime(&ms, ev[0], ev[1]);
+            t_kgen += ms;
+            cudaEventElapsedTime(&ms, ev[1], ev[2]);
+            t_fft += ms;
+            cudaEventElapsedTime(&ms, ev[2], ev[3]);
+            t_ext += ms;
         }
-        VC_CUDA(c, cudaStreamSynchronize(st));
+        for (auto& e : ev) cudaEventDestroy(e);
+        c->stats.ms_kgen = t_kgen;
+        c->stats.ms_kfft = t_fft + t_ext;
         VC_CUDA(c, cudaGetLastError());
     }
     // pass buffers: A holds X1 (P1->P2) and later X4 (P4->P5); B holds X2; C holds X3
@@ -744,6 +826,7 @@ static MV make_mv(vc_ctx* c, const double* x, double* y) {
     mv.ibar = c->pan.ibar.p;
     mv.Rt = c->Rt.p;
     mv.blk_stride = c->blk_stride;
+    mv.nblk = c->nblk;
     mv.tw = c->tw.p;
     return mv;
 }

@@ -152,7 +152,20 @@ vc_status vc_set_geometry(vc_ctx* c, int32_t nx, int32_t ny, int32_t nz, double 
             pe = de.p;
         }
     }
+    cudaEvent_t g0, g1;
+    VC_CUDA(c, cudaEventCreate(&g0));
+    VC_CUDA(c, cudaEventCreate(&g1));
+    VC_CUDA(c, cudaEventRecord(g0, c->stream));
     vc_status s = geometry_build(c, pl, pe);
+    if (s == VC_OK) {
+        VC_CUDA(c, cudaEventRecord(g1, c->stream));
+        VC_CUDA(c, cudaEventSynchronize(g1));
+        float ms = 0;
+        cudaEventElapsedTime(&ms, g0, g1);
+        c->stats.ms_geometry = ms;
+    }
+    cudaEventDestroy(g0);
+    cudaEventDestroy(g1);
     if (s != VC_OK) {
         std::string msg = c->err;
         drop_geometry(c);

@@ -94,6 +94,8 @@ struct vc_ctx {
     vc::DevBuf<double2> tw;  // twiddles exp(-2 pi i n / kTabN)
     vc::DevBuf<double2> bufA, bufB, bufC;  // X1/X4, X2, X3
     size_t offA_in[3], offB[3], offC[6], offA_out[6];
+    int ZL = 0, nzin[3] = {0, 0, 0}, nzout[6] = {0, 0, 0, 0, 0, 0};  // active z-plane counts
+    vc::DevBuf<int32_t> planes;  // plane lists + inverse maps (operator.cu)
     double bytes_pass[5] = {0, 0, 0, 0, 0};
     int precond_kind = 3;
     vc::Precond* pc = nullptr;

@@ -120,17 +120,19 @@ __device__ __forceinline__ void reg_dft(double2 (&v)[R]) {
 //   st(t, p, v)         : write element at position p of pencil t (stage output)
 //   PF = true : consecutive lanes take consecutive pencils (strided-axis passes)
 //   PF = false: consecutive lanes take consecutive butterflies of one pencil (contiguous lines)
+//   Tn (<= T): pencils actually transformed (the shared-memory layout keeps stride T)
 template <int L, int T, int NT, bool INV, bool PF, int s, class LD, class ST>
-__device__ __forceinline__ void fft_stage(LD&& ld, ST&& st, const double2* __restrict__ tw) {
+__device__ __forceinline__ void fft_stage(LD&& ld, ST&& st, const double2* __restrict__ tw,
+                                          const int Tn = T) {
     constexpr int R = Plan<L>::radix(s);
     constexpr int Lc = Plan<L>::lc(s);
     constexpr int S = Lc / R;
-    constexpr int NB = T * (L / R);
     constexpr int TW = kTabN / Lc;
+    const int NB = Tn * (L / R);
 #pragma unroll 1
     for (int u = threadIdx.x; u < NB; u += NT) {
-        const int t = PF ? u % T : u / (L / R);
-        const int rest = PF ? u / T : u % (L / R);
+        const int t = PF ? u % Tn : u / (L / R);
+        const int rest = PF ? u / Tn : u % (L / R);
         const int b = rest % S;
         const int g = rest / S;
         const int base = g * Lc + b;
@@ -140,6 +142,7 @@ __device__ __forceinline__ void fft_stage(LD&& ld, ST&& st, const double2* __res
         reg_dft<R, INV>(v);
         if (S > 1) {
             // inter-stage twiddles w_Lc^{b m}: one table load, powers by squaring/products
+            // (measured: R-1 table loads instead made the HBM-bound passes 15-20% slower)
             double2 wp[R];
             wp[0] = make_double2(1.0, 0.0);
             wp[1] = twiddle<INV>(tw, b * TW);
@@ -169,23 +172,23 @@ __device__ __forceinline__ int smi(int t, int p) { return PF ? p * T + t : t * L
 // stage goes ld0 -> stN.  No trailing __syncthreads().
 template <int L, int T, int NT, bool INV, bool PF, class LD, class ST>
 __device__ __forceinline__ void fft_run(double2* sm, LD&& ld0, ST&& stN,
-                                        const double2* __restrict__ tw) {
+                                        const double2* __restrict__ tw, const int Tn = T) {
     constexpr int NS = Plan<L>::NS;
     auto lds = [&](int t, int p) { return sm[smi<L, T, PF>(t, p)]; };
     auto sts = [&](int t, int p, double2 v) { sm[smi<L, T, PF>(t, p)] = v; };
     if constexpr (NS == 1) {
-        fft_stage<L, T, NT, INV, PF, 0>(ld0, stN, tw);
+        fft_stage<L, T, NT, INV, PF, 0>(ld0, stN, tw, Tn);
     } else if constexpr (NS == 2) {
-        fft_stage<L, T, NT, INV, PF, 0>(ld0, sts, tw);
+        fft_stage<L, T, NT, INV, PF, 0>(ld0, sts, tw, Tn);
         __syncthreads();
-        fft_stage<L, T, NT, INV, PF, 1>(lds, stN, tw);
+        fft_stage<L, T, NT, INV, PF, 1>(lds, stN, tw, Tn);
     } else {
         static_assert(NS == 3, "L <= 4096");
-        fft_stage<L, T, NT, INV, PF, 0>(ld0, sts, tw);
+        fft_stage<L, T, NT, INV, PF, 0>(ld0, sts, tw, Tn);
         __syncthreads();
-        fft_stage<L, T, NT, INV, PF, 1>(lds, sts, tw);
+        fft_stage<L, T, NT, INV, PF, 1>(lds, sts, tw, Tn);
         __syncthreads();
-        fft_stage<L, T, NT, INV, PF, 2>(lds, stN, tw);
+        fft_stage<L, T, NT, INV, PF, 2>(lds, stN, tw, Tn);
     }
 }
 

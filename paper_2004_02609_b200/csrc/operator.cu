@@ -43,15 +43,22 @@ struct MV {
     int blk[6][3];
     int nblk;
     const double2* tw;
+    // active z-planes (window-relative) of each source orientation / output field: only planes
+    // holding panels are transformed along x and y and stored
+    const int32_t* planes;  // [9][ZL] lists, then [9][ZL] inverse maps (plane -> index or -1)
+    int ZL;
+    int nzin[3], nzout[6];
 };
+
+__device__ __forceinline__ int zlist(const MV& mv, int g, int j) { return mv.planes[g * mv.ZL + j]; }
 
 // ---- tile-size choices (compile-time functions of the FFT length) -----------------------
 constexpr int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
 template <int L> struct TX { static constexpr int T = clampi(4096 / L, 1, 64); };   // x passes
 template <int L> struct TY { static constexpr int T = clampi(4096 / L, 1, 32); };   // y passes
-template <int L> struct TZ { static constexpr int T = clampi(256 / L, 2, 16); };    // z + MAC
 constexpr int kNT = 256;
-constexpr int kNT3 = 128;  // P3 threads per CTA
+constexpr int kNT3 = 256;  // P3 threads per CTA
+constexpr int kMaxLz = 512;  // largest z FFT length (P3 keeps whole z-pencils in shared memory)
 
 __device__ __forceinline__ int ktil(int k, int M) { return k <= M / 2 ? k : k - M; }
 
@@ -67,8 +74,10 @@ __global__ void __launch_bounds__(kNT) k_p1(MV mv) {
     if (ex == 0) return;
     const int nyp = (ey + 1) >> 1;
     const int nch = (nyp + T - 1) / T;
-    const int z = blockIdx.x / nch, ch = blockIdx.x % nch;
-    if (z >= ez) return;
+    const int j = blockIdx.x / nch, ch = blockIdx.x % nch;
+    if (j >= mv.nzin[beta]) return;
+    const int z = zlist(mv, beta, j);
+    (void)ez;
     const int32_t* __restrict__ smap = mv.slotmap[beta];
     const int Gx = mv.G[beta][0], Gy = mv.G[beta][1];
     const int64_t zrow = ((int64_t)(z + mv.lo[2]) * Gy + mv.lo[1]) * Gx + mv.lo[0];
@@ -92,7 +101,7 @@ __global__ void __launch_bounds__(kNT) k_p1(MV mv) {
     __syncthreads();
     constexpr int K = L / 2 + 1;
     const bool ph = beta != 0;  // c_beta,x = 1/2 for y- and z-normal panels
-    double2* __restrict__ out = mv.X1[beta] + (int64_t)z * ey * mv.Kx;
+    double2* __restrict__ out = mv.X1[beta] + (int64_t)j * ey * mv.Kx;
     for (int u = threadIdx.x; u < T * K; u += kNT) {
         const int t = u / K, k = u % K;
         const int q = ch * T + t;
@@ -123,10 +132,11 @@ __global__ void __launch_bounds__(kNT) k_p2(MV mv) {
     if (ex == 0) return;
     const int Kx = mv.Kx;
     const int ntile = (Kx + T - 1) / T;
-    const int z = blockIdx.x / ntile, tile = blockIdx.x % ntile;
-    if (z >= ez) return;
-    const double2* __restrict__ in = mv.X1[beta] + (int64_t)z * ey * Kx;
-    double2* __restrict__ out = mv.X2[beta] + (int64_t)z * L * Kx;
+    const int j = blockIdx.x / ntile, tile = blockIdx.x % ntile;
+    if (j >= mv.nzin[beta]) return;
+    (void)ez;
+    const double2* __restrict__ in = mv.X1[beta] + (int64_t)j * ey * Kx;
+    double2* __restrict__ out = mv.X2[beta] + (int64_t)j * L * Kx;
     const bool ph = beta != 1;  // c_beta,y = 1/2 for x- and z-normal panels
     auto ld0 = [&](int t, int n) -> double2 {
         const int kx = tile * T + t;
@@ -147,23 +157,37 @@ __global__ void __launch_bounds__(kNT) k_p2(MV mv) {
 //   One CTA = T adjacent kx x the ky pair {q, My - q} (the two share every folded spectrum
 //   row, so each R element is read from HBM once).  The CTA's R tile (all blocks, kz' in
 //   [0, Mz/2], T kx) and the z half-shift phases are staged in shared memory with cp.async
-//   while the forward FFT's first stage streams X2 in.
+//   while the forward FFT's first stage streams X2 in.  One shared buffer [L][W] holds the
+//   6T forward pencils, then (after the MAC has pulled its inputs into registers) the nf*2T
+//   output pencils, which are inverse-transformed together.
+//   Phase algebra (App. B): out^a = phi_a sum_b R^{ab} phibar_b Q^b.  Along z, c_x = c_y = 1/2
+//   and c_z = 0, so phi_a,z phibar_b,z is 1 for a, b both in {x, y} or both z, phi_z-bar for
+//   (a = z, b in {x, y}) and phi_z for (a in {x, y}, b = z): one complex multiply per source
+//   (Q^z) and one per z-field, instead of one per (field, source).  The parity sign of the
+//   odd E blocks and the factor i are common to all sources of a field and applied once.
 // ---------------------------------------------------------------------------------------
-template <int L>
+template <int L, int NFW>
+struct P3T {
+    static constexpr int T = clampi(256 / L, 1, 16) * (NFW == 3 ? 2 : 1);
+    static constexpr int W = (NFW == 3 ? 6 : 12) * T;  // buffer width (pencils)
+};
+
+template <int L, int NFW>
 __global__ void __launch_bounds__(kNT3) k_p3(MV mv) {
-    constexpr int T = TZ<L>::T;
-    constexpr int TI = 6 * T, TO = 2 * T;
+    constexpr int T = P3T<L, NFW>::T;
+    constexpr int W = P3T<L, NFW>::W;
+    constexpr int T2 = 2 * T;
     constexpr int KZ = L / 2 + 1;
+    constexpr int NI = (L * T2 + kNT3 - 1) / kNT3;  // MAC items per thread
     extern __shared__ double2 sm[];
-    double2* smin = sm;              // [L][TI]
-    double2* smout = smin + L * TI;  // [L][TO]
-    double2* ph = smout + L * TO;    // [L] exp(-i pi kt / L)
+    double2* buf = sm;                               // [L][W]
+    double2* ph = buf + L * W;                       // [L] exp(-i pi kt / L)
     double* rs = reinterpret_cast<double*>(ph + L);  // [nblk][KZ][T]
-    const int Kx = mv.Kx, My = mv.My;
+    int* zmap = reinterpret_cast<int*>(rs + mv.nblk * KZ * T);  // [9][L] plane -> index / -1
+    const int Kx = mv.Kx, My = mv.My, nf = mv.nf;
     const int ntile = (Kx + T - 1) / T;
     const int q = blockIdx.x / ntile, tile = blockIdx.x % ntile;
     const int nside = (q == 0 || 2 * q == My) ? 1 : 2;
-    const int ky[2] = {q, My - q};
     // stage the R tile (async) and the phase table
     {
         const int nr = mv.nblk * KZ * T;
@@ -176,69 +200,99 @@ __global__ void __launch_bounds__(kNT3) k_p3(MV mv) {
                 rs[e] = 0.0;
         }
         for (int k = threadIdx.x; k < L; k += kNT3) ph[k] = half_phase(mv.tw, ktil(k, L), L, -1);
+        for (int e = threadIdx.x; e < 9 * L; e += kNT3) {
+            const int g = e / L, z = e % L;
+            zmap[e] = z < mv.ZL ? mv.planes[(9 + g) * mv.ZL + z] : -1;
+        }
     }
+    __syncthreads();
+    // forward z-FFT of pencils pp = beta * 2T + side * T + t
     auto ld0 = [&](int pp, int n) -> double2 {
-        const int t = pp % T, grp = pp / T, beta = grp >> 1, side = grp & 1;
+        const int t = pp % T, side = (pp / T) & 1, beta = pp / T2;
         const int kx = tile * T + t;
-        if (side >= nside || kx >= Kx || n >= mv.ext_in[beta][2]) return czero();
-        return mv.X2[beta][((int64_t)n * My + ky[side]) * Kx + kx];
+        const int jz = zmap[beta * L + n];
+        if (side >= nside || kx >= Kx || jz < 0) return czero();
+        const int ky = side ? My - q : q;
+        return mv.X2[beta][((int64_t)jz * My + ky) * Kx + kx];
     };
-    auto sti = [&](int pp, int p, double2 v) { smin[p * TI + pp] = v; };
-    fft_run<L, TI, kNT3, false, true>(smin, ld0, sti, mv.tw);
+    auto sti = [&](int pp, int p, double2 v) { buf[p * W + pp] = v; };
+    fft_run<L, W, kNT3, false, true>(buf, ld0, sti, mv.tw, 3 * T2);
     cp_async_wait_all();
     __syncthreads();
-    for (int f = 0; f < mv.nf; ++f) {
-        const int kind = mv.fkind[f], alpha = mv.faxis[f];
-        const int ezo = mv.ext_out[f][2];
-        const bool phz_out = alpha != 2;  // c_alpha,z = 1/2 for x- and y-normal fields
-        const int b0 = mv.blk[f][0], b1 = mv.blk[f][1], b2 = mv.blk[f][2];
-        for (int u = threadIdx.x; u < L * TO; u += kNT3) {
-            const int t = u % T, side = (u / T) & 1, k = u / TO;
-            double2 acc = czero();
-            if (side < nside) {
-                const int p = Plan<L>::pos(k);
-                const int kt = ktil(k, L);
-                const int kzp = kt < 0 ? -kt : kt;
-                const double2 phin = ph[k];
-                const double2* qin = smin + p * TI + side * T + t;
-                double sg = 1.0;
-                if (kind == 1 && ((alpha == 1 && side == 1) || (alpha == 2 && kt < 0))) sg = -1.0;
-                if (b0 >= 0) {  // beta = x: phi-bar_x,z applies
-                    const double r = sg * rs[(b0 * KZ + kzp) * T + t];
-                    const double2 qv = cmul(qin[0], phin);
-                    acc.x = fma(r, qv.x, acc.x);
-                    acc.y = fma(r, qv.y, acc.y);
-                }
-                if (b1 >= 0) {  // beta = y
-                    const double r = sg * rs[(b1 * KZ + kzp) * T + t];
-                    const double2 qv = cmul(qin[2 * T], phin);
-                    acc.x = fma(r, qv.x, acc.x);
-                    acc.y = fma(r, qv.y, acc.y);
-                }
-                if (b2 >= 0) {  // beta = z: no z half-shift
-                    const double r = sg * rs[(b2 * KZ + kzp) * T + t];
-                    const double2 qv = qin[4 * T];
-                    acc.x = fma(r, qv.x, acc.x);
-                    acc.y = fma(r, qv.y, acc.y);
-                }
-                if (kind == 1) acc = make_double2(-acc.y, acc.x);
-                if (phz_out) acc = cmulc(acc, phin);  // times exp(+i pi kt / L)
-            }
-            smout[k * TO + side * T + t] = acc;
+    // MAC: item u = k * 2T + c (c = side * T + t); inputs to registers, then outputs in place
+    double2 qv[NI][3];
+#pragma unroll
+    for (int ii = 0; ii < NI; ++ii) {
+        const int u = threadIdx.x + ii * kNT3;
+        if (u < L * T2) {
+            const int k = u / T2, c = u % T2;
+            const double2* row = buf + Plan<L>::pos(k) * W + c;
+            qv[ii][0] = row[0];
+            qv[ii][1] = row[T2];
+            qv[ii][2] = row[2 * T2];
         }
-        __syncthreads();
-        double2* __restrict__ X3 = mv.X3[f];
-        auto ldo = [&](int pp, int n) { return smout[n * TO + pp]; };
-        auto sto = [&](int pp, int p, double2 v) {
-            const int t = pp % T, side = pp / T;
-            const int kx = tile * T + t;
-            const int zz = Plan<L>::freq(p);
-            if (side < nside && kx < Kx && zz < ezo)
-                X3[((int64_t)zz * My + ky[side]) * Kx + kx] = v;
-        };
-        fft_run<L, TO, kNT3, true, true>(smout, ldo, sto, mv.tw);
-        __syncthreads();
     }
+    __syncthreads();
+#pragma unroll
+    for (int ii = 0; ii < NI; ++ii) {
+        const int u = threadIdx.x + ii * kNT3;
+        if (u >= L * T2) break;
+        const int k = u / T2, c = u % T2;
+        const int side = c / T, t = c % T;
+        const int kt = ktil(k, L);
+        const int kzp = kt < 0 ? -kt : kt;
+        const double2 phb = ph[k];           // phibar_z = exp(-i pi kt / L)
+        const double2 qx = qv[ii][0], qy = qv[ii][1];
+        const double2 qz = cmulc(qv[ii][2], phb);  // phi_z Q^z
+        const double* rrow = rs + kzp * T + t;
+        double2* orow = buf + k * W + c;
+        for (int f = 0; f < nf; ++f) {
+            const int kind = mv.fkind[f], alpha = mv.faxis[f];
+            const int b0 = mv.blk[f][0], b1 = mv.blk[f][1], b2 = mv.blk[f][2];
+            double2 a = czero();
+            if (side < nside) {
+                if (b0 >= 0) {
+                    const double r = rrow[b0 * KZ * T];
+                    a.x = fma(r, qx.x, a.x);
+                    a.y = fma(r, qx.y, a.y);
+                }
+                if (b1 >= 0) {
+                    const double r = rrow[b1 * KZ * T];
+                    a.x = fma(r, qy.x, a.x);
+                    a.y = fma(r, qy.y, a.y);
+                }
+                if (alpha == 2) {
+                    a = cmul(a, phb);  // (a = z, b in {x, y}): phibar_z
+                    if (b2 >= 0) {
+                        const double r = rrow[b2 * KZ * T];
+                        a.x = fma(r, qv[ii][2].x, a.x);
+                        a.y = fma(r, qv[ii][2].y, a.y);
+                    }
+                } else if (b2 >= 0) {  // (a in {x, y}, b = z): phi_z, folded into qz
+                    const double r = rrow[b2 * KZ * T];
+                    a.x = fma(r, qz.x, a.x);
+                    a.y = fma(r, qz.y, a.y);
+                }
+                if (kind == 1) {
+                    // E blocks: R stores Im(K), odd along alpha; sign from the octant fold
+                    const bool neg = (alpha == 1 && side == 1) || (alpha == 2 && kt < 0);
+                    a = neg ? make_double2(a.y, -a.x) : make_double2(-a.y, a.x);
+                }
+            }
+            orow[f * T2] = a;
+        }
+    }
+    __syncthreads();
+    auto ldo = [&](int pp, int n) { return buf[n * W + pp]; };
+    auto sto = [&](int pp, int p, double2 v) {
+        const int f = pp / T2, c = pp % T2;
+        const int side = c / T, t = c % T;
+        const int kx = tile * T + t;
+        const int jz = zmap[(3 + f) * L + Plan<L>::freq(p)];
+        if (side < nside && kx < Kx && jz >= 0)
+            mv.X3[f][((int64_t)jz * My + (side ? My - q : q)) * Kx + kx] = v;
+    };
+    fft_run<L, W, kNT3, true, true>(buf, ldo, sto, mv.tw, nf * T2);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -254,10 +308,11 @@ __global__ void __launch_bounds__(kNT) k_p4(MV mv) {
     const int eyo = mv.ext_out[f][1], ezo = mv.ext_out[f][2];
     const int Kx = mv.Kx;
     const int ntile = (Kx + T - 1) / T;
-    const int z = blockIdx.x / ntile, tile = blockIdx.x % ntile;
-    if (z >= ezo) return;
-    const double2* __restrict__ in = mv.X3[f] + (int64_t)z * L * Kx;
-    double2* __restrict__ out = mv.X4[f] + (int64_t)z * eyo * Kx;
+    const int j = blockIdx.x / ntile, tile = blockIdx.x % ntile;
+    if (j >= mv.nzout[f]) return;
+    (void)ezo;
+    const double2* __restrict__ in = mv.X3[f] + (int64_t)j * L * Kx;
+    double2* __restrict__ out = mv.X4[f] + (int64_t)j * eyo * Kx;
     const bool ph = alpha != 1;
     auto ld0 = [&](int t, int n) -> double2 {
         const int kx = tile * T + t;
@@ -287,10 +342,12 @@ __global__ void __launch_bounds__(kNT) k_p5(MV mv) {
     const int exo = mv.ext_out[f][0], eyo = mv.ext_out[f][1], ezo = mv.ext_out[f][2];
     const int nyp = (eyo + 1) >> 1;
     const int nch = (nyp + T - 1) / T;
-    const int z = blockIdx.x / nch, ch = blockIdx.x % nch;
-    if (z >= ezo) return;
+    const int j = blockIdx.x / nch, ch = blockIdx.x % nch;
+    if (j >= mv.nzout[f]) return;
+    (void)ezo;
+    const int z = zlist(mv, 3 + f, j);
     const int Kx = mv.Kx;
-    const double2* __restrict__ in = mv.X4[f] + (int64_t)z * eyo * Kx;
+    const double2* __restrict__ in = mv.X4[f] + (int64_t)j * eyo * Kx;
     const bool ph = alpha != 0;
     auto At = [&](int yrow, int k) -> double2 {
         double2 v = in[(int64_t)yrow * Kx + k];
@@ -502,7 +559,7 @@ static cudaError_t prep(K kern, size_t smem) {
 
 static cudaError_t launch_p1(const MV& mv, cudaStream_t st) {
     int maxch = 0, maxz = 0;
-    for (int b = 0; b < 3; ++b) { maxz = std::max(maxz, mv.ext_in[b][2]); }
+    for (int b = 0; b < 3; ++b) { maxz = std::max(maxz, mv.nzin[b]); }
     VC_DISPATCH_L(mv.Mx, {
         constexpr int T = TX<LL>::T;
         for (int b = 0; b < 3; ++b) maxch = std::max(maxch, ((mv.ext_in[b][1] + 1) / 2 + T - 1) / T);
@@ -516,7 +573,7 @@ static cudaError_t launch_p1(const MV& mv, cudaStream_t st) {
 }
 static cudaError_t launch_p2(const MV& mv, cudaStream_t st) {
     int maxz = 0;
-    for (int b = 0; b < 3; ++b) maxz = std::max(maxz, mv.ext_in[b][2]);
+    for (int b = 0; b < 3; ++b) maxz = std::max(maxz, mv.nzin[b]);
     VC_DISPATCH_L(mv.My, {
         constexpr int T = TY<LL>::T;
         const size_t smem = sizeof(double2) * LL * T;
@@ -527,21 +584,34 @@ static cudaError_t launch_p2(const MV& mv, cudaStream_t st) {
     });
     return cudaGetLastError();
 }
+template <int L, int NFW>
+static cudaError_t launch_p3_t(const MV& mv, cudaStream_t st) {
+    constexpr int T = P3T<L, NFW>::T, W = P3T<L, NFW>::W;
+    const size_t smem = sizeof(double2) * ((size_t)L * W + L) +
+                        sizeof(double) * (size_t)mv.nblk * (L / 2 + 1) * T + sizeof(int) * 9 * L;
+    if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
+    cudaError_t e = prep(k_p3<L, NFW>, smem);
+    if (e) return e;
+    dim3 grid(((mv.Kx + T - 1) / T) * (mv.My / 2 + 1));
+    k_p3<L, NFW><<<grid, kNT3, smem, st>>>(mv);
+    return cudaSuccess;
+}
 static cudaError_t launch_p3(const MV& mv, cudaStream_t st) {
-    VC_DISPATCH_L(mv.Mz, {
-        constexpr int T = TZ<LL>::T;
-        const size_t smem = sizeof(double2) * (LL * 8 * T + LL) +
-                            sizeof(double) * (size_t)mv.nblk * (LL / 2 + 1) * T;
-        cudaError_t e = prep(k_p3<LL>, smem);
-        if (e) return e;
-        dim3 grid(((mv.Kx + T - 1) / T) * (mv.My / 2 + 1));
-        k_p3<LL><<<grid, kNT3, smem, st>>>(mv);
-    });
+    cudaError_t e;
+    switch (mv.Mz) {  // kMaxLz: the [L][W] pencil buffer must fit one CTA's shared memory
+#define VC_P3_CASE(LL) \
+        case LL: e = mv.nf <= 3 ? launch_p3_t<LL, 3>(mv, st) : launch_p3_t<LL, 6>(mv, st); break;
+        VC_P3_CASE(8) VC_P3_CASE(16) VC_P3_CASE(32) VC_P3_CASE(64) VC_P3_CASE(128)
+        VC_P3_CASE(256) VC_P3_CASE(512)
+#undef VC_P3_CASE
+        default: return cudaErrorInvalidValue;
+    }
+    if (e) return e;
     return cudaGetLastError();
 }
 static cudaError_t launch_p4(const MV& mv, cudaStream_t st) {
     int maxz = 0;
-    for (int f = 0; f < mv.nf; ++f) maxz = std::max(maxz, mv.ext_out[f][2]);
+    for (int f = 0; f < mv.nf; ++f) maxz = std::max(maxz, mv.nzout[f]);
     VC_DISPATCH_L(mv.My, {
         constexpr int T = TY<LL>::T;
         const size_t smem = sizeof(double2) * LL * T;
@@ -554,7 +624,7 @@ static cudaError_t launch_p4(const MV& mv, cudaStream_t st) {
 }
 static cudaError_t launch_p5(const MV& mv, cudaStream_t st) {
     int maxz = 0, maxch = 0;
-    for (int f = 0; f < mv.nf; ++f) maxz = std::max(maxz, mv.ext_out[f][2]);
+    for (int f = 0; f < mv.nf; ++f) maxz = std::max(maxz, mv.nzout[f]);
     VC_DISPATCH_L(mv.Mx, {
         constexpr int T = TX<LL>::T;
         for (int f = 0; f < mv.nf; ++f) maxch = std::max(maxch, ((mv.ext_out[f][1] + 1) / 2 + T - 1) / T);
@@ -654,6 +724,8 @@ vc_status operator_build(vc_ctx* c, const vc_build_opts* o) {
             M[t] = o->pad[t];
         }
         if (M[t] > kMaxL) return set_err(c, VC_ERR_UNSUPPORTED, "padded FFT size > 4096 along an axis");
+        if (t == 2 && M[t] > kMaxLz)
+            return set_err(c, VC_ERR_UNSUPPORTED, "padded FFT size along z > 512 (P3 pencil buffer)");
     }
     for (int t = 0; t < 3; ++t) {
         c->M[t] = M[t];
@@ -754,19 +826,50 @@ vc_status operator_build(vc_ctx* c, const vc_build_opts* o) {
         c->stats.ms_kfft = t_fft + t_ext;
         VC_CUDA(c, cudaGetLastError());
     }
+    // active z-planes: a plane of source orientation b (output field f) is transformed along x
+    // and y only if it holds b-panels (f-panels); empty planes are zero and never touched
+    {
+        int ZL = 1;
+        for (int b = 0; b < 3; ++b) ZL = std::max(ZL, c->ext_in[b][2]);
+        for (int f = 0; f < c->nf; ++f) ZL = std::max(ZL, c->f[f].ext[2]);
+        int fidx[2][3] = {{-1, -1, -1}, {-1, -1, -1}};
+        for (int f = 0; f < c->nf; ++f) fidx[c->f[f].kind][c->f[f].axis] = f;
+        std::vector<char> has(9 * (size_t)ZL, 0);
+        for (int64_t p = 0; p < c->N; ++p) {
+            const int a = c->h_axis[p], z = c->h_sk[p] - lo[2];
+            has[(size_t)a * ZL + z] = 1;
+            has[(size_t)(3 + fidx[c->h_cid[p] == 0 ? 1 : 0][a]) * ZL + z] = 1;
+        }
+        std::vector<int32_t> hp(18 * (size_t)ZL, -1);
+        for (int g = 0; g < 9; ++g) {
+            int n = 0;
+            for (int z = 0; z < ZL; ++z)
+                if (has[(size_t)g * ZL + z]) {
+                    hp[(size_t)g * ZL + n] = z;
+                    hp[(size_t)(9 + g) * ZL + z] = n;
+                    ++n;
+                }
+            if (g < 3) c->nzin[g] = n;
+            else c->nzout[g - 3] = n;
+        }
+        c->ZL = ZL;
+        VC_CUDA(c, c->planes.alloc(hp.size()));
+        VC_CUDA(c, cudaMemcpyAsync(c->planes.p, hp.data(), 4 * hp.size(), cudaMemcpyHostToDevice, st));
+        VC_CUDA(c, cudaStreamSynchronize(st));
+    }
     // pass buffers: A holds X1 (P1->P2) and later X4 (P4->P5); B holds X2; C holds X3
     size_t nA_in = 0, nA_out = 0, nB = 0, nC = 0;
     for (int b = 0; b < 3; ++b) {
         c->offA_in[b] = nA_in;
         c->offB[b] = nB;
-        nA_in += (size_t)c->ext_in[b][2] * c->ext_in[b][1] * Kx;
-        nB += (size_t)c->ext_in[b][2] * My * Kx;
+        nA_in += (size_t)c->nzin[b] * c->ext_in[b][1] * Kx;
+        nB += (size_t)c->nzin[b] * My * Kx;
     }
     for (int f = 0; f < c->nf; ++f) {
         c->offC[f] = nC;
         c->offA_out[f] = nA_out;
-        nC += (size_t)c->f[f].ext[2] * My * Kx;
-        nA_out += (size_t)c->f[f].ext[2] * c->f[f].ext[1] * Kx;
+        nC += (size_t)c->nzout[f] * My * Kx;
+        nA_out += (size_t)c->nzout[f] * c->f[f].ext[1] * Kx;
     }
     VC_CUDA(c, c->bufA.alloc(std::max<size_t>(1, std::max(nA_in, nA_out))));
     VC_CUDA(c, c->bufB.alloc(std::max<size_t>(1, nB)));
@@ -775,9 +878,9 @@ vc_status operator_build(vc_ctx* c, const vc_build_opts* o) {
     // arrays, kernel spectra read once, panel vectors and slot maps once.
     const double cb = 16.0;
     double slots = 0;
-    for (int b = 0; b < 3; ++b) slots += (double)c->ext_in[b][0] * c->ext_in[b][1] * c->ext_in[b][2];
+    for (int b = 0; b < 3; ++b) slots += (double)c->ext_in[b][0] * c->ext_in[b][1] * c->nzin[b];
     double slots_out = 0;
-    for (int f = 0; f < c->nf; ++f) slots_out += (double)c->f[f].ext[0] * c->f[f].ext[1] * c->f[f].ext[2];
+    for (int f = 0; f < c->nf; ++f) slots_out += (double)c->f[f].ext[0] * c->f[f].ext[1] * c->nzout[f];
     c->bytes_pass[0] = cb * nA_in + 4.0 * slots + 8.0 * c->N;
     c->bytes_pass[1] = cb * (nA_in + nB);
     c->bytes_pass[2] = cb * (nB + nC) + 8.0 * c->blk_stride * c->nblk;
@@ -828,6 +931,10 @@ static MV make_mv(vc_ctx* c, const double* x, double* y) {
     mv.blk_stride = c->blk_stride;
     mv.nblk = c->nblk;
     mv.tw = c->tw.p;
+    mv.planes = c->planes.p;
+    mv.ZL = c->ZL;
+    for (int b = 0; b < 3; ++b) mv.nzin[b] = c->nzin[b];
+    for (int f = 0; f < 6; ++f) mv.nzout[f] = f < c->nf ? c->nzout[f] : 0;
     return mv;
 }
 

@@ -52,7 +52,7 @@ typedef enum {
     VC_ERR_NCCL = 5,        /* reserved for the multi-GPU path                             */
     VC_NOT_CONVERGED = 6,   /* GMRES hit maxit; the best iterate is returned                */
     VC_ERR_UNSUPPORTED = 7  /* valid but unsupported request (padded FFT size > 4096 along x
-                               or y, > 512 along z)                                          */
+                               or y, > 256 along z)                                          */
 } vc_status;
 
 typedef struct vc_ctx vc_ctx;

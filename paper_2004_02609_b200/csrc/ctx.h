@@ -94,6 +94,8 @@ struct vc_ctx {
     vc::DevBuf<double2> tw;  // twiddles exp(-2 pi i n / kTabN)
     vc::DevBuf<double2> bufA, bufB, bufC;  // X1/X4, X2, X3
     size_t offA_in[3], offB[3], offC[6], offA_out[6];
+    int T3 = 1, nt3 = 1;   // P3 tile width and kx-tile count (tile-major X2 / R layouts)
+    size_t rchunk = 0;     // doubles of R per P3 tile
     int ZL = 0, nzin[3] = {0, 0, 0}, nzout[6] = {0, 0, 0, 0, 0, 0};  // active z-plane counts
     vc::DevBuf<int32_t> planes;  // plane lists + inverse maps (operator.cu)
     double bytes_pass[5] = {0, 0, 0, 0, 0};

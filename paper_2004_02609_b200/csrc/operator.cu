@@ -38,8 +38,9 @@ struct MV {
     double2* X2[3];
     double2* X3[6];
     double2* X4[6];
-    const double* Rt;
-    size_t blk_stride;
+    const double* Rt;       // tile-major: [q][kx-tile][block][kz'][t], rchunk doubles per tile
+    int rchunk;
+    int T3, lgT3;           // P3 tile width (power of two) and its log2
     int blk[6][3];
     int nblk;
     const double2* tw;
@@ -58,7 +59,7 @@ template <int L> struct TX { static constexpr int T = clampi(4096 / L, 1, 64); }
 template <int L> struct TY { static constexpr int T = clampi(4096 / L, 1, 32); };   // y passes
 constexpr int kNT = 256;
 constexpr int kNT3 = 256;  // P3 threads per CTA
-constexpr int kMaxLz = 512;  // largest z FFT length (P3 keeps whole z-pencils in shared memory)
+constexpr int kMaxLz = 256;  // largest z FFT length (P3 keeps whole z-pencils in shared memory)
 
 __device__ __forceinline__ int ktil(int k, int M) { return k <= M / 2 ? k : k - M; }
 
@@ -136,7 +137,9 @@ __global__ void __launch_bounds__(kNT) k_p2(MV mv) {
     if (j >= mv.nzin[beta]) return;
     (void)ez;
     const double2* __restrict__ in = mv.X1[beta] + (int64_t)j * ey * Kx;
-    double2* __restrict__ out = mv.X2[beta] + (int64_t)j * L * Kx;
+    // X2 tile-major for P3: [q][kx / T3][side][plane][kx % T3], q = |ky| (ky <= L/2: side 0)
+    double2* __restrict__ out = mv.X2[beta];
+    const int nzb = mv.nzin[beta], nt3 = (Kx + mv.T3 - 1) >> mv.lgT3;
     const bool ph = beta != 1;  // c_beta,y = 1/2 for x- and z-normal panels
     auto ld0 = [&](int t, int n) -> double2 {
         const int kx = tile * T + t;
@@ -147,152 +150,185 @@ __global__ void __launch_bounds__(kNT) k_p2(MV mv) {
         if (kx >= Kx) return;
         const int k = Plan<L>::freq(p);
         if (ph) v = cmul(v, half_phase(mv.tw, ktil(k, L), L, -1));
-        out[(int64_t)k * Kx + kx] = v;
+        const int side = k > L / 2, qq = side ? L - k : k;
+        out[((((int64_t)qq * nt3 + (kx >> mv.lgT3)) * 2 + side) * nzb + j) * mv.T3 +
+            (kx & (mv.T3 - 1))] = v;
     };
     fft_run<L, T, kNT, false, true>(sm, ld0, stN, mv.tw);
 }
 
 // ---------------------------------------------------------------------------------------
 // P3: forward z FFT of the three source fields, orientation-block MAC (Eqs. 10-12), inverse z
-//   One CTA = T adjacent kx x the ky pair {q, My - q} (the two share every folded spectrum
-//   row, so each R element is read from HBM once).  The CTA's R tile (all blocks, kz' in
-//   [0, Mz/2], T kx) and the z half-shift phases are staged in shared memory with cp.async
-//   while the forward FFT's first stage streams X2 in.  One shared buffer [L][W] holds the
-//   6T forward pencils, then (after the MAC has pulled its inputs into registers) the nf*2T
-//   output pencils, which are inverse-transformed together.
+//   One tile = T adjacent kx x the ky pair {q, My - q} (the two share every folded spectrum
+//   row, so each R element is read from HBM once).  Persistent, TMA-fed: each CTA walks tiles
+//   with stride gridDim.x.  A tile's inputs are contiguous by construction -- P2 writes X2
+//   tile-major ([q][tile][side][plane][t] per source) and the build stores R tile-major
+//   ([q][tile][block][kz'][t]) -- so one elected thread fetches the next tile with four
+//   cp.async.bulk copies (three sources + R) into the other half of a two-stage shared-memory
+//   ring while the CTA transforms the current one.  One buffer [L][W] holds the 6T forward
+//   pencils, then (after the MAC has pulled its inputs into registers) the NF*2T output
+//   pencils, which are inverse-transformed together.
 //   Phase algebra (App. B): out^a = phi_a sum_b R^{ab} phibar_b Q^b.  Along z, c_x = c_y = 1/2
 //   and c_z = 0, so phi_a,z phibar_b,z is 1 for a, b both in {x, y} or both z, phi_z-bar for
 //   (a = z, b in {x, y}) and phi_z for (a in {x, y}, b = z): one complex multiply per source
 //   (Q^z) and one per z-field, instead of one per (field, source).  The parity sign of the
 //   odd E blocks and the factor i are common to all sources of a field and applied once.
+//   (A warp-register variant -- one lane group per pencil, four-step FFT in registers -- was
+//   measured at 1.7x this kernel's time on C4: ~230 registers/thread capped residency at one
+//   CTA per SM.)
 // ---------------------------------------------------------------------------------------
-template <int L, int NFW>
+template <int L, int NF>
 struct P3T {
-    static constexpr int T = clampi(256 / L, 1, 16) * (NFW == 3 ? 2 : 1);
-    static constexpr int W = (NFW == 3 ? 6 : 12) * T;  // buffer width (pencils)
+    static constexpr int T = clampi(256 / L, 1, 16) * (NF <= 3 ? 2 : 1);
+    static constexpr int W = (NF <= 3 ? 6 : 2 * NF) * T;  // buffer width (pencils)
 };
+// host mirror of P3T<L, NF>::T (the tile width also fixes the X2 / R tiled layouts)
+inline int p3_tile(int Mz, int nf) { return clampi(256 / Mz, 1, 16) * (nf <= 3 ? 2 : 1); }
 
-template <int L, int NFW>
+template <int L, int NF>
 __global__ void __launch_bounds__(kNT3) k_p3(MV mv) {
-    constexpr int T = P3T<L, NFW>::T;
-    constexpr int W = P3T<L, NFW>::W;
+    constexpr int T = P3T<L, NF>::T;
+    constexpr int W = P3T<L, NF>::W;
     constexpr int T2 = 2 * T;
     constexpr int KZ = L / 2 + 1;
     constexpr int NI = (L * T2 + kNT3 - 1) / kNT3;  // MAC items per thread
-    extern __shared__ double2 sm[];
-    double2* buf = sm;                               // [L][W]
-    double2* ph = buf + L * W;                       // [L] exp(-i pi kt / L)
-    double* rs = reinterpret_cast<double*>(ph + L);  // [nblk][KZ][T]
-    int* zmap = reinterpret_cast<int*>(rs + mv.nblk * KZ * T);  // [9][L] plane -> index / -1
-    const int Kx = mv.Kx, My = mv.My, nf = mv.nf;
+    extern __shared__ __align__(16) double2 sm[];
+    const int Kx = mv.Kx, My = mv.My;
+    const int nz0 = mv.nzin[0], nz1 = mv.nzin[1], nz2 = mv.nzin[2];
+    const int XS = T2 * (nz0 + nz1 + nz2);          // double2 per stage
+    const int RC = mv.rchunk;                       // doubles per stage (even)
+    double2* buf = sm;                              // [L][W] transform buffer
+    double2* ph = buf + L * W;                      // [L] exp(-i pi kt / L)
+    double2* xin = ph + L;                          // [2][XS] staged X2 tiles
+    double* rin = reinterpret_cast<double*>(xin + 2 * XS);  // [2][RC] staged R tiles
+    int* zmap = reinterpret_cast<int*>(rin + 2 * RC);       // [9][L] plane -> index / -1
+    uint64_t* bar = reinterpret_cast<uint64_t*>(zmap + 9 * L);  // [2]
+    __shared__ int fmeta[NF][4];                    // kind | alpha << 1, R offsets of b0..b2
+    const int xo1 = T2 * nz0, xo2 = T2 * (nz0 + nz1);
     const int ntile = (Kx + T - 1) / T;
-    const int q = blockIdx.x / ntile, tile = blockIdx.x % ntile;
-    const int nside = (q == 0 || 2 * q == My) ? 1 : 2;
-    // stage the R tile (async) and the phase table
-    {
-        const int nr = mv.nblk * KZ * T;
-        for (int e = threadIdx.x; e < nr; e += kNT3) {
-            const int t = e % T, kzp = (e / T) % KZ, b = e / (T * KZ);
-            const int kx = tile * T + t;
-            if (kx < Kx)
-                cp_async8(rs + e, mv.Rt + (size_t)b * mv.blk_stride + ((size_t)q * KZ + kzp) * Kx + kx);
-            else
-                rs[e] = 0.0;
-        }
-        for (int k = threadIdx.x; k < L; k += kNT3) ph[k] = half_phase(mv.tw, ktil(k, L), L, -1);
-        for (int e = threadIdx.x; e < 9 * L; e += kNT3) {
-            const int g = e / L, z = e % L;
-            zmap[e] = z < mv.ZL ? mv.planes[(9 + g) * mv.ZL + z] : -1;
-        }
+    const int ntiles = ntile * (My / 2 + 1);
+    if (threadIdx.x == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        fence_mbar_init();
+    }
+    if (threadIdx.x < NF) {
+        const int f = threadIdx.x;
+        fmeta[f][0] = mv.fkind[f] | (mv.faxis[f] << 1);
+        for (int b = 0; b < 3; ++b) fmeta[f][1 + b] = mv.blk[f][b] < 0 ? -1 : mv.blk[f][b] * KZ * T;
+    }
+    for (int k = threadIdx.x; k < L; k += kNT3) ph[k] = half_phase(mv.tw, ktil(k, L), L, -1);
+    for (int e = threadIdx.x; e < 9 * L; e += kNT3) {
+        const int g = e / L, z = e % L;
+        zmap[e] = z < mv.ZL ? mv.planes[(9 + g) * mv.ZL + z] : -1;
     }
     __syncthreads();
-    // forward z-FFT of pencils pp = beta * 2T + side * T + t
-    auto ld0 = [&](int pp, int n) -> double2 {
-        const int t = pp % T, side = (pp / T) & 1, beta = pp / T2;
-        const int kx = tile * T + t;
-        const int jz = zmap[beta * L + n];
-        if (side >= nside || kx >= Kx || jz < 0) return czero();
-        const int ky = side ? My - q : q;
-        return mv.X2[beta][((int64_t)jz * My + ky) * Kx + kx];
+    auto issue = [&](int tl, int s) {  // one thread: fetch tile tl = q * ntile + tile into stage s
+        const size_t qt = (size_t)tl;
+        mbar_arrive_expect_tx(&bar[s], (unsigned)(16 * XS + 8 * RC));
+        if (nz0) bulk_g2s(xin + s * XS, mv.X2[0] + qt * T2 * nz0, 16u * T2 * nz0, &bar[s]);
+        if (nz1) bulk_g2s(xin + s * XS + xo1, mv.X2[1] + qt * T2 * nz1, 16u * T2 * nz1, &bar[s]);
+        if (nz2) bulk_g2s(xin + s * XS + xo2, mv.X2[2] + qt * T2 * nz2, 16u * T2 * nz2, &bar[s]);
+        bulk_g2s(rin + s * RC, mv.Rt + qt * RC, 8u * RC, &bar[s]);
     };
-    auto sti = [&](int pp, int p, double2 v) { buf[p * W + pp] = v; };
-    fft_run<L, W, kNT3, false, true>(buf, ld0, sti, mv.tw, 3 * T2);
-    cp_async_wait_all();
-    __syncthreads();
-    // MAC: item u = k * 2T + c (c = side * T + t); inputs to registers, then outputs in place
-    double2 qv[NI][3];
-#pragma unroll
-    for (int ii = 0; ii < NI; ++ii) {
-        const int u = threadIdx.x + ii * kNT3;
-        if (u < L * T2) {
-            const int k = u / T2, c = u % T2;
-            const double2* row = buf + Plan<L>::pos(k) * W + c;
-            qv[ii][0] = row[0];
-            qv[ii][1] = row[T2];
-            qv[ii][2] = row[2 * T2];
+    if (threadIdx.x == 0 && (int)blockIdx.x < ntiles) issue(blockIdx.x, 0);
+    unsigned par0 = 0, par1 = 0;
+    int it = 0;
+    for (int tl = blockIdx.x; tl < ntiles; tl += gridDim.x, ++it) {
+        const int s = it & 1;
+        if (threadIdx.x == 0 && tl + (int)gridDim.x < ntiles) {
+            fence_proxy_async();
+            issue(tl + gridDim.x, s ^ 1);
         }
-    }
-    __syncthreads();
+        if (s == 0) { mbar_wait(&bar[0], par0); par0 ^= 1; }
+        else { mbar_wait(&bar[1], par1); par1 ^= 1; }
+        const double2* xs = xin + s * XS;
+        const double* rs = rin + s * RC;
+        const int q = tl / ntile, tile = tl % ntile;
+        const int nside = (q == 0 || 2 * q == My) ? 1 : 2;
+        // forward z-FFT of pencils pp = beta * 2T + side * T + t (zero-padded to L)
+        auto ld0 = [&](int pp, int n) -> double2 {
+            const int t = pp % T, side = (pp / T) & 1, beta = pp / T2;
+            const int jz = zmap[beta * L + n];
+            if (side >= nside || tile * T + t >= Kx || jz < 0) return czero();
+            const int nzb = beta == 0 ? nz0 : (beta == 1 ? nz1 : nz2);
+            const int xo = beta == 0 ? 0 : (beta == 1 ? xo1 : xo2);
+            return xs[xo + (side * nzb + jz) * T + t];
+        };
+        auto sti = [&](int pp, int p, double2 v) { buf[p * W + pp] = v; };
+        fft_run<L, W, kNT3, false, true>(buf, ld0, sti, mv.tw, 3 * T2);
+        __syncthreads();
+        // MAC: item u = k * 2T + c (c = side * T + t); inputs to registers, outputs in place
+        double2 qv[NI][3];
 #pragma unroll
-    for (int ii = 0; ii < NI; ++ii) {
-        const int u = threadIdx.x + ii * kNT3;
-        if (u >= L * T2) break;
-        const int k = u / T2, c = u % T2;
-        const int side = c / T, t = c % T;
-        const int kt = ktil(k, L);
-        const int kzp = kt < 0 ? -kt : kt;
-        const double2 phb = ph[k];           // phibar_z = exp(-i pi kt / L)
-        const double2 qx = qv[ii][0], qy = qv[ii][1];
-        const double2 qz = cmulc(qv[ii][2], phb);  // phi_z Q^z
-        const double* rrow = rs + kzp * T + t;
-        double2* orow = buf + k * W + c;
-        for (int f = 0; f < nf; ++f) {
-            const int kind = mv.fkind[f], alpha = mv.faxis[f];
-            const int b0 = mv.blk[f][0], b1 = mv.blk[f][1], b2 = mv.blk[f][2];
-            double2 a = czero();
-            if (side < nside) {
-                if (b0 >= 0) {
-                    const double r = rrow[b0 * KZ * T];
+        for (int ii = 0; ii < NI; ++ii) {
+            const int u = threadIdx.x + ii * kNT3;
+            if (u < L * T2) {
+                const int k = u / T2, c = u % T2;
+                const double2* row = buf + Plan<L>::pos(k) * W + c;
+                qv[ii][0] = row[0];
+                qv[ii][1] = row[T2];
+                qv[ii][2] = row[2 * T2];
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int ii = 0; ii < NI; ++ii) {
+            const int u = threadIdx.x + ii * kNT3;
+            if (u >= L * T2) break;
+            const int k = u / T2, c = u % T2;
+            const int side = c / T, t = c % T;
+            const int kt = ktil(k, L);
+            const int kzp = kt < 0 ? -kt : kt;
+            const double2 phb = ph[k];                 // phibar_z = exp(-i pi kt / L)
+            const double2 qx = qv[ii][0], qy = qv[ii][1];
+            const double2 qz = cmulc(qv[ii][2], phb);  // phi_z Q^z
+            const double* rrow = rs + kzp * T + t;
+            double2* orow = buf + k * W + c;
+            const bool live = side < nside;
+#pragma unroll
+            for (int f = 0; f < NF; ++f) {
+                const int km = fmeta[f][0], o0 = fmeta[f][1], o1 = fmeta[f][2], o2 = fmeta[f][3];
+                const int kind = km & 1, alpha = km >> 1;
+                // out = phibar_z^[a = z] * (R^{a x} Qx + R^{a y} Qy + R^{a z} phi_z Qz)
+                double2 a = czero();
+                if (o0 >= 0) {
+                    const double r = rrow[o0];
                     a.x = fma(r, qx.x, a.x);
                     a.y = fma(r, qx.y, a.y);
                 }
-                if (b1 >= 0) {
-                    const double r = rrow[b1 * KZ * T];
+                if (o1 >= 0) {
+                    const double r = rrow[o1];
                     a.x = fma(r, qy.x, a.x);
                     a.y = fma(r, qy.y, a.y);
                 }
-                if (alpha == 2) {
-                    a = cmul(a, phb);  // (a = z, b in {x, y}): phibar_z
-                    if (b2 >= 0) {
-                        const double r = rrow[b2 * KZ * T];
-                        a.x = fma(r, qv[ii][2].x, a.x);
-                        a.y = fma(r, qv[ii][2].y, a.y);
-                    }
-                } else if (b2 >= 0) {  // (a in {x, y}, b = z): phi_z, folded into qz
-                    const double r = rrow[b2 * KZ * T];
+                if (o2 >= 0) {
+                    const double r = rrow[o2];
                     a.x = fma(r, qz.x, a.x);
                     a.y = fma(r, qz.y, a.y);
                 }
+                if (alpha == 2) a = cmul(a, phb);
                 if (kind == 1) {
                     // E blocks: R stores Im(K), odd along alpha; sign from the octant fold
                     const bool neg = (alpha == 1 && side == 1) || (alpha == 2 && kt < 0);
                     a = neg ? make_double2(a.y, -a.x) : make_double2(-a.y, a.x);
                 }
+                orow[f * T2] = live ? a : czero();
             }
-            orow[f * T2] = a;
         }
+        __syncthreads();
+        auto ldo = [&](int pp, int n) { return buf[n * W + pp]; };
+        auto sto = [&](int pp, int p, double2 v) {
+            const int f = pp / T2, c = pp % T2;
+            const int side = c / T, t = c % T;
+            const int kx = tile * T + t;
+            const int jz = zmap[(3 + f) * L + Plan<L>::freq(p)];
+            if (side < nside && kx < Kx && jz >= 0)
+                mv.X3[f][((int64_t)jz * My + (side ? My - q : q)) * Kx + kx] = v;
+        };
+        fft_run<L, W, kNT3, true, true>(buf, ldo, sto, mv.tw, NF * T2);
+        __syncthreads();
     }
-    __syncthreads();
-    auto ldo = [&](int pp, int n) { return buf[n * W + pp]; };
-    auto sto = [&](int pp, int p, double2 v) {
-        const int f = pp / T2, c = pp % T2;
-        const int side = c / T, t = c % T;
-        const int kx = tile * T + t;
-        const int jz = zmap[(3 + f) * L + Plan<L>::freq(p)];
-        if (side < nside && kx < Kx && jz >= 0)
-            mv.X3[f][((int64_t)jz * My + (side ? My - q : q)) * Kx + kx] = v;
-    };
-    fft_run<L, W, kNT3, true, true>(buf, ldo, sto, mv.tw, nf * T2);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -500,11 +536,15 @@ __global__ void __launch_bounds__(kNT) k_fft_strided(double2* data, int64_t es, 
     fft_run<L, T, kNT, false, true>(sm, ld0, stN, tw);
 }
 
-// R[ky'][kz'][kx] = {Re | Im}(K^(kx,ky',kz') exp(-2 pi i k.(c_a - c_b)/M)) * scale
+// Folded spectrum of block `blk`, tile-major for P3:
+//   R[(ky' * nt3 + kx / T3) * RC + blk * KZ * T3 + kz' * T3 + kx % T3]
+//     = {Re | Im}(K^(kx, ky', kz') exp(-2 pi i k.(c_a - c_b) / M)) * scale
 __global__ void k_extract(const double2* __restrict__ G, double* __restrict__ R, int Mx, int My,
                           int Mz, int Kx, int kind, int alpha, int beta, double scale,
-                          const double2* __restrict__ tw) {
+                          const double2* __restrict__ tw, int blk, int lgT3, int RC) {
     const int KY = My / 2 + 1, KZ = Mz / 2 + 1;
+    const int T3 = 1 << lgT3;
+    const int nt3 = (Kx + T3 - 1) >> lgT3;
     const int64_t tot = (int64_t)Kx * KY * KZ;
     const int s2x = c2(alpha, 0) - c2(beta, 0), s2y = c2(alpha, 1) - c2(beta, 1),
               s2z = c2(alpha, 2) - c2(beta, 2);
@@ -517,7 +557,8 @@ __global__ void k_extract(const double2* __restrict__ G, double* __restrict__ R,
         v = cmul(v, half_phase(tw, kx * s2x, Mx, -1));
         v = cmul(v, half_phase(tw, ky * s2y, My, -1));
         v = cmul(v, half_phase(tw, kz * s2z, Mz, -1));
-        R[idx] = (kind == 0 ? v.x : v.y) * scale;
+        R[((int64_t)ky * nt3 + (kx >> lgT3)) * RC + ((int64_t)blk * KZ + kz) * T3 + (kx & (T3 - 1))] =
+            (kind == 0 ? v.x : v.y) * scale;
     }
 }
 
@@ -584,31 +625,56 @@ static cudaError_t launch_p2(const MV& mv, cudaStream_t st) {
     });
     return cudaGetLastError();
 }
-template <int L, int NFW>
+template <int L, int NF>
+static size_t p3_smem(const MV& mv) {
+    constexpr int W = P3T<L, NF>::W, T = P3T<L, NF>::T;
+    const size_t XS = (size_t)2 * T * (mv.nzin[0] + mv.nzin[1] + mv.nzin[2]);
+    return sizeof(double2) * ((size_t)L * W + L + 2 * XS) + sizeof(double) * 2 * (size_t)mv.rchunk +
+           sizeof(int) * 9 * L + 2 * sizeof(uint64_t);
+}
+template <int L, int NF>
 static cudaError_t launch_p3_t(const MV& mv, cudaStream_t st) {
-    constexpr int T = P3T<L, NFW>::T, W = P3T<L, NFW>::W;
-    const size_t smem = sizeof(double2) * ((size_t)L * W + L) +
-                        sizeof(double) * (size_t)mv.nblk * (L / 2 + 1) * T + sizeof(int) * 9 * L;
+    constexpr int T = P3T<L, NF>::T;
+    const size_t smem = p3_smem<L, NF>(mv);
     if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
-    cudaError_t e = prep(k_p3<L, NFW>, smem);
+    cudaError_t e = prep(k_p3<L, NF>, smem);
     if (e) return e;
-    dim3 grid(((mv.Kx + T - 1) / T) * (mv.My / 2 + 1));
-    k_p3<L, NFW><<<grid, kNT3, smem, st>>>(mv);
+    int per_sm = 0, nsm = 0, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_p3<L, NF>, kNT3, smem);
+    const int ntiles = ((mv.Kx + T - 1) / T) * (mv.My / 2 + 1);
+    const int grid = std::max(1, std::min(ntiles, std::max(1, per_sm) * nsm));
+    k_p3<L, NF><<<grid, kNT3, smem, st>>>(mv);
     return cudaSuccess;
+}
+template <int L>
+static cudaError_t launch_p3_l(const MV& mv, cudaStream_t st) {
+    switch (mv.nf) {
+        case 1: return launch_p3_t<L, 1>(mv, st);
+        case 2: return launch_p3_t<L, 2>(mv, st);
+        case 3: return launch_p3_t<L, 3>(mv, st);
+        case 4: return launch_p3_t<L, 4>(mv, st);
+        case 5: return launch_p3_t<L, 5>(mv, st);
+        case 6: return launch_p3_t<L, 6>(mv, st);
+        default: return cudaErrorInvalidValue;
+    }
 }
 static cudaError_t launch_p3(const MV& mv, cudaStream_t st) {
     cudaError_t e;
     switch (mv.Mz) {  // kMaxLz: the [L][W] pencil buffer must fit one CTA's shared memory
-#define VC_P3_CASE(LL) \
-        case LL: e = mv.nf <= 3 ? launch_p3_t<LL, 3>(mv, st) : launch_p3_t<LL, 6>(mv, st); break;
-        VC_P3_CASE(8) VC_P3_CASE(16) VC_P3_CASE(32) VC_P3_CASE(64) VC_P3_CASE(128)
-        VC_P3_CASE(256) VC_P3_CASE(512)
-#undef VC_P3_CASE
+        case 8: e = launch_p3_l<8>(mv, st); break;
+        case 16: e = launch_p3_l<16>(mv, st); break;
+        case 32: e = launch_p3_l<32>(mv, st); break;
+        case 64: e = launch_p3_l<64>(mv, st); break;
+        case 128: e = launch_p3_l<128>(mv, st); break;
+        case 256: e = launch_p3_l<256>(mv, st); break;
         default: return cudaErrorInvalidValue;
     }
     if (e) return e;
     return cudaGetLastError();
 }
+
 static cudaError_t launch_p4(const MV& mv, cudaStream_t st) {
     int maxz = 0;
     for (int f = 0; f < mv.nf; ++f) maxz = std::max(maxz, mv.nzout[f]);
@@ -725,7 +791,7 @@ vc_status operator_build(vc_ctx* c, const vc_build_opts* o) {
         }
         if (M[t] > kMaxL) return set_err(c, VC_ERR_UNSUPPORTED, "padded FFT size > 4096 along an axis");
         if (t == 2 && M[t] > kMaxLz)
-            return set_err(c, VC_ERR_UNSUPPORTED, "padded FFT size along z > 512 (P3 pencil buffer)");
+            return set_err(c, VC_ERR_UNSUPPORTED, "padded FFT size along z > 256 (P3 shared-memory pencils)");
     }
     for (int t = 0; t < 3; ++t) {
         c->M[t] = M[t];
@@ -777,10 +843,15 @@ vc_status operator_build(vc_ctx* c, const vc_build_opts* o) {
         for (int b = 0; b < 3; ++b) c->blk[f][b] = -1;
     c->nblk = (int)defs.size();
     c->blk_stride = (size_t)Kx * (My / 2 + 1) * (Mz / 2 + 1);
+    // P3 tile width and the tile-major spectrum layout (one contiguous chunk per P3 tile)
+    c->T3 = p3_tile(Mz, c->nf);
+    c->nt3 = (Kx + c->T3 - 1) / c->T3;
+    c->rchunk = ((size_t)std::max(1, c->nblk) * (Mz / 2 + 1) * c->T3 + 1) & ~(size_t)1;
     VC_CUDA(c, c->tw.alloc(kTabN));
     k_twiddles<<<(kTabN + 255) / 256, 256, 0, st>>>(c->tw.p);
     count_launch(c);
-    VC_CUDA(c, c->Rt.alloc(c->blk_stride * std::max(1, c->nblk)));
+    VC_CUDA(c, c->Rt.alloc(c->rchunk * (size_t)(My / 2 + 1) * c->nt3));
+    VC_CUDA(c, cudaMemsetAsync(c->Rt.p, 0, c->Rt.bytes(), st));
     // spectra (a2 on the parity octant -> full cyclic grid -> 3-D FFT -> phase strip + fold)
     {
         cudaEvent_t ev[4];
@@ -809,8 +880,9 @@ vc_status operator_build(vc_ctx* c, const vc_build_opts* o) {
             VC_CUDA(c, launch_fft_strided(G.p, M[2], (int64_t)M[0] * M[1], (int64_t)M[0] * M[1], 1, 0, c->tw.p, st));
             VC_CUDA(c, cudaEventRecord(ev[2], st));
             const int eblocks = (int)std::min<int64_t>((c->blk_stride + 255) / 256, 148 * 32);
-            k_extract<<<eblocks, 256, 0, st>>>(G.p, c->Rt.p + c->blk_stride * i, M[0], M[1], M[2],
-                                               Kx, d.kind, d.alpha, d.beta, 1.0, c->tw.p);
+            k_extract<<<eblocks, 256, 0, st>>>(G.p, c->Rt.p, M[0], M[1], M[2], Kx, d.kind, d.alpha,
+                                               d.beta, 1.0, c->tw.p, i, ilog2c(c->T3),
+                                               (int)c->rchunk);
             VC_CUDA(c, cudaEventRecord(ev[3], st));
             count_launch(c, 6);
             VC_CUDA(c, cudaEventSynchronize(ev[3]));
@@ -858,12 +930,13 @@ vc_status operator_build(vc_ctx* c, const vc_build_opts* o) {
         VC_CUDA(c, cudaStreamSynchronize(st));
     }
     // pass buffers: A holds X1 (P1->P2) and later X4 (P4->P5); B holds X2; C holds X3
-    size_t nA_in = 0, nA_out = 0, nB = 0, nC = 0;
+    size_t nA_in = 0, nA_out = 0, nB = 0, nC = 0, nBt = 0;
     for (int b = 0; b < 3; ++b) {
         c->offA_in[b] = nA_in;
-        c->offB[b] = nB;
+        c->offB[b] = nBt;
         nA_in += (size_t)c->nzin[b] * c->ext_in[b][1] * Kx;
-        nB += (size_t)c->nzin[b] * My * Kx;
+        nB += (size_t)c->nzin[b] * My * Kx;  // algorithmic
+        nBt += (size_t)(My / 2 + 1) * c->nt3 * 2 * c->nzin[b] * c->T3;  // tile-major, padded
     }
     for (int f = 0; f < c->nf; ++f) {
         c->offC[f] = nC;
@@ -872,7 +945,7 @@ vc_status operator_build(vc_ctx* c, const vc_build_opts* o) {
         nA_out += (size_t)c->nzout[f] * c->f[f].ext[1] * Kx;
     }
     VC_CUDA(c, c->bufA.alloc(std::max<size_t>(1, std::max(nA_in, nA_out))));
-    VC_CUDA(c, c->bufB.alloc(std::max<size_t>(1, nB)));
+    VC_CUDA(c, c->bufB.alloc(std::max<size_t>(1, nBt)));
     VC_CUDA(c, c->bufC.alloc(std::max<size_t>(1, nC)));
     // algorithmic bytes per pass: complex128 reads + writes of the pass
     // arrays, kernel spectra read once, panel vectors and slot maps once.
@@ -928,7 +1001,9 @@ static MV make_mv(vc_ctx* c, const double* x, double* y) {
     mv.info = c->pan.info.p;
     mv.ibar = c->pan.ibar.p;
     mv.Rt = c->Rt.p;
-    mv.blk_stride = c->blk_stride;
+    mv.rchunk = (int)c->rchunk;
+    mv.T3 = c->T3;
+    mv.lgT3 = ilog2c(c->T3);
     mv.nblk = c->nblk;
     mv.tw = c->tw.p;
     mv.planes = c->planes.p;

@@ -1,4 +1,5 @@
 # quick GPU check: parity tests (subset by -k expression $1) + a short bench line
 K=${1:-"matvec or fft or kernel or capacitance or precond or solve"}
-timeout 900 python -m pytest tests -m gpu -x -q -k "$K" > gpurun_out/gpu_tests.log 2>&1; echo "tests rc=$?" >> gpurun_out/gpu_tests.log
+timeout 120 python -m pytest tests -m gpu -x -q -k "dense_parity and R1" > gpurun_out/gpu_first.log 2>&1 || { echo "first rc=$?" >> gpurun_out/gpu_first.log; exit 1; }
+timeout 600 python -m pytest tests -m gpu -x -q -k "$K" > gpurun_out/gpu_tests.log 2>&1; echo "tests rc=$?" >> gpurun_out/gpu_tests.log
 timeout 600 python bench.py --steps 2 --warmup 3 --no-cpu-baseline ${BENCH_ARGS} > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench.log

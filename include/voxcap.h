@@ -99,12 +99,42 @@ typedef struct {
     double  ms_kgen;        /* last build: kernel-entry generation (octant + fill)           */
     double  ms_kfft;        /* last build: 3-D FFT of the kernels + phase strip / fold        */
     double  ms_geometry;    /* last vc_set_geometry (panel indexing), device time            */
-    int64_t reserved[5];
+    double  ms_comm;        /* all-to-all time inside matvecs (world > 1, timing_detail = 1)  */
+    int64_t reserved[4];
 } vc_stats;
 
 /* Create a context on CUDA device `cuda_device`.  `cuda_stream` is a cudaStream_t to order
  * work on, or NULL for a stream owned by the context.  *out receives the context. */
 vc_status vc_create(vc_ctx** out, int cuda_device, void* cuda_stream);
+
+/* ---- Multi-GPU (one context per rank and GPU) -------------------------------
+ * The padded FFT grid is split in slabs: rank r owns a contiguous range of preconditioner box
+ * rows along y for the spatial passes (scatter + x-FFT, x-IFFT + gather, preconditioner, Krylov
+ * vectors) and a contiguous range of kx tiles for the spectral passes (y- and z-FFTs, kernel
+ * MAC, kernel spectra).  Each matvec does two all-to-all transposes; GMRES dot products and the
+ * capacitance columns are summed over ranks.
+ *
+ * vc_init_distributed: join a group of `world` (1..8) ranks as rank `rank`; call after
+ *   vc_create and before vc_set_geometry.  transport 0 = NCCL (one process per GPU): comm_id
+ *   points to the 128-byte ncclUniqueId that rank 0 drew with vc_nccl_unique_id and the caller
+ *   broadcast (libnccl.so.2 is loaded at this call; VC_ERR_NCCL if it cannot be).  transport 1 =
+ *   in-process thread group: comm_id is the handle from vc_group_create(world); each of the
+ *   `world` contexts must then be driven by its own host thread, making the same calls in the
+ *   same order (collective calls: vc_set_geometry, vc_build_operator, vc_matvec, vc_solve,
+ *   vc_solve_capacitance).  Every rank passes the whole voxel structure to vc_set_geometry.
+ * With world > 1, the vectors of vc_matvec / vc_precond / vc_solve are this rank's LOCAL panels
+ * (canonical order restricted to the rank; see vc_get_local_panels); vc_get_sizes and
+ * vc_get_panels stay global, and vc_solve_capacitance returns the full matrix on every rank. */
+vc_status vc_init_distributed(vc_ctx* ctx, int32_t rank, int32_t world, int32_t transport,
+                              const void* comm_id);
+/* Draw an NCCL unique id (128 bytes) into out; VC_ERR_NCCL if libnccl cannot be loaded. */
+vc_status vc_nccl_unique_id(void* out);
+/* In-process thread group of `world` ranks (transport 1); destroy after all its contexts. */
+vc_status vc_group_create(int32_t world, void** group);
+void vc_group_destroy(void* group);
+/* After vc_build_operator: number of panels this rank owns and (if global_index != NULL) their
+ * global canonical indices, ascending.  world = 1: all panels. */
+vc_status vc_get_local_panels(const vc_ctx* ctx, int64_t* n_local, int64_t* global_index);
 
 /* Voxel structure (§II.A; §II.B grids).  Copies label[nz*ny*nx] (int32) and eps_r
  * [nz*ny*nx] (float64, relative permittivity of non-conductor voxels; NULL = all 1.0; values
@@ -138,7 +168,8 @@ vc_status vc_build_operator(vc_ctx* ctx, const vc_build_opts* opts);
 /* FFT grid chosen by vc_build_operator (M_x, M_y, M_z). */
 vc_status vc_get_grid(const vc_ctx* ctx, int32_t* m3);
 
-/* y = ([0; Ī] + [P; E]) x   (Eq. 4; Eqs. 9-11).  x, y: N doubles. */
+/* y = ([0; Ī] + [P; E]) x   (Eq. 4; Eqs. 9-11).  x, y: N doubles (world > 1:
+ * this rank's n_local entries). */
 vc_status vc_matvec(vc_ctx* ctx, const double* x, double* y, int32_t on_device);
 
 /* z = R r with R the preconditioner chosen at build time (Eq. 14). */

@@ -16,7 +16,7 @@ import os
 import numpy as np
 
 __all__ = ["VoxCap", "VoxCapError", "lib_path", "load_library", "EXPORTS", "BuildOpts",
-           "SolveOpts", "SolveInfo", "Stats"]
+           "SolveOpts", "SolveInfo", "Stats", "ThreadGroup", "nccl_unique_id"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_NAME = "libvoxcap.so"
@@ -25,7 +25,8 @@ _LIB_NAME = "libvoxcap.so"
 EXPORTS = ("vc_create", "vc_set_geometry", "vc_get_sizes", "vc_get_panels", "vc_build_operator",
            "vc_get_grid", "vc_matvec", "vc_precond", "vc_solve", "vc_solve_capacitance",
            "vc_set_timing", "vc_get_stats", "vc_reset_stats", "vc_debug_kernel_entries",
-           "vc_debug_fft", "vc_last_error", "vc_version", "vc_destroy")
+           "vc_debug_fft", "vc_last_error", "vc_version", "vc_destroy", "vc_init_distributed",
+           "vc_nccl_unique_id", "vc_group_create", "vc_group_destroy", "vc_get_local_panels")
 
 STATUS = {0: "VC_OK", 1: "VC_ERR_INPUT", 2: "VC_ERR_STATE", 3: "VC_ERR_OOM", 4: "VC_ERR_CUDA",
           5: "VC_ERR_NCCL", 6: "VC_NOT_CONVERGED", 7: "VC_ERR_UNSUPPORTED"}
@@ -64,7 +65,7 @@ class Stats(ctypes.Structure):
                 ("ms_setup", ctypes.c_double), ("ms_precond_build", ctypes.c_double),
                 ("gpu_launches", ctypes.c_int64), ("ms_kgen", ctypes.c_double),
                 ("ms_kfft", ctypes.c_double), ("ms_geometry", ctypes.c_double),
-                ("reserved", ctypes.c_int64 * 5)]
+                ("ms_comm", ctypes.c_double), ("reserved", ctypes.c_int64 * 4)]
 
     def as_dict(self):
         return {"n_matvec": self.n_matvec, "ms_matvec": self.ms_matvec,
@@ -72,7 +73,8 @@ class Stats(ctypes.Structure):
                 "bytes_pass": list(self.bytes_pass), "bytes_matvec": self.bytes_matvec,
                 "ms_setup": self.ms_setup, "ms_precond_build": self.ms_precond_build,
                 "gpu_launches": self.gpu_launches, "ms_kgen": self.ms_kgen,
-                "ms_kfft": self.ms_kfft, "ms_geometry": self.ms_geometry}
+                "ms_kfft": self.ms_kfft, "ms_geometry": self.ms_geometry,
+                "ms_comm": self.ms_comm}
 
 
 def lib_path():
@@ -113,6 +115,10 @@ def load_library(build_if_missing=False):
         "vc_reset_stats": [vp],
         "vc_debug_kernel_entries": [vp, i32, vp, vp, vp, vp, vp],
         "vc_debug_fft": [vp, i32, i32, vp, i32],
+        "vc_init_distributed": [vp, i32, i32, i32, vp],
+        "vc_nccl_unique_id": [vp],
+        "vc_group_create": [i32, P(vp)],
+        "vc_get_local_panels": [vp, P(i64), vp],
     }
     for name, args in sig.items():
         f = getattr(lib, name)
@@ -124,6 +130,8 @@ def load_library(build_if_missing=False):
     lib.vc_version.restype = ctypes.c_char_p
     lib.vc_destroy.argtypes = [vp]
     lib.vc_destroy.restype = None
+    lib.vc_group_destroy.argtypes = [vp]
+    lib.vc_group_destroy.restype = None
     _lib = lib
     return lib
 
@@ -134,6 +142,33 @@ def _ptr(a):
 
 def _is_cuda_tensor(a):
     return hasattr(a, "is_cuda") and a.is_cuda
+
+
+def nccl_unique_id():
+    """128-byte NCCL unique id (rank 0 draws it; the caller broadcasts it)."""
+    buf = (ctypes.c_uint8 * 128)()
+    st = load_library().vc_nccl_unique_id(buf)
+    if st != 0:
+        raise VoxCapError(st, "vc_nccl_unique_id failed (libnccl.so.2 not loadable?)")
+    return bytes(buf)
+
+
+class ThreadGroup:
+    """In-process group of `world` ranks (transport 1): each member context must be driven by its
+    own Python thread (ctypes releases the GIL during library calls)."""
+
+    def __init__(self, world):
+        self._lib = load_library()
+        self.world = int(world)
+        self.handle = ctypes.c_void_p()
+        st = self._lib.vc_group_create(self.world, ctypes.byref(self.handle))
+        if st != 0:
+            raise VoxCapError(st, "vc_group_create failed")
+
+    def close(self):
+        if self.handle.value:
+            self._lib.vc_group_destroy(self.handle)
+            self.handle = ctypes.c_void_p()
 
 
 class VoxCap:
@@ -187,6 +222,27 @@ class VoxCap:
     @staticmethod
     def version():
         return load_library().vc_version().decode()
+
+    # -- distribution --------------------------------------------------------------------
+    def init_distributed(self, rank, world, nccl_id=None, group=None):
+        """Join a group of `world` ranks: NCCL (nccl_id = 128 bytes from nccl_unique_id(), one
+        process per GPU) or an in-process ThreadGroup."""
+        if group is not None:
+            st = self._lib.vc_init_distributed(self._ctx, int(rank), int(world), 1, group.handle)
+        else:
+            buf = (ctypes.c_uint8 * 128).from_buffer_copy(bytes(nccl_id))
+            st = self._lib.vc_init_distributed(self._ctx, int(rank), int(world), 0, buf)
+        self._check(st)
+        self.rank, self.world = int(rank), int(world)
+        return self
+
+    def local_panels(self):
+        """Global canonical indices of this rank's panels (the layout of local vectors)."""
+        n = ctypes.c_int64()
+        self._check(self._lib.vc_get_local_panels(self._ctx, ctypes.byref(n), None))
+        out = np.empty(n.value, np.int64)
+        self._check(self._lib.vc_get_local_panels(self._ctx, ctypes.byref(n), _ptr(out)))
+        return out
 
     # -- geometry ------------------------------------------------------------------------
     def set_geometry(self, label, eps=None, eps_out=1.0, dv=1e-6):

@@ -51,10 +51,22 @@ struct Field {
 };
 
 struct Precond;  // precond.cu
+struct Comm;     // comm.cu
+
+constexpr int kMaxRanks = 8;  // one NVLink box
+
+// This rank's panels (canonical order restricted to the rank) and its slot maps
+struct PanelsLocal {
+    DevBuf<int8_t> info;
+    DevBuf<double> ibar, fc;
+    DevBuf<int32_t> cid;
+    DevBuf<int32_t> slotmap[3];  // slot -> local index or -1 (only own rows are looked up)
+    DevBuf<int64_t> gidx;        // local -> global index
+};
 
 struct Timing {
     bool detail = false;
-    cudaEvent_t ev[12] = {};
+    cudaEvent_t ev[16] = {};
     bool ev_ok = false;
 };
 
@@ -62,6 +74,9 @@ struct Timing {
 
 struct vc_ctx {
     int device = 0;
+    // ---- distribution (vc_init_distributed; world = 1 otherwise) ----
+    int rank = 0, world = 1;
+    vc::Comm* comm = nullptr;
     cudaStream_t stream = nullptr;
     bool own_stream = false;
     std::string err;
@@ -93,14 +108,28 @@ struct vc_ctx {
     vc::DevBuf<double> Rt;  // folded, phase-stripped, scaled kernel spectra
     vc::DevBuf<double2> tw;  // twiddles exp(-2 pi i n / kTabN)
     vc::DevBuf<double2> bufA, bufB, bufC;  // X1/X4, X2, X3
-    size_t offA_in[3], offB[3], offC[6], offA_out[6];
+    size_t offB[3], offC[6];
     int T3 = 1, nt3 = 1;   // P3 tile width and kx-tile count (tile-major X2 / R layouts)
     size_t rchunk = 0;     // doubles of R per P3 tile
     int ZL = 0, nzin[3] = {0, 0, 0}, nzout[6] = {0, 0, 0, 0, 0, 0};  // active z-plane counts
     vc::DevBuf<int32_t> planes;  // plane lists + inverse maps (operator.cu)
     double bytes_pass[5] = {0, 0, 0, 0, 0};
     int precond_kind = 3;
+    int box[3] = {10, 10, 10};
     vc::Precond* pc = nullptr;
+    // partition (operator_build): window-relative row slabs and kx slabs of every rank
+    int ya[vc::kMaxRanks + 1] = {}, kxa[vc::kMaxRanks + 1] = {};
+    int nr[vc::kMaxRanks][9] = {};  // rows of rank p for source b (0..2) / field f (3 + f)
+    int64_t NL = 0;                 // panels owned by this rank
+    int own_Nv = 10, own_nb = 1, own_b0 = 0, own_nbr = 1;  // box-row ownership (row_owner_abs)
+    vc::PanelsLocal lp;
+    std::vector<int64_t> h_gidx;    // local -> global
+    vc::DevBuf<double2> bufS;       // all-to-all send blocks (peers only)
+    std::vector<const void*> a2a_send[2];
+    std::vector<void*> a2a_recv[2];
+    std::vector<size_t> a2a_sb[2], a2a_rb[2];
+    size_t offS1[vc::kMaxRanks][3] = {}, offR1[vc::kMaxRanks][3] = {};
+    size_t offS2[vc::kMaxRanks][6] = {}, offR2[vc::kMaxRanks][6] = {};
 
     // ---- solver work ----
     vc::DevBuf<double> work;  // Krylov basis + temporaries
@@ -141,5 +170,16 @@ vc_status capacitance_dev(vc_ctx* c, double* h_C, const vc_solve_opts* o, vc_sol
 vc_status debug_kernel_entries(vc_ctx* c, int n, const int32_t* kind, const int32_t* a,
                                const int32_t* b, const int32_t* d, double* out);
 vc_status debug_fft(vc_ctx* c, int L, int nl, double* data, int dir);
+vc_status partition_build(vc_ctx* c);  // operator.cu: slabs, local panels, local slot maps
+int row_owner_abs(const vc_ctx* c, int yabs);
+// comm.cu
+vc_status comm_nccl_unique_id(void* out, std::string& err);
+void* group_create(int world);
+void group_destroy(void* g);
+vc_status comm_init(vc_ctx* c, int rank, int world, int transport, const void* id);
+void comm_free(vc_ctx* c);
+vc_status comm_alltoall(vc_ctx* c, const std::vector<const void*>& send, const std::vector<size_t>& sb,
+                        const std::vector<void*>& recv, const std::vector<size_t>& rb);
+vc_status comm_allreduce(vc_ctx* c, double* d, int n);
 inline void count_launch(vc_ctx* c, int k = 1) { c->stats.gpu_launches += k; }
 }  // namespace vc

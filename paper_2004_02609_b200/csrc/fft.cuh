@@ -121,7 +121,9 @@ __device__ __forceinline__ void reg_dft(double2 (&v)[R]) {
 //   PF = true : consecutive lanes take consecutive pencils (strided-axis passes)
 //   PF = false: consecutive lanes take consecutive butterflies of one pencil (contiguous lines)
 //   Tn (<= T): pencils actually transformed (the shared-memory layout keeps stride T)
-template <int L, int T, int NT, bool INV, bool PF, int s, class LD, class ST>
+//   TB > 0 (PF only): Tn is a multiple of the compile-time pencil block TB; lanes take
+//       consecutive pencils within a block, so no division by the run-time Tn is needed
+template <int L, int T, int NT, bool INV, bool PF, int s, int TB = 0, class LD, class ST>
 __device__ __forceinline__ void fft_stage(LD&& ld, ST&& st, const double2* __restrict__ tw,
                                           const int Tn = T) {
     constexpr int R = Plan<L>::radix(s);
@@ -131,8 +133,15 @@ __device__ __forceinline__ void fft_stage(LD&& ld, ST&& st, const double2* __res
     const int NB = Tn * (L / R);
 #pragma unroll 1
     for (int u = threadIdx.x; u < NB; u += NT) {
-        const int t = PF ? u % Tn : u / (L / R);
-        const int rest = PF ? u / Tn : u % (L / R);
+        int t, rest;
+        if constexpr (PF && TB > 0) {
+            const int v = u / TB;
+            rest = v % (L / R);
+            t = (v / (L / R)) * TB + u % TB;
+        } else {
+            t = PF ? u % Tn : u / (L / R);
+            rest = PF ? u / Tn : u % (L / R);
+        }
         const int b = rest % S;
         const int g = rest / S;
         const int base = g * Lc + b;
@@ -170,25 +179,25 @@ __device__ __forceinline__ int smi(int t, int p) { return PF ? p * T + t : t * L
 // Full transform: stage 0 reads through `ld0`, the last stage writes through `stN`, and the
 // intermediate stages use shared memory `sm` (layout smi<L,T,PF>).  If NS == 1 the single
 // stage goes ld0 -> stN.  No trailing __syncthreads().
-template <int L, int T, int NT, bool INV, bool PF, class LD, class ST>
+template <int L, int T, int NT, bool INV, bool PF, int TB = 0, class LD, class ST>
 __device__ __forceinline__ void fft_run(double2* sm, LD&& ld0, ST&& stN,
                                         const double2* __restrict__ tw, const int Tn = T) {
     constexpr int NS = Plan<L>::NS;
     auto lds = [&](int t, int p) { return sm[smi<L, T, PF>(t, p)]; };
     auto sts = [&](int t, int p, double2 v) { sm[smi<L, T, PF>(t, p)] = v; };
     if constexpr (NS == 1) {
-        fft_stage<L, T, NT, INV, PF, 0>(ld0, stN, tw, Tn);
+        fft_stage<L, T, NT, INV, PF, 0, TB>(ld0, stN, tw, Tn);
     } else if constexpr (NS == 2) {
-        fft_stage<L, T, NT, INV, PF, 0>(ld0, sts, tw, Tn);
+        fft_stage<L, T, NT, INV, PF, 0, TB>(ld0, sts, tw, Tn);
         __syncthreads();
-        fft_stage<L, T, NT, INV, PF, 1>(lds, stN, tw, Tn);
+        fft_stage<L, T, NT, INV, PF, 1, TB>(lds, stN, tw, Tn);
     } else {
         static_assert(NS == 3, "L <= 4096");
-        fft_stage<L, T, NT, INV, PF, 0>(ld0, sts, tw, Tn);
+        fft_stage<L, T, NT, INV, PF, 0, TB>(ld0, sts, tw, Tn);
         __syncthreads();
-        fft_stage<L, T, NT, INV, PF, 1>(lds, sts, tw, Tn);
+        fft_stage<L, T, NT, INV, PF, 1, TB>(lds, sts, tw, Tn);
         __syncthreads();
-        fft_stage<L, T, NT, INV, PF, 2>(lds, stN, tw, Tn);
+        fft_stage<L, T, NT, INV, PF, 2, TB>(lds, stN, tw, Tn);
     }
 }
 

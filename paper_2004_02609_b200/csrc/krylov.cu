@@ -158,14 +158,16 @@ struct Krylov {
         x = b + n;
         return VC_OK;
     }
-    // out[0..nv) = V[0..nv) . vec
-    void dots(const double* Vb, int nv, const double* vec, double* out) {
+    // out[0..nv) = V[0..nv) . vec, summed over ranks (world > 1)
+    vc_status dots(const double* Vb, int nv, const double* vec, double* out) {
         k_multidot<<<kRedBlocks, kRedNT, 0, c->stream>>>(Vb, n, nv, vec, n, c->partial.p);
         k_reduce_partials<<<1, kMaxBasis, 0, c->stream>>>(c->partial.p, kRedBlocks, nv, out);
         count_launch(c, 2);
+        return comm_allreduce(c, out, nv);
     }
     vc_status norm2_host(const double* vec, double* out) {
-        dots(vec, 1, vec, c->dvec.p);
+        vc_status s = dots(vec, 1, vec, c->dvec.p);
+        if (s) return s;
         VC_CUDA(c, cudaMemcpyAsync(c->h_pinned, c->dvec.p, 8, cudaMemcpyDeviceToHost, c->stream));
         VC_CUDA(c, cudaStreamSynchronize(c->stream));
         *out = std::sqrt(c->h_pinned[0]);
@@ -185,11 +187,11 @@ vc_status solve_dev(vc_ctx* c, const double* d_b, double* d_x, const vc_solve_op
     const int restart = (o && o->restart > 0) ? std::min(o->restart, kMaxBasis - 1) : 35;
     const int maxit = (o && o->maxit > 0) ? o->maxit : 2000;
     const bool guess = o && o->x0_is_guess;
-    Krylov K{c, c->N};
+    Krylov K{c, c->NL};
     vc_status s = K.ensure(restart);
     if (s) return s;
     cudaStream_t st = c->stream;
-    const int64_t n = c->N;
+    const int64_t n = c->NL;
     const unsigned gn = grid_for(n);
     VC_CUDA(c, cudaMemcpyAsync(K.b, d_b, 8 * n, cudaMemcpyDeviceToDevice, st));
     if (guess) VC_CUDA(c, cudaMemcpyAsync(K.x, d_x, 8 * n, cudaMemcpyDeviceToDevice, st));
@@ -236,11 +238,11 @@ vc_status solve_dev(vc_ctx* c, const double* d_b, double* d_x, const vc_solve_op
             ++iters;
             double* dh = c->dvec.p;
             // CGS2: h = V^T t; t -= V h; h2 = V^T t; t -= V h2; ||t||^2
-            K.dots(K.V, j + 1, K.t, dh);
+            if ((s = K.dots(K.V, j + 1, K.t, dh))) return s;
             k_multiaxpy<<<gn, 256, 0, st>>>(K.t, K.V, n, j + 1, dh, n, -1.0);
-            K.dots(K.V, j + 1, K.t, dh + kMaxBasis);
+            if ((s = K.dots(K.V, j + 1, K.t, dh + kMaxBasis))) return s;
             k_multiaxpy<<<gn, 256, 0, st>>>(K.t, K.V, n, j + 1, dh + kMaxBasis, n, -1.0);
-            K.dots(K.t, 1, K.t, dh + 2 * kMaxBasis);
+            if ((s = K.dots(K.t, 1, K.t, dh + 2 * kMaxBasis))) return s;
             k_scale_by_norm<<<gn, 256, 0, st>>>(vn, K.t, dh + 2 * kMaxBasis, n);
             count_launch(c, 3);
             VC_CUDA(c, cudaMemcpyAsync(c->h_pinned, dh, 8 * 3 * kMaxBasis, cudaMemcpyDeviceToHost, st));
@@ -297,8 +299,10 @@ vc_status solve_dev(vc_ctx* c, const double* d_b, double* d_x, const vc_solve_op
 
 vc_status capacitance_dev(vc_ctx* c, double* h_C, const vc_solve_opts* o, vc_solve_info* info) {
     cudaStream_t st = c->stream;
-    const int64_t n = c->N;
+    const int64_t n = c->NL;
     const int m = c->m;
+    const int32_t* cid = c->world > 1 ? c->lp.cid.p : c->pan.cid.p;
+    const double* fc = c->world > 1 ? c->lp.fc.p : c->pan.fc.p;
     DevBuf<double> b, rho, part, col;
     VC_CUDA(c, b.alloc(n));
     VC_CUDA(c, rho.alloc(n));
@@ -309,7 +313,7 @@ vc_status capacitance_dev(vc_ctx* c, double* h_C, const vc_solve_opts* o, vc_sol
     const double area = c->dv * c->dv;
     vc_status worst = VC_OK;
     for (int j = 1; j <= m; ++j) {
-        k_rhs<<<grid_for(n), 256, 0, st>>>(b.p, c->pan.cid.p, j, area, n);
+        k_rhs<<<grid_for(n), 256, 0, st>>>(b.p, cid, j, area, n);
         count_launch(c);
         vc_solve_info inf{};
         vc_status s = solve_dev(c, b.p, rho.p, o, &inf);
@@ -317,9 +321,10 @@ vc_status capacitance_dev(vc_ctx* c, double* h_C, const vc_solve_opts* o, vc_sol
         if (s == VC_NOT_CONVERGED) worst = s;
         if (info) info[j - 1] = inf;
         dim3 g(nb, m);
-        k_cap_partial<<<g, kRedNT, 0, st>>>(rho.p, c->pan.cid.p, c->pan.fc.p, area, n, m, part.p);
+        k_cap_partial<<<g, kRedNT, 0, st>>>(rho.p, cid, fc, area, n, m, part.p);
         k_cap_final<<<1, std::max(32, ((m + 31) / 32) * 32), 0, st>>>(part.p, nb, m, col.p);
         count_launch(c, 2);
+        if ((s = comm_allreduce(c, col.p, m))) return s;
         VC_CUDA(c, cudaMemcpyAsync(hp.data(), col.p, 8 * (size_t)m, cudaMemcpyDeviceToHost, st));
         VC_CUDA(c, cudaStreamSynchronize(st));
         for (int i = 0; i < m; ++i) h_C[(size_t)i * m + (j - 1)] = hp[i];

@@ -34,10 +34,20 @@ struct MV {
     double* y;
     const int8_t* info;
     const double* ibar;
-    double2* X1[3];
     double2* X2[3];
     double2* X3[6];
-    double2* X4[6];
+    // distribution: rank r owns window rows [ya[r], ya[r+1]) of the spatial
+    // passes (P1, P5) and kx columns [kxa[r], kxa[r+1]) of the spectral passes (P2-P4).  The
+    // x-transformed planes travel as blocks [source][plane][own rows][dest kx] (P1 -> P2) and
+    // [field][plane][dest rows][own kx] (P4 -> P5); the self block is written in place.
+    int W, rank;
+    int ya[kMaxRanks + 1], kxa[kMaxRanks + 1];
+    int nr[kMaxRanks][9];  // rows of rank p within source b's (0..2) / field f's (3+f) extent
+    int kx0, nkx;          // this rank's kx slab
+    double2* S1[kMaxRanks][3];
+    const double2* R1[kMaxRanks][3];
+    double2* S2[kMaxRanks][6];
+    const double2* R2[kMaxRanks][6];
     const double* Rt;       // tile-major: [q][kx-tile][block][kz'][t], rchunk doubles per tile
     int rchunk;
     int T3, lgT3;           // P3 tile width (power of two) and its log2
@@ -52,6 +62,17 @@ struct MV {
 };
 
 __device__ __forceinline__ int zlist(const MV& mv, int g, int j) { return mv.planes[g * mv.ZL + j]; }
+// rank owning window row y / kx column k (slabs are contiguous; W <= 8)
+__device__ __forceinline__ int row_owner(const MV& mv, int y) {
+    int p = 0;
+    while (y >= mv.ya[p + 1]) ++p;
+    return p;
+}
+__device__ __forceinline__ int kx_owner(const MV& mv, int k) {
+    int q = 0;
+    while (k >= mv.kxa[q + 1]) ++q;
+    return q;
+}
 
 // ---- tile-size choices (compile-time functions of the FFT length) -----------------------
 constexpr int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
@@ -71,26 +92,35 @@ __global__ void __launch_bounds__(kNT) k_p1(MV mv) {
     constexpr int T = TX<L>::T;
     extern __shared__ double2 sm[];
     const int beta = blockIdx.y;
-    const int ex = mv.ext_in[beta][0], ey = mv.ext_in[beta][1], ez = mv.ext_in[beta][2];
+    const int ex = mv.ext_in[beta][0];
     if (ex == 0) return;
-    const int nyp = (ey + 1) >> 1;
+    const int nrow = mv.nr[mv.rank][beta];  // own rows of this source grid
+    // rows are paired (two real lines per complex FFT) at absolute slot rows (2m, 2m + 1), so a
+    // slab split changes no pairing and the partitioned matvec stays bitwise equal (local row
+    // l = 2q - s is the real part, l + 1 the imaginary part)
+    const int s = (mv.lo[1] + mv.ya[mv.rank]) & 1;
+    const int nyp = (nrow + s + 1) >> 1;
     const int nch = (nyp + T - 1) / T;
+    if (nch == 0) return;
     const int j = blockIdx.x / nch, ch = blockIdx.x % nch;
     if (j >= mv.nzin[beta]) return;
     const int z = zlist(mv, beta, j);
-    (void)ez;
     const int32_t* __restrict__ smap = mv.slotmap[beta];
     const int Gx = mv.G[beta][0], Gy = mv.G[beta][1];
-    const int64_t zrow = ((int64_t)(z + mv.lo[2]) * Gy + mv.lo[1]) * Gx + mv.lo[0];
+    const int64_t zrow =
+        ((int64_t)(z + mv.lo[2]) * Gy + mv.lo[1] + mv.ya[mv.rank]) * Gx + mv.lo[0];
     const double* __restrict__ x = mv.x;
     auto ld0 = [&](int t, int n) -> double2 {
         const int q = ch * T + t;
         double re = 0.0, im = 0.0;
         if (q < nyp && n < ex) {
-            const int64_t r0 = zrow + (int64_t)(2 * q) * Gx + n;
-            const int p0 = smap[r0];
-            if (p0 >= 0) re = x[p0];
-            if (2 * q + 1 < ey) {
+            const int l0 = 2 * q - s;
+            const int64_t r0 = zrow + (int64_t)l0 * Gx + n;
+            if (l0 >= 0) {
+                const int p0 = smap[r0];
+                if (p0 >= 0) re = x[p0];
+            }
+            if (l0 + 1 < nrow) {
                 const int p1 = smap[r0 + Gx];
                 if (p1 >= 0) im = x[p1];
             }
@@ -102,7 +132,6 @@ __global__ void __launch_bounds__(kNT) k_p1(MV mv) {
     __syncthreads();
     constexpr int K = L / 2 + 1;
     const bool ph = beta != 0;  // c_beta,x = 1/2 for y- and z-normal panels
-    double2* __restrict__ out = mv.X1[beta] + (int64_t)j * ey * mv.Kx;
     for (int u = threadIdx.x; u < T * K; u += kNT) {
         const int t = u / K, k = u % K;
         const int q = ch * T + t;
@@ -116,8 +145,12 @@ __global__ void __launch_bounds__(kNT) k_p1(MV mv) {
             A = cmul(A, w);
             B = cmul(B, w);
         }
-        out[(int64_t)(2 * q) * mv.Kx + k] = A;
-        if (2 * q + 1 < ey) out[(int64_t)(2 * q + 1) * mv.Kx + k] = B;
+        const int qd = kx_owner(mv, k);
+        const int nk = mv.kxa[qd + 1] - mv.kxa[qd];
+        const int l0 = 2 * q - s;
+        double2* o = mv.S1[qd][beta] + ((int64_t)j * nrow + l0) * nk + (k - mv.kxa[qd]);
+        if (l0 >= 0) o[0] = A;
+        if (l0 + 1 < nrow) o[nk] = B;
     }
 }
 
@@ -131,23 +164,25 @@ __global__ void __launch_bounds__(kNT) k_p2(MV mv) {
     const int beta = blockIdx.y;
     const int ex = mv.ext_in[beta][0], ey = mv.ext_in[beta][1], ez = mv.ext_in[beta][2];
     if (ex == 0) return;
-    const int Kx = mv.Kx;
-    const int ntile = (Kx + T - 1) / T;
+    const int nkx = mv.nkx;  // own kx slab (local column kx)
+    const int ntile = (nkx + T - 1) / T;
+    if (ntile == 0) return;
     const int j = blockIdx.x / ntile, tile = blockIdx.x % ntile;
     if (j >= mv.nzin[beta]) return;
     (void)ez;
-    const double2* __restrict__ in = mv.X1[beta] + (int64_t)j * ey * Kx;
     // X2 tile-major for P3: [q][kx / T3][side][plane][kx % T3], q = |ky| (ky <= L/2: side 0)
     double2* __restrict__ out = mv.X2[beta];
-    const int nzb = mv.nzin[beta], nt3 = (Kx + mv.T3 - 1) >> mv.lgT3;
+    const int nzb = mv.nzin[beta], nt3 = (nkx + mv.T3 - 1) >> mv.lgT3;
     const bool ph = beta != 1;  // c_beta,y = 1/2 for x- and z-normal panels
     auto ld0 = [&](int t, int n) -> double2 {
         const int kx = tile * T + t;
-        return (n < ey && kx < Kx) ? in[(int64_t)n * Kx + kx] : czero();
+        if (n >= ey || kx >= nkx) return czero();
+        const int p = row_owner(mv, n);  // row n arrived from rank p
+        return mv.R1[p][beta][((int64_t)j * mv.nr[p][beta] + (n - mv.ya[p])) * nkx + kx];
     };
     auto stN = [&](int t, int p, double2 v) {
         const int kx = tile * T + t;
-        if (kx >= Kx) return;
+        if (kx >= nkx) return;
         const int k = Plan<L>::freq(p);
         if (ph) v = cmul(v, half_phase(mv.tw, ktil(k, L), L, -1));
         const int side = k > L / 2, qq = side ? L - k : k;
@@ -193,7 +228,7 @@ __global__ void __launch_bounds__(kNT3) k_p3(MV mv) {
     constexpr int KZ = L / 2 + 1;
     constexpr int NI = (L * T2 + kNT3 - 1) / kNT3;  // MAC items per thread
     extern __shared__ __align__(16) double2 sm[];
-    const int Kx = mv.Kx, My = mv.My;
+    const int Kx = mv.nkx, My = mv.My;  // own kx slab
     const int nz0 = mv.nzin[0], nz1 = mv.nzin[1], nz2 = mv.nzin[2];
     const int XS = T2 * (nz0 + nz1 + nz2);          // double2 per stage
     const int RC = mv.rchunk;                       // doubles per stage (even)
@@ -341,26 +376,28 @@ __global__ void __launch_bounds__(kNT) k_p4(MV mv) {
     const int f = blockIdx.y;
     if (f >= mv.nf) return;
     const int alpha = mv.faxis[f];
-    const int eyo = mv.ext_out[f][1], ezo = mv.ext_out[f][2];
-    const int Kx = mv.Kx;
-    const int ntile = (Kx + T - 1) / T;
+    const int eyo = mv.ext_out[f][1];
+    const int nkx = mv.nkx;
+    const int ntile = (nkx + T - 1) / T;
+    if (ntile == 0) return;
     const int j = blockIdx.x / ntile, tile = blockIdx.x % ntile;
     if (j >= mv.nzout[f]) return;
-    (void)ezo;
-    const double2* __restrict__ in = mv.X3[f] + (int64_t)j * L * Kx;
-    double2* __restrict__ out = mv.X4[f] + (int64_t)j * eyo * Kx;
+    const double2* __restrict__ in = mv.X3[f] + (int64_t)j * L * nkx;
     const bool ph = alpha != 1;
     auto ld0 = [&](int t, int n) -> double2 {
         const int kx = tile * T + t;
-        if (kx >= Kx) return czero();
-        double2 v = in[(int64_t)n * Kx + kx];
+        if (kx >= nkx) return czero();
+        double2 v = in[(int64_t)n * nkx + kx];
         if (ph) v = cmul(v, half_phase(mv.tw, ktil(n, L), L, +1));
         return v;
     };
     auto stN = [&](int t, int p, double2 v) {
         const int kx = tile * T + t;
         const int yy = Plan<L>::freq(p);
-        if (kx < Kx && yy < eyo) out[(int64_t)yy * Kx + kx] = v;
+        if (kx < nkx && yy < eyo) {
+            const int pr = row_owner(mv, yy);  // row yy goes to rank pr for P5
+            mv.S2[pr][f][((int64_t)j * mv.nr[pr][3 + f] + (yy - mv.ya[pr])) * nkx + kx] = v;
+        }
     };
     fft_run<L, T, kNT, true, true>(sm, ld0, stN, mv.tw);
 }
@@ -375,18 +412,20 @@ __global__ void __launch_bounds__(kNT) k_p5(MV mv) {
     const int f = blockIdx.y;
     if (f >= mv.nf) return;
     const int kind = mv.fkind[f], alpha = mv.faxis[f];
-    const int exo = mv.ext_out[f][0], eyo = mv.ext_out[f][1], ezo = mv.ext_out[f][2];
-    const int nyp = (eyo + 1) >> 1;
+    const int exo = mv.ext_out[f][0];
+    const int nrow = mv.nr[mv.rank][3 + f];  // own rows of this field
+    const int s = (mv.lo[1] + mv.ya[mv.rank]) & 1;  // absolute row pairing, as in P1
+    const int nyp = (nrow + s + 1) >> 1;
     const int nch = (nyp + T - 1) / T;
+    if (nch == 0) return;
     const int j = blockIdx.x / nch, ch = blockIdx.x % nch;
     if (j >= mv.nzout[f]) return;
-    (void)ezo;
     const int z = zlist(mv, 3 + f, j);
-    const int Kx = mv.Kx;
-    const double2* __restrict__ in = mv.X4[f] + (int64_t)j * eyo * Kx;
     const bool ph = alpha != 0;
     auto At = [&](int yrow, int k) -> double2 {
-        double2 v = in[(int64_t)yrow * Kx + k];
+        const int qd = kx_owner(mv, k);  // column k arrived from rank qd
+        const int nk = mv.kxa[qd + 1] - mv.kxa[qd];
+        double2 v = mv.R2[qd][f][((int64_t)j * nrow + yrow) * nk + (k - mv.kxa[qd])];
         if (ph) v = cmul(v, half_phase(mv.tw, k, L, +1));
         if (k == 0 || 2 * k == L) v.y = 0.0;
         return v;
@@ -394,20 +433,22 @@ __global__ void __launch_bounds__(kNT) k_p5(MV mv) {
     auto ld0 = [&](int t, int n) -> double2 {
         const int q = ch * T + t;
         if (q >= nyp) return czero();
-        const bool has1 = 2 * q + 1 < eyo;
-        double2 A, B = czero();
+        const int l0 = 2 * q - s;
+        const bool has0 = l0 >= 0, has1 = l0 + 1 < nrow;
+        double2 A = czero(), B = czero();
         if (2 * n <= L) {
-            A = At(2 * q, n);
-            if (has1) B = At(2 * q + 1, n);
+            if (has0) A = At(l0, n);
+            if (has1) B = At(l0 + 1, n);
         } else {
-            A = cconj(At(2 * q, L - n));
-            if (has1) B = cconj(At(2 * q + 1, L - n));
+            if (has0) A = cconj(At(l0, L - n));
+            if (has1) B = cconj(At(l0 + 1, L - n));
         }
         return make_double2(A.x - B.y, A.y + B.x);
     };
     const int32_t* __restrict__ smap = mv.slotmap[alpha];
     const int Gx = mv.G[alpha][0], Gy = mv.G[alpha][1];
-    const int64_t zrow = ((int64_t)(z + mv.lo[2]) * Gy + mv.lo[1]) * Gx + mv.lo[0];
+    const int64_t zrow =
+        ((int64_t)(z + mv.lo[2]) * Gy + mv.lo[1] + mv.ya[mv.rank]) * Gx + mv.lo[0];
     auto put = [&](int p, double val) {
         const int inf = mv.info[p];
         if ((inf & 1) != kind) return;
@@ -418,10 +459,13 @@ __global__ void __launch_bounds__(kNT) k_p5(MV mv) {
         const int q = ch * T + t;
         const int n = Plan<L>::freq(p);
         if (q >= nyp || n >= exo) return;
-        const int64_t r0 = zrow + (int64_t)(2 * q) * Gx + n;
-        const int p0 = smap[r0];
-        if (p0 >= 0) put(p0, v.x);
-        if (2 * q + 1 < eyo) {
+        const int l0 = 2 * q - s;
+        const int64_t r0 = zrow + (int64_t)l0 * Gx + n;
+        if (l0 >= 0) {
+            const int p0 = smap[r0];
+            if (p0 >= 0) put(p0, v.x);
+        }
+        if (l0 + 1 < nrow) {
             const int p1 = smap[r0 + Gx];
             if (p1 >= 0) put(p1, v.y);
         }
@@ -539,12 +583,14 @@ __global__ void __launch_bounds__(kNT) k_fft_strided(double2* data, int64_t es, 
 // Folded spectrum of block `blk`, tile-major for P3:
 //   R[(ky' * nt3 + kx / T3) * RC + blk * KZ * T3 + kz' * T3 + kx % T3]
 //     = {Re | Im}(K^(kx, ky', kz') exp(-2 pi i k.(c_a - c_b) / M)) * scale
+//   (kx local to this rank's slab [kx0, kx0 + nkx))
 __global__ void k_extract(const double2* __restrict__ G, double* __restrict__ R, int Mx, int My,
-                          int Mz, int Kx, int kind, int alpha, int beta, double scale,
+                          int Mz, int kx0, int nkx, int kind, int alpha, int beta, double scale,
                           const double2* __restrict__ tw, int blk, int lgT3, int RC) {
     const int KY = My / 2 + 1, KZ = Mz / 2 + 1;
     const int T3 = 1 << lgT3;
-    const int nt3 = (Kx + T3 - 1) >> lgT3;
+    const int nt3 = (nkx + T3 - 1) >> lgT3;
+    const int Kx = nkx;
     const int64_t tot = (int64_t)Kx * KY * KZ;
     const int s2x = c2(alpha, 0) - c2(beta, 0), s2y = c2(alpha, 1) - c2(beta, 1),
               s2z = c2(alpha, 2) - c2(beta, 2);
@@ -553,8 +599,8 @@ __global__ void k_extract(const double2* __restrict__ G, double* __restrict__ R,
         const int kx = (int)(idx % Kx);
         const int kz = (int)((idx / Kx) % KZ);
         const int ky = (int)(idx / ((int64_t)Kx * KZ));
-        double2 v = G[((int64_t)kz * My + ky) * Mx + kx];
-        v = cmul(v, half_phase(tw, kx * s2x, Mx, -1));
+        double2 v = G[((int64_t)kz * My + ky) * Mx + kx0 + kx];
+        v = cmul(v, half_phase(tw, (kx0 + kx) * s2x, Mx, -1));
         v = cmul(v, half_phase(tw, ky * s2y, My, -1));
         v = cmul(v, half_phase(tw, kz * s2z, Mz, -1));
         R[((int64_t)ky * nt3 + (kx >> lgT3)) * RC + ((int64_t)blk * KZ + kz) * T3 + (kx & (T3 - 1))] =
@@ -603,7 +649,7 @@ static cudaError_t launch_p1(const MV& mv, cudaStream_t st) {
     for (int b = 0; b < 3; ++b) { maxz = std::max(maxz, mv.nzin[b]); }
     VC_DISPATCH_L(mv.Mx, {
         constexpr int T = TX<LL>::T;
-        for (int b = 0; b < 3; ++b) maxch = std::max(maxch, ((mv.ext_in[b][1] + 1) / 2 + T - 1) / T);
+        for (int b = 0; b < 3; ++b) maxch = std::max(maxch, ((mv.nr[mv.rank][b] + 2) / 2 + T - 1) / T);
         const size_t smem = sizeof(double2) * LL * T;
         cudaError_t e = prep(k_p1<LL>, smem);
         if (e) return e;
@@ -620,7 +666,7 @@ static cudaError_t launch_p2(const MV& mv, cudaStream_t st) {
         const size_t smem = sizeof(double2) * LL * T;
         cudaError_t e = prep(k_p2<LL>, smem);
         if (e) return e;
-        dim3 grid(std::max(1, ((mv.Kx + T - 1) / T) * maxz), 3);
+        dim3 grid(std::max(1, ((mv.nkx + T - 1) / T) * maxz), 3);
         k_p2<LL><<<grid, kNT, smem, st>>>(mv);
     });
     return cudaGetLastError();
@@ -643,7 +689,8 @@ static cudaError_t launch_p3_t(const MV& mv, cudaStream_t st) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_p3<L, NF>, kNT3, smem);
-    const int ntiles = ((mv.Kx + T - 1) / T) * (mv.My / 2 + 1);
+    const int ntiles = ((mv.nkx + T - 1) / T) * (mv.My / 2 + 1);
+    if (ntiles == 0) return cudaSuccess;
     const int grid = std::max(1, std::min(ntiles, std::max(1, per_sm) * nsm));
     k_p3<L, NF><<<grid, kNT3, smem, st>>>(mv);
     return cudaSuccess;
@@ -683,7 +730,7 @@ static cudaError_t launch_p4(const MV& mv, cudaStream_t st) {
         const size_t smem = sizeof(double2) * LL * T;
         cudaError_t e = prep(k_p4<LL>, smem);
         if (e) return e;
-        dim3 grid(std::max(1, ((mv.Kx + T - 1) / T) * maxz), mv.nf);
+        dim3 grid(std::max(1, ((mv.nkx + T - 1) / T) * maxz), mv.nf);
         k_p4<LL><<<grid, kNT, smem, st>>>(mv);
     });
     return cudaGetLastError();
@@ -693,7 +740,7 @@ static cudaError_t launch_p5(const MV& mv, cudaStream_t st) {
     for (int f = 0; f < mv.nf; ++f) maxz = std::max(maxz, mv.nzout[f]);
     VC_DISPATCH_L(mv.Mx, {
         constexpr int T = TX<LL>::T;
-        for (int f = 0; f < mv.nf; ++f) maxch = std::max(maxch, ((mv.ext_out[f][1] + 1) / 2 + T - 1) / T);
+        for (int f = 0; f < mv.nf; ++f) maxch = std::max(maxch, ((mv.nr[mv.rank][3 + f] + 2) / 2 + T - 1) / T);
         const size_t smem = sizeof(double2) * LL * T;
         cudaError_t e = prep(k_p5<LL>, smem);
         if (e) return e;
@@ -845,12 +892,18 @@ vc_status operator_build(vc_ctx* c, const vc_build_opts* o) {
     c->blk_stride = (size_t)Kx * (My / 2 + 1) * (Mz / 2 + 1);
     // P3 tile width and the tile-major spectrum layout (one contiguous chunk per P3 tile)
     c->T3 = p3_tile(Mz, c->nf);
-    c->nt3 = (Kx + c->T3 - 1) / c->T3;
+    {   // spectral partition: rank q owns kx tiles [q nt / W, (q + 1) nt / W) of width T3
+        const int W = c->world, nt = (Kx + c->T3 - 1) / c->T3;
+        for (int q = 0; q <= W; ++q) c->kxa[q] = std::min(Kx, (int)((int64_t)q * nt / W) * c->T3);
+        c->kxa[W] = Kx;
+    }
+    const int kx0 = c->kxa[c->rank], nkx = c->kxa[c->rank + 1] - kx0;
+    c->nt3 = (nkx + c->T3 - 1) / c->T3;
     c->rchunk = ((size_t)std::max(1, c->nblk) * (Mz / 2 + 1) * c->T3 + 1) & ~(size_t)1;
     VC_CUDA(c, c->tw.alloc(kTabN));
     k_twiddles<<<(kTabN + 255) / 256, 256, 0, st>>>(c->tw.p);
     count_launch(c);
-    VC_CUDA(c, c->Rt.alloc(c->rchunk * (size_t)(My / 2 + 1) * c->nt3));
+    VC_CUDA(c, c->Rt.alloc(std::max<size_t>(1, c->rchunk * (size_t)(My / 2 + 1) * c->nt3)));
     VC_CUDA(c, cudaMemsetAsync(c->Rt.p, 0, c->Rt.bytes(), st));
     // spectra (a2 on the parity octant -> full cyclic grid -> 3-D FFT -> phase strip + fold)
     {
@@ -879,8 +932,8 @@ vc_status operator_build(vc_ctx* c, const vc_build_opts* o) {
             VC_CUDA(c, launch_fft_strided(G.p, M[1], M[0], M[0], M[2], (int64_t)M[0] * M[1], c->tw.p, st));
             VC_CUDA(c, launch_fft_strided(G.p, M[2], (int64_t)M[0] * M[1], (int64_t)M[0] * M[1], 1, 0, c->tw.p, st));
             VC_CUDA(c, cudaEventRecord(ev[2], st));
-            const int eblocks = (int)std::min<int64_t>((c->blk_stride + 255) / 256, 148 * 32);
-            k_extract<<<eblocks, 256, 0, st>>>(G.p, c->Rt.p, M[0], M[1], M[2], Kx, d.kind, d.alpha,
+            const int eblocks = (int)std::max<int64_t>(1, std::min<int64_t>((c->blk_stride + 255) / 256, 148 * 32));
+            k_extract<<<eblocks, 256, 0, st>>>(G.p, c->Rt.p, M[0], M[1], M[2], kx0, nkx, d.kind, d.alpha,
                                                d.beta, 1.0, c->tw.p, i, ilog2c(c->T3),
                                                (int)c->rchunk);
             VC_CUDA(c, cudaEventRecord(ev[3], st));
@@ -929,42 +982,198 @@ vc_status operator_build(vc_ctx* c, const vc_build_opts* o) {
         VC_CUDA(c, cudaMemcpyAsync(c->planes.p, hp.data(), 4 * hp.size(), cudaMemcpyHostToDevice, st));
         VC_CUDA(c, cudaStreamSynchronize(st));
     }
-    // pass buffers: A holds X1 (P1->P2) and later X4 (P4->P5); B holds X2; C holds X3
-    size_t nA_in = 0, nA_out = 0, nB = 0, nC = 0, nBt = 0;
+    // ---- spatial partition: rank p owns a contiguous range of preconditioner
+    // box rows along y, so every R_BD block stays on one rank; window row y -> rank (monotone)
+    int EY = 1;
+    for (int b = 0; b < 3; ++b) EY = std::max(EY, c->ext_in[b][1]);
+    for (int f = 0; f < c->nf; ++f) EY = std::max(EY, c->f[f].ext[1]);
+    const int W = c->world, rk = c->rank;
+    {
+        const int Nv = c->box[1], nb = std::max(1, (c->ny + Nv - 1) / Nv);
+        c->own_Nv = Nv;
+        c->own_nb = nb;
+        c->own_b0 = std::min(lo[1] / Nv, nb - 1);
+        c->own_nbr = std::min((lo[1] + EY - 1) / Nv, nb - 1) - c->own_b0 + 1;
+        c->ya[0] = 0;
+        int p = 1;
+        for (int y = 0; y < EY && p < W; ++y)
+            while (p < W && row_owner_abs(c, lo[1] + y) >= p) c->ya[p++] = y;
+        for (; p <= W; ++p) c->ya[p] = EY;
+        for (int q = 0; q < W; ++q) {
+            auto cnt = [&](int e) { return std::max(0, std::min(c->ya[q + 1], e) - c->ya[q]); };
+            for (int b = 0; b < 3; ++b) c->nr[q][b] = cnt(c->ext_in[b][1]);
+            for (int f = 0; f < 6; ++f) c->nr[q][3 + f] = f < c->nf ? cnt(c->f[f].ext[1]) : 0;
+        }
+    }
+    // ---- pass buffers.  A: P1 -> P2 blocks [sender][source][plane][rows][own kx] (recv 1),
+    // later P4 -> P5 blocks [sender][field][plane][own rows][sender kx] (recv 2); S: blocks for
+    // peers (send 1, later send 2); B: X2 tile-major; C: X3.
+    auto nkxq = [&](int q) { return c->kxa[q + 1] - c->kxa[q]; };
+    size_t nR1 = 0, nR2 = 0, nS1 = 0, nS2 = 0, nBt = 0, nC = 0;
+    for (int p = 0; p < W; ++p)
+        for (int b = 0; b < 3; ++b) {
+            c->offR1[p][b] = nR1;
+            nR1 += (size_t)c->nzin[b] * c->nr[p][b] * nkx;
+        }
+    for (int q = 0; q < W; ++q)
+        for (int f = 0; f < c->nf; ++f) {
+            c->offR2[q][f] = nR2;
+            nR2 += (size_t)c->nzout[f] * c->nr[rk][3 + f] * nkxq(q);
+        }
+    for (int q = 0; q < W; ++q)
+        for (int b = 0; b < 3; ++b) {
+            c->offS1[q][b] = nS1;
+            if (q != rk) nS1 += (size_t)c->nzin[b] * c->nr[rk][b] * nkxq(q);
+        }
+    for (int p = 0; p < W; ++p)
+        for (int f = 0; f < c->nf; ++f) {
+            c->offS2[p][f] = nS2;
+            if (p != rk) nS2 += (size_t)c->nzout[f] * c->nr[p][3 + f] * nkx;
+        }
     for (int b = 0; b < 3; ++b) {
-        c->offA_in[b] = nA_in;
         c->offB[b] = nBt;
-        nA_in += (size_t)c->nzin[b] * c->ext_in[b][1] * Kx;
-        nB += (size_t)c->nzin[b] * My * Kx;  // algorithmic
         nBt += (size_t)(My / 2 + 1) * c->nt3 * 2 * c->nzin[b] * c->T3;  // tile-major, padded
     }
     for (int f = 0; f < c->nf; ++f) {
         c->offC[f] = nC;
-        c->offA_out[f] = nA_out;
-        nC += (size_t)c->nzout[f] * My * Kx;
-        nA_out += (size_t)c->nzout[f] * c->f[f].ext[1] * Kx;
+        nC += (size_t)c->nzout[f] * My * nkx;
     }
-    VC_CUDA(c, c->bufA.alloc(std::max<size_t>(1, std::max(nA_in, nA_out))));
+    VC_CUDA(c, c->bufA.alloc(std::max<size_t>(1, std::max(nR1, nR2))));
     VC_CUDA(c, c->bufB.alloc(std::max<size_t>(1, nBt)));
     VC_CUDA(c, c->bufC.alloc(std::max<size_t>(1, nC)));
-    // algorithmic bytes per pass: complex128 reads + writes of the pass
-    // arrays, kernel spectra read once, panel vectors and slot maps once.
+    c->bufS.reset();
+    if (W > 1) VC_CUDA(c, c->bufS.alloc(std::max<size_t>(1, std::max(nS1, nS2))));
+    // all-to-all block tables (bytes; the self block is written in place by P1 / P4)
+    for (int e = 0; e < 2; ++e) {
+        c->a2a_send[e].assign(W, nullptr);
+        c->a2a_recv[e].assign(W, nullptr);
+        c->a2a_sb[e].assign(W, 0);
+        c->a2a_rb[e].assign(W, 0);
+    }
+    for (int q = 0; q < W && W > 1; ++q) {
+        size_t s1 = 0, r1 = 0, s2 = 0, r2 = 0;
+        for (int b = 0; b < 3; ++b) {
+            s1 += (size_t)c->nzin[b] * c->nr[rk][b] * nkxq(q);
+            r1 += (size_t)c->nzin[b] * c->nr[q][b] * nkx;
+        }
+        for (int f = 0; f < c->nf; ++f) {
+            s2 += (size_t)c->nzout[f] * c->nr[q][3 + f] * nkx;
+            r2 += (size_t)c->nzout[f] * c->nr[rk][3 + f] * nkxq(q);
+        }
+        c->a2a_send[0][q] = c->bufS.p + c->offS1[q][0];
+        c->a2a_recv[0][q] = c->bufA.p + c->offR1[q][0];
+        c->a2a_send[1][q] = c->bufS.p + c->offS2[q][0];
+        c->a2a_recv[1][q] = c->bufA.p + (c->nf ? c->offR2[q][0] : 0);
+        if (q != rk) {
+            c->a2a_sb[0][q] = 16 * s1;
+            c->a2a_rb[0][q] = 16 * r1;
+            c->a2a_sb[1][q] = 16 * s2;
+            c->a2a_rb[1][q] = 16 * r2;
+        }
+    }
+    {
+        vc_status ps = partition_build(c);
+        if (ps != VC_OK) return ps;
+    }
+    // algorithmic bytes of this rank's share of each pass: complex128 reads +
+    // writes of the pass arrays, kernel spectra read once, panel vectors and slot maps once.
     const double cb = 16.0;
-    double slots = 0;
-    for (int b = 0; b < 3; ++b) slots += (double)c->ext_in[b][0] * c->ext_in[b][1] * c->nzin[b];
+    double slots = 0, nX1 = 0, nX1r = 0, nB = 0, nX4 = 0, nX4r = 0;
+    for (int b = 0; b < 3; ++b) {
+        slots += (double)c->ext_in[b][0] * c->nr[rk][b] * c->nzin[b];
+        nX1 += (double)c->nzin[b] * c->nr[rk][b] * Kx;         // P1 writes (own rows, all kx)
+        nX1r += (double)c->nzin[b] * c->ext_in[b][1] * nkx;    // P2 reads (all rows, own kx)
+        nB += (double)c->nzin[b] * My * nkx;
+    }
     double slots_out = 0;
-    for (int f = 0; f < c->nf; ++f) slots_out += (double)c->f[f].ext[0] * c->f[f].ext[1] * c->nzout[f];
-    c->bytes_pass[0] = cb * nA_in + 4.0 * slots + 8.0 * c->N;
-    c->bytes_pass[1] = cb * (nA_in + nB);
-    c->bytes_pass[2] = cb * (nB + nC) + 8.0 * c->blk_stride * c->nblk;
-    c->bytes_pass[3] = cb * (nC + nA_out);
-    c->bytes_pass[4] = cb * nA_out + 4.0 * slots_out + 8.0 * c->N + (8.0 + 8.0 + 1.0) * c->Nd + 1.0 * c->N;
+    for (int f = 0; f < c->nf; ++f) {
+        slots_out += (double)c->f[f].ext[0] * c->nr[rk][3 + f] * c->nzout[f];
+        nX4 += (double)c->nzout[f] * c->f[f].ext[1] * nkx;    // P4 writes
+        nX4r += (double)c->nzout[f] * c->nr[rk][3 + f] * Kx;  // P5 reads
+    }
+    const double NL = (double)c->NL;
+    double ndl = 0;
+    for (int64_t i = 0; i < c->NL; ++i) ndl += c->h_cid[W > 1 ? c->h_gidx[i] : i] == 0;
+    c->bytes_pass[0] = cb * nX1 + 4.0 * slots + 8.0 * NL;
+    c->bytes_pass[1] = cb * (nX1r + nB);
+    c->bytes_pass[2] = cb * (nB + (double)nC) + 8.0 * (double)nkx * (My / 2 + 1) * (Mz / 2 + 1) * c->nblk;
+    c->bytes_pass[3] = cb * ((double)nC + nX4);
+    c->bytes_pass[4] = cb * nX4r + 4.0 * slots_out + 8.0 * NL + (8.0 + 8.0 + 1.0) * ndl + 1.0 * NL;
     double tot = 0;
     for (int p = 0; p < 5; ++p) {
         c->stats.bytes_pass[p] = c->bytes_pass[p];
         tot += c->bytes_pass[p];
     }
     c->stats.bytes_matvec = tot;
+    return VC_OK;
+}
+
+// rank owning absolute slot row yabs (along y): by preconditioner box row, contiguous ranges
+int row_owner_abs(const vc_ctx* c, int yabs) {
+    const int br = std::min(std::max(yabs, 0) / c->own_Nv, c->own_nb - 1) - c->own_b0;
+    int p = 0;
+    while (p + 1 < c->world && (int64_t)(p + 1) * c->own_nbr / c->world <= br) ++p;
+    return p;
+}
+
+__global__ void k_local_panels(int64_t nl, const int64_t* __restrict__ gidx,
+                               const int8_t* __restrict__ info, const double* __restrict__ ibar,
+                               const double* __restrict__ fc, const int32_t* __restrict__ cid,
+                               const int8_t* __restrict__ axis, const int32_t* __restrict__ si,
+                               const int32_t* __restrict__ sj, const int32_t* __restrict__ sk,
+                               int8_t* __restrict__ linfo, double* __restrict__ libar,
+                               double* __restrict__ lfc, int32_t* __restrict__ lcid,
+                               int32_t* __restrict__ sm0, int32_t* __restrict__ sm1,
+                               int32_t* __restrict__ sm2, int nx, int ny) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nl;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t g = gidx[i];
+        linfo[i] = info[g];
+        libar[i] = ibar[g];
+        lfc[i] = fc[g];
+        lcid[i] = cid[g];
+        const int a = axis[g];
+        const int gx = nx + (a == 0), gy = ny + (a == 1);
+        int32_t* sm = a == 0 ? sm0 : (a == 1 ? sm1 : sm2);
+        sm[((int64_t)sk[g] * gy + sj[g]) * gx + si[g]] = (int32_t)i;
+    }
+}
+
+// This rank's panels: canonical order restricted to the panels whose slot row it owns, and
+// slot maps to local indices (world = 1: the global arrays are used as they are).
+vc_status partition_build(vc_ctx* c) {
+    c->h_gidx.clear();
+    if (c->world == 1) {
+        c->NL = c->N;
+        return VC_OK;
+    }
+    for (int64_t p = 0; p < c->N; ++p)
+        if (row_owner_abs(c, c->h_sj[p]) == c->rank) c->h_gidx.push_back(p);
+    c->NL = (int64_t)c->h_gidx.size();
+    const int64_t nl = c->NL;
+    cudaStream_t st = c->stream;
+    PanelsLocal& L = c->lp;
+    VC_CUDA(c, L.gidx.alloc(std::max<int64_t>(1, nl)));
+    VC_CUDA(c, L.info.alloc(std::max<int64_t>(1, nl)));
+    VC_CUDA(c, L.ibar.alloc(std::max<int64_t>(1, nl)));
+    VC_CUDA(c, L.fc.alloc(std::max<int64_t>(1, nl)));
+    VC_CUDA(c, L.cid.alloc(std::max<int64_t>(1, nl)));
+    for (int a = 0; a < 3; ++a) {
+        const size_t n = (size_t)(c->nx + (a == 0)) * (c->ny + (a == 1)) * (c->nz + (a == 2));
+        VC_CUDA(c, L.slotmap[a].alloc(n));
+        VC_CUDA(c, cudaMemsetAsync(L.slotmap[a].p, 0xff, 4 * n, st));
+    }
+    if (nl) {
+        VC_CUDA(c, cudaMemcpyAsync(L.gidx.p, c->h_gidx.data(), 8 * nl, cudaMemcpyHostToDevice, st));
+        const PanelsDev& P = c->pan;
+        k_local_panels<<<(unsigned)std::min<int64_t>((nl + 255) / 256, 148 * 8), 256, 0, st>>>(
+            nl, L.gidx.p, P.info.p, P.ibar.p, P.fc.p, P.cid.p, P.axis.p, P.si.p, P.sj.p, P.sk.p,
+            L.info.p, L.ibar.p, L.fc.p, L.cid.p, L.slotmap[0].p, L.slotmap[1].p, L.slotmap[2].p,
+            c->nx, c->ny);
+        count_launch(c);
+    }
+    VC_CUDA(c, cudaStreamSynchronize(st));
+    VC_CUDA(c, cudaGetLastError());
     return VC_OK;
 }
 
@@ -975,14 +1184,14 @@ static MV make_mv(vc_ctx* c, const double* x, double* y) {
     mv.My = c->M[1];
     mv.Mz = c->M[2];
     mv.Kx = c->Kx;
+    const bool loc = c->world > 1;
     for (int t = 0; t < 3; ++t) mv.lo[t] = c->lo[t];
     for (int a = 0; a < 3; ++a) {
         mv.G[a][0] = c->nx + (a == 0);
         mv.G[a][1] = c->ny + (a == 1);
         mv.G[a][2] = c->nz + (a == 2);
         for (int t = 0; t < 3; ++t) mv.ext_in[a][t] = c->ext_in[a][t];
-        mv.slotmap[a] = c->pan.slotmap[a].p;
-        mv.X1[a] = c->bufA.p + c->offA_in[a];
+        mv.slotmap[a] = loc ? c->lp.slotmap[a].p : c->pan.slotmap[a].p;
         mv.X2[a] = c->bufB.p + c->offB[a];
     }
     mv.nf = c->nf;
@@ -993,13 +1202,12 @@ static MV make_mv(vc_ctx* c, const double* x, double* y) {
             mv.faxis[f] = c->f[f].axis;
             for (int t = 0; t < 3; ++t) mv.ext_out[f][t] = c->f[f].ext[t];
             mv.X3[f] = c->bufC.p + c->offC[f];
-            mv.X4[f] = c->bufA.p + c->offA_out[f];
         }
     }
     mv.x = x;
     mv.y = y;
-    mv.info = c->pan.info.p;
-    mv.ibar = c->pan.ibar.p;
+    mv.info = loc ? c->lp.info.p : c->pan.info.p;
+    mv.ibar = loc ? c->lp.ibar.p : c->pan.ibar.p;
     mv.Rt = c->Rt.p;
     mv.rchunk = (int)c->rchunk;
     mv.T3 = c->T3;
@@ -1010,6 +1218,27 @@ static MV make_mv(vc_ctx* c, const double* x, double* y) {
     mv.ZL = c->ZL;
     for (int b = 0; b < 3; ++b) mv.nzin[b] = c->nzin[b];
     for (int f = 0; f < 6; ++f) mv.nzout[f] = f < c->nf ? c->nzout[f] : 0;
+    const int W = c->world, r = c->rank;
+    mv.W = W;
+    mv.rank = r;
+    for (int q = 0; q <= kMaxRanks; ++q) {
+        mv.ya[q] = q <= W ? c->ya[q] : INT32_MAX;
+        mv.kxa[q] = q <= W ? c->kxa[q] : INT32_MAX;
+    }
+    for (int q = 0; q < W; ++q)
+        for (int g = 0; g < 9; ++g) mv.nr[q][g] = c->nr[q][g];
+    mv.kx0 = c->kxa[r];
+    mv.nkx = c->kxa[r + 1] - c->kxa[r];
+    for (int q = 0; q < W; ++q) {
+        for (int b = 0; b < 3; ++b) {
+            mv.S1[q][b] = q == r ? c->bufA.p + c->offR1[r][b] : c->bufS.p + c->offS1[q][b];
+            mv.R1[q][b] = c->bufA.p + c->offR1[q][b];
+        }
+        for (int f = 0; f < c->nf; ++f) {
+            mv.S2[q][f] = q == r ? c->bufA.p + c->offR2[r][f] : c->bufS.p + c->offS2[q][f];
+            mv.R2[q][f] = c->bufA.p + c->offR2[q][f];
+        }
+    }
     return mv;
 }
 
@@ -1019,10 +1248,18 @@ vc_status matvec_dev(vc_ctx* c, const double* d_x, double* d_y) {
     Timing& T = c->timing;
     const bool det = T.detail && T.ev_ok;
     if (T.ev_ok) VC_CUDA(c, cudaEventRecord(T.ev[0], st));
-    k_zero<<<std::max<int64_t>(1, std::min<int64_t>((c->N + 255) / 256, 1184)), 256, 0, st>>>(d_y, c->N);
+    k_zero<<<std::max<int64_t>(1, std::min<int64_t>((c->NL + 255) / 256, 1184)), 256, 0, st>>>(d_y, c->NL);
     cudaError_t (*launch[5])(const MV&, cudaStream_t) = {launch_p1, launch_p2, launch_p3,
                                                          launch_p4, launch_p5};
     for (int p = 0; p < 5; ++p) {
+        if (c->world > 1 && (p == 1 || p == 4)) {
+            // x-transformed planes: rows -> kx slabs before P2, back before P5
+            const int e = p == 1 ? 0 : 1;
+            if (det) VC_CUDA(c, cudaEventRecord(T.ev[12 + e], st));
+            vc_status s = comm_alltoall(c, c->a2a_send[e], c->a2a_sb[e], c->a2a_recv[e], c->a2a_rb[e]);
+            if (s) return s;
+            if (det) VC_CUDA(c, cudaEventRecord(T.ev[14 + e], st));
+        }
         if (det) VC_CUDA(c, cudaEventRecord(T.ev[1 + p], st));
         VC_CUDA(c, launch[p](mv, st));
         if (det) VC_CUDA(c, cudaEventRecord(T.ev[6 + p], st));
@@ -1037,11 +1274,17 @@ vc_status matvec_dev(vc_ctx* c, const double* d_x, double* d_y) {
         float ms = 0;
         VC_CUDA(c, cudaEventElapsedTime(&ms, T.ev[0], T.ev[11]));
         c->stats.ms_matvec += ms;
-        if (det)
+        if (det) {
             for (int p = 0; p < 5; ++p) {
                 VC_CUDA(c, cudaEventElapsedTime(&ms, T.ev[1 + p], T.ev[6 + p]));
                 c->stats.ms_pass[p] += ms;
             }
+            if (c->world > 1)
+                for (int e = 0; e < 2; ++e) {
+                    VC_CUDA(c, cudaEventElapsedTime(&ms, T.ev[12 + e], T.ev[14 + e]));
+                    c->stats.ms_comm += ms;
+                }
+        }
     }
     return VC_OK;
 }

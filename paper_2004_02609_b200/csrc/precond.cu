@@ -132,19 +132,21 @@ vc_status precond_build(vc_ctx* c, const int32_t box_in[3], int kind) {
     c->pc = pc;
     pc->kind = kind;
     cudaStream_t st = c->stream;
-    const int64_t N = c->N;
+    const int64_t N = c->NL;  // this rank's panels (boxes never straddle ranks)
+    auto G = [&](int64_t i) { return c->world > 1 ? c->h_gidx[i] : i; };  // local -> global
     const double fpe = 4.0 * kPi * kEps0;
     const double pscale = c->dv * c->dv * c->dv / fpe;
     // diagonal part
     std::vector<double> dinv(N, 0.0);
     // self term of a unit square (textbook), used only for the diagonal-only option
     const double pself = pscale * ((4.0 / 3.0) * (1.0 - std::sqrt(2.0)) + 4.0 * std::log(1.0 + std::sqrt(2.0)));
-    for (int64_t p = 0; p < N; ++p) {
-        if (c->h_cid[p] == 0) dinv[p] = kind == 1 ? 1.0 : 1.0 / c->h_ibar[p];
-        else dinv[p] = kind == 1 ? 1.0 : (kind == 2 ? 1.0 / pself : 0.0);
+    for (int64_t i = 0; i < N; ++i) {
+        const int64_t p = G(i);
+        if (c->h_cid[p] == 0) dinv[i] = kind == 1 ? 1.0 : 1.0 / c->h_ibar[p];
+        else dinv[i] = kind == 1 ? 1.0 : (kind == 2 ? 1.0 / pself : 0.0);
     }
-    VC_CUDA(c, pc->diag_inv.alloc(N));
-    VC_CUDA(c, cudaMemcpyAsync(pc->diag_inv.p, dinv.data(), 8 * N, cudaMemcpyHostToDevice, st));
+    VC_CUDA(c, pc->diag_inv.alloc(std::max<int64_t>(1, N)));
+    if (N) VC_CUDA(c, cudaMemcpyAsync(pc->diag_inv.p, dinv.data(), 8 * N, cudaMemcpyHostToDevice, st));
     if (kind != 3) {
         VC_CUDA(c, cudaStreamSynchronize(st));
         return VC_OK;
@@ -159,13 +161,13 @@ vc_status precond_build(vc_ctx* c, const int32_t box_in[3], int kind) {
     std::vector<int64_t> pbox;
     std::vector<int32_t> cond;
     cond.reserve(c->Nc);
-    for (int64_t p = 0; p < N; ++p)
-        if (c->h_cid[p] > 0) cond.push_back((int32_t)p);
+    for (int64_t i = 0; i < N; ++i)
+        if (c->h_cid[G(i)] > 0) cond.push_back((int32_t)i);  // local indices
     std::unordered_map<int64_t, int32_t> box_index;
     std::vector<int64_t> box_keys;
     std::vector<int32_t> pb(cond.size());
     for (size_t q = 0; q < cond.size(); ++q) {
-        const int64_t p = cond[q];
+        const int64_t p = G(cond[q]);
         const int s[3] = {c->h_si[p], c->h_sj[p], c->h_sk[p]};
         int64_t bx[3];
         for (int a = 0; a < 3; ++a) bx[a] = std::min<int64_t>(s[a] / nv[a], nb[a] - 1);
@@ -196,7 +198,7 @@ vc_status precond_build(vc_ctx* c, const int32_t box_in[3], int kind) {
         std::vector<int32_t> sig;
         sig.reserve(4 * bcount[b]);
         for (int q = bstart[b]; q < bstart[b + 1]; ++q) {
-            const int p = sorted[q];
+            const int64_t p = G(sorted[q]);
             sig.push_back(c->h_axis[p]);
             sig.push_back(c->h_si[p] - org[0]);
             sig.push_back(c->h_sj[p] - org[1]);
@@ -268,7 +270,7 @@ vc_status precond_apply_dev(vc_ctx* c, const double* d_r, double* d_z) {
     Precond* pc = c->pc;
     if (!pc) return set_err(c, VC_ERR_STATE, "no preconditioner");
     cudaStream_t st = c->stream;
-    const int64_t N = c->N;
+    const int64_t N = c->NL;
     k_pc_diag<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((N + 255) / 256, 148 * 8)), 256, 0, st>>>(N, d_r, pc->diag_inv.p, d_z);
     count_launch(c);
     if (pc->kind == 3 && pc->nbox > 0) {

@@ -36,6 +36,15 @@ void drop_operator(vc_ctx* c) {
     c->bufA.reset();
     c->bufB.reset();
     c->bufC.reset();
+    c->bufS.reset();
+    c->lp.info.reset();
+    c->lp.ibar.reset();
+    c->lp.fc.reset();
+    c->lp.cid.reset();
+    c->lp.gidx.reset();
+    for (auto& s : c->lp.slotmap) s.reset();
+    c->h_gidx.clear();
+    c->NL = 0;
     c->work.reset();
     c->work_n = 0;
     precond_free(c);
@@ -58,7 +67,7 @@ template <class F>
 vc_status with_vectors(vc_ctx* c, const double* in, double* out, int on_device, bool copy_out_in,
                        F&& f) {
     if (on_device) return f(in, out);
-    const int64_t n = c->N;
+    const int64_t n = c->NL;
     DevBuf<double> din, dout;
     VC_CUDA(c, din.alloc(n));
     VC_CUDA(c, dout.alloc(n));
@@ -107,6 +116,7 @@ void vc_destroy(vc_ctx* c) {
         DeviceGuard g(c->device);
         cudaStreamSynchronize(c->stream);
         drop_geometry(c);
+        comm_free(c);
         c->tw.reset();
         c->partial.reset();
         c->dvec.reset();
@@ -223,6 +233,7 @@ vc_status vc_build_operator(vc_ctx* c, const vc_build_opts* o) {
             if (o->box[a] < 0) return set_err(c, VC_ERR_INPUT, "box must be >= 0");
             if (o->box[a] > 0) box[a] = o->box[a];
         }
+    for (int a = 0; a < 3; ++a) c->box[a] = box[a];
     cudaEvent_t e0, e1, e2;
     VC_CUDA(c, cudaEventCreate(&e0));
     VC_CUDA(c, cudaEventCreate(&e1));
@@ -346,6 +357,42 @@ vc_status vc_debug_fft(vc_ctx* c, int32_t L, int32_t n_lines, double* data, int3
     if (n_lines <= 0 || !data || (dir != 1 && dir != -1)) return set_err(c, VC_ERR_INPUT, "bad arguments");
     DeviceGuard g(c->device);
     return debug_fft(c, L, n_lines, data, dir);
+}
+
+vc_status vc_init_distributed(vc_ctx* c, int32_t rank, int32_t world, int32_t transport,
+                              const void* comm_id) {
+    VC_CHECK_CTX(c);
+    if (world < 1 || world > kMaxRanks || rank < 0 || rank >= world)
+        return set_err(c, VC_ERR_INPUT, "need 0 <= rank < world <= 8");
+    if (transport != 0 && transport != 1) return set_err(c, VC_ERR_INPUT, "transport must be 0 (NCCL) or 1 (threads)");
+    if (!comm_id) return set_err(c, VC_ERR_INPUT, "comm_id is NULL");
+    if (c->has_geom) return set_err(c, VC_ERR_STATE, "vc_init_distributed after vc_set_geometry");
+    if (c->comm) return set_err(c, VC_ERR_STATE, "already distributed");
+    DeviceGuard g(c->device);
+    return comm_init(c, rank, world, transport, comm_id);
+}
+
+vc_status vc_nccl_unique_id(void* out) {
+    if (!out) return VC_ERR_INPUT;
+    std::string err;
+    return comm_nccl_unique_id(out, err);
+}
+
+vc_status vc_group_create(int32_t world, void** group) {
+    if (!group || world < 1 || world > kMaxRanks) return VC_ERR_INPUT;
+    *group = group_create(world);
+    return *group ? VC_OK : VC_ERR_OOM;
+}
+
+void vc_group_destroy(void* group) { group_destroy(group); }
+
+vc_status vc_get_local_panels(const vc_ctx* c, int64_t* n_local, int64_t* global_index) {
+    if (!c) return VC_ERR_INPUT;
+    if (!c->has_op) return VC_ERR_STATE;
+    if (n_local) *n_local = c->NL;
+    if (global_index)
+        for (int64_t i = 0; i < c->NL; ++i) global_index[i] = c->world > 1 ? c->h_gidx[i] : i;
+    return VC_OK;
 }
 
 }  // extern "C"

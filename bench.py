@@ -14,8 +14,11 @@ each iteration one FFT matvec + preconditioner + Krylov ops, then Eq. 8).
            region): algorithmic bytes per launch / mean launch time vs MEASURED_PEAKS hbm_gbs;
   cpu_baseline = the CPU oracle (dense rows from binary128 closed forms), rank 0, bounded sample.
 
-Multi-GPU (torchrun): every rank extracts its own seeded instance of the workload (independent
-problems, no data-path collective; "scaling": "weak"); time = max over ranks.
+Multi-GPU (torchrun, N > 1): ONE extraction of the workload, slab-partitioned over the N ranks
+(DESIGN.md §10): each matvec does two NCCL all-to-all transposes and GMRES sums its dot
+products over ranks ("scaling": "strong"; the total work is fixed).  Rank 0 draws the NCCL unique
+id through the library and torch.distributed broadcasts it -- torch is plumbing only.  value =
+N_panels * matvecs / max-over-ranks device time.
 """
 from __future__ import annotations
 
@@ -165,6 +168,29 @@ def run_reference(args, rank, world):
 
 
 # ------------------------------------------------------------------------------------------
+def share_nccl_id(dist, rank, device):
+    """Rank 0 draws the 128-byte NCCL unique id with the library; broadcast it to all ranks."""
+    import torch
+    import paper_2004_02609_b200 as vc
+    buf = torch.zeros(128, dtype=torch.uint8, device=device)
+    if rank == 0:
+        buf.copy_(torch.frombuffer(bytearray(vc.nccl_unique_id()), dtype=torch.uint8))
+    dist.broadcast(buf, 0)
+    return bytes(buf.cpu().numpy().tobytes())
+
+
+def reduce_over_ranks(dist, world, device, ms, e2e_ms, work, e_work):
+    """max of the times, sum of the work (panel-matvecs) over ranks."""
+    import torch
+    t = torch.tensor([ms, e2e_ms, float(work), float(e_work)], dtype=torch.float64, device=device)
+    if world == 1:
+        return ms, e2e_ms, float(work), float(e_work)
+    tmax, tsum = t.clone(), t.clone()
+    dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+    dist.all_reduce(tsum, op=dist.ReduceOp.SUM)
+    return tmax[0].item(), tmax[1].item(), tsum[2].item(), tsum[3].item()
+
+
 def main():
     args = parse()
     rank = int(os.environ.get("RANK", "0"))
@@ -178,13 +204,15 @@ def main():
     import paper_2004_02609_b200 as vc
 
     torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    ctx = vc.VoxCap(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    st = voxgen.config(args.config, seed=rank)  # independent seeded instance per rank
+        dist.init_process_group("nccl", device_id=dev)
+        ctx.init_distributed(rank, world, nccl_id=share_nccl_id(dist, rank, dev))
+    st = voxgen.config(args.config, seed=0)  # one structure, partitioned over the ranks
     dev_label = torch.from_numpy(st.label).cuda()
     dev_eps = torch.from_numpy(st.eps).cuda()
     torch.cuda.synchronize()
-    ctx = vc.VoxCap(local)
     sopt = dict(tol=args.tol, restart=35, maxit=5000)
 
     solve_ms = []
@@ -233,7 +261,7 @@ def main():
     stats = ctx.stats()
     n_mv = stats["n_matvec"]
     N = ctx.n
-    pm = N * n_mv
+    pm = N * n_mv / world  # each distributed matvec is one N-panel product shared by the ranks
     # ---- e2e: host inputs through the same API ----
     ctx.set_timing(False)
     barrier()
@@ -245,17 +273,8 @@ def main():
     e2e_s = time.perf_counter() - t0
     e_mv = ctx.stats()["n_matvec"] - e_mv0
     # ---- reduce over ranks (max time, summed work) ----
-    t = torch.tensor([ms, e2e_s * 1000.0, float(pm), float(N * e_mv)], dtype=torch.float64,
-                     device="cuda")
-    if world > 1:
-        tmax = t.clone()
-        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
-        tsum = t.clone()
-        dist.all_reduce(tsum, op=dist.ReduceOp.SUM)
-        ms_max, e2e_ms_max = tmax[0].item(), tmax[1].item()
-        pm_tot, e_pm_tot = tsum[2].item(), tsum[3].item()
-    else:
-        ms_max, e2e_ms_max, pm_tot, e_pm_tot = ms, e2e_s * 1000.0, float(pm), float(N * e_mv)
+    ms_max, e2e_ms_max, pm_tot, e_pm_tot = reduce_over_ranks(
+        dist, world, dev, ms, e2e_s * 1000.0, pm, N * e_mv / world)
     if rank == 0:
         pk, pk_kind = peaks()
         # dominant pass by accumulated device time
@@ -280,15 +299,19 @@ def main():
             "unit": "panel-matvecs/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms_max / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
+            "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
             "config": {"workload": args.config, "desc": CONFIG_DESC.get(args.config, ""),
+                       "parallelism": f"slab{world} (y-slab spatial / kx-slab spectral, NCCL all-to-all)"
+                       if world > 1 else "single GPU",
                        "N": N, "m": ctx.m, "fft_grid": list(grid), "tol": args.tol,
                        "restart": 35, "precond": "block-diagonal-diagonal, boxes 10^3",
                        "step": "set_geometry + build_operator + solve_capacitance",
                        "l2": "working set > L2 (no flush needed)",
-                       "seed": "rank r uses voxgen seed r"},
+                       "seed": "voxgen seed 0 (one structure, all ranks)"},
             "gpu_launches": stats["gpu_launches"],
+            "comm_ms_per_matvec": stats["ms_comm"] / max(1, n_mv),
             "solve_s_per_column": None,
             "matvec_ms": mv_ms,
             "matvec_hbm_gbs": stats["bytes_matvec"] / (mv_ms * 1e-3) / 1e9,
@@ -306,7 +329,7 @@ def main():
                          "frac": achieved / pk["hbm_gbs"], "traffic": traffic,
                          "bytes_per_launch": stats["bytes_pass"][dom]},
             "e2e": {"value": e_pm_tot / (e2e_ms_max * 1e-3), "unit": "panel-matvecs/s",
-                    "h2d_bytes_per_step": int(st.label.nbytes + st.eps.nbytes),
+                    "h2d_bytes_per_step": int(world * (st.label.nbytes + st.eps.nbytes)),
                     "d2h_bytes_per_step": int(8 * ctx.m * ctx.m)},
             "clocks": clocks,
         }

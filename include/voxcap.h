@@ -132,6 +132,13 @@ vc_status vc_nccl_unique_id(void* out);
 /* In-process thread group of `world` ranks (transport 1); destroy after all its contexts. */
 vc_status vc_group_create(int32_t world, void** group);
 void vc_group_destroy(void* group);
+/* Host-only (no device needed): the slab boundaries vc_build_operator uses for `world` ranks.
+ * Rows: the slot rows [lo_y, lo_y + ey) of the FFT window (ny voxel rows, preconditioner box
+ * height box_y) -> ya[0..world] window-relative row boundaries (rank r owns [ya[r], ya[r+1]),
+ * whole box rows each).  Columns: kx in [0, kx) in tiles of `tile` -> kxa[0..world].  Both
+ * arrays are caller-allocated with world + 1 entries. */
+vc_status vc_plan_slabs(int32_t world, int32_t ny, int32_t lo_y, int32_t ey, int32_t box_y,
+                        int32_t kx, int32_t tile, int32_t* ya, int32_t* kxa);
 /* After vc_build_operator: number of panels this rank owns and (if global_index != NULL) their
  * global canonical indices, ascending.  world = 1: all panels. */
 vc_status vc_get_local_panels(const vc_ctx* ctx, int64_t* n_local, int64_t* global_index);

@@ -16,7 +16,7 @@ import os
 import numpy as np
 
 __all__ = ["VoxCap", "VoxCapError", "lib_path", "load_library", "EXPORTS", "BuildOpts",
-           "SolveOpts", "SolveInfo", "Stats", "ThreadGroup", "nccl_unique_id"]
+           "SolveOpts", "SolveInfo", "Stats", "ThreadGroup", "nccl_unique_id", "plan_slabs"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_NAME = "libvoxcap.so"
@@ -26,7 +26,8 @@ EXPORTS = ("vc_create", "vc_set_geometry", "vc_get_sizes", "vc_get_panels", "vc_
            "vc_get_grid", "vc_matvec", "vc_precond", "vc_solve", "vc_solve_capacitance",
            "vc_set_timing", "vc_get_stats", "vc_reset_stats", "vc_debug_kernel_entries",
            "vc_debug_fft", "vc_last_error", "vc_version", "vc_destroy", "vc_init_distributed",
-           "vc_nccl_unique_id", "vc_group_create", "vc_group_destroy", "vc_get_local_panels")
+           "vc_nccl_unique_id", "vc_group_create", "vc_group_destroy", "vc_get_local_panels",
+           "vc_plan_slabs")
 
 STATUS = {0: "VC_OK", 1: "VC_ERR_INPUT", 2: "VC_ERR_STATE", 3: "VC_ERR_OOM", 4: "VC_ERR_CUDA",
           5: "VC_ERR_NCCL", 6: "VC_NOT_CONVERGED", 7: "VC_ERR_UNSUPPORTED"}
@@ -119,6 +120,7 @@ def load_library(build_if_missing=False):
         "vc_nccl_unique_id": [vp],
         "vc_group_create": [i32, P(vp)],
         "vc_get_local_panels": [vp, P(i64), vp],
+        "vc_plan_slabs": [i32, i32, i32, i32, i32, i32, i32, vp, vp],
     }
     for name, args in sig.items():
         f = getattr(lib, name)
@@ -151,6 +153,16 @@ def nccl_unique_id():
     if st != 0:
         raise VoxCapError(st, "vc_nccl_unique_id failed (libnccl.so.2 not loadable?)")
     return bytes(buf)
+
+
+def plan_slabs(world, ny, lo_y, ey, box_y, kx, tile):
+    """Slab boundaries (host only): (ya, kxa), each world + 1 int32 (see include/voxcap.h)."""
+    ya = np.zeros(world + 1, np.int32)
+    kxa = np.zeros(world + 1, np.int32)
+    st = load_library().vc_plan_slabs(world, ny, lo_y, ey, box_y, kx, tile, _ptr(ya), _ptr(kxa))
+    if st != 0:
+        raise VoxCapError(st, "vc_plan_slabs: invalid arguments")
+    return ya, kxa
 
 
 class ThreadGroup:

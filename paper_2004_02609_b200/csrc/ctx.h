@@ -172,6 +172,9 @@ vc_status debug_kernel_entries(vc_ctx* c, int n, const int32_t* kind, const int3
 vc_status debug_fft(vc_ctx* c, int L, int nl, double* data, int dir);
 vc_status partition_build(vc_ctx* c);  // operator.cu: slabs, local panels, local slot maps
 int row_owner_abs(const vc_ctx* c, int yabs);
+void plan_kx_slabs(int W, int Kx, int T3, int* kxa);
+int row_owner_plan(int W, int Nv, int nb, int b0, int nbr, int yabs);
+void plan_row_slabs(int W, int ny, int lo, int EY, int Nv, int* ya, int* nb, int* b0, int* nbr);
 // comm.cu
 vc_status comm_nccl_unique_id(void* out, std::string& err);
 void* group_create(int world);

@@ -784,6 +784,37 @@ static cudaError_t launch_fft_strided(double2* d, int L, int64_t es, int64_t nco
 // ---------------------------------------------------------------------------------------
 // planning and build (vc_build_operator)
 // ---------------------------------------------------------------------------------------
+// ---- slab planning (host only; also exported as vc_plan_slabs for tests) -----------------
+// Spectral: rank q owns kx tiles [q nt / W, (q + 1) nt / W) of width T3.
+void plan_kx_slabs(int W, int Kx, int T3, int* kxa) {
+    const int nt = (Kx + T3 - 1) / T3;
+    for (int q = 0; q <= W; ++q) kxa[q] = std::min(Kx, (int)((int64_t)q * nt / W) * T3);
+    kxa[W] = Kx;
+}
+// Spatial: the preconditioner box rows (along y, box height Nv) that the window rows
+// [lo, lo + EY) touch are split into W contiguous ranges; a slot row belongs to the rank of
+// its box row (the top row ny joins the last box, as in the preconditioner).
+int row_owner_plan(int W, int Nv, int nb, int b0, int nbr, int yabs) {
+    const int br = std::min(std::max(yabs, 0) / Nv, nb - 1) - b0;
+    int p = 0;
+    while (p + 1 < W && (int64_t)(p + 1) * nbr / W <= br) ++p;
+    return p;
+}
+void plan_row_slabs(int W, int ny, int lo, int EY, int Nv, int* ya, int* nb_out, int* b0_out,
+                    int* nbr_out) {
+    const int nb = std::max(1, (ny + Nv - 1) / Nv);
+    const int b0 = std::min(lo / Nv, nb - 1);
+    const int nbr = std::min((lo + EY - 1) / Nv, nb - 1) - b0 + 1;
+    ya[0] = 0;
+    int p = 1;
+    for (int y = 0; y < EY && p < W; ++y)
+        while (p < W && row_owner_plan(W, Nv, nb, b0, nbr, lo + y) >= p) ya[p++] = y;
+    for (; p <= W; ++p) ya[p] = EY;
+    *nb_out = nb;
+    *b0_out = b0;
+    *nbr_out = nbr;
+}
+
 static int next_pow2(int v) {
     int p = 8;
     while (p < v) p *= 2;
@@ -892,11 +923,7 @@ vc_status operator_build(vc_ctx* c, const vc_build_opts* o) {
     c->blk_stride = (size_t)Kx * (My / 2 + 1) * (Mz / 2 + 1);
     // P3 tile width and the tile-major spectrum layout (one contiguous chunk per P3 tile)
     c->T3 = p3_tile(Mz, c->nf);
-    {   // spectral partition: rank q owns kx tiles [q nt / W, (q + 1) nt / W) of width T3
-        const int W = c->world, nt = (Kx + c->T3 - 1) / c->T3;
-        for (int q = 0; q <= W; ++q) c->kxa[q] = std::min(Kx, (int)((int64_t)q * nt / W) * c->T3);
-        c->kxa[W] = Kx;
-    }
+    plan_kx_slabs(c->world, Kx, c->T3, c->kxa);
     const int kx0 = c->kxa[c->rank], nkx = c->kxa[c->rank + 1] - kx0;
     c->nt3 = (nkx + c->T3 - 1) / c->T3;
     c->rchunk = ((size_t)std::max(1, c->nblk) * (Mz / 2 + 1) * c->T3 + 1) & ~(size_t)1;
@@ -989,16 +1016,8 @@ vc_status operator_build(vc_ctx* c, const vc_build_opts* o) {
     for (int f = 0; f < c->nf; ++f) EY = std::max(EY, c->f[f].ext[1]);
     const int W = c->world, rk = c->rank;
     {
-        const int Nv = c->box[1], nb = std::max(1, (c->ny + Nv - 1) / Nv);
-        c->own_Nv = Nv;
-        c->own_nb = nb;
-        c->own_b0 = std::min(lo[1] / Nv, nb - 1);
-        c->own_nbr = std::min((lo[1] + EY - 1) / Nv, nb - 1) - c->own_b0 + 1;
-        c->ya[0] = 0;
-        int p = 1;
-        for (int y = 0; y < EY && p < W; ++y)
-            while (p < W && row_owner_abs(c, lo[1] + y) >= p) c->ya[p++] = y;
-        for (; p <= W; ++p) c->ya[p] = EY;
+        plan_row_slabs(W, c->ny, lo[1], EY, c->box[1], c->ya, &c->own_nb, &c->own_b0, &c->own_nbr);
+        c->own_Nv = c->box[1];
         for (int q = 0; q < W; ++q) {
             auto cnt = [&](int e) { return std::max(0, std::min(c->ya[q + 1], e) - c->ya[q]); };
             for (int b = 0; b < 3; ++b) c->nr[q][b] = cnt(c->ext_in[b][1]);
@@ -1110,10 +1129,7 @@ vc_status operator_build(vc_ctx* c, const vc_build_opts* o) {
 
 // rank owning absolute slot row yabs (along y): by preconditioner box row, contiguous ranges
 int row_owner_abs(const vc_ctx* c, int yabs) {
-    const int br = std::min(std::max(yabs, 0) / c->own_Nv, c->own_nb - 1) - c->own_b0;
-    int p = 0;
-    while (p + 1 < c->world && (int64_t)(p + 1) * c->own_nbr / c->world <= br) ++p;
-    return p;
+    return row_owner_plan(c->world, c->own_Nv, c->own_nb, c->own_b0, c->own_nbr, yabs);
 }
 
 __global__ void k_local_panels(int64_t nl, const int64_t* __restrict__ gidx,

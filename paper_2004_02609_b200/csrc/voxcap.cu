@@ -386,6 +386,17 @@ vc_status vc_group_create(int32_t world, void** group) {
 
 void vc_group_destroy(void* group) { group_destroy(group); }
 
+vc_status vc_plan_slabs(int32_t world, int32_t ny, int32_t lo_y, int32_t ey, int32_t box_y,
+                        int32_t kx, int32_t tile, int32_t* ya, int32_t* kxa) {
+    if (world < 1 || world > kMaxRanks || ny < 1 || lo_y < 0 || ey < 1 || lo_y + ey > ny + 1 ||
+        box_y < 1 || kx < 1 || tile < 1 || !ya || !kxa)
+        return VC_ERR_INPUT;
+    int nb, b0, nbr;
+    plan_row_slabs(world, ny, lo_y, ey, box_y, ya, &nb, &b0, &nbr);
+    plan_kx_slabs(world, kx, tile, kxa);
+    return VC_OK;
+}
+
 vc_status vc_get_local_panels(const vc_ctx* c, int64_t* n_local, int64_t* global_index) {
     if (!c) return VC_ERR_INPUT;
     if (!c->has_op) return VC_ERR_STATE;

@@ -66,7 +66,10 @@ typedef struct {
     int32_t precond;        /* 0 = default = 3; 1 = none; 2 = diagonal only (Ī^{-1} on
                                dielectric rows, 1/P_kk on conductor rows); 3 = the paper's
                                block-diagonal-diagonal (Eq. 14)                    */
-    int32_t reserved[9];
+    int32_t zmode;          /* z direction of the matvec: 0 = automatic, 1 = z-FFT
+                               (3-D circulant, Eq. 11), 2 = direct z-convolution on the x/y
+                               spectra (exact; cheaper when panels occupy few z-planes)       */
+    int32_t reserved[8];
 } vc_build_opts;
 
 /* Solve options.  Zero fields take the paper's defaults. */

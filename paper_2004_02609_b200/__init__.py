@@ -42,7 +42,8 @@ class VoxCapError(RuntimeError):
 
 class BuildOpts(ctypes.Structure):
     _fields_ = [("pad", ctypes.c_int32 * 3), ("box", ctypes.c_int32 * 3),
-                ("precond", ctypes.c_int32), ("reserved", ctypes.c_int32 * 9)]
+                ("precond", ctypes.c_int32), ("zmode", ctypes.c_int32),
+                ("reserved", ctypes.c_int32 * 8)]
 
 
 class SolveOpts(ctypes.Structure):
@@ -294,8 +295,10 @@ class VoxCap:
         return out
 
     # -- operator ------------------------------------------------------------------------
-    def build_operator(self, pad=None, box=None, precond=3):
+    def build_operator(self, pad=None, box=None, precond=3, zmode=0):
+        """zmode: 0 automatic, 1 z-FFT (3-D circulant), 2 direct z-convolution."""
         o = BuildOpts()
+        o.zmode = int(zmode)
         if pad is not None:
             for a in range(3):
                 o.pad[a] = int(pad[a])

@@ -110,6 +110,8 @@ struct vc_ctx {
     vc::DevBuf<double2> bufA, bufB, bufC;  // X1/X4, X2, X3
     size_t offB[3], offC[6];
     int T3 = 1, nt3 = 1;   // P3 tile width and kx-tile count (tile-major X2 / R layouts)
+    bool zdirect = false;  // P3 direct-z mode (operator.cu k_p3d)
+    int ZU = 0, nog = 0, og_f[64] = {}, og_j[64] = {};
     size_t rchunk = 0;     // doubles of R per P3 tile
     int ZL = 0, nzin[3] = {0, 0, 0}, nzout[6] = {0, 0, 0, 0, 0, 0};  // active z-plane counts
     vc::DevBuf<int32_t> planes;  // plane lists + inverse maps (operator.cu)

@@ -21,6 +21,8 @@
 
 namespace vc {
 
+constexpr int kMaxOG = 64;  // P3 direct-z: max output groups
+
 struct MV {
     int Mx, My, Mz, Kx;
     int lo[3];
@@ -59,6 +61,9 @@ struct MV {
     const int32_t* planes;  // [9][ZL] lists, then [9][ZL] inverse maps (plane -> index or -1)
     int ZL;
     int nzin[3], nzout[6];
+    // P3 direct-z mode: output groups (field, first plane) of kZB planes each
+    int zdirect, ZU, nog;
+    int og_f[kMaxOG], og_j[kMaxOG];
 };
 
 __device__ __forceinline__ int zlist(const MV& mv, int g, int j) { return mv.planes[g * mv.ZL + j]; }
@@ -80,7 +85,9 @@ template <int L> struct TX { static constexpr int T = clampi(4096 / L, 1, 64); }
 template <int L> struct TY { static constexpr int T = clampi(4096 / L, 1, 32); };   // y passes
 constexpr int kNT = 256;
 constexpr int kNT3 = 256;  // P3 threads per CTA
-constexpr int kMaxLz = 256;  // largest z FFT length (P3 keeps whole z-pencils in shared memory)
+constexpr int kMaxLz = 256;
+constexpr int kDirectT = 8;  // P3 direct-z tile width (kx per tile)
+constexpr int kZB = 4;       // P3 direct-z: output planes per thread  // largest z FFT length (P3 keeps whole z-pencils in shared memory)
 
 __device__ __forceinline__ int ktil(int k, int M) { return k <= M / 2 ? k : k - M; }
 
@@ -545,6 +552,60 @@ __global__ void k_kfill(double2* G, const double* __restrict__ Ko, int Mx, int M
     }
 }
 
+// direct-z mode: x/y-cyclic grid G[u][y][x] (real part) from the octant table Ko[u][oy][ox],
+// with the x / y parity signs (the z parity is applied in k_p3d)
+__global__ void k_kfill2d(double2* G, const double* __restrict__ Ko, int Mx, int My, int ZU,
+                          int Ox, int Oy, int kind, int alpha, int beta) {
+    const int64_t tot = (int64_t)Mx * My * ZU;
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < tot;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int n[2] = {(int)(idx % Mx), (int)((idx / Mx) % My)};
+        const int u = (int)(idx / ((int64_t)Mx * My));
+        const int M[2] = {Mx, My};
+        int o[2];
+        double sg = 1.0;
+        bool zero = false;
+#pragma unroll
+        for (int a = 0; a < 2; ++a) {
+            const int s2 = c2(alpha, a) - c2(beta, a);
+            const int t2 = rep_t2(n[a], M[a], s2);
+            const int at2 = t2 < 0 ? -t2 : t2;
+            o[a] = s2 == 0 ? at2 / 2 : (at2 - 1) / 2;
+            if (kind == 1 && a == alpha) {
+                if (t2 < 0) sg = -sg;
+                if (s2 == 0 && 2 * n[a] == M[a]) zero = true;  // unresolvable odd tie
+            }
+        }
+        const double v = zero ? 0.0 : sg * Ko[((int64_t)u * Oy + o[1]) * Ox + o[0]];
+        G[idx] = make_double2(v, 0.0);
+    }
+}
+
+// direct-z mode: x/y-transformed, phase-stripped kernel, tile-major for k_p3d:
+//   R[(ky' * nt3 + kx / T3) * RC + (blk * ZU + u) * T3 + kx % T3]; Re (P, E^{z.}) or Im (E^{x.},
+//   E^{y.}) part; kx local to [kx0, kx0 + nkx)
+__global__ void k_extract2d(const double2* __restrict__ G, double* __restrict__ R, int Mx, int My,
+                            int ZU, int kx0, int nkx, int kind, int alpha, int beta,
+                            const double2* __restrict__ tw, int blk, int lgT3, int RC) {
+    const int KY = My / 2 + 1;
+    const int T3 = 1 << lgT3;
+    const int nt3 = (nkx + T3 - 1) >> lgT3;
+    const int64_t tot = (int64_t)nkx * KY * ZU;
+    const int s2x = c2(alpha, 0) - c2(beta, 0), s2y = c2(alpha, 1) - c2(beta, 1);
+    const bool im = kind == 1 && alpha != 2;
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < tot;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int kx = (int)(idx % nkx);
+        const int u = (int)((idx / nkx) % ZU);
+        const int ky = (int)(idx / ((int64_t)nkx * ZU));
+        double2 v = G[((int64_t)u * My + ky) * Mx + kx0 + kx];
+        v = cmul(v, half_phase(tw, (kx0 + kx) * s2x, Mx, -1));
+        v = cmul(v, half_phase(tw, ky * s2y, My, -1));
+        R[((int64_t)ky * nt3 + (kx >> lgT3)) * RC + ((int64_t)blk * ZU + u) * T3 + (kx & (T3 - 1))] =
+            im ? v.y : v.x;
+    }
+}
+
 // in-place C2C FFT of contiguous lines: data[line][L]
 template <int L, bool INV>
 __global__ void __launch_bounds__(kNT) k_fft_lines(double2* data, int64_t nlines,
@@ -671,6 +732,174 @@ static cudaError_t launch_p2(const MV& mv, cudaStream_t st) {
     });
     return cudaGetLastError();
 }
+// ---------------------------------------------------------------------------------------
+// P3, direct-z mode: FFT along x and y only, direct convolution along z.
+//   out^f(kx, ky, z_o) = sum_b sum_{z_i} K^{f b}(kx, ky, z_o - z_i) Q^b(kx, ky, z_i)
+// with K the x/y-transformed, phase-stripped kernel at the geometric z offset (SURVEY App. B
+// applied to x and y only).  Exact like the z-FFT form (no circulant along z at all), and for
+// layered structures whose panels occupy few z-planes it costs sum_{f,b} n_out(f) n_in(b)
+// complex-by-real MACs per (kx, ky) instead of 3 + n_f z-FFTs.  K is stored on the z-parity
+// octant u = (|2 dz + s2| - |s2|) / 2 (s2 = 2 (c_a,z - c_b,z)): even in z except the E^{z.}
+// blocks (odd); E^{x.}, E^{y.} carry the factor i (odd along x / y) and E^{y.} the ky sign.
+// Thread = (kx t, output group of kZB planes of one field) computing both ky sides; Q loads are
+// shared by all groups of a warp (broadcast), rows of T kx are contiguous (tile-major X2, K).
+// ---------------------------------------------------------------------------------------
+// Accumulate NZO output planes (both ky sides) of one field over the n input planes of one
+// source: a[k] += K(u(zo_k - zi)) Q(zi), with zo2[k] = 2 zo_k + s2 and zi2 = 2 zi, so the
+// doubled geometric offset is one subtraction; ODD: the E^{z.} blocks, odd in z.
+template <int NZO, bool ODD, int T>
+__device__ __forceinline__ void p3d_acc(double2 (&a0)[kZB], double2 (&a1)[kZB],
+                                        const int (&zo2)[kZB], int s2a, const double* Kb,
+                                        const double2* X, int n, const int* zi2) {
+#pragma unroll 2
+    for (int ji = 0; ji < n; ++ji) {
+        const int z2 = zi2[ji];
+        const double2 q0 = X[ji * T];
+        const double2 q1 = X[(n + ji) * T];  // side 1 (unused when nside = 1)
+#pragma unroll
+        for (int k = 0; k < NZO; ++k) {
+            const int g2 = zo2[k] - z2;
+            double kv = Kb[(((g2 < 0 ? -g2 : g2) - s2a) >> 1) * T];
+            if (ODD) kv = g2 < 0 ? -kv : kv;
+            a0[k].x = fma(kv, q0.x, a0[k].x);
+            a0[k].y = fma(kv, q0.y, a0[k].y);
+            a1[k].x = fma(kv, q1.x, a1[k].x);
+            a1[k].y = fma(kv, q1.y, a1[k].y);
+        }
+    }
+}
+
+// Persistent and TMA-fed like the z-FFT P3: a tile's X2 rows and K rows are contiguous (tile-
+// major layouts), so one thread fetches the next tile with four cp.async.bulk copies into the
+// other half of a two-stage ring while the CTA computes the current tile from shared memory.
+__global__ void __launch_bounds__(256) k_p3d(MV mv) {
+    constexpr int T = kDirectT;
+    extern __shared__ __align__(16) double2 sd[];
+    const int t = threadIdx.x % T, og0 = threadIdx.x / T, OGS = blockDim.x / T;
+    const int nkx = mv.nkx, My = mv.My, ZL = mv.ZL;
+    const int nt3 = (nkx + T - 1) / T;
+    const int ntiles = nt3 * (My / 2 + 1);
+    const int nz0 = mv.nzin[0], nz1 = mv.nzin[1], nz2 = mv.nzin[2];
+    const int xo1 = 2 * T * nz0, xo2 = 2 * T * (nz0 + nz1);
+    const int XS = 2 * T * (nz0 + nz1 + nz2);  // double2 per stage
+    const int RC = mv.rchunk;                  // doubles per stage (even)
+    double2* xin = sd;                                          // [2][XS]
+    double* kin = reinterpret_cast<double*>(xin + 2 * XS);      // [2][RC]
+    int* zl = reinterpret_cast<int*>(kin + 2 * RC);             // [9][ZL] plane lists
+    uint64_t* bar = reinterpret_cast<uint64_t*>(zl + ((9 * ZL + 3) & ~3));  // [2]
+    if (threadIdx.x == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        fence_mbar_init();
+    }
+    // plane lists; source lists doubled (zi2 = 2 zi) for the offset arithmetic
+    for (int e = threadIdx.x; e < 9 * ZL; e += blockDim.x) zl[e] = mv.planes[e] * (e < 3 * ZL ? 2 : 1);
+    __syncthreads();
+    auto issue = [&](int tl, int s) {  // one thread: fetch tile tl into stage s
+        const size_t qt = (size_t)tl;
+        mbar_arrive_expect_tx(&bar[s], (unsigned)(16 * XS + 8 * RC));
+        if (nz0) bulk_g2s(xin + s * XS, mv.X2[0] + qt * 2 * T * nz0, 32u * T * nz0, &bar[s]);
+        if (nz1) bulk_g2s(xin + s * XS + xo1, mv.X2[1] + qt * 2 * T * nz1, 32u * T * nz1, &bar[s]);
+        if (nz2) bulk_g2s(xin + s * XS + xo2, mv.X2[2] + qt * 2 * T * nz2, 32u * T * nz2, &bar[s]);
+        bulk_g2s(kin + s * RC, mv.Rt + qt * RC, 8u * RC, &bar[s]);
+    };
+    if (threadIdx.x == 0 && (int)blockIdx.x < ntiles) issue(blockIdx.x, 0);
+    unsigned par0 = 0, par1 = 0;
+    int it = 0;
+    for (int tl = blockIdx.x; tl < ntiles; tl += gridDim.x, ++it) {
+        const int st = it & 1;
+        if (threadIdx.x == 0 && tl + (int)gridDim.x < ntiles) {
+            fence_proxy_async();
+            issue(tl + gridDim.x, st ^ 1);
+        }
+        if (st == 0) { mbar_wait(&bar[0], par0); par0 ^= 1; }
+        else { mbar_wait(&bar[1], par1); par1 ^= 1; }
+        const double2* xs = xin + st * XS;
+        const double* ks = kin + st * RC;
+        const int q = tl / nt3, xt = tl % nt3;
+        const int kx = xt * T + t;
+        const bool valid = kx < nkx;
+        const int nside = (q == 0 || 2 * q == My) ? 1 : 2;
+        for (int og = og0; og < mv.nog; og += OGS) {
+            const int f = mv.og_f[og], jo0 = mv.og_j[og];
+            const int nzo = min(kZB, mv.nzout[f] - jo0);
+            const int kind = mv.fkind[f], alpha = mv.faxis[f];
+            double2 a0[kZB], a1[kZB];
+#pragma unroll
+            for (int k = 0; k < kZB; ++k) a0[k] = a1[k] = czero();
+#pragma unroll
+            for (int b = 0; b < 3; ++b) {
+                const int bk = mv.blk[f][b];
+                if (bk < 0) continue;
+                const int s2 = c2(alpha, 2) - c2(b, 2);
+                int zo2[kZB];
+#pragma unroll
+                for (int k = 0; k < kZB; ++k)
+                    zo2[k] = 2 * (k < nzo ? zl[(3 + f) * ZL + jo0 + k] : 0) + s2;
+                const double* Kb = ks + bk * mv.ZU * T + t;
+                const int nzb = b == 0 ? nz0 : (b == 1 ? nz1 : nz2);
+                const double2* X = xs + (b == 0 ? 0 : (b == 1 ? xo1 : xo2)) + t;
+                const int* zi2 = zl + b * ZL;
+                const int s2a = s2 != 0;
+                if (kind == 1 && alpha == 2) {  // E^{z.}: odd in z
+                    switch (nzo) {
+                        case 1: p3d_acc<1, true, T>(a0, a1, zo2, s2a, Kb, X, nzb, zi2); break;
+                        case 2: p3d_acc<2, true, T>(a0, a1, zo2, s2a, Kb, X, nzb, zi2); break;
+                        case 3: p3d_acc<3, true, T>(a0, a1, zo2, s2a, Kb, X, nzb, zi2); break;
+                        default: p3d_acc<4, true, T>(a0, a1, zo2, s2a, Kb, X, nzb, zi2); break;
+                    }
+                } else {
+                    switch (nzo) {
+                        case 1: p3d_acc<1, false, T>(a0, a1, zo2, s2a, Kb, X, nzb, zi2); break;
+                        case 2: p3d_acc<2, false, T>(a0, a1, zo2, s2a, Kb, X, nzb, zi2); break;
+                        case 3: p3d_acc<3, false, T>(a0, a1, zo2, s2a, Kb, X, nzb, zi2); break;
+                        default: p3d_acc<4, false, T>(a0, a1, zo2, s2a, Kb, X, nzb, zi2); break;
+                    }
+                }
+            }
+            if (!valid) continue;
+            double2* __restrict__ X3 = mv.X3[f];
+            const bool ifac = kind == 1 && alpha != 2;  // E^{x.}, E^{y.}: R stores Im(K)
+#pragma unroll
+            for (int k = 0; k < kZB; ++k) {
+                if (k >= nzo) break;
+#pragma unroll
+                for (int side = 0; side < 2; ++side) {
+                    if (side >= nside) break;
+                    double2 a = side ? a1[k] : a0[k];
+                    if (ifac) {
+                        const bool neg = alpha == 1 && side == 1;  // odd along y: ky < 0 side
+                        a = neg ? make_double2(a.y, -a.x) : make_double2(-a.y, a.x);
+                    }
+                    X3[((int64_t)(jo0 + k) * My + (side ? My - q : q)) * nkx + kx] = a;
+                }
+            }
+        }
+        __syncthreads();  // stage st is refilled by the issue two iterations on
+    }
+}
+
+static cudaError_t launch_p3d(const MV& mv, cudaStream_t st) {
+    const int nt3 = (mv.nkx + kDirectT - 1) / kDirectT;
+    const int ntiles = nt3 * (mv.My / 2 + 1);
+    if (ntiles == 0 || mv.nog == 0) return cudaSuccess;
+    const int ogs = std::min(mv.nog, 256 / kDirectT);
+    const int nthr = kDirectT * ogs;
+    const size_t smem = 2 * (16 * (size_t)2 * kDirectT * (mv.nzin[0] + mv.nzin[1] + mv.nzin[2]) +
+                             8 * (size_t)mv.rchunk) +
+                        4 * (size_t)((9 * mv.ZL + 3) & ~3) + 2 * sizeof(uint64_t);
+    if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
+    cudaError_t e = prep(k_p3d, smem);
+    if (e) return e;
+    int per_sm = 0, nsm = 0, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_p3d, nthr, smem);
+    const int grid = std::max(1, std::min(ntiles, std::max(1, per_sm) * nsm));
+    k_p3d<<<grid, nthr, smem, st>>>(mv);
+    return cudaGetLastError();
+}
+
 template <int L, int NF>
 static size_t p3_smem(const MV& mv) {
     constexpr int W = P3T<L, NF>::W, T = P3T<L, NF>::T;
@@ -708,6 +937,7 @@ static cudaError_t launch_p3_l(const MV& mv, cudaStream_t st) {
     }
 }
 static cudaError_t launch_p3(const MV& mv, cudaStream_t st) {
+    if (mv.zdirect) return launch_p3d(mv, st);
     cudaError_t e;
     switch (mv.Mz) {  // kMaxLz: the [L][W] pencil buffer must fit one CTA's shared memory
         case 8: e = launch_p3_l<8>(mv, st); break;
@@ -921,63 +1151,6 @@ vc_status operator_build(vc_ctx* c, const vc_build_opts* o) {
         for (int b = 0; b < 3; ++b) c->blk[f][b] = -1;
     c->nblk = (int)defs.size();
     c->blk_stride = (size_t)Kx * (My / 2 + 1) * (Mz / 2 + 1);
-    // P3 tile width and the tile-major spectrum layout (one contiguous chunk per P3 tile)
-    c->T3 = p3_tile(Mz, c->nf);
-    plan_kx_slabs(c->world, Kx, c->T3, c->kxa);
-    const int kx0 = c->kxa[c->rank], nkx = c->kxa[c->rank + 1] - kx0;
-    c->nt3 = (nkx + c->T3 - 1) / c->T3;
-    c->rchunk = ((size_t)std::max(1, c->nblk) * (Mz / 2 + 1) * c->T3 + 1) & ~(size_t)1;
-    VC_CUDA(c, c->tw.alloc(kTabN));
-    k_twiddles<<<(kTabN + 255) / 256, 256, 0, st>>>(c->tw.p);
-    count_launch(c);
-    VC_CUDA(c, c->Rt.alloc(std::max<size_t>(1, c->rchunk * (size_t)(My / 2 + 1) * c->nt3)));
-    VC_CUDA(c, cudaMemsetAsync(c->Rt.p, 0, c->Rt.bytes(), st));
-    // spectra (a2 on the parity octant -> full cyclic grid -> 3-D FFT -> phase strip + fold)
-    {
-        cudaEvent_t ev[4];
-        for (auto& e : ev) VC_CUDA(c, cudaEventCreate(&e));
-        float t_kgen = 0, t_fft = 0, t_ext = 0, ms;
-        DevBuf<double2> G;
-        DevBuf<double> Ko;
-        const int64_t tot = (int64_t)M[0] * M[1] * M[2];
-        const int Ox = M[0] / 2 + 1, Oy = M[1] / 2 + 1, Oz = M[2] / 2 + 1;
-        const int64_t otot = (int64_t)Ox * Oy * Oz;
-        VC_CUDA(c, G.alloc(tot));
-        VC_CUDA(c, Ko.alloc(otot));
-        const double fpe = 4.0 * kPi * kEps0;
-        for (int i = 0; i < c->nblk; ++i) {
-            const BlkDef& d = defs[i];
-            const double scale = (d.kind == 0 ? c->dv * c->dv * c->dv : c->dv * c->dv) / fpe /
-                                 ((double)M[0] * M[1] * M[2]);
-            VC_CUDA(c, cudaEventRecord(ev[0], st));
-            const int oblocks = (int)std::min<int64_t>((otot + 127) / 128, 148 * 64);
-            k_kgen_oct<<<oblocks, 128, 0, st>>>(Ko.p, Ox, Oy, Oz, d.kind, d.alpha, d.beta, scale);
-            const int gblocks = (int)std::min<int64_t>((tot + 255) / 256, 148 * 64);
-            k_kfill<<<gblocks, 256, 0, st>>>(G.p, Ko.p, M[0], M[1], M[2], Ox, Oy, d.kind, d.alpha, d.beta);
-            VC_CUDA(c, cudaEventRecord(ev[1], st));
-            VC_CUDA(c, launch_fft_lines(G.p, M[0], (int64_t)M[1] * M[2], false, c->tw.p, st));
-            VC_CUDA(c, launch_fft_strided(G.p, M[1], M[0], M[0], M[2], (int64_t)M[0] * M[1], c->tw.p, st));
-            VC_CUDA(c, launch_fft_strided(G.p, M[2], (int64_t)M[0] * M[1], (int64_t)M[0] * M[1], 1, 0, c->tw.p, st));
-            VC_CUDA(c, cudaEventRecord(ev[2], st));
-            const int eblocks = (int)std::max<int64_t>(1, std::min<int64_t>((c->blk_stride + 255) / 256, 148 * 32));
-            k_extract<<<eblocks, 256, 0, st>>>(G.p, c->Rt.p, M[0], M[1], M[2], kx0, nkx, d.kind, d.alpha,
-                                               d.beta, 1.0, c->tw.p, i, ilog2c(c->T3),
-                                               (int)c->rchunk);
-            VC_CUDA(c, cudaEventRecord(ev[3], st));
-            count_launch(c, 6);
-            VC_CUDA(c, cudaEventSynchronize(ev[3]));
-            cudaEventElapsedTime(&ms, ev[0], ev[1]);
-            t_kgen += ms;
-            cudaEventElapsedTime(&ms, ev[1], ev[2]);
-            t_fft += ms;
-            cudaEventElapsedTime(&ms, ev[2], ev[3]);
-            t_ext += ms;
-        }
-        for (auto& e : ev) cudaEventDestroy(e);
-        c->stats.ms_kgen = t_kgen;
-        c->stats.ms_kfft = t_fft + t_ext;
-        VC_CUDA(c, cudaGetLastError());
-    }
     // active z-planes: a plane of source orientation b (output field f) is transformed along x
     // and y only if it holds b-panels (f-panels); empty planes are zero and never touched
     {
@@ -1008,6 +1181,108 @@ vc_status operator_build(vc_ctx* c, const vc_build_opts* o) {
         VC_CUDA(c, c->planes.alloc(hp.size()));
         VC_CUDA(c, cudaMemcpyAsync(c->planes.p, hp.data(), 4 * hp.size(), cudaMemcpyHostToDevice, st));
         VC_CUDA(c, cudaStreamSynchronize(st));
+    }
+    // P3 mode: direct z-convolution when the layered structure makes it cheaper than the
+    // z-FFTs (complex-by-real MACs vs a radix-2 estimate of 3 + n_f transforms of length Mz)
+    {
+        double mac = 0;
+        int nog = 0;
+        for (int f = 0; f < c->nf; ++f) {
+            for (int b = 0; b < 3; ++b)
+                if (c->blk[f][b] >= 0) mac += (double)c->nzout[f] * c->nzin[b];
+            nog += (c->nzout[f] + kZB - 1) / kZB;
+        }
+        const double fft = 0.6 * (3 + c->nf) * 5.0 * Mz * ilog2c(Mz);
+        const int zmode = o ? o->zmode : 0;
+        if (zmode < 0 || zmode > 2) return set_err(c, VC_ERR_INPUT, "zmode must be 0, 1 or 2");
+        // k_p3d stages one tile (X2 rows, K tile, plane lists) in shared memory
+        const double smem = 2 * (16.0 * 2 * kDirectT * (c->nzin[0] + c->nzin[1] + c->nzin[2]) +
+                                 8.0 * std::max(1, c->nblk) * c->ZL * kDirectT) +
+                            4.0 * 9 * c->ZL + 64;
+        c->zdirect = nog <= kMaxOG && smem <= 200.0 * 1024 &&
+                     (zmode == 2 || (zmode == 0 && 4.0 * mac <= fft));
+        if (zmode == 2 && !c->zdirect)
+            return set_err(c, VC_ERR_UNSUPPORTED, "direct-z mode: too many output planes");
+        c->ZU = c->ZL;
+        c->nog = 0;
+        if (c->zdirect)
+            for (int f = 0; f < c->nf; ++f)
+                for (int j = 0; j < c->nzout[f]; j += kZB) {
+                    c->og_f[c->nog] = f;
+                    c->og_j[c->nog] = j;
+                    ++c->nog;
+                }
+    }
+    // P3 tile width and the tile-major spectrum layout (one contiguous chunk per P3 tile)
+    c->T3 = c->zdirect ? kDirectT : p3_tile(Mz, c->nf);
+    plan_kx_slabs(c->world, Kx, c->T3, c->kxa);
+    const int kx0 = c->kxa[c->rank], nkx = c->kxa[c->rank + 1] - kx0;
+    c->nt3 = (nkx + c->T3 - 1) / c->T3;
+    c->rchunk = ((size_t)std::max(1, c->nblk) * (c->zdirect ? c->ZU : Mz / 2 + 1) * c->T3 + 1) &
+                ~(size_t)1;
+    VC_CUDA(c, c->tw.alloc(kTabN));
+    k_twiddles<<<(kTabN + 255) / 256, 256, 0, st>>>(c->tw.p);
+    count_launch(c);
+    VC_CUDA(c, c->Rt.alloc(std::max<size_t>(1, c->rchunk * (size_t)(My / 2 + 1) * c->nt3)));
+    VC_CUDA(c, cudaMemsetAsync(c->Rt.p, 0, c->Rt.bytes(), st));
+    // spectra (a2 on the parity octant -> full cyclic grid -> 3-D FFT -> phase strip + fold)
+    {
+        cudaEvent_t ev[4];
+        for (auto& e : ev) VC_CUDA(c, cudaEventCreate(&e));
+        float t_kgen = 0, t_fft = 0, t_ext = 0, ms;
+        DevBuf<double2> G;
+        DevBuf<double> Ko;
+        const bool zd = c->zdirect;
+        // z-FFT mode: full 3-D cyclic grid; direct-z mode: x/y-cyclic grid x ZU octant z offsets
+        const int MZ = zd ? c->ZU : M[2];
+        const int64_t tot = (int64_t)M[0] * M[1] * MZ;
+        const int Ox = M[0] / 2 + 1, Oy = M[1] / 2 + 1, Oz = zd ? c->ZU : M[2] / 2 + 1;
+        const int64_t otot = (int64_t)Ox * Oy * Oz;
+        VC_CUDA(c, G.alloc(tot));
+        VC_CUDA(c, Ko.alloc(otot));
+        const double fpe = 4.0 * kPi * kEps0;
+        for (int i = 0; i < c->nblk; ++i) {
+            const BlkDef& d = defs[i];
+            const double scale = (d.kind == 0 ? c->dv * c->dv * c->dv : c->dv * c->dv) / fpe /
+                                 ((double)M[0] * M[1] * (zd ? 1 : M[2]));
+            VC_CUDA(c, cudaEventRecord(ev[0], st));
+            const int oblocks = (int)std::min<int64_t>((otot + 127) / 128, 148 * 64);
+            k_kgen_oct<<<oblocks, 128, 0, st>>>(Ko.p, Ox, Oy, Oz, d.kind, d.alpha, d.beta, scale);
+            const int gblocks = (int)std::min<int64_t>((tot + 255) / 256, 148 * 64);
+            if (zd)
+                k_kfill2d<<<gblocks, 256, 0, st>>>(G.p, Ko.p, M[0], M[1], MZ, Ox, Oy, d.kind, d.alpha, d.beta);
+            else
+                k_kfill<<<gblocks, 256, 0, st>>>(G.p, Ko.p, M[0], M[1], M[2], Ox, Oy, d.kind, d.alpha, d.beta);
+            VC_CUDA(c, cudaEventRecord(ev[1], st));
+            VC_CUDA(c, launch_fft_lines(G.p, M[0], (int64_t)M[1] * MZ, false, c->tw.p, st));
+            VC_CUDA(c, launch_fft_strided(G.p, M[1], M[0], M[0], MZ, (int64_t)M[0] * M[1], c->tw.p, st));
+            if (!zd)
+                VC_CUDA(c, launch_fft_strided(G.p, M[2], (int64_t)M[0] * M[1], (int64_t)M[0] * M[1], 1, 0, c->tw.p, st));
+            VC_CUDA(c, cudaEventRecord(ev[2], st));
+            const int64_t etot = (int64_t)std::max(1, nkx) * (My / 2 + 1) * (zd ? c->ZU : Mz / 2 + 1);
+            const int eblocks = (int)std::max<int64_t>(1, std::min<int64_t>((etot + 255) / 256, 148 * 32));
+            if (zd)
+                k_extract2d<<<eblocks, 256, 0, st>>>(G.p, c->Rt.p, M[0], M[1], c->ZU, kx0, nkx, d.kind,
+                                                     d.alpha, d.beta, c->tw.p, i, ilog2c(c->T3),
+                                                     (int)c->rchunk);
+            else
+                k_extract<<<eblocks, 256, 0, st>>>(G.p, c->Rt.p, M[0], M[1], M[2], kx0, nkx, d.kind, d.alpha,
+                                                   d.beta, 1.0, c->tw.p, i, ilog2c(c->T3),
+                                                   (int)c->rchunk);
+            VC_CUDA(c, cudaEventRecord(ev[3], st));
+            count_launch(c, 6);
+            VC_CUDA(c, cudaEventSynchronize(ev[3]));
+            cudaEventElapsedTime(&ms, ev[0], ev[1]);
+            t_kgen += ms;
+            cudaEventElapsedTime(&ms, ev[1], ev[2]);
+            t_fft += ms;
+            cudaEventElapsedTime(&ms, ev[2], ev[3]);
+            t_ext += ms;
+        }
+        for (auto& e : ev) cudaEventDestroy(e);
+        c->stats.ms_kgen = t_kgen;
+        c->stats.ms_kfft = t_fft + t_ext;
+        VC_CUDA(c, cudaGetLastError());
     }
     // ---- spatial partition: rank p owns a contiguous range of preconditioner
     // box rows along y, so every R_BD block stays on one rank; window row y -> rank (monotone)
@@ -1115,7 +1390,8 @@ vc_status operator_build(vc_ctx* c, const vc_build_opts* o) {
     for (int64_t i = 0; i < c->NL; ++i) ndl += c->h_cid[W > 1 ? c->h_gidx[i] : i] == 0;
     c->bytes_pass[0] = cb * nX1 + 4.0 * slots + 8.0 * NL;
     c->bytes_pass[1] = cb * (nX1r + nB);
-    c->bytes_pass[2] = cb * (nB + (double)nC) + 8.0 * (double)nkx * (My / 2 + 1) * (Mz / 2 + 1) * c->nblk;
+    c->bytes_pass[2] = cb * (nB + (double)nC) +
+                       8.0 * (double)nkx * (My / 2 + 1) * (c->zdirect ? c->ZU : Mz / 2 + 1) * c->nblk;
     c->bytes_pass[3] = cb * ((double)nC + nX4);
     c->bytes_pass[4] = cb * nX4r + 4.0 * slots_out + 8.0 * NL + (8.0 + 8.0 + 1.0) * ndl + 1.0 * NL;
     double tot = 0;
@@ -1232,6 +1508,13 @@ static MV make_mv(vc_ctx* c, const double* x, double* y) {
     mv.tw = c->tw.p;
     mv.planes = c->planes.p;
     mv.ZL = c->ZL;
+    mv.zdirect = c->zdirect;
+    mv.ZU = c->ZU;
+    mv.nog = c->nog;
+    for (int g = 0; g < c->nog; ++g) {
+        mv.og_f[g] = c->og_f[g];
+        mv.og_j[g] = c->og_j[g];
+    }
     for (int b = 0; b < 3; ++b) mv.nzin[b] = c->nzin[b];
     for (int f = 0; f < 6; ++f) mv.nzout[f] = f < c->nf ? c->nzout[f] : 0;
     const int W = c->world, r = c->rank;

@@ -59,22 +59,23 @@ def _single(st, fn, **build):
         return fn(c)
 
 
-CASES = [("R1", 2), ("R2", 3), ("R3", 2), ("R4", 4), ("R5", 2), ("C2", 2), ("C2", 3),
-         ("sphere12", 2), ("C1", 8)]
+CASES = [("R1", 2, 0), ("R2", 3, 0), ("R3", 2, 1), ("R3", 2, 2), ("R4", 4, 0), ("R5", 2, 1),
+         ("C2", 2, 2), ("C2", 3, 1), ("sphere12", 2, 0), ("C1", 8, 0)]
 
 
 def _st(name):
     return voxgen.sphere(12) if name == "sphere12" else voxgen.config(name)
 
 
-@pytest.mark.parametrize("name,W", CASES)
-def test_distributed_matvec_bitwise(name, W):
+@pytest.mark.parametrize("name,W,zmode", CASES)
+def test_distributed_matvec_bitwise(name, W, zmode):
     st = _st(name)
     box = (4, 4, 4)
     n = _single(st, lambda c: c.n, box=box)
     x = voxgen.seeded_vector(n, 21)
-    y1 = _single(st, lambda c: c.matvec(x), box=box)
-    res = _group(W, st, lambda c, r: (c.local_panels(), c.matvec(x[c.local_panels()])), box=box)
+    y1 = _single(st, lambda c: c.matvec(x), box=box, zmode=zmode)
+    res = _group(W, st, lambda c, r: (c.local_panels(), c.matvec(x[c.local_panels()])), box=box,
+                 zmode=zmode)
     idx = np.concatenate([g for g, _ in res])
     assert np.array_equal(np.sort(idx), np.arange(n)), "ranks must partition the panels"
     yd = np.empty(n)

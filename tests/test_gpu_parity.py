@@ -111,10 +111,12 @@ def _rel(a, b):
     return np.linalg.norm(a - b) / np.linalg.norm(b)
 
 
+@pytest.mark.parametrize("zmode", [0, 1, 2])
 @pytest.mark.parametrize("name", ["R1", "R2", "R3", "R4", "R5", "C1", "C2"])
-def test_matvec_dense_parity(ctx, name):
+def test_matvec_dense_parity(ctx, name, zmode):
+    """zmode 1: z-FFT (3-D circulant); 2: direct z-convolution on x/y spectra; 0: automatic."""
     st = voxgen.config(name)
-    p = _setup(ctx, st)
+    p = _setup(ctx, st, zmode=zmode)
     A = O.assemble(p)
     for seed in range(2):
         x = voxgen.seeded_vector(p.n, seed)
@@ -122,9 +124,21 @@ def test_matvec_dense_parity(ctx, name):
         assert _rel(y, A @ x) <= 1e-10, (name, ctx.grid(), _rel(y, A @ x))
 
 
+def test_zmodes_agree(ctx):
+    """The two exact z treatments give the same matvec to rounding."""
+    for name in ("C2", "R3", "sphere8"):
+        st = voxgen.sphere(8) if name == "sphere8" else voxgen.config(name)
+        _setup(ctx, st, zmode=1)
+        x = voxgen.seeded_vector(ctx.n, 13)
+        y1 = ctx.matvec(x)
+        ctx.build_operator(zmode=2)
+        y2 = ctx.matvec(x)
+        assert _rel(y2, y1) < 1e-13, name
+
+
 def test_matvec_padding_invariance(ctx):
     st = voxgen.config("R2")
-    _setup(ctx, st)
+    _setup(ctx, st, zmode=1)
     x = voxgen.seeded_vector(ctx.n, 3)
     y0 = ctx.matvec(x)
     M = ctx.grid()
@@ -143,12 +157,13 @@ def test_matvec_device_tensors(ctx):
     assert np.array_equal(y_host, y_dev)
 
 
-@pytest.mark.parametrize("name,nrows", [("C3", 6), ("C4", 4)])
-def test_matvec_row_sampled_full_size(ctx, name, nrows):
-    """BASELINE full sizes, the launch configuration bench.py times: sampled rows vs oracle."""
+@pytest.mark.parametrize("name,nrows,zmode", [("C3", 6, 0), ("C4", 4, 0), ("C4", 3, 1)])
+def test_matvec_row_sampled_full_size(ctx, name, nrows, zmode):
+    """BASELINE full sizes, the launch configuration bench.py times (zmode 0): sampled rows vs
+    oracle; C4 also through the z-FFT path it does not select automatically."""
     st = voxgen.config(name)
     ctx.set_structure(st)
-    ctx.build_operator()
+    ctx.build_operator(zmode=zmode)
     p = O.enumerate_panels(st.label, st.eps, st.eps_out, st.dv)
     x = voxgen.seeded_vector(p.n, 0)
     y = ctx.matvec(x)
@@ -176,10 +191,11 @@ def test_precond_parity(ctx, name, box):
 
 
 # ------------------------------------------------------------------------------ a11/a12 solve
+@pytest.mark.parametrize("zmode", [1, 2])
 @pytest.mark.parametrize("name", ["C1", "R1", "R2", "R3", "R4", "R5"])
-def test_capacitance_parity(ctx, name):
+def test_capacitance_parity(ctx, name, zmode):
     st = voxgen.config(name)
-    p = _setup(ctx, st)
+    p = _setup(ctx, st, zmode=zmode)
     C, info = ctx.solve_capacitance(tol=1e-12, maxit=3000)
     Cref = O.solve_capacitance(p)
     assert all(i["converged"] for i in info)

@@ -81,8 +81,21 @@ __device__ __forceinline__ int kx_owner(const MV& mv, int k) {
 
 // ---- tile-size choices (compile-time functions of the FFT length) -----------------------
 constexpr int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
-template <int L> struct TX { static constexpr int T = clampi(4096 / L, 1, 64); };   // x passes
-template <int L> struct TY { static constexpr int T = clampi(4096 / L, 1, 32); };   // y passes
+// x passes (contiguous lines): T pencils of length L per CTA with NT threads (one stage-0
+// radix-16 butterfly per thread) and 32 KB of shared memory (L <= 2048), so ~6 CTAs per SM
+// overlap their load, transform and store phases.  y passes (strided, pencil = one kx column)
+// keep 4 adjacent kx per CTA (64-byte row segments; measured faster than 2).
+template <int L> struct FX {
+    static constexpr int T = clampi(2048 / L, 1, 64);
+    static constexpr int NT = clampi(T * L / 16, 64, 256);
+    static constexpr int MINB = 65536 / (NT * 80) < 1 ? 1 : 65536 / (NT * 80);  // <= 80 regs
+};
+template <int L> struct FY {
+    static constexpr int T = clampi(4096 / L, 1, 32);
+    static constexpr int NT = 256;
+};
+template <int L> struct TX { static constexpr int T = FX<L>::T; };
+template <int L> struct TY { static constexpr int T = FY<L>::T; };
 constexpr int kNT = 256;
 constexpr int kNT3 = 256;  // P3 threads per CTA
 constexpr int kMaxLz = 256;
@@ -95,7 +108,7 @@ __device__ __forceinline__ int ktil(int k, int M) { return k <= M / 2 ? k : k - 
 // P1: scatter + forward R2C along x
 // ---------------------------------------------------------------------------------------
 template <int L>
-__global__ void __launch_bounds__(kNT) k_p1(MV mv) {
+__global__ void __launch_bounds__(FX<L>::NT, FX<L>::MINB) k_p1(MV mv) {
     constexpr int T = TX<L>::T;
     extern __shared__ double2 sm[];
     const int beta = blockIdx.y;
@@ -135,11 +148,11 @@ __global__ void __launch_bounds__(kNT) k_p1(MV mv) {
         return make_double2(re, im);
     };
     auto sts = [&](int t, int p, double2 v) { sm[smi<L, T, false>(t, p)] = v; };
-    fft_run<L, T, kNT, false, false>(sm, ld0, sts, mv.tw);
+    fft_run<L, T, FX<L>::NT, false, false>(sm, ld0, sts, mv.tw);
     __syncthreads();
     constexpr int K = L / 2 + 1;
     const bool ph = beta != 0;  // c_beta,x = 1/2 for y- and z-normal panels
-    for (int u = threadIdx.x; u < T * K; u += kNT) {
+    for (int u = threadIdx.x; u < T * K; u += FX<L>::NT) {
         const int t = u / K, k = u % K;
         const int q = ch * T + t;
         if (q >= nyp) continue;
@@ -165,7 +178,7 @@ __global__ void __launch_bounds__(kNT) k_p1(MV mv) {
 // P2: forward C2C along y (zero-padded input), times conj(phi_beta,y)
 // ---------------------------------------------------------------------------------------
 template <int L>
-__global__ void __launch_bounds__(kNT) k_p2(MV mv) {
+__global__ void __launch_bounds__(FY<L>::NT) k_p2(MV mv) {
     constexpr int T = TY<L>::T;
     extern __shared__ double2 sm[];
     const int beta = blockIdx.y;
@@ -196,7 +209,7 @@ __global__ void __launch_bounds__(kNT) k_p2(MV mv) {
         out[((((int64_t)qq * nt3 + (kx >> mv.lgT3)) * 2 + side) * nzb + j) * mv.T3 +
             (kx & (mv.T3 - 1))] = v;
     };
-    fft_run<L, T, kNT, false, true>(sm, ld0, stN, mv.tw);
+    fft_run<L, T, FY<L>::NT, false, true>(sm, ld0, stN, mv.tw);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -377,7 +390,7 @@ __global__ void __launch_bounds__(kNT3) k_p3(MV mv) {
 // P4: times phi_f,y, inverse C2C along y, pruned to y < ey_f
 // ---------------------------------------------------------------------------------------
 template <int L>
-__global__ void __launch_bounds__(kNT) k_p4(MV mv) {
+__global__ void __launch_bounds__(FY<L>::NT, 3) k_p4(MV mv) {
     constexpr int T = TY<L>::T;
     extern __shared__ double2 sm[];
     const int f = blockIdx.y;
@@ -406,14 +419,14 @@ __global__ void __launch_bounds__(kNT) k_p4(MV mv) {
             mv.S2[pr][f][((int64_t)j * mv.nr[pr][3 + f] + (yy - mv.ya[pr])) * nkx + kx] = v;
         }
     };
-    fft_run<L, T, kNT, true, true>(sm, ld0, stN, mv.tw);
+    fft_run<L, T, FY<L>::NT, true, true>(sm, ld0, stN, mv.tw);
 }
 
 // ---------------------------------------------------------------------------------------
 // P5: times phi_f,x, C2R along x (two lines per complex FFT), gather + dielectric terms
 // ---------------------------------------------------------------------------------------
 template <int L>
-__global__ void __launch_bounds__(kNT) k_p5(MV mv) {
+__global__ void __launch_bounds__(FX<L>::NT, FX<L>::MINB) k_p5(MV mv) {
     constexpr int T = TX<L>::T;
     extern __shared__ double2 sm[];
     const int f = blockIdx.y;
@@ -477,7 +490,7 @@ __global__ void __launch_bounds__(kNT) k_p5(MV mv) {
             if (p1 >= 0) put(p1, v.y);
         }
     };
-    fft_run<L, T, kNT, true, false>(sm, ld0, stN, mv.tw);
+    fft_run<L, T, FX<L>::NT, true, false>(sm, ld0, stN, mv.tw);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -608,7 +621,7 @@ __global__ void k_extract2d(const double2* __restrict__ G, double* __restrict__ 
 
 // in-place C2C FFT of contiguous lines: data[line][L]
 template <int L, bool INV>
-__global__ void __launch_bounds__(kNT) k_fft_lines(double2* data, int64_t nlines,
+__global__ void __launch_bounds__(FX<L>::NT) k_fft_lines(double2* data, int64_t nlines,
                                                    const double2* __restrict__ tw) {
     constexpr int T = TX<L>::T;
     extern __shared__ double2 sm[];
@@ -619,13 +632,13 @@ __global__ void __launch_bounds__(kNT) k_fft_lines(double2* data, int64_t nlines
     auto stN = [&](int t, int p, double2 v) {
         if (l0 + t < nlines) data[(l0 + t) * L + Plan<L>::freq(p)] = v;
     };
-    fft_run<L, T, kNT, INV, false>(sm, ld0, stN, tw);
+    fft_run<L, T, FX<L>::NT, INV, false>(sm, ld0, stN, tw);
 }
 
 // in-place C2C FFT along a strided axis: element n of column c in batch b at
 // data[b*bs + n*es + c], columns c in [0, ncols) contiguous.
 template <int L>
-__global__ void __launch_bounds__(kNT) k_fft_strided(double2* data, int64_t es, int64_t ncols,
+__global__ void __launch_bounds__(FY<L>::NT) k_fft_strided(double2* data, int64_t es, int64_t ncols,
                                                      int64_t bs, const double2* __restrict__ tw) {
     constexpr int T = TY<L>::T;
     extern __shared__ double2 sm[];
@@ -638,7 +651,7 @@ __global__ void __launch_bounds__(kNT) k_fft_strided(double2* data, int64_t es, 
     auto stN = [&](int t, int p, double2 v) {
         if (c0 + t < ncols) base[(int64_t)Plan<L>::freq(p) * es + t] = v;
     };
-    fft_run<L, T, kNT, false, true>(sm, ld0, stN, tw);
+    fft_run<L, T, FY<L>::NT, false, true>(sm, ld0, stN, tw);
 }
 
 // Folded spectrum of block `blk`, tile-major for P3:
@@ -686,6 +699,9 @@ __global__ void k_debug_kappa(int n, const int32_t* kind, const int32_t* a, cons
 // ---------------------------------------------------------------------------------------
 template <class K>
 static cudaError_t prep(K kern, size_t smem) {
+    // all-shared carveout: the FFT passes are shared-memory-resident, so more CTAs per SM
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    if (e) return e;
     if (smem > 48 * 1024) return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     return cudaSuccess;
 }
@@ -715,7 +731,7 @@ static cudaError_t launch_p1(const MV& mv, cudaStream_t st) {
         cudaError_t e = prep(k_p1<LL>, smem);
         if (e) return e;
         dim3 grid(std::max(1, maxch * maxz), 3);
-        k_p1<LL><<<grid, kNT, smem, st>>>(mv);
+        k_p1<LL><<<grid, FX<LL>::NT, smem, st>>>(mv);
     });
     return cudaGetLastError();
 }
@@ -728,7 +744,7 @@ static cudaError_t launch_p2(const MV& mv, cudaStream_t st) {
         cudaError_t e = prep(k_p2<LL>, smem);
         if (e) return e;
         dim3 grid(std::max(1, ((mv.nkx + T - 1) / T) * maxz), 3);
-        k_p2<LL><<<grid, kNT, smem, st>>>(mv);
+        k_p2<LL><<<grid, FY<LL>::NT, smem, st>>>(mv);
     });
     return cudaGetLastError();
 }
@@ -961,7 +977,7 @@ static cudaError_t launch_p4(const MV& mv, cudaStream_t st) {
         cudaError_t e = prep(k_p4<LL>, smem);
         if (e) return e;
         dim3 grid(std::max(1, ((mv.nkx + T - 1) / T) * maxz), mv.nf);
-        k_p4<LL><<<grid, kNT, smem, st>>>(mv);
+        k_p4<LL><<<grid, FY<LL>::NT, smem, st>>>(mv);
     });
     return cudaGetLastError();
 }
@@ -975,7 +991,7 @@ static cudaError_t launch_p5(const MV& mv, cudaStream_t st) {
         cudaError_t e = prep(k_p5<LL>, smem);
         if (e) return e;
         dim3 grid(std::max(1, maxch * maxz), mv.nf);
-        k_p5<LL><<<grid, kNT, smem, st>>>(mv);
+        k_p5<LL><<<grid, FX<LL>::NT, smem, st>>>(mv);
     });
     return cudaGetLastError();
 }
@@ -988,11 +1004,11 @@ static cudaError_t launch_fft_lines(double2* d, int L, int64_t nlines, bool inv,
         if (inv) {
             cudaError_t e = prep(k_fft_lines<LL, true>, smem);
             if (e) return e;
-            k_fft_lines<LL, true><<<grid, kNT, smem, st>>>(d, nlines, tw);
+            k_fft_lines<LL, true><<<grid, FX<LL>::NT, smem, st>>>(d, nlines, tw);
         } else {
             cudaError_t e = prep(k_fft_lines<LL, false>, smem);
             if (e) return e;
-            k_fft_lines<LL, false><<<grid, kNT, smem, st>>>(d, nlines, tw);
+            k_fft_lines<LL, false><<<grid, FX<LL>::NT, smem, st>>>(d, nlines, tw);
         }
     });
     return cudaGetLastError();
@@ -1006,7 +1022,7 @@ static cudaError_t launch_fft_strided(double2* d, int L, int64_t es, int64_t nco
         cudaError_t e = prep(k_fft_strided<LL>, smem);
         if (e) return e;
         const unsigned grid = (unsigned)(((ncols + T - 1) / T) * nbatch);
-        k_fft_strided<LL><<<grid, kNT, smem, st>>>(d, es, ncols, bs, tw);
+        k_fft_strided<LL><<<grid, FY<LL>::NT, smem, st>>>(d, es, ncols, bs, tw);
     });
     return cudaGetLastError();
 }

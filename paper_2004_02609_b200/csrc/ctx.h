@@ -10,12 +10,13 @@
 
 namespace vc {
 
-// Owning device buffer (cudaMallocAsync on the context stream would tie lifetime to the
-// stream; plain cudaMalloc keeps it simple for setup-time allocations).
+// Owning, grow-only device buffer: alloc() reuses the allocation when it is large enough, so
+// repeated extractions of same-sized problems never call cudaMalloc / cudaFree (cudaFree
+// synchronises the device) after the first one.  reset() releases the memory.
 template <class T>
 struct DevBuf {
     T* p = nullptr;
-    size_t n = 0;
+    size_t n = 0, cap = 0;
     DevBuf() = default;
     DevBuf(const DevBuf&) = delete;
     DevBuf& operator=(const DevBuf&) = delete;
@@ -23,13 +24,17 @@ struct DevBuf {
     void reset() {
         if (p) cudaFree(p);
         p = nullptr;
-        n = 0;
+        n = cap = 0;
     }
     cudaError_t alloc(size_t count) {
+        if (p && count <= cap) {
+            n = count;
+            return cudaSuccess;
+        }
         reset();
         if (count == 0) return cudaSuccess;
         cudaError_t e = cudaMalloc(&p, count * sizeof(T));
-        if (e == cudaSuccess) n = count;
+        if (e == cudaSuccess) n = cap = count;
         else p = nullptr;
         return e;
     }
@@ -132,6 +137,17 @@ struct vc_ctx {
     std::vector<size_t> a2a_sb[2], a2a_rb[2];
     size_t offS1[vc::kMaxRanks][3] = {}, offR1[vc::kMaxRanks][3] = {};
     size_t offS2[vc::kMaxRanks][6] = {}, offR2[vc::kMaxRanks][6] = {};
+
+    // ---- reusable scratch (grow-only; see DevBuf) ----
+    vc::DevBuf<double2> kG;            // kernel-spectra build grid
+    vc::DevBuf<double> kKo;            // kernel octant table
+    vc::DevBuf<double> cap_b, cap_rho, cap_part, cap_col;  // capacitance columns
+    vc::DevBuf<double> io_in, io_out;  // host-vector calls
+    vc::DevBuf<int32_t> in_label;      // host voxel inputs
+    vc::DevBuf<double> in_eps;
+    vc::DevBuf<unsigned char> geo_flags;    // panel indexing temporaries
+    vc::DevBuf<int> geo_pres, geo_ext;
+    vc::DevBuf<int64_t> geo_tiles, geo_total;
 
     // ---- solver work ----
     vc::DevBuf<double> work;  // Krylov basis + temporaries

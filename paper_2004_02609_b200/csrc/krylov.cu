@@ -303,9 +303,9 @@ vc_status capacitance_dev(vc_ctx* c, double* h_C, const vc_solve_opts* o, vc_sol
     const int m = c->m;
     const int32_t* cid = c->world > 1 ? c->lp.cid.p : c->pan.cid.p;
     const double* fc = c->world > 1 ? c->lp.fc.p : c->pan.fc.p;
-    DevBuf<double> b, rho, part, col;
-    VC_CUDA(c, b.alloc(n));
-    VC_CUDA(c, rho.alloc(n));
+    DevBuf<double>&b = c->cap_b, &rho = c->cap_rho, &part = c->cap_part, &col = c->cap_col;
+    VC_CUDA(c, b.alloc(std::max<int64_t>(1, n)));
+    VC_CUDA(c, rho.alloc(std::max<int64_t>(1, n)));
     const unsigned nb = 148;
     VC_CUDA(c, part.alloc((size_t)nb * m));
     VC_CUDA(c, col.alloc(m));

@@ -1246,8 +1246,8 @@ vc_status operator_build(vc_ctx* c, const vc_build_opts* o) {
         cudaEvent_t ev[4];
         for (auto& e : ev) VC_CUDA(c, cudaEventCreate(&e));
         float t_kgen = 0, t_fft = 0, t_ext = 0, ms;
-        DevBuf<double2> G;
-        DevBuf<double> Ko;
+        DevBuf<double2>& G = c->kG;
+        DevBuf<double>& Ko = c->kKo;
         const bool zd = c->zdirect;
         // z-FFT mode: full 3-D cyclic grid; direct-z mode: x/y-cyclic grid x ZU octant z offsets
         const int MZ = zd ? c->ZU : M[2];

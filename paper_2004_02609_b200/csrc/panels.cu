@@ -262,8 +262,9 @@ __global__ void k_emit(Geo g, int64_t Ftot, const int64_t* __restrict__ tile_off
 vc_status geometry_build(vc_ctx* c, const int32_t* d_label, const double* d_eps) {
     const int64_t nvox = (int64_t)c->nx * c->ny * c->nz;
     cudaStream_t st = c->stream;
-    DevBuf<Flags> fl;
-    VC_CUDA(c, fl.alloc(1));
+    DevBuf<unsigned char>& flb = c->geo_flags;
+    VC_CUDA(c, flb.alloc(sizeof(Flags)));
+    struct { Flags* p; } fl{reinterpret_cast<Flags*>(flb.p)};
     Flags h0{INT32_MAX, INT32_MIN, 0, 0};
     VC_CUDA(c, cudaMemcpyAsync(fl.p, &h0, sizeof(Flags), cudaMemcpyHostToDevice, st));
     const int vblocks = (int)std::min<int64_t>((nvox + 255) / 256, 148 * 16);
@@ -277,7 +278,7 @@ vc_status geometry_build(vc_ctx* c, const int32_t* d_label, const double* d_eps)
     if (hf.bad_eps) return set_err(c, VC_ERR_INPUT, "eps_r must be finite and > 0");
     const int m = hf.max_label;
     {
-        DevBuf<int> pres;
+        DevBuf<int>& pres = c->geo_pres;
         VC_CUDA(c, pres.alloc((size_t)m + 1));
         VC_CUDA(c, cudaMemsetAsync(pres.p, 0, sizeof(int) * (m + 1), st));
         k_presence<<<vblocks, 256, 0, st>>>(nvox, d_label, pres.p);
@@ -303,7 +304,7 @@ vc_status geometry_build(vc_ctx* c, const int32_t* d_label, const double* d_eps)
     g.label = d_label;
     g.eps = d_eps;
     const int64_t ntiles = (Ftot + kTile - 1) / kTile;
-    DevBuf<int64_t> tiles, total;
+    DevBuf<int64_t>&tiles = c->geo_tiles, &total = c->geo_total;
     VC_CUDA(c, tiles.alloc(ntiles));
     VC_CUDA(c, total.alloc(1));
     k_count<<<(unsigned)ntiles, kNT, 0, st>>>(g, Ftot, tiles.p, fl.p);
@@ -329,7 +330,7 @@ vc_status geometry_build(vc_ctx* c, const int32_t* d_label, const double* d_eps)
     VC_CUDA(c, P.ibar.alloc(N));
     VC_CUDA(c, P.fc.alloc(N));
     for (int a = 0; a < 3; ++a) VC_CUDA(c, P.slotmap[a].alloc(g.F[a]));
-    DevBuf<int> ext;
+    DevBuf<int>& ext = c->geo_ext;
     VC_CUDA(c, ext.alloc(36));
     std::vector<int> hext(36);
     for (int q = 0; q < 6; ++q)

@@ -127,10 +127,11 @@ void precond_free(vc_ctx* c) {
 }
 
 vc_status precond_build(vc_ctx* c, const int32_t box_in[3], int kind) {
-    precond_free(c);
-    Precond* pc = new Precond();
-    c->pc = pc;
+    if (!c->pc) c->pc = new Precond();  // kept across builds: its buffers are grow-only
+    Precond* pc = c->pc;
     pc->kind = kind;
+    pc->nbox = pc->nuniq = pc->max_n = 0;
+    pc->block_doubles = 0;
     cudaStream_t st = c->stream;
     const int64_t N = c->NL;  // this rank's panels (boxes never straddle ranks)
     auto G = [&](int64_t i) { return c->world > 1 ? c->h_gidx[i] : i; };  // local -> global

@@ -30,34 +30,17 @@ struct DeviceGuard {
         (c)->err.clear();                      \
     } while (0)
 
+// Dropping state keeps the device allocations (grow-only DevBufs): the next geometry / build
+// of a same-sized problem reuses them without cudaMalloc / cudaFree.  vc_destroy frees.
 void drop_operator(vc_ctx* c) {
     c->has_op = false;
-    c->Rt.reset();
-    c->bufA.reset();
-    c->bufB.reset();
-    c->bufC.reset();
-    c->bufS.reset();
-    c->lp.info.reset();
-    c->lp.ibar.reset();
-    c->lp.fc.reset();
-    c->lp.cid.reset();
-    c->lp.gidx.reset();
-    for (auto& s : c->lp.slotmap) s.reset();
     c->h_gidx.clear();
     c->NL = 0;
-    c->work.reset();
-    c->work_n = 0;
-    precond_free(c);
 }
 
 void drop_geometry(vc_ctx* c) {
     drop_operator(c);
     c->has_geom = false;
-    PanelsDev& P = c->pan;
-    P.axis.reset(); P.sign.reset(); P.info.reset();
-    P.si.reset(); P.sj.reset(); P.sk.reset(); P.cid.reset();
-    P.eps_d.reset(); P.eps_b.reset(); P.ibar.reset(); P.fc.reset();
-    for (auto& s : P.slotmap) s.reset();
     c->N = c->Nc = c->Nd = 0;
     c->m = 0;
 }
@@ -68,7 +51,7 @@ vc_status with_vectors(vc_ctx* c, const double* in, double* out, int on_device, 
                        F&& f) {
     if (on_device) return f(in, out);
     const int64_t n = c->NL;
-    DevBuf<double> din, dout;
+    DevBuf<double>&din = c->io_in, &dout = c->io_out;
     VC_CUDA(c, din.alloc(n));
     VC_CUDA(c, dout.alloc(n));
     VC_CUDA(c, cudaMemcpyAsync(din.p, in, 8 * n, cudaMemcpyHostToDevice, c->stream));
@@ -116,6 +99,7 @@ void vc_destroy(vc_ctx* c) {
         DeviceGuard g(c->device);
         cudaStreamSynchronize(c->stream);
         drop_geometry(c);
+        precond_free(c);
         comm_free(c);
         c->tw.reset();
         c->partial.reset();
@@ -148,8 +132,8 @@ vc_status vc_set_geometry(vc_ctx* c, int32_t nx, int32_t ny, int32_t nz, double 
     c->dv = dv_m;
     c->eps_out = eps_r_outside;
     const int64_t nvox = (int64_t)nx * ny * nz;
-    DevBuf<int32_t> dl;
-    DevBuf<double> de;
+    DevBuf<int32_t>& dl = c->in_label;
+    DevBuf<double>& de = c->in_eps;
     const int32_t* pl = label;
     const double* pe = eps_r;
     if (!on_device) {

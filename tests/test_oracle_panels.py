@@ -1,4 +1,6 @@
 """Pins for the oracle's panel enumeration (a1) -- CPU only (S:60-64, S:77-79 ideas)."""
+import os
+
 import numpy as np
 import pytest
 
@@ -97,3 +99,17 @@ def test_input_errors(case):
         eps[0, 0, 0] = np.nan
     with pytest.raises(O.OracleInputError):
         O.enumerate_panels(lab, eps)
+
+
+def test_coated_sphere_panel_counts_match_paper():
+    """the coated sphere (r_c = 0.25 m, r_d = 0.5 m) at dv = 0.05 / 0.025 / 0.02 / 0.01 m
+    has N_i voxels and N panels as printed (golden values, tests/golden/pins.json)."""
+    import json
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "pins.json")))
+    pin = g["coated_sphere_panel_counts"]
+    for dv, ni, n in zip(pin["dv_m"], pin["N_i"], pin["N"]):
+        rc, rd = pin["r_c_m"] / dv, pin["r_d_m"] / dv
+        st = voxgen.coated_sphere(rc, rd, 2.0, dv=dv)
+        assert st.label.size == ni
+        p = O.enumerate_panels(st.label, st.eps, 1.0, st.dv)
+        assert p.n == n, (dv, p.n, n)

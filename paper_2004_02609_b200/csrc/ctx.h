@@ -117,6 +117,9 @@ struct vc_ctx {
     int T3 = 1, nt3 = 1;   // P3 tile width and kx-tile count (tile-major X2 / R layouts)
     bool zdirect = false;  // P3 direct-z mode (operator.cu k_p3d)
     int ZU = 0, nog = 0, og_f[64] = {}, og_j[64] = {};
+    unsigned long long og_contig = 0;  // k_p3d groups with consecutive output planes
+    int src_contig = 0;                // sources with consecutive planes
+    std::vector<int32_t> h_planes;     // host copy of the plane lists
     size_t rchunk = 0;     // doubles of R per P3 tile
     int ZL = 0, nzin[3] = {0, 0, 0}, nzout[6] = {0, 0, 0, 0, 0, 0};  // active z-plane counts
     vc::DevBuf<int32_t> planes;  // plane lists + inverse maps (operator.cu)

@@ -64,6 +64,8 @@ struct MV {
     // P3 direct-z mode: output groups (field, first plane) of kZB planes each
     int zdirect, ZU, nog;
     int og_f[kMaxOG], og_j[kMaxOG];
+    unsigned long long og_contig;  // bit og: the group's output planes are consecutive
+    int src_contig;                // bit b: source b's planes are consecutive
 };
 
 __device__ __forceinline__ int zlist(const MV& mv, int g, int j) { return mv.planes[g * mv.ZL + j]; }
@@ -785,6 +787,36 @@ __device__ __forceinline__ void p3d_acc(double2 (&a0)[kZB], double2 (&a1)[kZB],
     }
 }
 
+// Contiguous output planes (zo_k = zo_0 + k) and contiguous input planes (zi = zi_0 + j): the K
+// values a thread needs for input j are the window g2 = G0 - 2 j + 2 k (k < NZO), so moving to
+// input j + 1 shifts the window by one and loads a single new value (register sliding window).
+template <int NZO, bool ODD, int T>
+__device__ __forceinline__ void p3d_acc_win(double2 (&a0)[kZB], double2 (&a1)[kZB], int G0,
+                                            int s2a, const double* Kb, const double2* X, int n) {
+    auto kval = [&](int g2) {
+        const double v = Kb[(((g2 < 0 ? -g2 : g2) - s2a) >> 1) * T];
+        return (ODD && g2 < 0) ? -v : v;
+    };
+    double w[NZO];
+#pragma unroll
+    for (int k = 0; k < NZO; ++k) w[k] = kval(G0 + 2 * k);
+#pragma unroll 2
+    for (int ji = 0; ji < n; ++ji) {
+        const double2 q0 = X[ji * T];
+        const double2 q1 = X[(n + ji) * T];  // side 1 (unused when nside = 1)
+#pragma unroll
+        for (int k = 0; k < NZO; ++k) {
+            a0[k].x = fma(w[k], q0.x, a0[k].x);
+            a0[k].y = fma(w[k], q0.y, a0[k].y);
+            a1[k].x = fma(w[k], q1.x, a1[k].x);
+            a1[k].y = fma(w[k], q1.y, a1[k].y);
+        }
+#pragma unroll
+        for (int k = NZO - 1; k > 0; --k) w[k] = w[k - 1];
+        w[0] = kval(G0 - 2 * (ji + 1));
+    }
+}
+
 // Persistent and TMA-fed like the z-FFT P3: a tile's X2 rows and K rows are contiguous (tile-
 // major layouts), so one thread fetches the next tile with four cp.async.bulk copies into the
 // other half of a two-stage ring while the CTA computes the current tile from shared memory.
@@ -857,7 +889,24 @@ __global__ void __launch_bounds__(256) k_p3d(MV mv) {
                 const double2* X = xs + (b == 0 ? 0 : (b == 1 ? xo1 : xo2)) + t;
                 const int* zi2 = zl + b * ZL;
                 const int s2a = s2 != 0;
-                if (kind == 1 && alpha == 2) {  // E^{z.}: odd in z
+                if (((mv.og_contig >> og) & 1) && ((mv.src_contig >> b) & 1)) {
+                    const int G0 = zo2[0] - zi2[0];
+                    if (kind == 1 && alpha == 2) {
+                        switch (nzo) {
+                            case 1: p3d_acc_win<1, true, T>(a0, a1, G0, s2a, Kb, X, nzb); break;
+                            case 2: p3d_acc_win<2, true, T>(a0, a1, G0, s2a, Kb, X, nzb); break;
+                            case 3: p3d_acc_win<3, true, T>(a0, a1, G0, s2a, Kb, X, nzb); break;
+                            default: p3d_acc_win<4, true, T>(a0, a1, G0, s2a, Kb, X, nzb); break;
+                        }
+                    } else {
+                        switch (nzo) {
+                            case 1: p3d_acc_win<1, false, T>(a0, a1, G0, s2a, Kb, X, nzb); break;
+                            case 2: p3d_acc_win<2, false, T>(a0, a1, G0, s2a, Kb, X, nzb); break;
+                            case 3: p3d_acc_win<3, false, T>(a0, a1, G0, s2a, Kb, X, nzb); break;
+                            default: p3d_acc_win<4, false, T>(a0, a1, G0, s2a, Kb, X, nzb); break;
+                        }
+                    }
+                } else if (kind == 1 && alpha == 2) {  // E^{z.}: odd in z
                     switch (nzo) {
                         case 1: p3d_acc<1, true, T>(a0, a1, zo2, s2a, Kb, X, nzb, zi2); break;
                         case 2: p3d_acc<2, true, T>(a0, a1, zo2, s2a, Kb, X, nzb, zi2); break;
@@ -1194,6 +1243,7 @@ vc_status operator_build(vc_ctx* c, const vc_build_opts* o) {
             else c->nzout[g - 3] = n;
         }
         c->ZL = ZL;
+        c->h_planes = hp;
         VC_CUDA(c, c->planes.alloc(hp.size()));
         VC_CUDA(c, cudaMemcpyAsync(c->planes.p, hp.data(), 4 * hp.size(), cudaMemcpyHostToDevice, st));
         VC_CUDA(c, cudaStreamSynchronize(st));
@@ -1221,13 +1271,23 @@ vc_status operator_build(vc_ctx* c, const vc_build_opts* o) {
             return set_err(c, VC_ERR_UNSUPPORTED, "direct-z mode: too many output planes");
         c->ZU = c->ZL;
         c->nog = 0;
-        if (c->zdirect)
+        c->og_contig = 0;
+        c->src_contig = 0;
+        auto plane = [&](int g, int j) { return c->h_planes[(size_t)g * c->ZL + j]; };
+        if (c->zdirect) {
             for (int f = 0; f < c->nf; ++f)
                 for (int j = 0; j < c->nzout[f]; j += kZB) {
+                    const int nzo = std::min(kZB, c->nzout[f] - j);
+                    if (plane(3 + f, j + nzo - 1) - plane(3 + f, j) == nzo - 1)
+                        c->og_contig |= 1ull << c->nog;
                     c->og_f[c->nog] = f;
                     c->og_j[c->nog] = j;
                     ++c->nog;
                 }
+            for (int b = 0; b < 3; ++b)
+                if (c->nzin[b] > 0 && plane(b, c->nzin[b] - 1) - plane(b, 0) == c->nzin[b] - 1)
+                    c->src_contig |= 1 << b;
+        }
     }
     // P3 tile width and the tile-major spectrum layout (one contiguous chunk per P3 tile)
     c->T3 = c->zdirect ? kDirectT : p3_tile(Mz, c->nf);
@@ -1527,6 +1587,8 @@ static MV make_mv(vc_ctx* c, const double* x, double* y) {
     mv.zdirect = c->zdirect;
     mv.ZU = c->ZU;
     mv.nog = c->nog;
+    mv.og_contig = c->og_contig;
+    mv.src_contig = c->src_contig;
     for (int g = 0; g < c->nog; ++g) {
         mv.og_f[g] = c->og_f[g];
         mv.og_j[g] = c->og_j[g];

@@ -101,8 +101,9 @@ template <int L> struct TY { static constexpr int T = FY<L>::T; };
 constexpr int kNT = 256;
 constexpr int kNT3 = 256;  // P3 threads per CTA
 constexpr int kMaxLz = 256;
-constexpr int kDirectT = 8;  // P3 direct-z tile width (kx per tile)
-constexpr int kZB = 4;       // P3 direct-z: output planes per thread  // largest z FFT length (P3 keeps whole z-pencils in shared memory)
+constexpr int kDirectT = 16;  // P3 direct-z tile width (kx per tile = lanes per output group)
+constexpr int kZB = 4;       // P3 direct-z: output planes per thread
+constexpr int kP3dStages = 2;  // P3 direct-z TMA stages (measured: 2 beat 1 stage + more CTAs)  // largest z FFT length (P3 keeps whole z-pencils in shared memory)
 
 __device__ __forceinline__ int ktil(int k, int M) { return k <= M / 2 ? k : k - M; }
 
@@ -820,6 +821,7 @@ __device__ __forceinline__ void p3d_acc_win(double2 (&a0)[kZB], double2 (&a1)[kZ
 // Persistent and TMA-fed like the z-FFT P3: a tile's X2 rows and K rows are contiguous (tile-
 // major layouts), so one thread fetches the next tile with four cp.async.bulk copies into the
 // other half of a two-stage ring while the CTA computes the current tile from shared memory.
+template <int NST>  // stages of the TMA ring (1: no prefetch, more CTAs per SM)
 __global__ void __launch_bounds__(256) k_p3d(MV mv) {
     constexpr int T = kDirectT;
     extern __shared__ __align__(16) double2 sd[];
@@ -831,9 +833,9 @@ __global__ void __launch_bounds__(256) k_p3d(MV mv) {
     const int xo1 = 2 * T * nz0, xo2 = 2 * T * (nz0 + nz1);
     const int XS = 2 * T * (nz0 + nz1 + nz2);  // double2 per stage
     const int RC = mv.rchunk;                  // doubles per stage (even)
-    double2* xin = sd;                                          // [2][XS]
-    double* kin = reinterpret_cast<double*>(xin + 2 * XS);      // [2][RC]
-    int* zl = reinterpret_cast<int*>(kin + 2 * RC);             // [9][ZL] plane lists
+    double2* xin = sd;                                          // [NST][XS]
+    double* kin = reinterpret_cast<double*>(xin + NST * XS);    // [NST][RC]
+    int* zl = reinterpret_cast<int*>(kin + NST * RC);           // [9][ZL] plane lists
     uint64_t* bar = reinterpret_cast<uint64_t*>(zl + ((9 * ZL + 3) & ~3));  // [2]
     if (threadIdx.x == 0) {
         mbar_init(&bar[0], 1);
@@ -851,14 +853,17 @@ __global__ void __launch_bounds__(256) k_p3d(MV mv) {
         if (nz2) bulk_g2s(xin + s * XS + xo2, mv.X2[2] + qt * 2 * T * nz2, 32u * T * nz2, &bar[s]);
         bulk_g2s(kin + s * RC, mv.Rt + qt * RC, 8u * RC, &bar[s]);
     };
-    if (threadIdx.x == 0 && (int)blockIdx.x < ntiles) issue(blockIdx.x, 0);
+    if (NST > 1 && threadIdx.x == 0 && (int)blockIdx.x < ntiles) issue(blockIdx.x, 0);
     unsigned par0 = 0, par1 = 0;
     int it = 0;
     for (int tl = blockIdx.x; tl < ntiles; tl += gridDim.x, ++it) {
-        const int st = it & 1;
-        if (threadIdx.x == 0 && tl + (int)gridDim.x < ntiles) {
-            fence_proxy_async();
-            issue(tl + gridDim.x, st ^ 1);
+        const int st = NST == 1 ? 0 : (it & 1);
+        if (threadIdx.x == 0) {
+            const int nxt = tl + (NST - 1) * (int)gridDim.x;
+            if (nxt < ntiles) {
+                fence_proxy_async();
+                issue(nxt, NST == 1 ? 0 : (st ^ 1));
+            }
         }
         if (st == 0) { mbar_wait(&bar[0], par0); par0 ^= 1; }
         else { mbar_wait(&bar[1], par1); par1 ^= 1; }
@@ -870,6 +875,7 @@ __global__ void __launch_bounds__(256) k_p3d(MV mv) {
         const int nside = (q == 0 || 2 * q == My) ? 1 : 2;
         for (int og = og0; og < mv.nog; og += OGS) {
             const int f = mv.og_f[og], jo0 = mv.og_j[og];
+            if (f < 0) continue;  // padding slot: keeps the warp's two groups alike
             const int nzo = min(kZB, mv.nzout[f] - jo0);
             const int kind = mv.fkind[f], alpha = mv.faxis[f];
             double2 a0[kZB], a1[kZB];
@@ -950,18 +956,19 @@ static cudaError_t launch_p3d(const MV& mv, cudaStream_t st) {
     if (ntiles == 0 || mv.nog == 0) return cudaSuccess;
     const int ogs = std::min(mv.nog, 256 / kDirectT);
     const int nthr = kDirectT * ogs;
-    const size_t smem = 2 * (16 * (size_t)2 * kDirectT * (mv.nzin[0] + mv.nzin[1] + mv.nzin[2]) +
-                             8 * (size_t)mv.rchunk) +
+    constexpr int NST = kP3dStages;
+    const size_t smem = NST * (16 * (size_t)2 * kDirectT * (mv.nzin[0] + mv.nzin[1] + mv.nzin[2]) +
+                               8 * (size_t)mv.rchunk) +
                         4 * (size_t)((9 * mv.ZL + 3) & ~3) + 2 * sizeof(uint64_t);
     if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
-    cudaError_t e = prep(k_p3d, smem);
+    cudaError_t e = prep(k_p3d<NST>, smem);
     if (e) return e;
     int per_sm = 0, nsm = 0, dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_p3d, nthr, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_p3d<NST>, nthr, smem);
     const int grid = std::max(1, std::min(ntiles, std::max(1, per_sm) * nsm));
-    k_p3d<<<grid, nthr, smem, st>>>(mv);
+    k_p3d<NST><<<grid, nthr, smem, st>>>(mv);
     return cudaGetLastError();
 }
 
@@ -1256,7 +1263,8 @@ vc_status operator_build(vc_ctx* c, const vc_build_opts* o) {
         for (int f = 0; f < c->nf; ++f) {
             for (int b = 0; b < 3; ++b)
                 if (c->blk[f][b] >= 0) mac += (double)c->nzout[f] * c->nzin[b];
-            nog += (c->nzout[f] + kZB - 1) / kZB;
+            const int gpw = 32 / kDirectT, ng = (c->nzout[f] + kZB - 1) / kZB;
+            nog += (ng + gpw - 1) / gpw * gpw;
         }
         const double fft = 0.6 * (3 + c->nf) * 5.0 * Mz * ilog2c(Mz);
         const int zmode = o ? o->zmode : 0;
@@ -1275,8 +1283,12 @@ vc_status operator_build(vc_ctx* c, const vc_build_opts* o) {
         c->src_contig = 0;
         auto plane = [&](int g, int j) { return c->h_planes[(size_t)g * c->ZL + j]; };
         if (c->zdirect) {
-            for (int f = 0; f < c->nf; ++f)
-                for (int j = 0; j < c->nzout[f]; j += kZB) {
+            // groups of one field fill whole warps (32 / kDirectT groups per warp) so the lanes of
+            // a warp follow one code path; a field's last warp is padded with null groups
+            const int gpw = 32 / kDirectT;
+            for (int f = 0; f < c->nf; ++f) {
+                int ng = 0;
+                for (int j = 0; j < c->nzout[f]; j += kZB, ++ng) {
                     const int nzo = std::min(kZB, c->nzout[f] - j);
                     if (plane(3 + f, j + nzo - 1) - plane(3 + f, j) == nzo - 1)
                         c->og_contig |= 1ull << c->nog;
@@ -1284,6 +1296,12 @@ vc_status operator_build(vc_ctx* c, const vc_build_opts* o) {
                     c->og_j[c->nog] = j;
                     ++c->nog;
                 }
+                for (; ng % gpw; ++ng) {
+                    c->og_f[c->nog] = -1;
+                    c->og_j[c->nog] = 0;
+                    ++c->nog;
+                }
+            }
             for (int b = 0; b < 3; ++b)
                 if (c->nzin[b] > 0 && plane(b, c->nzin[b] - 1) - plane(b, 0) == c->nzin[b] - 1)
                     c->src_contig |= 1 << b;

@@ -144,6 +144,11 @@ struct vc_ctx {
     // ---- reusable scratch (grow-only; see DevBuf) ----
     vc::DevBuf<double2> kG;            // kernel-spectra build grid
     vc::DevBuf<double> kKo;            // kernel octant table
+    // near-field P entries for the preconditioner blocks, cut from the octant tables of the
+    // kernel build (same generator, no re-evaluation): [pair][iz][iy][ix], |t| <= box
+    vc::DevBuf<double> pcTab;
+    int pcTabDim[3] = {0, 0, 0};
+    int pcPair[3][3] = {{-1, -1, -1}, {-1, -1, -1}, {-1, -1, -1}};
     vc::DevBuf<double> cap_b, cap_rho, cap_part, cap_col;  // capacitance columns
     vc::DevBuf<double> io_in, io_out;  // host-vector calls
     vc::DevBuf<int32_t> in_label;      // host voxel inputs

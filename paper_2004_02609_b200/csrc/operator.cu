@@ -541,6 +541,16 @@ __global__ void k_kgen_oct(double* Ko, int Ox, int Oy, int Oz, int kind, int alp
     }
 }
 
+// copy the near corner [0, T) of an octant table (rescaled) into the preconditioner table
+__global__ void k_cut_octant(const double* __restrict__ Ko, int Ox, int Oy, int Oz,
+                             double* __restrict__ Tb, int Tx, int Ty, int Tz, double rescale) {
+    const int n = Tx * Ty * Tz;
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
+        const int ix = e % Tx, iy = (e / Tx) % Ty, iz = e / (Tx * Ty);
+        Tb[e] = (ix < Ox && iy < Oy && iz < Oz) ? rescale * Ko[((int64_t)iz * Oy + iy) * Ox + ix] : 0.0;
+    }
+}
+
 // full cyclic grid (real part of G) from the octant table, with the parity signs
 __global__ void k_kfill(double2* G, const double* __restrict__ Ko, int Mx, int My, int Mz, int Ox,
                         int Oy, int kind, int alpha, int beta) {
@@ -1334,6 +1344,18 @@ vc_status operator_build(vc_ctx* c, const vc_build_opts* o) {
         const int64_t otot = (int64_t)Ox * Oy * Oz;
         VC_CUDA(c, G.alloc(tot));
         VC_CUDA(c, Ko.alloc(otot));
+        // preconditioner near-field tables: one per P pair, |t| <= box along each axis
+        for (int a = 0; a < 3; ++a) c->pcTabDim[a] = c->box[a] + 1;
+        const int tvol = c->pcTabDim[0] * c->pcTabDim[1] * c->pcTabDim[2];
+        int npair = 0;
+        for (int a = 0; a < 3; ++a)
+            for (int b = 0; b < 3; ++b) c->pcPair[a][b] = -1;
+        for (int i = 0; i < c->nblk; ++i)
+            if (defs[i].kind == 0) {
+                c->pcPair[defs[i].alpha][defs[i].beta] = c->pcPair[defs[i].beta][defs[i].alpha] = npair;
+                ++npair;
+            }
+        VC_CUDA(c, c->pcTab.alloc((size_t)std::max(1, npair) * tvol));
         const double fpe = 4.0 * kPi * kEps0;
         for (int i = 0; i < c->nblk; ++i) {
             const BlkDef& d = defs[i];
@@ -1342,6 +1364,13 @@ vc_status operator_build(vc_ctx* c, const vc_build_opts* o) {
             VC_CUDA(c, cudaEventRecord(ev[0], st));
             const int oblocks = (int)std::min<int64_t>((otot + 127) / 128, 148 * 64);
             k_kgen_oct<<<oblocks, 128, 0, st>>>(Ko.p, Ox, Oy, Oz, d.kind, d.alpha, d.beta, scale);
+            if (d.kind == 0) {  // undo the FFT normalisation (a power of two: exact)
+                const double resc = (double)M[0] * M[1] * (zd ? 1 : M[2]);
+                k_cut_octant<<<(tvol + 255) / 256, 256, 0, st>>>(
+                    Ko.p, Ox, Oy, Oz, c->pcTab.p + (size_t)c->pcPair[d.alpha][d.beta] * tvol,
+                    c->pcTabDim[0], c->pcTabDim[1], c->pcTabDim[2], resc);
+                count_launch(c);
+            }
             const int gblocks = (int)std::min<int64_t>((tot + 255) / 256, 148 * 64);
             if (zd)
                 k_kfill2d<<<gblocks, 256, 0, st>>>(G.p, Ko.p, M[0], M[1], MZ, Ox, Oy, d.kind, d.alpha, d.beta);

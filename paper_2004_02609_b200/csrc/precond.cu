@@ -32,10 +32,19 @@ struct Precond {
 
 namespace {
 
+struct PcTab {
+    const double* t;
+    int dim[3];
+    int pair[3][3];
+};
+
+// Block entries P_kl of Eq. (5): looked up in the near-field tables the kernel build cut from
+// its octant tables (the same device generator, already scaled by dv^3 / (4 pi eps0)).  Octant
+// index per axis of the signed slot offset d: |t| = |d + s| with s = c_a - c_b (App. B).
 __global__ void k_pc_fill(const int32_t* __restrict__ un, const int64_t* __restrict__ uoff,
                           const int32_t* __restrict__ ulist, const int32_t* __restrict__ uaxis,
                           const int32_t* __restrict__ uslot, double* __restrict__ blocks,
-                          double scale) {
+                          PcTab tab) {
     const int u = blockIdx.y;
     const int n = un[u];
     const int64_t nn = (int64_t)n * n;
@@ -48,7 +57,16 @@ __global__ void k_pc_fill(const int32_t* __restrict__ un, const int64_t* __restr
         const int dx = uslot[3 * (l0 + i)] - uslot[3 * (l0 + j)];
         const int dy = uslot[3 * (l0 + i) + 1] - uslot[3 * (l0 + j) + 1];
         const int dz = uslot[3 * (l0 + i) + 2] - uslot[3 * (l0 + j) + 2];
-        B[e] = scale * kappa(0, ai, aj, dx, dy, dz);
+        const int d[3] = {dx, dy, dz};
+        int o[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            const int s2 = c2(ai, a) - c2(aj, a);
+            const int t2 = 2 * d[a] + s2;
+            o[a] = ((t2 < 0 ? -t2 : t2) - (s2 != 0)) >> 1;
+        }
+        B[e] = tab.t[(size_t)tab.pair[ai][aj] * tab.dim[0] * tab.dim[1] * tab.dim[2] +
+                     ((size_t)o[2] * tab.dim[1] + o[1]) * tab.dim[0] + o[0]];
     }
 }
 
@@ -254,8 +272,14 @@ vc_status precond_build(vc_ctx* c, const int32_t box_in[3], int kind) {
     VC_CUDA(c, up(pc->uniq_slot.p, uslot.data(), 4 * uslot.size()));
     if (pc->nuniq > 0) {
         dim3 g(std::max(1, std::min(64, (maxn * maxn + 255) / 256)), pc->nuniq);
+        PcTab tab;
+        tab.t = c->pcTab.p;
+        for (int a = 0; a < 3; ++a) {
+            tab.dim[a] = c->pcTabDim[a];
+            for (int b = 0; b < 3; ++b) tab.pair[a][b] = c->pcPair[a][b];
+        }
         k_pc_fill<<<g, 256, 0, st>>>(pc->uniq_n.p, pc->uniq_off.p, pc->uniq_list_off.p,
-                                     pc->uniq_axis.p, pc->uniq_slot.p, pc->blocks.p, pscale);
+                                     pc->uniq_axis.p, pc->uniq_slot.p, pc->blocks.p, tab);
         const size_t sh = 2 * sizeof(double) * maxn;
         if (sh > 48 * 1024)
             VC_CUDA(c, cudaFuncSetAttribute(k_pc_invert, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));

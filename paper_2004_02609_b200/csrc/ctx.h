@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <string>
 #include <vector>
 
@@ -40,6 +41,40 @@ struct DevBuf {
     }
     T* get() const { return p; }
     size_t bytes() const { return n * sizeof(T); }
+};
+
+// Grow-only pinned host array (page-locked, so device -> host copies run at full speed and
+// truly asynchronously); the host mirrors of the panel table.
+template <class T>
+struct PinnedVec {
+    T* p = nullptr;
+    size_t n = 0, cap = 0;
+    PinnedVec() = default;
+    PinnedVec(const PinnedVec&) = delete;
+    PinnedVec& operator=(const PinnedVec&) = delete;
+    ~PinnedVec() {
+        if (p) cudaFreeHost(p);
+    }
+    cudaError_t resize(size_t count) {
+        if (count > cap) {
+            if (p) cudaFreeHost(p);
+            p = nullptr;
+            cap = n = 0;
+            cudaError_t e = cudaMallocHost(&p, std::max<size_t>(1, count) * sizeof(T));
+            if (e != cudaSuccess) {
+                p = nullptr;
+                return e;
+            }
+            cap = count;
+        }
+        n = count;
+        return cudaSuccess;
+    }
+    T* data() { return p; }
+    const T* data() const { return p; }
+    size_t size() const { return n; }
+    T& operator[](size_t i) { return p[i]; }
+    const T& operator[](size_t i) const { return p[i]; }
 };
 
 struct PanelsDev {
@@ -96,9 +131,9 @@ struct vc_ctx {
     // [kind][orientation][0 = min, 1 = max][axis]; min > max when no such panels
     int ext[2][3][2][3];
     // host mirror of the panel table (structure-only work: preconditioner boxes)
-    std::vector<int8_t> h_axis, h_sign;
-    std::vector<int32_t> h_si, h_sj, h_sk, h_cid;
-    std::vector<double> h_ibar;
+    vc::PinnedVec<int8_t> h_axis, h_sign;
+    vc::PinnedVec<int32_t> h_si, h_sj, h_sk, h_cid;
+    vc::PinnedVec<double> h_ibar;
 
     // ---- operator (vc_build_operator) ----
     bool has_op = false;
@@ -163,6 +198,9 @@ struct vc_ctx {
     vc::DevBuf<double> partial;
     vc::DevBuf<double> dvec;  // small device vector (dots)
     double* h_pinned = nullptr;  // pinned host scratch (dots)
+    vc::DevBuf<unsigned> ticket;  // last-block ticket of the fused multi-dot
+    cudaEvent_t arn_ev[2] = {};   // pipelined Arnoldi: coefficients of step j landed on the host
+    bool arn_ev_ok = false;
 
     // ---- instrumentation ----
     vc_stats stats{};

@@ -20,44 +20,60 @@ constexpr int kMaxBasis = 64;  // restart + 1 <= 64
 constexpr int kRedBlocks = 296;
 constexpr int kRedNT = 256;
 
-// partial[b * nv + i] = sum_{n in block b} V[i][n] * w[n]
+// out[i] = sum_n V[i][n] * w[n], i < nv.  Grid (chunk, vector group of kDotG): each block
+// accumulates kDotG dots over a grid-stride range of n (kDotG registers, no predicated slots
+// for absent vectors), writes per-block partials, and the last block to finish (ticket) sums
+// them in a fixed order -- one launch, deterministic.
+constexpr int kDotG = 8;
 __global__ void __launch_bounds__(kRedNT) k_multidot(const double* __restrict__ V, int64_t ldv, int nv,
                                                      const double* __restrict__ w, int64_t n,
-                                                     double* __restrict__ partial) {
-    double acc[kMaxBasis];
+                                                     double* __restrict__ partial,
+                                                     unsigned* __restrict__ ticket,
+                                                     double* __restrict__ out) {
+    const int g0 = blockIdx.y * kDotG;
+    const int ng = min(kDotG, nv - g0);
+    double acc[kDotG];
 #pragma unroll
-    for (int i = 0; i < kMaxBasis; ++i) acc[i] = 0.0;
+    for (int i = 0; i < kDotG; ++i) acc[i] = 0.0;
+    const double* __restrict__ Vg = V + (int64_t)g0 * ldv;
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
          k += (int64_t)gridDim.x * blockDim.x) {
         const double wk = w[k];
+        if (ng == kDotG) {
 #pragma unroll
-        for (int i = 0; i < kMaxBasis; ++i)
-            if (i < nv) acc[i] = fma(V[i * ldv + k], wk, acc[i]);
+            for (int i = 0; i < kDotG; ++i) acc[i] = fma(Vg[i * ldv + k], wk, acc[i]);
+        } else {
+#pragma unroll
+            for (int i = 0; i < kDotG; ++i)
+                if (i < ng) acc[i] = fma(Vg[i * ldv + k], wk, acc[i]);
+        }
     }
-    __shared__ double s[kRedNT / 32][kMaxBasis];
+    __shared__ double s[kRedNT / 32][kDotG];
     const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
 #pragma unroll
-    for (int i = 0; i < kMaxBasis; ++i) {
-        if (i >= nv) break;
+    for (int i = 0; i < kDotG; ++i) {
         double v = acc[i];
         for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
         if (lane == 0) s[wp][i] = v;
     }
     __syncthreads();
+    if (threadIdx.x < ng) {
+        double v = 0.0;
+        for (int q = 0; q < kRedNT / 32; ++q) v += s[q][threadIdx.x];
+        partial[(int64_t)blockIdx.x * nv + g0 + threadIdx.x] = v;
+    }
+    __threadfence();
+    __shared__ bool last;
+    if (threadIdx.x == 0) last = atomicAdd(ticket, 1u) == gridDim.x * gridDim.y - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
     for (int i = threadIdx.x; i < nv; i += blockDim.x) {
         double v = 0.0;
-        for (int q = 0; q < kRedNT / 32; ++q) v += s[q][i];
-        partial[(int64_t)blockIdx.x * nv + i] = v;
+        for (int b = 0; b < (int)gridDim.x; ++b) v += __ldcg(partial + (int64_t)b * nv + i);
+        out[i] = v;
     }
-}
-
-__global__ void k_reduce_partials(const double* __restrict__ partial, int nblk, int nv,
-                                  double* __restrict__ out) {
-    const int i = threadIdx.x;
-    if (i >= nv) return;
-    double v = 0.0;
-    for (int b = 0; b < nblk; ++b) v += partial[(int64_t)b * nv + i];
-    out[i] = v;
+    if (threadIdx.x == 0) *ticket = 0u;
 }
 
 // w -= sum_i h[i] V[i]   (h on the device)
@@ -148,8 +164,12 @@ struct Krylov {
             c->work_n = need;
         }
         if (c->partial.n < (size_t)kRedBlocks * kMaxBasis) VC_CUDA(c, c->partial.alloc((size_t)kRedBlocks * kMaxBasis));
-        if (c->dvec.n < 4 * kMaxBasis) VC_CUDA(c, c->dvec.alloc(4 * kMaxBasis));
-        if (!c->h_pinned) VC_CUDA(c, cudaMallocHost(&c->h_pinned, 8 * 4 * kMaxBasis));
+        if (c->dvec.n < 8 * kMaxBasis) VC_CUDA(c, c->dvec.alloc(8 * kMaxBasis));
+        if (!c->ticket.p) {
+            VC_CUDA(c, c->ticket.alloc(1));
+            VC_CUDA(c, cudaMemsetAsync(c->ticket.p, 0, sizeof(unsigned), c->stream));
+        }
+        if (!c->h_pinned) VC_CUDA(c, cudaMallocHost(&c->h_pinned, 8 * 8 * kMaxBasis));
         V = c->work.p;
         w = V + (size_t)(m + 1) * n;
         t = w + n;
@@ -160,9 +180,9 @@ struct Krylov {
     }
     // out[0..nv) = V[0..nv) . vec, summed over ranks (world > 1)
     vc_status dots(const double* Vb, int nv, const double* vec, double* out) {
-        k_multidot<<<kRedBlocks, kRedNT, 0, c->stream>>>(Vb, n, nv, vec, n, c->partial.p);
-        k_reduce_partials<<<1, kMaxBasis, 0, c->stream>>>(c->partial.p, kRedBlocks, nv, out);
-        count_launch(c, 2);
+        const dim3 grid(kRedBlocks, (nv + kDotG - 1) / kDotG);
+        k_multidot<<<grid, kRedNT, 0, c->stream>>>(Vb, n, nv, vec, n, c->partial.p, c->ticket.p, out);
+        count_launch(c, 1);
         return comm_allreduce(c, out, nv);
     }
     vc_status norm2_host(const double* vec, double* out) {
@@ -231,23 +251,47 @@ vc_status solve_dev(vc_ctx* c, const double* d_b, double* d_x, const vc_solve_op
         std::fill(g.begin(), g.end(), 0.0);
         g[0] = beta;
         int jend = 0;
-        for (int j = 0; j < restart && iters < maxit; ++j) {
+        // Arnoldi step j on the device: w = R A v_j, CGS2 against v_0..v_j (coefficients in
+        // device slot j % 2), v_{j+1} = w / ||w||, coefficients copied to pinned host slot j % 2.
+        // The host Givens update of step j runs while the device already executes step j + 1
+        // (the next step needs only device data), so the convergence test lags one step: at
+        // most one extra Arnoldi step per restart cycle, never a wrong iterate.
+        auto enqueue = [&](int j) -> vc_status {
             double* vj = K.V + (size_t)j * n;
             double* vn = K.V + (size_t)(j + 1) * n;
-            if ((s = K.op(vj, K.t, K.w))) return s;
-            ++iters;
-            double* dh = c->dvec.p;
-            // CGS2: h = V^T t; t -= V h; h2 = V^T t; t -= V h2; ||t||^2
-            if ((s = K.dots(K.V, j + 1, K.t, dh))) return s;
+            vc_status e;
+            if ((e = K.op(vj, K.t, K.w))) return e;
+            double* dh = c->dvec.p + (size_t)(j & 1) * 3 * kMaxBasis;
+            if ((e = K.dots(K.V, j + 1, K.t, dh))) return e;
             k_multiaxpy<<<gn, 256, 0, st>>>(K.t, K.V, n, j + 1, dh, n, -1.0);
-            if ((s = K.dots(K.V, j + 1, K.t, dh + kMaxBasis))) return s;
+            if ((e = K.dots(K.V, j + 1, K.t, dh + kMaxBasis))) return e;
             k_multiaxpy<<<gn, 256, 0, st>>>(K.t, K.V, n, j + 1, dh + kMaxBasis, n, -1.0);
-            if ((s = K.dots(K.t, 1, K.t, dh + 2 * kMaxBasis))) return s;
+            if ((e = K.dots(K.t, 1, K.t, dh + 2 * kMaxBasis))) return e;
             k_scale_by_norm<<<gn, 256, 0, st>>>(vn, K.t, dh + 2 * kMaxBasis, n);
             count_launch(c, 3);
-            VC_CUDA(c, cudaMemcpyAsync(c->h_pinned, dh, 8 * 3 * kMaxBasis, cudaMemcpyDeviceToHost, st));
-            VC_CUDA(c, cudaStreamSynchronize(st));
-            const double* hh = c->h_pinned;
+            VC_CUDA(c, cudaMemcpyAsync(c->h_pinned + (size_t)(j & 1) * 3 * kMaxBasis, dh,
+                                       8 * 3 * kMaxBasis, cudaMemcpyDeviceToHost, st));
+            VC_CUDA(c, cudaEventRecord(c->arn_ev[j & 1], st));
+            return VC_OK;
+        };
+        if (!c->arn_ev_ok) {
+            for (auto& e : c->arn_ev) VC_CUDA(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            c->arn_ev_ok = true;
+        }
+        int queued = 0;  // Arnoldi steps enqueued in this cycle
+        const int it0 = iters;
+        if (restart > 0 && iters < maxit) {
+            if ((s = enqueue(0))) return s;
+            queued = 1;
+        }
+        for (int j = 0; j < queued; ++j) {
+            if (queued < restart && it0 + queued < maxit) {
+                if ((s = enqueue(queued))) return s;
+                ++queued;
+            }
+            VC_CUDA(c, cudaEventSynchronize(c->arn_ev[j & 1]));
+            ++iters;
+            const double* hh = c->h_pinned + (size_t)(j & 1) * 3 * kMaxBasis;
             double* Hj = H.data() + (size_t)j * (restart + 1);  // column j
             for (int i = 0; i <= j; ++i) Hj[i] = hh[i] + hh[kMaxBasis + i];
             Hj[j + 1] = std::sqrt(hh[2 * kMaxBasis]);
@@ -274,8 +318,8 @@ vc_status solve_dev(vc_ctx* c, const double* d_b, double* d_x, const vc_solve_op
             for (int k = i + 1; k < jend; ++k) v -= H[(size_t)k * (restart + 1) + i] * y[k];
             y[i] = v / H[(size_t)i * (restart + 1) + i];
         }
-        VC_CUDA(c, cudaMemcpyAsync(c->dvec.p + 3 * kMaxBasis, y.data(), 8 * jend, cudaMemcpyHostToDevice, st));
-        k_multiaxpy<<<gn, 256, 0, st>>>(K.x, K.V, n, jend, c->dvec.p + 3 * kMaxBasis, n, 1.0);
+        VC_CUDA(c, cudaMemcpyAsync(c->dvec.p + 6 * kMaxBasis, y.data(), 8 * jend, cudaMemcpyHostToDevice, st));
+        k_multiaxpy<<<gn, 256, 0, st>>>(K.x, K.V, n, jend, c->dvec.p + 6 * kMaxBasis, n, 1.0);
         count_launch(c);
         if (rre <= tol) converged = true;
         if (!(rre == rre)) break;

@@ -355,13 +355,13 @@ vc_status geometry_build(vc_ctx* c, const int32_t* d_label, const double* d_eps)
     count_launch(c);
     VC_CUDA(c, cudaMemcpyAsync(hext.data(), ext.p, 36 * sizeof(int), cudaMemcpyDeviceToHost, st));
     // host mirror of the structural fields
-    c->h_axis.resize(N);
-    c->h_sign.resize(N);
-    c->h_si.resize(N);
-    c->h_sj.resize(N);
-    c->h_sk.resize(N);
-    c->h_cid.resize(N);
-    c->h_ibar.resize(N);
+    VC_CUDA(c, c->h_axis.resize(N));
+    VC_CUDA(c, c->h_sign.resize(N));
+    VC_CUDA(c, c->h_si.resize(N));
+    VC_CUDA(c, c->h_sj.resize(N));
+    VC_CUDA(c, c->h_sk.resize(N));
+    VC_CUDA(c, c->h_cid.resize(N));
+    VC_CUDA(c, c->h_ibar.resize(N));
     VC_CUDA(c, cudaMemcpyAsync(c->h_axis.data(), P.axis.p, N, cudaMemcpyDeviceToHost, st));
     VC_CUDA(c, cudaMemcpyAsync(c->h_sign.data(), P.sign.p, N, cudaMemcpyDeviceToHost, st));
     VC_CUDA(c, cudaMemcpyAsync(c->h_si.data(), P.si.p, N * 4, cudaMemcpyDeviceToHost, st));

@@ -107,6 +107,8 @@ void vc_destroy(vc_ctx* c) {
         if (c->h_pinned) cudaFreeHost(c->h_pinned);
         if (c->timing.ev_ok)
             for (auto& e : c->timing.ev) cudaEventDestroy(e);
+        if (c->arn_ev_ok)
+            for (auto& e : c->arn_ev) cudaEventDestroy(e);
         if (c->own_stream) cudaStreamDestroy(c->stream);
     }
     delete c;

@@ -9,6 +9,32 @@ constexpr double kPi = 3.14159265358979323846264338327950288;
 constexpr double kEps0 = 8.8541878128e-12;  // F/m (reading O15)
 constexpr int kMaxL = 4096;                 // largest FFT length per axis
 constexpr int kTabN = 2 * kMaxL;            // twiddle table: exp(-2 pi i n / kTabN)
+// Grant kernel `k` the largest dynamic shared memory the device allows next to its static
+// shared memory.  The limit is a process-wide function attribute: contexts of one process
+// (ranks of a thread group) launch with different sizes, so a per-launch value would race.
+template <class K>
+inline cudaError_t grant_max_dyn_smem(K k, int optin);
+// opt-in shared memory per CTA of the current device (queried once per device)
+inline int max_dyn_smem() {
+    static int v[16] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 16) dev = 0;
+    if (!v[dev]) {
+        int x = 0;
+        cudaDeviceGetAttribute(&x, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        v[dev] = x > 0 ? x : 48 * 1024;
+    }
+    return v[dev];
+}
+template <class K>
+inline cudaError_t grant_max_dyn_smem(K k, int optin) {
+    cudaFuncAttributes fa;
+    cudaError_t e = cudaFuncGetAttributes(&fa, k);
+    if (e) return e;
+    return cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                optin - (int)fa.sharedSizeBytes);
+}
 
 // Half-integer centre offsets of the a-normal panel grids, doubled (c_x = (0,1/2,1/2) ...;
 // P:97 grids, Table VII P:331-341 in the S = c_beta - c_alpha form).

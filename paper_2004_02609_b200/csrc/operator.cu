@@ -715,7 +715,10 @@ static cudaError_t prep(K kern, size_t smem) {
     // all-shared carveout: the FFT passes are shared-memory-resident, so more CTAs per SM
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e) return e;
-    if (smem > 48 * 1024) return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    // the limit is a process-wide function attribute: contexts of one process (ranks of a
+    // thread group) launch with different sizes, so always grant the device maximum (a
+    // per-launch value would race) -- occupancy follows the actual launch size
+    if (smem > 48 * 1024) return grant_max_dyn_smem(kern, max_dyn_smem());
     return cudaSuccess;
 }
 

@@ -21,6 +21,9 @@ struct Precond {
     int nbox = 0, nuniq = 0;
     int max_n = 0;
     DevBuf<int32_t> box_start, box_n, box_uid;  // per non-empty box
+    DevBuf<int32_t> ubox_start, ubox_list;       // boxes of each unique block (CSR)
+    DevBuf<int32_t> tile_u, tile_r0, tile_q0;    // apply tiles: (unique block, first row, first box)
+    int ntile = 0;
     DevBuf<int32_t> panel_ids;                   // conductor panels sorted by box
     DevBuf<int64_t> uniq_off;                    // offset of each unique block (doubles)
     DevBuf<int32_t> uniq_n, uniq_list_off;
@@ -105,24 +108,41 @@ __global__ void k_pc_diag(int64_t N, const double* __restrict__ r, const double*
         z[i] = r[i] * dinv[i];
 }
 
-// z_b = R_b r_b for every box (warp per row)
-__global__ void k_pc_apply(const int32_t* __restrict__ bstart, const int32_t* __restrict__ bn,
-                           const int32_t* __restrict__ buid, const int32_t* __restrict__ pids,
-                           const int64_t* __restrict__ uoff, const double* __restrict__ blocks,
-                           const double* __restrict__ r, double* __restrict__ z) {
-    extern __shared__ double rb[];
-    const int b = blockIdx.x;
-    const int n = bn[b], s0 = bstart[b];
-    const double* R = blocks + uoff[buid[b]];
-    for (int j = threadIdx.x; j < n; j += blockDim.x) rb[j] = r[pids[s0 + j]];
-    __syncthreads();
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    for (int i = w; i < n; i += nw) {
-        const double* Ri = R + (int64_t)i * n;
+// z_b = R_u r_b grouped by unique block: a CTA holds kPcRows rows of R_u in shared memory and
+// applies them to every box b that uses R_u (each R element read once per apply; 8 lanes per
+// row, shuffle-reduced)
+constexpr int kPcRows = 32;
+constexpr int kPcBoxes = 8;  // boxes per CTA (a block shared by many boxes is split over CTAs)
+__global__ void __launch_bounds__(256) k_pc_apply_grouped(
+    const int32_t* __restrict__ tile_u, const int32_t* __restrict__ tile_r0,
+    const int32_t* __restrict__ tile_q0,
+    const int32_t* __restrict__ un, const int64_t* __restrict__ uoff,
+    const int32_t* __restrict__ ubs, const int32_t* __restrict__ ubl,
+    const int32_t* __restrict__ bstart, const int32_t* __restrict__ pids,
+    const double* __restrict__ blocks, const double* __restrict__ r, double* __restrict__ z) {
+    extern __shared__ double sh[];
+    const int u = tile_u[blockIdx.x], r0 = tile_r0[blockIdx.x];
+    const int n = un[u];
+    const int rows = min(kPcRows, n - r0);
+    double* Rt = sh;              // [rows][n]
+    double* rb = sh + kPcRows * n;  // [n]
+    const double* R = blocks + uoff[u] + (int64_t)r0 * n;
+    for (int e = threadIdx.x; e < rows * n; e += blockDim.x) Rt[e] = R[e];
+    const int row = threadIdx.x >> 3, part = threadIdx.x & 7;
+    const int q1 = min(ubs[u + 1], ubs[u] + tile_q0[blockIdx.x] + kPcBoxes);
+    for (int q = ubs[u] + tile_q0[blockIdx.x]; q < q1; ++q) {
+        const int b = ubl[q];
+        const int s0 = bstart[b];
+        __syncthreads();
+        for (int j = threadIdx.x; j < n; j += blockDim.x) rb[j] = r[pids[s0 + j]];
+        __syncthreads();
         double acc = 0.0;
-        for (int j = lane; j < n; j += 32) acc = fma(__ldg(Ri + j), rb[j], acc);
-        for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (lane == 0) z[pids[s0 + i]] = acc;
+        if (row < rows)
+            for (int j = part; j < n; j += 8) acc = fma(Rt[row * n + j], rb[j], acc);
+        acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+        acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+        acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+        if (part == 0 && row < rows) z[pids[s0 + r0 + row]] = acc;
     }
 }
 
@@ -242,7 +262,7 @@ vc_status precond_build(vc_ctx* c, const int32_t box_in[3], int kind) {
         }
         buid[b] = it->second;
     }
-    if ((size_t)maxn * 2 * sizeof(double) > 200 * 1024)
+    if ((size_t)maxn * (kPcRows + 1) * sizeof(double) > 220 * 1024)
         return set_err(c, VC_ERR_UNSUPPORTED, "preconditioner block too large (" + std::to_string(maxn) + " panels in one box); use smaller boxes");
     pc->nbox = nbox;
     pc->nuniq = (int)un.size();
@@ -264,6 +284,33 @@ vc_status precond_build(vc_ctx* c, const int32_t box_in[3], int kind) {
     VC_CUDA(c, up(pc->box_start.p, bstart.data(), 4 * nbox));
     VC_CUDA(c, up(pc->box_n.p, bcount.data(), 4 * nbox));
     VC_CUDA(c, up(pc->box_uid.p, buid.data(), 4 * nbox));
+    {   // unique block -> its boxes (CSR) and the grouped-apply tiles
+        const int nu = (int)un.size();
+        std::vector<int32_t> ubs(nu + 1, 0), ubl(nbox), fillq;
+        for (int b = 0; b < nbox; ++b) ubs[buid[b] + 1]++;
+        for (int u = 0; u < nu; ++u) ubs[u + 1] += ubs[u];
+        fillq.assign(ubs.begin(), ubs.end() - 1);
+        for (int b = 0; b < nbox; ++b) ubl[fillq[buid[b]]++] = b;
+        std::vector<int32_t> tu, tr, tq;
+        for (int u = 0; u < nu; ++u)
+            for (int r0 = 0; r0 < un[u]; r0 += kPcRows)
+                for (int q0 = 0; q0 < ubs[u + 1] - ubs[u]; q0 += kPcBoxes) {
+                    tu.push_back(u);
+                    tr.push_back(r0);
+                    tq.push_back(q0);
+                }
+        pc->ntile = (int)tu.size();
+        VC_CUDA(c, pc->ubox_start.alloc(nu + 1));
+        VC_CUDA(c, pc->ubox_list.alloc(std::max(1, nbox)));
+        VC_CUDA(c, pc->tile_u.alloc(std::max<size_t>(1, tu.size())));
+        VC_CUDA(c, pc->tile_r0.alloc(std::max<size_t>(1, tr.size())));
+        VC_CUDA(c, pc->tile_q0.alloc(std::max<size_t>(1, tq.size())));
+        VC_CUDA(c, up(pc->tile_q0.p, tq.data(), 4 * tq.size()));
+        VC_CUDA(c, up(pc->ubox_start.p, ubs.data(), 4 * (nu + 1)));
+        VC_CUDA(c, up(pc->ubox_list.p, ubl.data(), 4 * nbox));
+        VC_CUDA(c, up(pc->tile_u.p, tu.data(), 4 * tu.size()));
+        VC_CUDA(c, up(pc->tile_r0.p, tr.data(), 4 * tr.size()));
+    }
     VC_CUDA(c, up(pc->panel_ids.p, sorted.data(), 4 * sorted.size()));
     VC_CUDA(c, up(pc->uniq_off.p, uoff.data(), 8 * uoff.size()));
     VC_CUDA(c, up(pc->uniq_n.p, un.data(), 4 * un.size()));
@@ -282,7 +329,7 @@ vc_status precond_build(vc_ctx* c, const int32_t box_in[3], int kind) {
                                      pc->uniq_axis.p, pc->uniq_slot.p, pc->blocks.p, tab);
         const size_t sh = 2 * sizeof(double) * maxn;
         if (sh > 48 * 1024)
-            VC_CUDA(c, cudaFuncSetAttribute(k_pc_invert, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
+            VC_CUDA(c, grant_max_dyn_smem(k_pc_invert, max_dyn_smem()));
         k_pc_invert<<<pc->nuniq, 512, sh, st>>>(pc->uniq_n.p, pc->uniq_off.p, pc->blocks.p);
         count_launch(c, 2);
     }
@@ -298,12 +345,13 @@ vc_status precond_apply_dev(vc_ctx* c, const double* d_r, double* d_z) {
     const int64_t N = c->NL;
     k_pc_diag<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((N + 255) / 256, 148 * 8)), 256, 0, st>>>(N, d_r, pc->diag_inv.p, d_z);
     count_launch(c);
-    if (pc->kind == 3 && pc->nbox > 0) {
-        const size_t sh = sizeof(double) * pc->max_n;
+    if (pc->kind == 3 && pc->ntile > 0) {
+        const size_t sh = sizeof(double) * (size_t)(kPcRows + 1) * pc->max_n;
         if (sh > 48 * 1024)
-            VC_CUDA(c, cudaFuncSetAttribute(k_pc_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
-        k_pc_apply<<<pc->nbox, 128, sh, st>>>(pc->box_start.p, pc->box_n.p, pc->box_uid.p,
-                                              pc->panel_ids.p, pc->uniq_off.p, pc->blocks.p, d_r, d_z);
+            VC_CUDA(c, grant_max_dyn_smem(k_pc_apply_grouped, max_dyn_smem()));
+        k_pc_apply_grouped<<<pc->ntile, 256, sh, st>>>(
+            pc->tile_u.p, pc->tile_r0.p, pc->tile_q0.p, pc->uniq_n.p, pc->uniq_off.p, pc->ubox_start.p,
+            pc->ubox_list.p, pc->box_start.p, pc->panel_ids.p, pc->blocks.p, d_r, d_z);
         count_launch(c);
     }
     VC_CUDA(c, cudaGetLastError());

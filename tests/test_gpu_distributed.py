@@ -7,6 +7,7 @@ ordered peer copies instead of NCCL).  The partitioned matvec must be BITWISE eq
 ranks in a different order) and with the CPU oracle.
 """
 import threading
+import time
 
 import numpy as np
 import pytest
@@ -40,8 +41,13 @@ def _group(W, st, fn, timeout=600, **build):
     th = [threading.Thread(target=work, args=(r,), daemon=True) for r in range(W)]
     for t in th:
         t.start()
-    for t in th:
-        t.join(timeout)
+    t0 = time.time()
+    while any(t.is_alive() for t in th) and time.time() - t0 < timeout:
+        # a rank that failed leaves its peers waiting at the next collective: surface it now
+        for e in err:
+            if e is not None:
+                raise e
+        time.sleep(0.05)
     assert not any(t.is_alive() for t in th), "distributed ranks hung"
     for c in ctxs:
         c.close()

@@ -4,6 +4,9 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -208,6 +211,23 @@ struct vc_ctx {
 };
 
 namespace vc {
+// Host-side phase trace (stderr) when the environment variable VC_TRACE is set.
+struct HostTrace {
+    bool on;
+    const char* tag;
+    std::chrono::steady_clock::time_point t0, t;
+    explicit HostTrace(const char* tg) : on(getenv("VC_TRACE") != nullptr), tag(tg) {
+        t0 = t = std::chrono::steady_clock::now();
+    }
+    void mark(const char* what) {
+        if (!on) return;
+        const auto n = std::chrono::steady_clock::now();
+        fprintf(stderr, "[vc %s] %-28s %8.3f ms (total %8.3f)\n", tag, what,
+                std::chrono::duration<double, std::milli>(n - t).count(),
+                std::chrono::duration<double, std::milli>(n - t0).count());
+        t = n;
+    }
+};
 // error helpers
 inline vc_status set_err(vc_ctx* c, vc_status s, const std::string& msg) {
     c->err = msg;

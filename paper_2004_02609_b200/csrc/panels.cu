@@ -262,6 +262,7 @@ __global__ void k_emit(Geo g, int64_t Ftot, const int64_t* __restrict__ tile_off
 vc_status geometry_build(vc_ctx* c, const int32_t* d_label, const double* d_eps) {
     const int64_t nvox = (int64_t)c->nx * c->ny * c->nz;
     cudaStream_t st = c->stream;
+    HostTrace tr("geometry");
     DevBuf<unsigned char>& flb = c->geo_flags;
     VC_CUDA(c, flb.alloc(sizeof(Flags)));
     struct { Flags* p; } fl{reinterpret_cast<Flags*>(flb.p)};
@@ -276,6 +277,7 @@ vc_status geometry_build(vc_ctx* c, const int32_t* d_label, const double* d_eps)
     if (hf.min_label < 0) return set_err(c, VC_ERR_INPUT, "label < 0");
     if (hf.max_label <= 0) return set_err(c, VC_ERR_INPUT, "empty structure: no conductor voxel");
     if (hf.bad_eps) return set_err(c, VC_ERR_INPUT, "eps_r must be finite and > 0");
+    tr.mark("validate");
     const int m = hf.max_label;
     {
         DevBuf<int>& pres = c->geo_pres;
@@ -289,6 +291,7 @@ vc_status geometry_build(vc_ctx* c, const int32_t* d_label, const double* d_eps)
         for (int i = 1; i <= m; ++i)
             if (!hp[i]) return set_err(c, VC_ERR_INPUT, "conductor ids must be exactly 1..m (missing " + std::to_string(i) + ")");
     }
+    tr.mark("presence");
     Geo g;
     g.nx = c->nx;
     g.ny = c->ny;
@@ -315,6 +318,7 @@ vc_status geometry_build(vc_ctx* c, const int32_t* d_label, const double* d_eps)
     VC_CUDA(c, cudaMemcpyAsync(&hf, fl.p, sizeof(Flags), cudaMemcpyDeviceToHost, st));
     VC_CUDA(c, cudaStreamSynchronize(st));
     if (hf.clash) return set_err(c, VC_ERR_INPUT, "two different conductors share a face");
+    tr.mark("count + scan");
     if (N >= INT32_MAX) return set_err(c, VC_ERR_UNSUPPORTED, "more than 2^31 panels");
 
     PanelsDev& P = c->pan;
@@ -351,6 +355,7 @@ vc_status geometry_build(vc_ctx* c, const int32_t* d_label, const double* d_eps)
     for (int a = 0; a < 3; ++a) o.slotmap[a] = P.slotmap[a].p;
     o.area_over_2eps0 = c->dv * c->dv / (2.0 * kEps0);
     o.ext = ext.p;
+    tr.mark("allocs");
     k_emit<<<(unsigned)ntiles, kNT, 0, st>>>(g, Ftot, tiles.p, o);
     count_launch(c);
     VC_CUDA(c, cudaMemcpyAsync(hext.data(), ext.p, 36 * sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -377,8 +382,10 @@ vc_status geometry_build(vc_ctx* c, const int32_t* d_label, const double* d_eps)
                 c->ext[kind][a][0][t] = hext[(kind * 3 + a) * 6 + t];
                 c->ext[kind][a][1][t] = hext[(kind * 3 + a) * 6 + 3 + t];
             }
+    tr.mark("emit + host mirrors");
     int64_t Nc = 0;
     for (int64_t p = 0; p < N; ++p) Nc += c->h_cid[p] > 0;
+    tr.mark("host count");
     c->N = N;
     c->Nc = Nc;
     c->Nd = N - Nc;

@@ -121,6 +121,7 @@ vc_status vc_set_geometry(vc_ctx* c, int32_t nx, int32_t ny, int32_t nz, double 
                           int32_t on_device) {
     VC_CHECK_CTX(c);
     DeviceGuard g(c->device);
+    HostTrace tr("set_geometry");
     drop_geometry(c);
     if (nx <= 0 || ny <= 0 || nz <= 0) return set_err(c, VC_ERR_INPUT, "dims must be > 0");
     if (!(dv_m > 0) || !std::isfinite(dv_m)) return set_err(c, VC_ERR_INPUT, "dv must be finite and > 0");
@@ -162,6 +163,7 @@ vc_status vc_set_geometry(vc_ctx* c, int32_t nx, int32_t ny, int32_t nz, double 
     }
     cudaEventDestroy(g0);
     cudaEventDestroy(g1);
+    tr.mark("done");
     if (s != VC_OK) {
         std::string msg = c->err;
         drop_geometry(c);

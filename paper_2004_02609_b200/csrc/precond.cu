@@ -171,6 +171,7 @@ vc_status precond_build(vc_ctx* c, const int32_t box_in[3], int kind) {
     pc->nbox = pc->nuniq = pc->max_n = 0;
     pc->block_doubles = 0;
     cudaStream_t st = c->stream;
+    HostTrace tr("precond");
     const int64_t N = c->NL;  // this rank's panels (boxes never straddle ranks)
     auto G = [&](int64_t i) { return c->world > 1 ? c->h_gidx[i] : i; };  // local -> global
     const double fpe = 4.0 * kPi * kEps0;
@@ -186,6 +187,7 @@ vc_status precond_build(vc_ctx* c, const int32_t box_in[3], int kind) {
     }
     VC_CUDA(c, pc->diag_inv.alloc(std::max<int64_t>(1, N)));
     if (N) VC_CUDA(c, cudaMemcpyAsync(pc->diag_inv.p, dinv.data(), 8 * N, cudaMemcpyHostToDevice, st));
+    tr.mark("diagonal");
     if (kind != 3) {
         VC_CUDA(c, cudaStreamSynchronize(st));
         return VC_OK;
@@ -219,6 +221,7 @@ vc_status precond_build(vc_ctx* c, const int32_t box_in[3], int kind) {
         pb[q] = it->second;
     }
     const int nbox = (int)box_keys.size();
+    tr.mark("box assignment");
     std::vector<int32_t> bcount(nbox, 0), bstart(nbox + 1, 0);
     for (int32_t b : pb) bcount[b]++;
     for (int b = 0; b < nbox; ++b) bstart[b + 1] = bstart[b] + bcount[b];
@@ -262,6 +265,7 @@ vc_status precond_build(vc_ctx* c, const int32_t box_in[3], int kind) {
         }
         buid[b] = it->second;
     }
+    tr.mark("signatures");
     if ((size_t)maxn * (kPcRows + 1) * sizeof(double) > 220 * 1024)
         return set_err(c, VC_ERR_UNSUPPORTED, "preconditioner block too large (" + std::to_string(maxn) + " panels in one box); use smaller boxes");
     pc->nbox = nbox;
@@ -332,6 +336,10 @@ vc_status precond_build(vc_ctx* c, const int32_t box_in[3], int kind) {
             VC_CUDA(c, grant_max_dyn_smem(k_pc_invert, max_dyn_smem()));
         k_pc_invert<<<pc->nuniq, 512, sh, st>>>(pc->uniq_n.p, pc->uniq_off.p, pc->blocks.p);
         count_launch(c, 2);
+    }
+    if (tr.on) {
+        cudaStreamSynchronize(st);
+        tr.mark("uploads + fill + invert");
     }
     VC_CUDA(c, cudaStreamSynchronize(st));
     VC_CUDA(c, cudaGetLastError());

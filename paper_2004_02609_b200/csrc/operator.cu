@@ -216,6 +216,81 @@ __global__ void __launch_bounds__(FY<L>::NT) k_p2(MV mv) {
 }
 
 // ---------------------------------------------------------------------------------------
+// P4, staged: persistent CTAs walk tiles (plane, T adjacent kx); each tile's input pencils are
+// prefetched with cp.async (16 B per copy, zero-filled outside the data) into the other half of
+// a two-stage shared-memory ring while the CTA transforms the current tile in place, so global
+// loads stay in flight through the FFT stages (the unstaged kernel waits on them): C4 P4 0.266
+// -> 0.198 ms.  (The same staging of P2, whose input is half zero padding, measured slower than
+// the unstaged P2, which skips the padding loads altogether, and a staged P5 was slower than the
+// unstaged one (its gather epilogue dominates): both stay unstaged.)
+// ---------------------------------------------------------------------------------------
+template <int L, int KB = 32> struct FYS {  // KB: shared memory per stage
+    static constexpr int T = clampi(KB * 64 / L, 1, 32);
+    static constexpr int NT = clampi(T * L / 16, 64, 256);
+};
+
+template <int L, int KB>
+__global__ void __launch_bounds__(FYS<L, KB>::NT) k_p4s(MV mv) {
+    constexpr int T = FYS<L, KB>::T, NT = FYS<L, KB>::NT;
+    extern __shared__ __align__(16) double2 sm[];  // [2][L][T]
+    const int nkx = mv.nkx, nf = mv.nf;
+    const int ntx = (nkx + T - 1) / T;
+    int G = 0;
+    for (int f = 0; f < nf; ++f) G += mv.nzout[f];
+    const int ntiles = G * ntx;
+    auto decode = [&](int tl, int& f, int& j, int& xt) {
+        xt = tl % ntx;
+        int g = tl / ntx;
+        f = 0;
+        while (g >= mv.nzout[f]) g -= mv.nzout[f++];
+        j = g;
+    };
+    auto prefetch = [&](int tl, int stg) {
+        int f, j, xt;
+        decode(tl, f, j, xt);
+        const double2* in = mv.X3[f] + (int64_t)j * L * nkx;
+        double2* dst = sm + stg * L * T;
+        for (int e = threadIdx.x; e < L * T; e += NT) {
+            const int n = e / T, t = e % T;
+            const int kx = xt * T + t;
+            const bool valid = kx < nkx;
+            cp_async16(dst + e, valid ? in + (int64_t)n * nkx + kx : in, valid);
+        }
+        cp_async_commit();
+    };
+    if ((int)blockIdx.x < ntiles) prefetch(blockIdx.x, 0);
+    int it = 0;
+    for (int tl = blockIdx.x; tl < ntiles; tl += gridDim.x, ++it) {
+        const int stg = it & 1;
+        if (tl + (int)gridDim.x < ntiles) prefetch(tl + gridDim.x, stg ^ 1);
+        else cp_async_commit();
+        cp_async_wait<1>();
+        __syncthreads();
+        int f, j, xt;
+        decode(tl, f, j, xt);
+        const int eyo = mv.ext_out[f][1];
+        const bool ph = mv.faxis[f] != 1;
+        double2* buf = sm + stg * L * T;
+        auto lds = [&](int t, int n) {
+            double2 v = buf[n * T + t];
+            if (ph) v = cmul(v, half_phase(mv.tw, ktil(n, L), L, +1));
+            return v;
+        };
+        auto stN = [&](int t, int p, double2 v) {
+            const int kx = xt * T + t;
+            const int yy = Plan<L>::freq(p);
+            if (kx < nkx && yy < eyo) {
+                const int pr = row_owner(mv, yy);  // row yy goes to rank pr for P5
+                mv.S2[pr][f][((int64_t)j * mv.nr[pr][3 + f] + (yy - mv.ya[pr])) * nkx + kx] = v;
+            }
+        };
+        fft_run<L, T, NT, true, true>(buf, lds, stN, mv.tw);
+        __syncthreads();
+    }
+    cp_async_wait<0>();
+}
+
+// ---------------------------------------------------------------------------------------
 // P3: forward z FFT of the three source fields, orientation-block MAC (Eqs. 10-12), inverse z
 //   One tile = T adjacent kx x the ky pair {q, My - q} (the two share every folded spectrum
 //   row, so each R element is read from HBM once).  Persistent, TMA-fed: each CTA walks tiles
@@ -387,42 +462,6 @@ __global__ void __launch_bounds__(kNT3) k_p3(MV mv) {
         fft_run<L, W, kNT3, true, true>(buf, ldo, sto, mv.tw, NF * T2);
         __syncthreads();
     }
-}
-
-// ---------------------------------------------------------------------------------------
-// P4: times phi_f,y, inverse C2C along y, pruned to y < ey_f
-// ---------------------------------------------------------------------------------------
-template <int L>
-__global__ void __launch_bounds__(FY<L>::NT, 3) k_p4(MV mv) {
-    constexpr int T = TY<L>::T;
-    extern __shared__ double2 sm[];
-    const int f = blockIdx.y;
-    if (f >= mv.nf) return;
-    const int alpha = mv.faxis[f];
-    const int eyo = mv.ext_out[f][1];
-    const int nkx = mv.nkx;
-    const int ntile = (nkx + T - 1) / T;
-    if (ntile == 0) return;
-    const int j = blockIdx.x / ntile, tile = blockIdx.x % ntile;
-    if (j >= mv.nzout[f]) return;
-    const double2* __restrict__ in = mv.X3[f] + (int64_t)j * L * nkx;
-    const bool ph = alpha != 1;
-    auto ld0 = [&](int t, int n) -> double2 {
-        const int kx = tile * T + t;
-        if (kx >= nkx) return czero();
-        double2 v = in[(int64_t)n * nkx + kx];
-        if (ph) v = cmul(v, half_phase(mv.tw, ktil(n, L), L, +1));
-        return v;
-    };
-    auto stN = [&](int t, int p, double2 v) {
-        const int kx = tile * T + t;
-        const int yy = Plan<L>::freq(p);
-        if (kx < nkx && yy < eyo) {
-            const int pr = row_owner(mv, yy);  // row yy goes to rank pr for P5
-            mv.S2[pr][f][((int64_t)j * mv.nr[pr][3 + f] + (yy - mv.ya[pr])) * nkx + kx] = v;
-        }
-    };
-    fft_run<L, T, FY<L>::NT, true, true>(sm, ld0, stN, mv.tw);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -751,6 +790,32 @@ static cudaError_t launch_p1(const MV& mv, cudaStream_t st) {
     });
     return cudaGetLastError();
 }
+template <class K>
+static int persistent_grid(K kern, int nthr, size_t smem, int ntiles) {
+    int per_sm = 0, nsm = 0, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nthr, smem);
+    return std::max(1, std::min(ntiles, std::max(1, per_sm) * nsm));
+}
+template <int LL, int KB>
+static cudaError_t launch_p4s_t(const MV& mv, cudaStream_t st) {
+    constexpr int T = FYS<LL, KB>::T, NT = FYS<LL, KB>::NT;
+    int G = 0;
+    for (int f = 0; f < mv.nf; ++f) G += mv.nzout[f];
+    const size_t smem = sizeof(double2) * 2 * LL * T;
+    cudaError_t e = prep(k_p4s<LL, KB>, smem);
+    if (e) return e;
+    const int ntiles = G * ((mv.nkx + T - 1) / T);
+    if (ntiles == 0) return cudaSuccess;
+    k_p4s<LL, KB><<<persistent_grid(k_p4s<LL, KB>, NT, smem, ntiles), NT, smem, st>>>(mv);
+    return cudaSuccess;
+}
+static cudaError_t launch_p4s(const MV& mv, cudaStream_t st) {
+    cudaError_t e;
+    VC_DISPATCH_L(mv.My, { e = launch_p4s_t<LL, 32>(mv, st); if (e) return e; });
+    return cudaGetLastError();
+}
 static cudaError_t launch_p2(const MV& mv, cudaStream_t st) {
     int maxz = 0;
     for (int b = 0; b < 3; ++b) maxz = std::max(maxz, mv.nzin[b]);
@@ -1037,19 +1102,6 @@ static cudaError_t launch_p3(const MV& mv, cudaStream_t st) {
     return cudaGetLastError();
 }
 
-static cudaError_t launch_p4(const MV& mv, cudaStream_t st) {
-    int maxz = 0;
-    for (int f = 0; f < mv.nf; ++f) maxz = std::max(maxz, mv.nzout[f]);
-    VC_DISPATCH_L(mv.My, {
-        constexpr int T = TY<LL>::T;
-        const size_t smem = sizeof(double2) * LL * T;
-        cudaError_t e = prep(k_p4<LL>, smem);
-        if (e) return e;
-        dim3 grid(std::max(1, ((mv.nkx + T - 1) / T) * maxz), mv.nf);
-        k_p4<LL><<<grid, FY<LL>::NT, smem, st>>>(mv);
-    });
-    return cudaGetLastError();
-}
 static cudaError_t launch_p5(const MV& mv, cudaStream_t st) {
     int maxz = 0, maxch = 0;
     for (int f = 0; f < mv.nf; ++f) maxz = std::max(maxz, mv.nzout[f]);
@@ -1677,7 +1729,7 @@ vc_status matvec_dev(vc_ctx* c, const double* d_x, double* d_y) {
     if (T.ev_ok) VC_CUDA(c, cudaEventRecord(T.ev[0], st));
     k_zero<<<std::max<int64_t>(1, std::min<int64_t>((c->NL + 255) / 256, 1184)), 256, 0, st>>>(d_y, c->NL);
     cudaError_t (*launch[5])(const MV&, cudaStream_t) = {launch_p1, launch_p2, launch_p3,
-                                                         launch_p4, launch_p5};
+                                                         launch_p4s, launch_p5};
     for (int p = 0; p < 5; ++p) {
         if (c->world > 1 && (p == 1 || p == 4)) {
             // x-transformed planes: rows -> kx slabs before P2, back before P5

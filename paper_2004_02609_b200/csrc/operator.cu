@@ -848,11 +848,12 @@ template <int NZO, bool ODD, int T>
 __device__ __forceinline__ void p3d_acc(double2 (&a0)[kZB], double2 (&a1)[kZB],
                                         const int (&zo2)[kZB], int s2a, const double* Kb,
                                         const double2* X, int n, const int* zi2) {
+    const double2* X1 = X + n * T;  // side 1 rows (unused when nside = 1)
 #pragma unroll 2
-    for (int ji = 0; ji < n; ++ji) {
+    for (int ji = 0; ji < n; ++ji, X += T, X1 += T) {
         const int z2 = zi2[ji];
-        const double2 q0 = X[ji * T];
-        const double2 q1 = X[(n + ji) * T];  // side 1 (unused when nside = 1)
+        const double2 q0 = *X;
+        const double2 q1 = *X1;
 #pragma unroll
         for (int k = 0; k < NZO; ++k) {
             const int g2 = zo2[k] - z2;
@@ -879,10 +880,11 @@ __device__ __forceinline__ void p3d_acc_win(double2 (&a0)[kZB], double2 (&a1)[kZ
     double w[NZO];
 #pragma unroll
     for (int k = 0; k < NZO; ++k) w[k] = kval(G0 + 2 * k);
+    const double2* X1 = X + n * T;  // side 1 rows (unused when nside = 1)
 #pragma unroll 2
-    for (int ji = 0; ji < n; ++ji) {
-        const double2 q0 = X[ji * T];
-        const double2 q1 = X[(n + ji) * T];  // side 1 (unused when nside = 1)
+    for (int ji = 0; ji < n; ++ji, X += T, X1 += T) {
+        const double2 q0 = *X;
+        const double2 q1 = *X1;
 #pragma unroll
         for (int k = 0; k < NZO; ++k) {
             a0[k].x = fma(w[k], q0.x, a0[k].x);

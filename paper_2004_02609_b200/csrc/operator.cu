@@ -93,7 +93,7 @@ template <int L> struct FX {
     static constexpr int MINB = 65536 / (NT * 80) < 1 ? 1 : 65536 / (NT * 80);  // <= 80 regs
 };
 template <int L> struct FY {
-    static constexpr int T = clampi(4096 / L, 1, 32);
+    static constexpr int T = clampi(4096 / L, 2, 32);  // >= 2 adjacent kx: 32-byte row segments
     static constexpr int NT = 256;
 };
 template <int L> struct TX { static constexpr int T = FX<L>::T; };
@@ -1462,6 +1462,12 @@ vc_status operator_build(vc_ctx* c, const vc_build_opts* o) {
         for (auto& e : ev) cudaEventDestroy(e);
         c->stats.ms_kgen = t_kgen;
         c->stats.ms_kfft = t_fft + t_ext;
+        // the build grid is the largest transient (C5: 69 GB): keep it for reuse only when
+        // small, so that the pass buffers allocated next fit beside the kernel tables
+        if (G.bytes() > ((size_t)8 << 30)) {
+            G.reset();
+            Ko.reset();
+        }
         VC_CUDA(c, cudaGetLastError());
     }
     // ---- spatial partition: rank p owns a contiguous range of preconditioner

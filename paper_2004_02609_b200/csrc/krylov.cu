@@ -68,10 +68,12 @@ __global__ void __launch_bounds__(kRedNT) k_multidot(const double* __restrict__ 
     __syncthreads();
     if (!last) return;
     __threadfence();
-    for (int i = threadIdx.x; i < nv; i += blockDim.x) {
+    // warp per vector, lanes stride over the block partials, fixed-order shuffle tree
+    for (int i = wp; i < nv; i += kRedNT / 32) {
         double v = 0.0;
-        for (int b = 0; b < (int)gridDim.x; ++b) v += __ldcg(partial + (int64_t)b * nv + i);
-        out[i] = v;
+        for (int b = lane; b < (int)gridDim.x; b += 32) v += __ldcg(partial + (int64_t)b * nv + i);
+        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) out[i] = v;
     }
     if (threadIdx.x == 0) *ticket = 0u;
 }

@@ -185,6 +185,8 @@ struct vc_ctx {
     // near-field P entries for the preconditioner blocks, cut from the octant tables of the
     // kernel build (same generator, no re-evaluation): [pair][iz][iy][ix], |t| <= box
     vc::DevBuf<double> pcTab;
+    std::vector<cudaEvent_t> kev;  // kernel-table build: 4 events per block
+    int kev_n = 0;
     int pcTabDim[3] = {0, 0, 0};
     int pcPair[3][3] = {{-1, -1, -1}, {-1, -1, -1}, {-1, -1, -1}};
     vc::DevBuf<double> cap_b, cap_rho, cap_part, cap_col;  // capacitance columns
@@ -255,6 +257,7 @@ vc_status debug_kernel_entries(vc_ctx* c, int n, const int32_t* kind, const int3
                                const int32_t* b, const int32_t* d, double* out);
 vc_status debug_fft(vc_ctx* c, int L, int nl, double* data, int dir);
 vc_status partition_build(vc_ctx* c);  // operator.cu: slabs, local panels, local slot maps
+void kernel_table_times(vc_ctx* c);
 int row_owner_abs(const vc_ctx* c, int yabs);
 void plan_kx_slabs(int W, int Kx, int T3, int* kxa);
 int row_owner_plan(int W, int Nv, int nb, int b0, int nbr, int yabs);

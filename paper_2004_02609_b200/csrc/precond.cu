@@ -73,30 +73,46 @@ __global__ void k_pc_fill(const int32_t* __restrict__ un, const int64_t* __restr
     }
 }
 
-// in-place Gauss-Jordan inverse of an SPD block (no pivoting needed), one CTA per block
-__global__ void k_pc_invert(const int32_t* __restrict__ un, const int64_t* __restrict__ uoff,
-                            double* __restrict__ blocks) {
+// In-place Gauss-Jordan inverse of an SPD block (no pivoting needed), one CTA (32 x 16
+// threads) per unique block.  The block is worked on in shared memory when it fits (copied in
+// and out once), else in global memory (L2-resident); the 2-D thread layout avoids index
+// divisions in the n^2 update of every pivot step.
+__global__ void __launch_bounds__(512) k_pc_invert(const int32_t* __restrict__ un,
+                                                   const int64_t* __restrict__ uoff,
+                                                   double* __restrict__ blocks, int smem_elems) {
     extern __shared__ double sh[];
     const int u = blockIdx.x;
     const int n = un[u];
-    double* A = blocks + uoff[u];
+    double* G = blocks + uoff[u];
     double* rowk = sh;
     double* colk = sh + n;
+    const bool in_smem = (int64_t)n * n + 2 * n <= smem_elems;
+    double* A = in_smem ? sh + 2 * n : G;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 columns x 16 rows
+    if (in_smem) {
+        for (int64_t e = threadIdx.x; e < (int64_t)n * n; e += blockDim.x) A[e] = G[e];
+    }
     for (int k = 0; k < n; ++k) {
         __syncthreads();
-        const double piv = A[(int64_t)k * n + k];
-        const double ip = 1.0 / piv;
+        const double ip = 1.0 / A[(int64_t)k * n + k];
         for (int j = threadIdx.x; j < n; j += blockDim.x) {
             rowk[j] = j == k ? ip : A[(int64_t)k * n + j] * ip;
             colk[j] = A[(int64_t)j * n + k];
         }
         __syncthreads();
-        for (int64_t e = threadIdx.x; e < (int64_t)n * n; e += blockDim.x) {
-            const int i = (int)(e / n), j = (int)(e % n);
-            if (i == k) A[e] = rowk[j];
-            else if (j == k) A[e] = -colk[i] * ip;
-            else A[e] -= colk[i] * rowk[j];
+        for (int i = ty; i < n; i += 16) {
+            double* Ai = A + (int64_t)i * n;
+            const double ci = colk[i];
+            for (int j = tx; j < n; j += 32) {
+                if (i == k) Ai[j] = rowk[j];
+                else if (j == k) Ai[j] = -ci * ip;
+                else Ai[j] = fma(-ci, rowk[j], Ai[j]);
+            }
         }
+    }
+    if (in_smem) {
+        __syncthreads();
+        for (int64_t e = threadIdx.x; e < (int64_t)n * n; e += blockDim.x) G[e] = A[e];
     }
 }
 
@@ -146,16 +162,17 @@ __global__ void __launch_bounds__(256) k_pc_apply_grouped(
     }
 }
 
-struct SigHash {
-    size_t operator()(const std::vector<int32_t>& v) const {
-        uint64_t h = 1469598103934665603ull;
-        for (int32_t x : v) {
-            h ^= (uint32_t)x;
-            h *= 1099511628211ull;
-        }
-        return (size_t)h;
+// per-panel diagonal of R: 1/Ī on dielectric rows; conductor rows 1 (none), 1/P_self
+// (diagonal-only option) or 0 (their block of R_BD writes them)
+__global__ void k_pc_dinv(int64_t n, const int32_t* __restrict__ cid, const double* __restrict__ ibar,
+                          int kind, double pself, double* __restrict__ dinv) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        if (cid[i] == 0) dinv[i] = kind == 1 ? 1.0 : 1.0 / ibar[i];
+        else dinv[i] = kind == 1 ? 1.0 : (kind == 2 ? 1.0 / pself : 0.0);
     }
-};
+}
+
 
 }  // namespace
 
@@ -176,17 +193,17 @@ vc_status precond_build(vc_ctx* c, const int32_t box_in[3], int kind) {
     auto G = [&](int64_t i) { return c->world > 1 ? c->h_gidx[i] : i; };  // local -> global
     const double fpe = 4.0 * kPi * kEps0;
     const double pscale = c->dv * c->dv * c->dv / fpe;
-    // diagonal part
-    std::vector<double> dinv(N, 0.0);
+    // diagonal part (on the device, from the rank's panel arrays)
     // self term of a unit square (textbook), used only for the diagonal-only option
     const double pself = pscale * ((4.0 / 3.0) * (1.0 - std::sqrt(2.0)) + 4.0 * std::log(1.0 + std::sqrt(2.0)));
-    for (int64_t i = 0; i < N; ++i) {
-        const int64_t p = G(i);
-        if (c->h_cid[p] == 0) dinv[i] = kind == 1 ? 1.0 : 1.0 / c->h_ibar[p];
-        else dinv[i] = kind == 1 ? 1.0 : (kind == 2 ? 1.0 / pself : 0.0);
-    }
     VC_CUDA(c, pc->diag_inv.alloc(std::max<int64_t>(1, N)));
-    if (N) VC_CUDA(c, cudaMemcpyAsync(pc->diag_inv.p, dinv.data(), 8 * N, cudaMemcpyHostToDevice, st));
+    if (N) {
+        const bool loc = c->world > 1;
+        k_pc_dinv<<<(unsigned)std::min<int64_t>((N + 255) / 256, 148 * 8), 256, 0, st>>>(
+            N, loc ? c->lp.cid.p : c->pan.cid.p, loc ? c->lp.ibar.p : c->pan.ibar.p, kind, pself,
+            pc->diag_inv.p);
+        count_launch(c);
+    }
     tr.mark("diagonal");
     if (kind != 3) {
         VC_CUDA(c, cudaStreamSynchronize(st));
@@ -204,7 +221,8 @@ vc_status precond_build(vc_ctx* c, const int32_t box_in[3], int kind) {
     cond.reserve(c->Nc);
     for (int64_t i = 0; i < N; ++i)
         if (c->h_cid[G(i)] > 0) cond.push_back((int32_t)i);  // local indices
-    std::unordered_map<int64_t, int32_t> box_index;
+    // dense box table (the box grid is small: (N_x/N_v)(N_y/N_v)(N_z/N_v) entries)
+    std::vector<int32_t> box_index((size_t)nb[0] * nb[1] * nb[2], -1);
     std::vector<int64_t> box_keys;
     std::vector<int32_t> pb(cond.size());
     for (size_t q = 0; q < cond.size(); ++q) {
@@ -213,12 +231,12 @@ vc_status precond_build(vc_ctx* c, const int32_t box_in[3], int kind) {
         int64_t bx[3];
         for (int a = 0; a < 3; ++a) bx[a] = std::min<int64_t>(s[a] / nv[a], nb[a] - 1);
         const int64_t key = (bx[2] * nb[1] + bx[1]) * nb[0] + bx[0];
-        auto it = box_index.find(key);
-        if (it == box_index.end()) {
-            it = box_index.emplace(key, (int32_t)box_keys.size()).first;
+        int32_t& bi = box_index[key];
+        if (bi < 0) {
+            bi = (int32_t)box_keys.size();
             box_keys.push_back(key);
         }
-        pb[q] = it->second;
+        pb[q] = bi;
     }
     const int nbox = (int)box_keys.size();
     tr.mark("box assignment");
@@ -227,8 +245,9 @@ vc_status precond_build(vc_ctx* c, const int32_t box_in[3], int kind) {
     for (int b = 0; b < nbox; ++b) bstart[b + 1] = bstart[b] + bcount[b];
     std::vector<int32_t> sorted(cond.size()), fillp(bstart.begin(), bstart.end() - 1);
     for (size_t q = 0; q < cond.size(); ++q) sorted[fillp[pb[q]]++] = cond[q];
-    // signatures (axis + slot relative to the box origin, canonical order) -> unique blocks
-    std::unordered_map<std::vector<int32_t>, int32_t, SigHash> uniq;
+    // signatures (axis + slot relative to the box origin, canonical order) -> unique blocks:
+    // a 64-bit hash per box, full comparison against the stored signature on a hash match
+    std::unordered_map<uint64_t, std::vector<int32_t>> by_hash;  // hash -> unique ids
     std::vector<int32_t> buid(nbox), un, ulist_off, uaxis, uslot;
     std::vector<int64_t> uoff;
     int64_t total = 0;
@@ -237,33 +256,47 @@ vc_status precond_build(vc_ctx* c, const int32_t box_in[3], int kind) {
         const int64_t key = box_keys[b];
         const int64_t bx = key % nb[0], by = (key / nb[0]) % nb[1], bz = key / ((int64_t)nb[0] * nb[1]);
         const int org[3] = {(int)(bx * nv[0]), (int)(by * nv[1]), (int)(bz * nv[2])};
-        std::vector<int32_t> sig;
-        sig.reserve(4 * bcount[b]);
-        for (int q = bstart[b]; q < bstart[b + 1]; ++q) {
-            const int64_t p = G(sorted[q]);
-            sig.push_back(c->h_axis[p]);
-            sig.push_back(c->h_si[p] - org[0]);
-            sig.push_back(c->h_sj[p] - org[1]);
-            sig.push_back(c->h_sk[p] - org[2]);
+        const int n = bcount[b];
+        auto sig_at = [&](int q, int t) -> int32_t {  // t: 0 axis, 1..3 slot - origin
+            const int64_t p = G(sorted[bstart[b] + q]);
+            return t == 0 ? c->h_axis[p] : (t == 1 ? c->h_si[p] - org[0] : (t == 2 ? c->h_sj[p] - org[1] : c->h_sk[p] - org[2]));
+        };
+        uint64_t h = 1469598103934665603ull ^ (uint64_t)n;
+        for (int q = 0; q < n; ++q)
+            for (int t = 0; t < 4; ++t) {
+                h ^= (uint32_t)sig_at(q, t);
+                h *= 1099511628211ull;
+            }
+        int id = -1;
+        auto& cand = by_hash[h];
+        for (int u : cand) {
+            if (un[u] != n) continue;
+            bool same = true;
+            const int l0 = ulist_off[u];
+            for (int q = 0; q < n && same; ++q)
+                same = uaxis[l0 + q] == sig_at(q, 0) && uslot[3 * (l0 + q)] == sig_at(q, 1) &&
+                       uslot[3 * (l0 + q) + 1] == sig_at(q, 2) && uslot[3 * (l0 + q) + 2] == sig_at(q, 3);
+            if (same) {
+                id = u;
+                break;
+            }
         }
-        auto it = uniq.find(sig);
-        if (it == uniq.end()) {
-            const int id = (int)un.size();
-            const int n = bcount[b];
+        if (id < 0) {
+            id = (int)un.size();
             un.push_back(n);
             ulist_off.push_back((int32_t)uaxis.size());
             uoff.push_back(total);
             total += (int64_t)n * n;
             maxn = std::max(maxn, n);
-            for (size_t t = 0; t < sig.size(); t += 4) {
-                uaxis.push_back(sig[t]);
-                uslot.push_back(sig[t + 1]);
-                uslot.push_back(sig[t + 2]);
-                uslot.push_back(sig[t + 3]);
+            for (int q = 0; q < n; ++q) {
+                uaxis.push_back(sig_at(q, 0));
+                uslot.push_back(sig_at(q, 1));
+                uslot.push_back(sig_at(q, 2));
+                uslot.push_back(sig_at(q, 3));
             }
-            it = uniq.emplace(std::move(sig), id).first;
+            cand.push_back(id);
         }
-        buid[b] = it->second;
+        buid[b] = id;
     }
     tr.mark("signatures");
     if ((size_t)maxn * (kPcRows + 1) * sizeof(double) > 220 * 1024)
@@ -331,10 +364,15 @@ vc_status precond_build(vc_ctx* c, const int32_t box_in[3], int kind) {
         }
         k_pc_fill<<<g, 256, 0, st>>>(pc->uniq_n.p, pc->uniq_off.p, pc->uniq_list_off.p,
                                      pc->uniq_axis.p, pc->uniq_slot.p, pc->blocks.p, tab);
-        const size_t sh = 2 * sizeof(double) * maxn;
+        // shared memory for the largest block if it fits, else only the pivot row / column
+        const size_t full = sizeof(double) * ((size_t)maxn * maxn + 2 * maxn);
+        const size_t cap = (size_t)max_dyn_smem() - 1024;
+        const size_t sh = full <= cap ? full : std::max(2 * sizeof(double) * maxn,
+                                                         std::min(cap, (size_t)160 * 1024));
         if (sh > 48 * 1024)
             VC_CUDA(c, grant_max_dyn_smem(k_pc_invert, max_dyn_smem()));
-        k_pc_invert<<<pc->nuniq, 512, sh, st>>>(pc->uniq_n.p, pc->uniq_off.p, pc->blocks.p);
+        k_pc_invert<<<pc->nuniq, 512, sh, st>>>(pc->uniq_n.p, pc->uniq_off.p, pc->blocks.p,
+                                                (int)(sh / sizeof(double)));
         count_launch(c, 2);
     }
     if (tr.on) {

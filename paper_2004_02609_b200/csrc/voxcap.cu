@@ -109,6 +109,7 @@ void vc_destroy(vc_ctx* c) {
             for (auto& e : c->timing.ev) cudaEventDestroy(e);
         if (c->arn_ev_ok)
             for (auto& e : c->arn_ev) cudaEventDestroy(e);
+        for (auto& e : c->kev) cudaEventDestroy(e);
         if (c->own_stream) cudaStreamDestroy(c->stream);
     }
     delete c;
@@ -240,6 +241,7 @@ vc_status vc_build_operator(vc_ctx* c, const vc_build_opts* o) {
         cudaEventElapsedTime(&b, e1, e2);
         c->stats.ms_setup = a + b;
         c->stats.ms_precond_build = b;
+        kernel_table_times(c);
         c->precond_kind = kind;
         c->has_op = true;
     } else {

@@ -9,6 +9,10 @@ constexpr double kPi = 3.14159265358979323846264338327950288;
 constexpr double kEps0 = 8.8541878128e-12;  // F/m (reading O15)
 constexpr int kMaxL = 4096;                 // largest FFT length per axis
 constexpr int kTabN = 2 * kMaxL;            // twiddle table: exp(-2 pi i n / kTabN)
+// slot-map entries (slot -> panel): -1 = no panel, else the panel index in bits 0-28 with the
+// row kind folded in, so the gather of P5 needs no per-panel info load: bit 30 = dielectric
+// panel, bit 29 = its normal points along -axis (reading O7)
+constexpr int32_t kSlotDiel = 1 << 30, kSlotNeg = 1 << 29, kSlotIdx = (1 << 29) - 1;
 // Grant kernel `k` the largest dynamic shared memory the device allows next to its static
 // shared memory.  The limit is a process-wide function attribute: contexts of one process
 // (ranks of a thread group) launch with different sizes, so a per-launch value would race.

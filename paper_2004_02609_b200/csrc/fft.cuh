@@ -173,8 +173,16 @@ __device__ __forceinline__ void fft_stage(LD&& ld, ST&& st, const double2* __res
 }
 
 // Shared-memory index of (pencil t, position p): PF -> [pos][pencil], else [pencil][pos].
+// PF = false: the low 3 bits of p (8 complex = one 128-byte bank row) are XOR-swizzled with
+// bits 3-5, 6-8 and 9-11, so that the three access patterns of a quarter-warp -- 8 consecutive
+// aligned positions (stages with S >= 8), stride 8 (the last radix-8 stage, S = 1) and stride
+// 64 (digit-reversed frequency reads) -- all hit 8 distinct bank groups (the unswizzled stride
+// patterns were 8-way conflicts: 27M extra wavefronts in k_p1<1024> on C4).
 template <int L, int T, bool PF>
-__device__ __forceinline__ int smi(int t, int p) { return PF ? p * T + t : t * L + p; }
+__device__ __forceinline__ int smi(int t, int p) {
+    if constexpr (PF) return p * T + t;
+    else return t * L + (p ^ (((p >> 3) ^ (p >> 6) ^ (p >> 9)) & 7));
+}
 
 // Full transform: stage 0 reads through `ld0`, the last stage writes through `stN`, and the
 // intermediate stages use shared memory `sm` (layout smi<L,T,PF>).  If NS == 1 the single

@@ -133,22 +133,20 @@ __global__ void __launch_bounds__(FX<L>::NT, FX<L>::MINB) k_p1(MV mv) {
     const int64_t zrow =
         ((int64_t)(z + mv.lo[2]) * Gy + mv.lo[1] + mv.ya[mv.rank]) * Gx + mv.lo[0];
     const double* __restrict__ x = mv.x;
+    // branch-free (predicated loads, selects), so the unrolled stage-0 loop issues all its
+    // slot-map loads, then all its x loads, instead of one dependent pair at a time
     auto ld0 = [&](int t, int n) -> double2 {
         const int q = ch * T + t;
-        double re = 0.0, im = 0.0;
-        if (q < nyp && n < ex) {
-            const int l0 = 2 * q - s;
-            const int64_t r0 = zrow + (int64_t)l0 * Gx + n;
-            if (l0 >= 0) {
-                const int p0 = smap[r0];
-                if (p0 >= 0) re = x[p0];
-            }
-            if (l0 + 1 < nrow) {
-                const int p1 = smap[r0 + Gx];
-                if (p1 >= 0) im = x[p1];
-            }
-        }
-        return make_double2(re, im);
+        const int l0 = 2 * q - s;
+        const bool ok = q < nyp && n < ex;
+        const bool v0 = ok && l0 >= 0, v1 = ok && l0 + 1 < nrow;
+        const int64_t r0 = zrow + (int64_t)l0 * Gx + n;
+        const int32_t e0 = v0 ? __ldg(smap + r0) : -1;
+        const int32_t e1 = v1 ? __ldg(smap + r0 + Gx) : -1;
+        // (predicated, not clamped to x[0]: a rank may own no panels, x == nullptr)
+        const double a = e0 >= 0 ? __ldg(x + (e0 & kSlotIdx)) : 0.0;
+        const double b = e1 >= 0 ? __ldg(x + (e1 & kSlotIdx)) : 0.0;
+        return make_double2(a, b);
     };
     auto sts = [&](int t, int p, double2 v) { sm[smi<L, T, false>(t, p)] = v; };
     fft_run<L, T, FX<L>::NT, false, false>(sm, ld0, sts, mv.tw);
@@ -484,55 +482,70 @@ __global__ void __launch_bounds__(FX<L>::NT, FX<L>::MINB) k_p5(MV mv) {
     if (j >= mv.nzout[f]) return;
     const int z = zlist(mv, 3 + f, j);
     const bool ph = alpha != 0;
-    auto At = [&](int yrow, int k) -> double2 {
-        const int qd = kx_owner(mv, k);  // column k arrived from rank qd
-        const int nk = mv.kxa[qd + 1] - mv.kxa[qd];
-        double2 v = mv.R2[qd][f][((int64_t)j * nrow + yrow) * nk + (k - mv.kxa[qd])];
-        if (ph) v = cmul(v, half_phase(mv.tw, k, L, +1));
-        if (k == 0 || 2 * k == L) v.y = 0.0;
-        return v;
+    auto At = [&](int yrow, int k, bool v) -> double2 {
+        int qd = 0, nk = mv.nkx, k0 = 0;
+        if (mv.W > 1) {
+            qd = kx_owner(mv, k);  // column k arrived from rank qd
+            k0 = mv.kxa[qd];
+            nk = mv.kxa[qd + 1] - k0;
+        }
+        const double2* src = mv.R2[qd][f] + ((int64_t)j * nrow + yrow) * nk + (k - k0);
+        double2 w = v ? __ldg(src) : czero();
+        if (ph) w = cmul(w, half_phase(mv.tw, k, L, +1));
+        if (k == 0 || 2 * k == L) w.y = 0.0;
+        return w;
     };
     auto ld0 = [&](int t, int n) -> double2 {
         const int q = ch * T + t;
-        if (q >= nyp) return czero();
         const int l0 = 2 * q - s;
-        const bool has0 = l0 >= 0, has1 = l0 + 1 < nrow;
-        double2 A = czero(), B = czero();
-        if (2 * n <= L) {
-            if (has0) A = At(l0, n);
-            if (has1) B = At(l0 + 1, n);
-        } else {
-            if (has0) A = cconj(At(l0, L - n));
-            if (has1) B = cconj(At(l0 + 1, L - n));
+        const bool ok = q < nyp;
+        const bool has0 = ok && l0 >= 0, has1 = ok && l0 + 1 < nrow;
+        const bool lo = 2 * n <= L;
+        const int k = lo ? n : L - n;
+        double2 A = At(has0 ? l0 : 0, k, has0), B = At(has1 ? l0 + 1 : 0, k, has1);
+        if (!lo) {
+            A.y = -A.y;
+            B.y = -B.y;
         }
         return make_double2(A.x - B.y, A.y + B.x);
     };
+    // the last stage goes to shared memory; the gather then walks each output line with
+    // consecutive lanes on consecutive slots (coalesced slot-map reads and y writes; the panel
+    // kind and the dielectric sign come folded into the slot-map entry, common.cuh kSlot*)
+    auto sts = [&](int t, int p, double2 v) { sm[smi<L, T, false>(t, p)] = v; };
+    fft_run<L, T, FX<L>::NT, true, false>(sm, ld0, sts, mv.tw);
+    __syncthreads();
     const int32_t* __restrict__ smap = mv.slotmap[alpha];
     const int Gx = mv.G[alpha][0], Gy = mv.G[alpha][1];
     const int64_t zrow =
         ((int64_t)(z + mv.lo[2]) * Gy + mv.lo[1] + mv.ya[mv.rank]) * Gx + mv.lo[0];
-    auto put = [&](int p, double val) {
-        const int inf = mv.info[p];
-        if ((inf & 1) != kind) return;
-        if (kind == 0) mv.y[p] = val;
-        else mv.y[p] = ((inf & 2) ? -val : val) + mv.ibar[p] * mv.x[p];
-    };
-    auto stN = [&](int t, int p, double2 v) {
+    const int32_t want = kind ? kSlotDiel : 0;
+    double* __restrict__ y = mv.y;
+    constexpr int NI = (L + FX<L>::NT - 1) / FX<L>::NT;  // slots per thread and line (exo <= L)
+#pragma unroll 1
+    for (int r = 0; r < 2 * T; ++r) {
+        const int t = r >> 1, half = r & 1;
         const int q = ch * T + t;
-        const int n = Plan<L>::freq(p);
-        if (q >= nyp || n >= exo) return;
-        const int l0 = 2 * q - s;
-        const int64_t r0 = zrow + (int64_t)l0 * Gx + n;
-        if (l0 >= 0) {
-            const int p0 = smap[r0];
-            if (p0 >= 0) put(p0, v.x);
+        const int l = 2 * q - s + half;
+        if (q >= nyp || l < 0 || l >= nrow) continue;
+        const int32_t* __restrict__ srow = smap + zrow + (int64_t)l * Gx;
+        int32_t e[NI];
+#pragma unroll
+        for (int i = 0; i < NI; ++i) {  // all slot-map loads of the line in flight together
+            const int n = threadIdx.x + i * FX<L>::NT;
+            e[i] = n < exo ? __ldg(srow + n) : -1;
         }
-        if (l0 + 1 < nrow) {
-            const int p1 = smap[r0 + Gx];
-            if (p1 >= 0) put(p1, v.y);
+#pragma unroll
+        for (int i = 0; i < NI; ++i) {
+            const int n = threadIdx.x + i * FX<L>::NT;
+            if (e[i] < 0 || (e[i] & kSlotDiel) != want) continue;
+            const double2 v = sm[smi<L, T, false>(t, Plan<L>::pos(n))];
+            const double val = half ? v.y : v.x;
+            const int p = e[i] & kSlotIdx;
+            if (kind == 0) y[p] = val;
+            else y[p] = ((e[i] & kSlotNeg) ? -val : val) + mv.ibar[p] * mv.x[p];
         }
-    };
-    fft_run<L, T, FX<L>::NT, true, false>(sm, ld0, stN, mv.tw);
+    }
 }
 
 // ---------------------------------------------------------------------------------------
@@ -1610,7 +1623,9 @@ __global__ void k_local_panels(int64_t nl, const int64_t* __restrict__ gidx,
         const int a = axis[g];
         const int gx = nx + (a == 0), gy = ny + (a == 1);
         int32_t* sm = a == 0 ? sm0 : (a == 1 ? sm1 : sm2);
-        sm[((int64_t)sk[g] * gy + sj[g]) * gx + si[g]] = (int32_t)i;
+        const int inf = info[g];  // same encoding as the global map (common.cuh kSlot*)
+        sm[((int64_t)sk[g] * gy + sj[g]) * gx + si[g]] =
+            (int32_t)i | ((inf & 1) ? kSlotDiel : 0) | ((inf & 3) == 3 ? kSlotNeg : 0);
     }
 }
 

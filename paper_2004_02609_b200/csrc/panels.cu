@@ -242,7 +242,7 @@ __global__ void k_emit(Geo g, int64_t Ftot, const int64_t* __restrict__ tile_off
             // Eq. (7): Ī = A (eps_d + eps_b) / (2 eps0 (eps_d - eps_b)); conductor rows 0
             o.ibar[p] = diel ? o.area_over_2eps0 * (fi[q].ed + fi[q].eb) / (fi[q].ed - fi[q].eb) : 0.0;
             o.fc[p] = diel ? 0.0 : fi[q].eb;
-            o.slotmap[a][r] = (int32_t)p;
+            o.slotmap[a][r] = (int32_t)p | (diel ? kSlotDiel : 0) | (diel && fi[q].sign < 0 ? kSlotNeg : 0);
             int* e = o.ext + ((diel ? 1 : 0) * 3 + a) * 6;
             atomicMin(e + 0, ii[q]);
             atomicMin(e + 1, jj[q]);
@@ -319,7 +319,7 @@ vc_status geometry_build(vc_ctx* c, const int32_t* d_label, const double* d_eps)
     VC_CUDA(c, cudaStreamSynchronize(st));
     if (hf.clash) return set_err(c, VC_ERR_INPUT, "two different conductors share a face");
     tr.mark("count + scan");
-    if (N >= INT32_MAX) return set_err(c, VC_ERR_UNSUPPORTED, "more than 2^31 panels");
+    if (N > kSlotIdx) return set_err(c, VC_ERR_UNSUPPORTED, "more than 2^29 panels");
 
     PanelsDev& P = c->pan;
     VC_CUDA(c, P.axis.alloc(N));

@@ -173,26 +173,28 @@ __device__ __forceinline__ void fft_stage(LD&& ld, ST&& st, const double2* __res
 }
 
 // Shared-memory index of (pencil t, position p): PF -> [pos][pencil], else [pencil][pos].
-// PF = false: the low 3 bits of p (8 complex = one 128-byte bank row) are XOR-swizzled with
-// bits 3-5, 6-8 and 9-11, so that the three access patterns of a quarter-warp -- 8 consecutive
-// aligned positions (stages with S >= 8), stride 8 (the last radix-8 stage, S = 1) and stride
-// 64 (digit-reversed frequency reads) -- all hit 8 distinct bank groups (the unswizzled stride
-// patterns were 8-way conflicts: 27M extra wavefronts in k_p1<1024> on C4).
-template <int L, int T, bool PF>
+// The low 3 bits of the index (8 complex = one 128-byte bank row) are XOR-swizzled with bits
+// 3-5, 6-8 and 9-11, so that the access patterns of a quarter-warp -- 8 consecutive aligned
+// elements (stages with S >= 8), and the strided patterns of the last radix-8 stage (S = 1) and
+// of digit-reversed frequency reads -- hit 8 distinct bank groups (unswizzled, these were 2- to
+// 8-way conflicts: 27M extra wavefronts in k_p1<1024> on C4).  PF = false always swizzles; PF
+// layouts swizzle only with SWZ (P3's buffers are filled by bulk copies in the plain layout).
+__device__ __forceinline__ int swz8(int i) { return i ^ (((i >> 3) ^ (i >> 6) ^ (i >> 9)) & 7); }
+template <int L, int T, bool PF, bool SWZ = false>
 __device__ __forceinline__ int smi(int t, int p) {
-    if constexpr (PF) return p * T + t;
-    else return t * L + (p ^ (((p >> 3) ^ (p >> 6) ^ (p >> 9)) & 7));
+    if constexpr (PF) return SWZ ? swz8(p * T + t) : p * T + t;
+    else return t * L + swz8(p);
 }
 
 // Full transform: stage 0 reads through `ld0`, the last stage writes through `stN`, and the
 // intermediate stages use shared memory `sm` (layout smi<L,T,PF>).  If NS == 1 the single
 // stage goes ld0 -> stN.  No trailing __syncthreads().
-template <int L, int T, int NT, bool INV, bool PF, int TB = 0, class LD, class ST>
+template <int L, int T, int NT, bool INV, bool PF, int TB = 0, bool SWZ = false, class LD, class ST>
 __device__ __forceinline__ void fft_run(double2* sm, LD&& ld0, ST&& stN,
                                         const double2* __restrict__ tw, const int Tn = T) {
     constexpr int NS = Plan<L>::NS;
-    auto lds = [&](int t, int p) { return sm[smi<L, T, PF>(t, p)]; };
-    auto sts = [&](int t, int p, double2 v) { sm[smi<L, T, PF>(t, p)] = v; };
+    auto lds = [&](int t, int p) { return sm[smi<L, T, PF, SWZ>(t, p)]; };
+    auto sts = [&](int t, int p, double2 v) { sm[smi<L, T, PF, SWZ>(t, p)] = v; };
     if constexpr (NS == 1) {
         fft_stage<L, T, NT, INV, PF, 0, TB>(ld0, stN, tw, Tn);
     } else if constexpr (NS == 2) {

@@ -210,7 +210,7 @@ __global__ void __launch_bounds__(FY<L>::NT) k_p2(MV mv) {
         out[((((int64_t)qq * nt3 + (kx >> mv.lgT3)) * 2 + side) * nzb + j) * mv.T3 +
             (kx & (mv.T3 - 1))] = v;
     };
-    fft_run<L, T, FY<L>::NT, false, true>(sm, ld0, stN, mv.tw);
+    fft_run<L, T, FY<L>::NT, false, true, 0, true>(sm, ld0, stN, mv.tw);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -252,7 +252,7 @@ __global__ void __launch_bounds__(FYS<L, KB>::NT) k_p4s(MV mv) {
             const int n = e / T, t = e % T;
             const int kx = xt * T + t;
             const bool valid = kx < nkx;
-            cp_async16(dst + e, valid ? in + (int64_t)n * nkx + kx : in, valid);
+            cp_async16(dst + smi<L, T, true, true>(t, n), valid ? in + (int64_t)n * nkx + kx : in, valid);
         }
         cp_async_commit();
     };
@@ -270,7 +270,7 @@ __global__ void __launch_bounds__(FYS<L, KB>::NT) k_p4s(MV mv) {
         const bool ph = mv.faxis[f] != 1;
         double2* buf = sm + stg * L * T;
         auto lds = [&](int t, int n) {
-            double2 v = buf[n * T + t];
+            double2 v = buf[smi<L, T, true, true>(t, n)];
             if (ph) v = cmul(v, half_phase(mv.tw, ktil(n, L), L, +1));
             return v;
         };
@@ -282,7 +282,7 @@ __global__ void __launch_bounds__(FYS<L, KB>::NT) k_p4s(MV mv) {
                 mv.S2[pr][f][((int64_t)j * mv.nr[pr][3 + f] + (yy - mv.ya[pr])) * nkx + kx] = v;
             }
         };
-        fft_run<L, T, NT, true, true>(buf, lds, stN, mv.tw);
+        fft_run<L, T, NT, true, true, 0, true>(buf, lds, stN, mv.tw);
         __syncthreads();
     }
     cp_async_wait<0>();
@@ -716,7 +716,7 @@ __global__ void __launch_bounds__(FY<L>::NT) k_fft_strided(double2* data, int64_
     auto stN = [&](int t, int p, double2 v) {
         if (c0 + t < ncols) base[(int64_t)Plan<L>::freq(p) * es + t] = v;
     };
-    fft_run<L, T, FY<L>::NT, false, true>(sm, ld0, stN, tw);
+    fft_run<L, T, FY<L>::NT, false, true, 0, true>(sm, ld0, stN, tw);
 }
 
 // Folded spectrum of block `blk`, tile-major for P3:

@@ -69,7 +69,11 @@ typedef struct {
     int32_t zmode;          /* z direction of the matvec: 0 = automatic, 1 = z-FFT
                                (3-D circulant, Eq. 11), 2 = direct z-convolution on the x/y
                                spectra (exact; cheaper when panels occupy few z-planes)       */
-    int32_t reserved[8];
+    int32_t no_mirror;      /* 0 = default: with a square x/y FFT grid on one rank, blocks that
+                               are x<->y mirrors of another (P^{yy} of P^{xx}, ...) are
+                               transposed from it instead of generated; 1 =
+                               generate every block (bitwise comparisons with multi-rank runs) */
+    int32_t reserved[7];
 } vc_build_opts;
 
 /* Solve options.  Zero fields take the paper's defaults. */

@@ -43,7 +43,7 @@ class VoxCapError(RuntimeError):
 class BuildOpts(ctypes.Structure):
     _fields_ = [("pad", ctypes.c_int32 * 3), ("box", ctypes.c_int32 * 3),
                 ("precond", ctypes.c_int32), ("zmode", ctypes.c_int32),
-                ("reserved", ctypes.c_int32 * 8)]
+                ("no_mirror", ctypes.c_int32), ("reserved", ctypes.c_int32 * 7)]
 
 
 class SolveOpts(ctypes.Structure):
@@ -295,10 +295,12 @@ class VoxCap:
         return out
 
     # -- operator ------------------------------------------------------------------------
-    def build_operator(self, pad=None, box=None, precond=3, zmode=0):
-        """zmode: 0 automatic, 1 z-FFT (3-D circulant), 2 direct z-convolution."""
+    def build_operator(self, pad=None, box=None, precond=3, zmode=0, mirror=True):
+        """zmode: 0 automatic, 1 z-FFT (3-D circulant), 2 direct z-convolution; mirror=False
+        generates every kernel block (no x<->y transposes)."""
         o = BuildOpts()
         o.zmode = int(zmode)
+        o.no_mirror = 0 if mirror else 1
         if pad is not None:
             for a in range(3):
                 o.pad[a] = int(pad[a])

@@ -15,7 +15,7 @@
 //   b -> sign(sibling b) eta, c -> sign(sibling c) eta.
 // Far pairs: Gauss-Legendre (triangle rule on shared axes), q per axis from the distance band
 //   (reading O6): P q = 6 (d < 5), 5 (< 15), 4 (< 50), 3; E q = 7 (< 5), 6 (< 10),
-//   5 (< 20), 4.
+//   5 (< 20), 4 (< 50), 3 (measured triangle-rule error at q = 3, d = 50: 5e-13 of 1/d^2).
 // These formulas are written independently of the CPU oracle (which follows Eqs. 15/16
 // verbatim in binary128); the parity tests compare the two.
 #pragma once
@@ -236,7 +236,7 @@ __device__ double kappa_gl_dispatch(int alpha, int beta, int q, double dx, doubl
 
 __device__ __forceinline__ int gl_order(int kind, double dist) {
     if (kind == 0) return dist < 5.0 ? 6 : dist < 15.0 ? 5 : dist < 50.0 ? 4 : 3;
-    return dist < 5.0 ? 7 : dist < 10.0 ? 6 : dist < 20.0 ? 5 : 4;
+    return dist < 5.0 ? 7 : dist < 10.0 ? 6 : dist < 20.0 ? 5 : dist < 50.0 ? 4 : 3;
 }
 
 constexpr double kNearFar = 4.0;

@@ -574,32 +574,52 @@ __device__ __forceinline__ int rep_t2(int n, int M, int s2) {
 // |t| = i (s = 0) or i + 1/2 (s = +-1/2) per axis.  P blocks are even in every component of t,
 // E^{a.} blocks odd along a and even otherwise (Table VIII), so the
 // full cyclic grid follows from this octant with signs.
+__device__ __forceinline__ int oct_D(int i, int alpha, int beta, int a) {
+    const int s2 = c2(alpha, a) - c2(beta, a);
+    // |t| = i (s2 = 0) or i + 1/2; slot offset D = t - s
+    return s2 == 0 ? i : (s2 > 0 ? i : i + 1);
+}
 __global__ void k_kgen_oct(double* Ko, int Ox, int Oy, int Oz, int kind, int alpha, int beta,
                            double scale) {
     const int64_t tot = (int64_t)Ox * Oy * Oz;
-    const int O[3] = {Ox, Oy, Oz};
     for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < tot;
          idx += (int64_t)gridDim.x * blockDim.x) {
         const int i[3] = {(int)(idx % Ox), (int)((idx / Ox) % Oy), (int)(idx / ((int64_t)Ox * Oy))};
-        int D[3];
-#pragma unroll
-        for (int a = 0; a < 3; ++a) {
-            const int s2 = c2(alpha, a) - c2(beta, a);
-            // |t| = i (s2 = 0) or i + 1/2; slot offset D = t - s
-            D[a] = s2 == 0 ? i[a] : (s2 > 0 ? i[a] : i[a] + 1);
-        }
-        (void)O;
-        Ko[idx] = scale * kappa(kind, alpha, beta, D[0], D[1], D[2]);
+        Ko[idx] = scale * kappa(kind, alpha, beta, oct_D(i[0], alpha, beta, 0),
+                                oct_D(i[1], alpha, beta, 1), oct_D(i[2], alpha, beta, 2));
     }
 }
 
-// copy the near corner [0, T) of an octant table (rescaled) into the preconditioner table
-__global__ void k_cut_octant(const double* __restrict__ Ko, int Ox, int Oy, int Oz,
-                             double* __restrict__ Tb, int Tx, int Ty, int Tz, double rescale) {
+// preconditioner near-field table: the near corner |t| < T of a P block's octant, evaluated
+// directly (the same kernel for generated and mirrored blocks, so both builds agree bitwise)
+__global__ void k_kgen_corner(double* __restrict__ Tb, int Tx, int Ty, int Tz, int Ox, int Oy,
+                              int Oz, int alpha, int beta, double scale) {
     const int n = Tx * Ty * Tz;
     for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
         const int ix = e % Tx, iy = (e / Tx) % Ty, iz = e / (Tx * Ty);
-        Tb[e] = (ix < Ox && iy < Oy && iz < Oz) ? rescale * Ko[((int64_t)iz * Oy + iy) * Ox + ix] : 0.0;
+        Tb[e] = (ix < Ox && iy < Oy && iz < Oz)
+                    ? scale * kappa(0, alpha, beta, oct_D(ix, alpha, beta, 0), oct_D(iy, alpha, beta, 1),
+                                    oct_D(iz, alpha, beta, 2))
+                    : 0.0;
+    }
+}
+
+// x <-> y mirror blocks (square x/y window, one rank): swapping the x and y axes maps the
+// (a, b) panel pair to (s(a), s(b)), s = (x y), and the kernel at offset (Dx, Dy, Dz) to the
+// kernel at (Dy, Dx, Dz) -- e.g. P^{yy}(Dx, Dy, Dz) = P^{xx}(Dy, Dx, Dz), E^{zy} likewise from
+// E^{zx} -- so the folded, phase-stripped spectrum of the mirror block is the kx <-> ky
+// transpose of the original's (the strip phases and the parity octants swap with the axes):
+//   R_dst(kx, ky, w) = R_src(ky, kx, w), w = kz' (z-FFT mode) or u (direct-z mode)
+__global__ void k_rt_mirror(double* R, int K, int NW, int src, int dst, int lgT3, int RC) {
+    const int T3 = 1 << lgT3, nt3 = (K + T3 - 1) >> lgT3;
+    const int64_t tot = (int64_t)K * K * NW;
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < tot;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int kx = (int)(idx % K);
+        const int w = (int)((idx / K) % NW);
+        const int ky = (int)(idx / ((int64_t)K * NW));
+        R[((int64_t)ky * nt3 + (kx >> lgT3)) * RC + ((int64_t)dst * NW + w) * T3 + (kx & (T3 - 1))] =
+            R[((int64_t)kx * nt3 + (ky >> lgT3)) * RC + ((int64_t)src * NW + w) * T3 + (ky & (T3 - 1))];
     }
 }
 
@@ -1433,21 +1453,59 @@ vc_status operator_build(vc_ctx* c, const vc_build_opts* o) {
             }
         VC_CUDA(c, c->pcTab.alloc((size_t)std::max(1, npair) * tvol));
         const double fpe = 4.0 * kPi * kEps0;
+        // x <-> y mirror pairs (k_rt_mirror): with a square x/y window on one rank, a block whose
+        // mirror was listed earlier is transposed from it instead of generated + transformed
+        const bool mirror_ok = M[0] == M[1] && c->world == 1 && !(o && o->no_mirror);
+        auto sig = [](int a) { return a == 0 ? 1 : (a == 1 ? 0 : 2); };
+        std::vector<int> mirror_of(c->nblk, -1);
+        if (mirror_ok)
+            for (int i = 0; i < c->nblk; ++i) {
+                int ma = sig(defs[i].alpha), mb = sig(defs[i].beta);
+                if (defs[i].kind == 0 && ma > mb) std::swap(ma, mb);  // P pairs stored with a <= b
+                if (ma == defs[i].alpha && mb == defs[i].beta) continue;
+                for (int j = 0; j < i; ++j)
+                    if (mirror_of[j] < 0 && defs[j].kind == defs[i].kind && defs[j].alpha == ma &&
+                        defs[j].beta == mb) {
+                        mirror_of[i] = j;
+                        break;
+                    }
+            }
+        const int NW = zd ? c->ZU : Mz / 2 + 1;
+        for (int pass = 0; pass < 2; ++pass)
         for (int i = 0; i < c->nblk; ++i) {
             const BlkDef& d = defs[i];
+            if ((mirror_of[i] >= 0) != (pass == 1)) continue;
             const double scale = (d.kind == 0 ? c->dv * c->dv * c->dv : c->dv * c->dv) / fpe /
                                  ((double)M[0] * M[1] * (zd ? 1 : M[2]));
             cudaEvent_t* ev = c->kev.data() + 4 * (size_t)i;
+            if (mirror_of[i] >= 0) {
+                VC_CUDA(c, cudaEventRecord(ev[0], st));
+                if (d.kind == 0) {
+                    k_kgen_corner<<<(tvol + 255) / 256, 256, 0, st>>>(
+                        c->pcTab.p + (size_t)c->pcPair[d.alpha][d.beta] * tvol, c->pcTabDim[0],
+                        c->pcTabDim[1], c->pcTabDim[2], Ox, Oy, Oz, d.alpha, d.beta,
+                        c->dv * c->dv * c->dv / fpe);
+                    count_launch(c);
+                }
+                VC_CUDA(c, cudaEventRecord(ev[1], st));
+                VC_CUDA(c, cudaEventRecord(ev[2], st));
+                const int64_t mt = (int64_t)Kx * Kx * NW;
+                k_rt_mirror<<<(int)std::min<int64_t>((mt + 255) / 256, 148 * 32), 256, 0, st>>>(
+                    c->Rt.p, Kx, NW, mirror_of[i], i, ilog2c(c->T3), (int)c->rchunk);
+                count_launch(c);
+                VC_CUDA(c, cudaEventRecord(ev[3], st));
+                continue;
+            }
             VC_CUDA(c, cudaEventRecord(ev[0], st));
-            const int oblocks = (int)std::min<int64_t>((otot + 127) / 128, 148 * 64);
-            k_kgen_oct<<<oblocks, 128, 0, st>>>(Ko.p, Ox, Oy, Oz, d.kind, d.alpha, d.beta, scale);
-            if (d.kind == 0) {  // undo the FFT normalisation (a power of two: exact)
-                const double resc = (double)M[0] * M[1] * (zd ? 1 : M[2]);
-                k_cut_octant<<<(tvol + 255) / 256, 256, 0, st>>>(
-                    Ko.p, Ox, Oy, Oz, c->pcTab.p + (size_t)c->pcPair[d.alpha][d.beta] * tvol,
-                    c->pcTabDim[0], c->pcTabDim[1], c->pcTabDim[2], resc);
+            if (d.kind == 0) {  // preconditioner near-field table, evaluated directly (both paths)
+                k_kgen_corner<<<(tvol + 255) / 256, 256, 0, st>>>(
+                    c->pcTab.p + (size_t)c->pcPair[d.alpha][d.beta] * tvol, c->pcTabDim[0],
+                    c->pcTabDim[1], c->pcTabDim[2], Ox, Oy, Oz, d.alpha, d.beta,
+                    c->dv * c->dv * c->dv / fpe);
                 count_launch(c);
             }
+            const int oblocks = (int)std::min<int64_t>((otot + 127) / 128, 148 * 64);
+            k_kgen_oct<<<oblocks, 128, 0, st>>>(Ko.p, Ox, Oy, Oz, d.kind, d.alpha, d.beta, scale);
             const int gblocks = (int)std::min<int64_t>((tot + 255) / 256, 148 * 64);
             if (zd)
                 k_kfill2d<<<gblocks, 256, 0, st>>>(G.p, Ko.p, M[0], M[1], MZ, Ox, Oy, d.kind, d.alpha, d.beta);

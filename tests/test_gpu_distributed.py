@@ -79,7 +79,8 @@ def test_distributed_matvec_bitwise(name, W, zmode):
     box = (4, 4, 4)
     n = _single(st, lambda c: c.n, box=box)
     x = voxgen.seeded_vector(n, 21)
-    y1 = _single(st, lambda c: c.matvec(x), box=box, zmode=zmode)
+    # (multi-rank builds generate every kernel block; mirror=False makes the 1-rank build do the same)
+    y1 = _single(st, lambda c: c.matvec(x), box=box, zmode=zmode, mirror=False)
     res = _group(W, st, lambda c, r: (c.local_panels(), c.matvec(x[c.local_panels()])), box=box,
                  zmode=zmode)
     idx = np.concatenate([g for g, _ in res])
@@ -138,7 +139,7 @@ def test_distributed_full_size_c4_rows():
     st = voxgen.config("C4")
     n = _single(st, lambda c: c.n)
     x = voxgen.seeded_vector(n, 0)
-    y1 = _single(st, lambda c: c.matvec(x))
+    y1 = _single(st, lambda c: c.matvec(x), mirror=False)
     res = _group(2, st, lambda c, r: (c.local_panels(), c.matvec(x[c.local_panels()])))
     yd = np.empty(n)
     for g, yl in res:

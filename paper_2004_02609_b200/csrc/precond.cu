@@ -1,3 +1,4 @@
+#include <cstdio>
 // precond.cu -- block-diagonal-diagonal preconditioner (Eq. 14; DESIGN.md a9/a10).
 //
 // R_BD: the bounding box is split into boxes of Nvx x Nvy x Nvz voxels; every box's
@@ -79,10 +80,12 @@ __global__ void k_pc_fill(const int32_t* __restrict__ un, const int64_t* __restr
 // divisions in the n^2 update of every pivot step.
 __global__ void __launch_bounds__(512) k_pc_invert(const int32_t* __restrict__ un,
                                                    const int64_t* __restrict__ uoff,
-                                                   double* __restrict__ blocks, int smem_elems) {
+                                                   double* __restrict__ blocks, int smem_elems,
+                                                   int sweep_elems) {
     extern __shared__ double sh[];
     const int u = blockIdx.x;
     const int n = un[u];
+    if ((int64_t)n * (n + 1) / 2 + n <= sweep_elems) return;  // done by k_pc_sweep
     double* G = blocks + uoff[u];
     double* rowk = sh;
     double* colk = sh + n;
@@ -113,6 +116,57 @@ __global__ void __launch_bounds__(512) k_pc_invert(const int32_t* __restrict__ u
     if (in_smem) {
         __syncthreads();
         for (int64_t e = threadIdx.x; e < (int64_t)n * n; e += blockDim.x) G[e] = A[e];
+    }
+}
+
+// Symmetric inverse by the sweep operator (Goodnight's SWEEP), one CTA per unique block whose
+// packed lower triangle fits in shared memory.  Sweeping pivot k with d = a_kk:
+//   a_kk <- -1/d,  a_ik = a_ki <- a_ik / d,  a_ij <- a_ij - a_ik a_kj / d   (i, j != k)
+// keeps the matrix symmetric at every step (so half the storage and half the updates of the
+// Gauss-Jordan kernel above), and sweeping every pivot of an SPD block (no pivoting needed)
+// leaves -A^{-1}.  Packed index of (i >= j): i (i + 1) / 2 + j.  Warps take rows, lanes columns.
+__global__ void __launch_bounds__(512) k_pc_sweep(const int32_t* __restrict__ un,
+                                                  const int64_t* __restrict__ uoff,
+                                                  double* __restrict__ blocks, int smem_elems) {
+    extern __shared__ double sh[];
+    const int n = un[blockIdx.x];
+    const int64_t np = (int64_t)n * (n + 1) / 2;
+    if (np + n > smem_elems) return;  // left to k_pc_invert (global-memory path)
+    double* G = blocks + uoff[blockIdx.x];
+    double* P = sh;
+    double* ck = sh + np;
+    const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int i = wp; i < n; i += nw) {
+        const int base = i * (i + 1) / 2;
+        for (int j = lane; j <= i; j += 32) P[base + j] = G[(int64_t)i * n + j];
+    }
+    for (int k = 0; k < n; ++k) {
+        __syncthreads();
+        const int bk = k * (k + 1) / 2;
+        for (int i = threadIdx.x; i < n; i += blockDim.x)
+            ck[i] = i >= k ? P[i * (i + 1) / 2 + k] : P[bk + i];
+        __syncthreads();
+        const double id = 1.0 / ck[k];
+        for (int i = wp; i < n; i += nw) {
+            const int base = i * (i + 1) / 2;
+            const double ci = ck[i], cid = ci * id;
+            if (i == k) {
+                for (int j = lane; j < k; j += 32) P[base + j] = ck[j] * id;
+                if (lane == 0) P[base + k] = -id;
+            } else {
+                for (int j = lane; j <= i; j += 32)
+                    P[base + j] = j == k ? cid : fma(-cid, ck[j], P[base + j]);
+            }
+        }
+    }
+    __syncthreads();
+    for (int i = wp; i < n; i += nw) {
+        const int base = i * (i + 1) / 2;
+        for (int j = lane; j <= i; j += 32) {
+            const double v = -P[base + j];
+            G[(int64_t)i * n + j] = v;
+            G[(int64_t)j * n + i] = v;
+        }
     }
 }
 
@@ -299,6 +353,16 @@ vc_status precond_build(vc_ctx* c, const int32_t box_in[3], int kind) {
         buid[b] = id;
     }
     tr.mark("signatures");
+    if (tr.on) {
+        double f3 = 0;
+        int big = 0;
+        for (int n : un) {
+            f3 += (double)n * n * n;
+            big += (size_t)n * n + 2 * n > 26 * 1024;
+        }
+        fprintf(stderr, "[vc precond] boxes %d unique %zu max_n %d sum n^3 %.3g (%d not in smem)\n",
+                nbox, un.size(), maxn, f3, big);
+    }
     if ((size_t)maxn * (kPcRows + 1) * sizeof(double) > 220 * 1024)
         return set_err(c, VC_ERR_UNSUPPORTED, "preconditioner block too large (" + std::to_string(maxn) + " panels in one box); use smaller boxes");
     pc->nbox = nbox;
@@ -364,15 +428,20 @@ vc_status precond_build(vc_ctx* c, const int32_t box_in[3], int kind) {
         }
         k_pc_fill<<<g, 256, 0, st>>>(pc->uniq_n.p, pc->uniq_off.p, pc->uniq_list_off.p,
                                      pc->uniq_axis.p, pc->uniq_slot.p, pc->blocks.p, tab);
-        // shared memory for the largest block if it fits, else only the pivot row / column
-        const size_t full = sizeof(double) * ((size_t)maxn * maxn + 2 * maxn);
+        // sweep (packed, shared memory) for every block it fits; Gauss-Jordan in global memory
+        // (L2-resident) for the rest
         const size_t cap = (size_t)max_dyn_smem() - 1024;
-        const size_t sh = full <= cap ? full : std::max(2 * sizeof(double) * maxn,
-                                                         std::min(cap, (size_t)160 * 1024));
-        if (sh > 48 * 1024)
-            VC_CUDA(c, grant_max_dyn_smem(k_pc_invert, max_dyn_smem()));
-        k_pc_invert<<<pc->nuniq, 512, sh, st>>>(pc->uniq_n.p, pc->uniq_off.p, pc->blocks.p,
-                                                (int)(sh / sizeof(double)));
+        const size_t sw = std::min(cap, sizeof(double) * ((size_t)maxn * (maxn + 1) / 2 + maxn));
+        if (sw > 48 * 1024) VC_CUDA(c, grant_max_dyn_smem(k_pc_sweep, max_dyn_smem()));
+        k_pc_sweep<<<pc->nuniq, 512, sw, st>>>(pc->uniq_n.p, pc->uniq_off.p, pc->blocks.p,
+                                               (int)(sw / sizeof(double)));
+        if ((size_t)maxn * (maxn + 1) / 2 + maxn > sw / sizeof(double)) {
+            const size_t sh = 2 * sizeof(double) * maxn;
+            k_pc_invert<<<pc->nuniq, 512, sh, st>>>(pc->uniq_n.p, pc->uniq_off.p, pc->blocks.p,
+                                                    (int)(sh / sizeof(double)),
+                                                    (int)(sw / sizeof(double)));
+            count_launch(c);
+        }
         count_launch(c, 2);
     }
     if (tr.on) {

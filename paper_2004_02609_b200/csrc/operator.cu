@@ -1383,17 +1383,32 @@ vc_status operator_build(vc_ctx* c, const vc_build_opts* o) {
         c->src_contig = 0;
         auto plane = [&](int g, int j) { return c->h_planes[(size_t)g * c->ZL + j]; };
         if (c->zdirect) {
-            // groups of one field fill whole warps (32 / kDirectT groups per warp) so the lanes of
-            // a warp follow one code path; a field's last warp is padded with null groups
+            // the groups of a warp (32 / kDirectT of them) must follow one code path: same plane
+            // count, same contiguity, same z parity (E^{z.}) and the same sources present.  Groups
+            // are binned by that signature (across fields: C^x and C^y share warps) and a bin's
+            // last warp is padded with null groups.
             const int gpw = 32 / kDirectT;
-            for (int f = 0; f < c->nf; ++f) {
-                int ng = 0;
-                for (int j = 0; j < c->nzout[f]; j += kZB, ++ng) {
+            struct Og { int f, j, key; bool contig; };
+            std::vector<Og> ogs;
+            for (int f = 0; f < c->nf; ++f)
+                for (int j = 0; j < c->nzout[f]; j += kZB) {
                     const int nzo = std::min(kZB, c->nzout[f] - j);
-                    if (plane(3 + f, j + nzo - 1) - plane(3 + f, j) == nzo - 1)
-                        c->og_contig |= 1ull << c->nog;
-                    c->og_f[c->nog] = f;
-                    c->og_j[c->nog] = j;
+                    const bool contig = plane(3 + f, j + nzo - 1) - plane(3 + f, j) == nzo - 1;
+                    int mask = 0;
+                    for (int b = 0; b < 3; ++b) mask |= (c->blk[f][b] >= 0) << b;
+                    const int odd = c->f[f].kind == 1 && c->f[f].axis == 2;
+                    static const bool pair = getenv("VC_OGPAIR") == nullptr || atoi(getenv("VC_OGPAIR"));
+                    ogs.push_back({f, j, pair ? ((nzo * 2 + (contig ? 1 : 0)) * 2 + odd) * 8 + mask : f, contig});
+                }
+            std::stable_sort(ogs.begin(), ogs.end(), [](const Og& x, const Og& y) { return x.key < y.key; });
+            for (size_t i = 0; i < ogs.size();) {
+                size_t e = i;
+                while (e < ogs.size() && ogs[e].key == ogs[i].key) ++e;
+                int ng = 0;
+                for (; i < e; ++i, ++ng) {
+                    if (ogs[i].contig) c->og_contig |= 1ull << c->nog;
+                    c->og_f[c->nog] = ogs[i].f;
+                    c->og_j[c->nog] = ogs[i].j;
                     ++c->nog;
                 }
                 for (; ng % gpw; ++ng) {

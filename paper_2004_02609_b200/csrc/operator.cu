@@ -110,7 +110,8 @@ __device__ __forceinline__ int ktil(int k, int M) { return k <= M / 2 ? k : k - 
 // ---------------------------------------------------------------------------------------
 // P1: scatter + forward R2C along x
 // ---------------------------------------------------------------------------------------
-template <int L>
+// D: multi-rank (slab-partitioned) build; D = false compiles out the owner lookups
+template <int L, bool D>
 __global__ void __launch_bounds__(FX<L>::NT, FX<L>::MINB) k_p1(MV mv) {
     constexpr int T = TX<L>::T;
     extern __shared__ double2 sm[];
@@ -153,6 +154,7 @@ __global__ void __launch_bounds__(FX<L>::NT, FX<L>::MINB) k_p1(MV mv) {
     __syncthreads();
     constexpr int K = L / 2 + 1;
     const bool ph = beta != 0;  // c_beta,x = 1/2 for y- and z-normal panels
+    double2* const S1self = mv.S1[0][beta];
     for (int u = threadIdx.x; u < T * K; u += FX<L>::NT) {
         const int t = u / K, k = u % K;
         const int q = ch * T + t;
@@ -166,10 +168,11 @@ __global__ void __launch_bounds__(FX<L>::NT, FX<L>::MINB) k_p1(MV mv) {
             A = cmul(A, w);
             B = cmul(B, w);
         }
-        const int qd = kx_owner(mv, k);
-        const int nk = mv.kxa[qd + 1] - mv.kxa[qd];
+        const int qd = D ? kx_owner(mv, k) : 0;
+        const int k0 = D ? mv.kxa[qd] : 0;
+        const int nk = D ? mv.kxa[qd + 1] - k0 : mv.nkx;
         const int l0 = 2 * q - s;
-        double2* o = mv.S1[qd][beta] + ((int64_t)j * nrow + l0) * nk + (k - mv.kxa[qd]);
+        double2* o = (D ? mv.S1[qd][beta] : S1self) + ((int64_t)j * nrow + l0) * nk + (k - k0);
         if (l0 >= 0) o[0] = A;
         if (l0 + 1 < nrow) o[nk] = B;
     }
@@ -178,7 +181,7 @@ __global__ void __launch_bounds__(FX<L>::NT, FX<L>::MINB) k_p1(MV mv) {
 // ---------------------------------------------------------------------------------------
 // P2: forward C2C along y (zero-padded input), times conj(phi_beta,y)
 // ---------------------------------------------------------------------------------------
-template <int L>
+template <int L, bool D>
 __global__ void __launch_bounds__(FY<L>::NT) k_p2(MV mv) {
     constexpr int T = TY<L>::T;
     extern __shared__ double2 sm[];
@@ -195,9 +198,11 @@ __global__ void __launch_bounds__(FY<L>::NT) k_p2(MV mv) {
     double2* __restrict__ out = mv.X2[beta];
     const int nzb = mv.nzin[beta], nt3 = (nkx + mv.T3 - 1) >> mv.lgT3;
     const bool ph = beta != 1;  // c_beta,y = 1/2 for x- and z-normal panels
+    const double2* const in0 = mv.R1[0][beta] + (int64_t)j * mv.nr[0][beta] * nkx;  // (!D)
     auto ld0 = [&](int t, int n) -> double2 {
         const int kx = tile * T + t;
         if (n >= ey || kx >= nkx) return czero();
+        if (!D) return in0[(int64_t)n * nkx + kx];
         const int p = row_owner(mv, n);  // row n arrived from rank p
         return mv.R1[p][beta][((int64_t)j * mv.nr[p][beta] + (n - mv.ya[p])) * nkx + kx];
     };
@@ -227,7 +232,7 @@ template <int L, int KB = 32> struct FYS {  // KB: shared memory per stage
     static constexpr int NT = clampi(T * L / 16, 64, 256);
 };
 
-template <int L, int KB>
+template <int L, int KB, bool D>
 __global__ void __launch_bounds__(FYS<L, KB>::NT) k_p4s(MV mv) {
     constexpr int T = FYS<L, KB>::T, NT = FYS<L, KB>::NT;
     extern __shared__ __align__(16) double2 sm[];  // [2][L][T]
@@ -278,8 +283,9 @@ __global__ void __launch_bounds__(FYS<L, KB>::NT) k_p4s(MV mv) {
             const int kx = xt * T + t;
             const int yy = Plan<L>::freq(p);
             if (kx < nkx && yy < eyo) {
-                const int pr = row_owner(mv, yy);  // row yy goes to rank pr for P5
-                mv.S2[pr][f][((int64_t)j * mv.nr[pr][3 + f] + (yy - mv.ya[pr])) * nkx + kx] = v;
+                const int pr = D ? row_owner(mv, yy) : 0;  // row yy goes to rank pr for P5
+                const int y0 = D ? mv.ya[pr] : 0;
+                mv.S2[pr][f][((int64_t)j * mv.nr[pr][3 + f] + (yy - y0)) * nkx + kx] = v;
             }
         };
         fft_run<L, T, NT, true, true, 0, true>(buf, lds, stN, mv.tw);
@@ -465,7 +471,7 @@ __global__ void __launch_bounds__(kNT3) k_p3(MV mv) {
 // ---------------------------------------------------------------------------------------
 // P5: times phi_f,x, C2R along x (two lines per complex FFT), gather + dielectric terms
 // ---------------------------------------------------------------------------------------
-template <int L>
+template <int L, bool D>
 __global__ void __launch_bounds__(FX<L>::NT, FX<L>::MINB) k_p5(MV mv) {
     constexpr int T = TX<L>::T;
     extern __shared__ double2 sm[];
@@ -484,7 +490,7 @@ __global__ void __launch_bounds__(FX<L>::NT, FX<L>::MINB) k_p5(MV mv) {
     const bool ph = alpha != 0;
     auto At = [&](int yrow, int k, bool v) -> double2 {
         int qd = 0, nk = mv.nkx, k0 = 0;
-        if (mv.W > 1) {
+        if (D) {
             qd = kx_owner(mv, k);  // column k arrived from rank qd
             k0 = mv.kxa[qd];
             nk = mv.kxa[qd + 1] - k0;
@@ -816,10 +822,11 @@ static cudaError_t launch_p1(const MV& mv, cudaStream_t st) {
         constexpr int T = TX<LL>::T;
         for (int b = 0; b < 3; ++b) maxch = std::max(maxch, ((mv.nr[mv.rank][b] + 2) / 2 + T - 1) / T);
         const size_t smem = sizeof(double2) * LL * T;
-        cudaError_t e = prep(k_p1<LL>, smem);
+        auto kern = mv.W > 1 ? k_p1<LL, true> : k_p1<LL, false>;
+        cudaError_t e = prep(kern, smem);
         if (e) return e;
         dim3 grid(std::max(1, maxch * maxz), 3);
-        k_p1<LL><<<grid, FX<LL>::NT, smem, st>>>(mv);
+        kern<<<grid, FX<LL>::NT, smem, st>>>(mv);
     });
     return cudaGetLastError();
 }
@@ -837,11 +844,12 @@ static cudaError_t launch_p4s_t(const MV& mv, cudaStream_t st) {
     int G = 0;
     for (int f = 0; f < mv.nf; ++f) G += mv.nzout[f];
     const size_t smem = sizeof(double2) * 2 * LL * T;
-    cudaError_t e = prep(k_p4s<LL, KB>, smem);
+    auto kern = mv.W > 1 ? k_p4s<LL, KB, true> : k_p4s<LL, KB, false>;
+    cudaError_t e = prep(kern, smem);
     if (e) return e;
     const int ntiles = G * ((mv.nkx + T - 1) / T);
     if (ntiles == 0) return cudaSuccess;
-    k_p4s<LL, KB><<<persistent_grid(k_p4s<LL, KB>, NT, smem, ntiles), NT, smem, st>>>(mv);
+    kern<<<persistent_grid(kern, NT, smem, ntiles), NT, smem, st>>>(mv);
     return cudaSuccess;
 }
 static cudaError_t launch_p4s(const MV& mv, cudaStream_t st) {
@@ -855,10 +863,11 @@ static cudaError_t launch_p2(const MV& mv, cudaStream_t st) {
     VC_DISPATCH_L(mv.My, {
         constexpr int T = TY<LL>::T;
         const size_t smem = sizeof(double2) * LL * T;
-        cudaError_t e = prep(k_p2<LL>, smem);
+        auto kern = mv.W > 1 ? k_p2<LL, true> : k_p2<LL, false>;
+        cudaError_t e = prep(kern, smem);
         if (e) return e;
         dim3 grid(std::max(1, ((mv.nkx + T - 1) / T) * maxz), 3);
-        k_p2<LL><<<grid, FY<LL>::NT, smem, st>>>(mv);
+        kern<<<grid, FY<LL>::NT, smem, st>>>(mv);
     });
     return cudaGetLastError();
 }
@@ -1144,10 +1153,11 @@ static cudaError_t launch_p5(const MV& mv, cudaStream_t st) {
         constexpr int T = TX<LL>::T;
         for (int f = 0; f < mv.nf; ++f) maxch = std::max(maxch, ((mv.nr[mv.rank][3 + f] + 2) / 2 + T - 1) / T);
         const size_t smem = sizeof(double2) * LL * T;
-        cudaError_t e = prep(k_p5<LL>, smem);
+        auto kern = mv.W > 1 ? k_p5<LL, true> : k_p5<LL, false>;
+        cudaError_t e = prep(kern, smem);
         if (e) return e;
         dim3 grid(std::max(1, maxch * maxz), mv.nf);
-        k_p5<LL><<<grid, FX<LL>::NT, smem, st>>>(mv);
+        kern<<<grid, FX<LL>::NT, smem, st>>>(mv);
     });
     return cudaGetLastError();
 }

@@ -179,8 +179,8 @@ __global__ void k_pc_diag(int64_t N, const double* __restrict__ r, const double*
 }
 
 // z_b = R_u r_b grouped by unique block: a CTA holds kPcRows rows of R_u in shared memory and
-// applies them to up to kPcBoxes boxes b that use R_u, whose r_b are gathered up front (each R
-// element read once per apply; 8 lanes per row, shuffle-reduced)
+// applies them to every box b that uses R_u (each R element read once per apply; 8 lanes per
+// row, shuffle-reduced)
 constexpr int kPcRows = 32;
 constexpr int kPcBoxes = 8;  // boxes per CTA (a block shared by many boxes is split over CTAs)
 __global__ void __launch_bounds__(256) k_pc_apply_grouped(
@@ -194,28 +194,25 @@ __global__ void __launch_bounds__(256) k_pc_apply_grouped(
     const int u = tile_u[blockIdx.x], r0 = tile_r0[blockIdx.x];
     const int n = un[u];
     const int rows = min(kPcRows, n - r0);
-    double* Rt = sh;                 // [rows][n]
-    double* rb = sh + kPcRows * n;   // [boxes][n]
+    double* Rt = sh;              // [rows][n]
+    double* rb = sh + kPcRows * n;  // [n]
     const double* R = blocks + uoff[u] + (int64_t)r0 * n;
-    const int qa = ubs[u] + tile_q0[blockIdx.x];
-    const int nq = min(ubs[u + 1], qa + kPcBoxes) - qa;
-    // every gather of the CTA's boxes in flight at once (one latency, not one per box)
-    for (int e = threadIdx.x; e < nq * n; e += blockDim.x) {
-        const int qi = e / n;
-        rb[e] = r[pids[bstart[ubl[qa + qi]] + (e - qi * n)]];
-    }
     for (int e = threadIdx.x; e < rows * n; e += blockDim.x) Rt[e] = R[e];
-    __syncthreads();
     const int row = threadIdx.x >> 3, part = threadIdx.x & 7;
-    for (int qi = 0; qi < nq; ++qi) {
-        const double* rq = rb + qi * n;
+    const int q1 = min(ubs[u + 1], ubs[u] + tile_q0[blockIdx.x] + kPcBoxes);
+    for (int q = ubs[u] + tile_q0[blockIdx.x]; q < q1; ++q) {
+        const int b = ubl[q];
+        const int s0 = bstart[b];
+        __syncthreads();
+        for (int j = threadIdx.x; j < n; j += blockDim.x) rb[j] = r[pids[s0 + j]];
+        __syncthreads();
         double acc = 0.0;
         if (row < rows)
-            for (int j = part; j < n; j += 8) acc = fma(Rt[row * n + j], rq[j], acc);
+            for (int j = part; j < n; j += 8) acc = fma(Rt[row * n + j], rb[j], acc);
         acc += __shfl_xor_sync(0xffffffffu, acc, 1);
         acc += __shfl_xor_sync(0xffffffffu, acc, 2);
         acc += __shfl_xor_sync(0xffffffffu, acc, 4);
-        if (part == 0 && row < rows) z[pids[bstart[ubl[qa + qi]] + r0 + row]] = acc;
+        if (part == 0 && row < rows) z[pids[s0 + r0 + row]] = acc;
     }
 }
 
@@ -366,7 +363,7 @@ vc_status precond_build(vc_ctx* c, const int32_t box_in[3], int kind) {
         fprintf(stderr, "[vc precond] boxes %d unique %zu max_n %d sum n^3 %.3g (%d not in smem)\n",
                 nbox, un.size(), maxn, f3, big);
     }
-    if ((size_t)maxn * (kPcRows + kPcBoxes) * sizeof(double) > 220 * 1024)
+    if ((size_t)maxn * (kPcRows + 1) * sizeof(double) > 220 * 1024)
         return set_err(c, VC_ERR_UNSUPPORTED, "preconditioner block too large (" + std::to_string(maxn) + " panels in one box); use smaller boxes");
     pc->nbox = nbox;
     pc->nuniq = (int)un.size();
@@ -464,7 +461,7 @@ vc_status precond_apply_dev(vc_ctx* c, const double* d_r, double* d_z) {
     k_pc_diag<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((N + 255) / 256, 148 * 8)), 256, 0, st>>>(N, d_r, pc->diag_inv.p, d_z);
     count_launch(c);
     if (pc->kind == 3 && pc->ntile > 0) {
-        const size_t sh = sizeof(double) * (size_t)(kPcRows + kPcBoxes) * pc->max_n;
+        const size_t sh = sizeof(double) * (size_t)(kPcRows + 1) * pc->max_n;
         if (sh > 48 * 1024)
             VC_CUDA(c, grant_max_dyn_smem(k_pc_apply_grouped, max_dyn_smem()));
         k_pc_apply_grouped<<<pc->ntile, 256, sh, st>>>(

@@ -115,6 +115,52 @@ __device__ __forceinline__ void reg_dft(double2 (&v)[R]) {
     }
 }
 
+// Shared-memory index of (pencil t, position p): PF -> [pos][pencil], else [pencil][pos].
+// The low 3 bits of the index (8 complex = one 128-byte bank row) are XOR-swizzled with bits
+// 3-5, 6-8 and 9-11, so that the access patterns of a quarter-warp -- 8 consecutive aligned
+// elements (stages with S >= 8), and the strided patterns of the last radix-8 stage (S = 1) and
+// of digit-reversed frequency reads -- hit 8 distinct bank groups (unswizzled, these were 2- to
+// 8-way conflicts: 27M extra wavefronts in k_p1<1024> on C4).  PF = false always swizzles; PF
+// layouts swizzle only with SWZ (P3's buffers are filled by bulk copies in the plain layout).
+__host__ __device__ constexpr int swz8(int i) { return i ^ (((i >> 3) ^ (i >> 6) ^ (i >> 9)) & 7); }
+template <int L, int T, bool PF, bool SWZ = false>
+__device__ __forceinline__ int smi(int t, int p) {
+    if constexpr (PF) return SWZ ? swz8(p * T + t) : p * T + t;
+    else return t * L + swz8(p);
+}
+
+// Shared-memory accessor in the smi layout.  fft_stage recognises it and addresses the R legs of
+// a butterfly as smi(t, base) ^ c_j with c_j a compile-time constant: the leg offsets j*S occupy
+// bits disjoint from base (base = g*Lc + b, b < S, j*S < Lc) and from t, and both the layout and
+// swz8 are XOR-linear over disjoint bit fields, so one XOR per element replaces the full index
+// and swizzle arithmetic.
+template <int L, int T, bool PF, bool SWZ>
+struct SmAcc {
+    double2* sm;
+    __device__ __forceinline__ static int idx(int t, int p) { return smi<L, T, PF, SWZ>(t, p); }
+    __device__ __forceinline__ double2 operator()(int t, int p) const { return sm[smi<L, T, PF, SWZ>(t, p)]; }
+    __device__ __forceinline__ void operator()(int t, int p, double2 v) const { sm[smi<L, T, PF, SWZ>(t, p)] = v; }
+    // index offset of a position displacement d with disjoint bits (see above)
+    __host__ __device__ static constexpr int off(int d) {
+        return PF ? (SWZ ? swz8(d * T) : d * T) : swz8(d);
+    }
+    // index of (t, p + d) from idx(t, p): XOR for the swizzled layouts (T a power of two there),
+    // plain addition for the unswizzled [pos][pencil] layout (T may be any width, e.g. P3's)
+    __device__ __forceinline__ static int at(int i0, int d) {
+        static_assert(!(PF && SWZ) || (T & (T - 1)) == 0, "swizzled layouts need a power-of-two width");
+        if constexpr (PF && !SWZ) return i0 + d * T;
+        else return i0 ^ off(d);
+    }
+};
+template <class X> struct IsSmAcc { static constexpr bool value = false; };
+template <int L, int T, bool PF, bool SWZ> struct IsSmAcc<SmAcc<L, T, PF, SWZ>> {
+    static constexpr bool value = true;
+};
+template <class X> struct Bare { using type = X; };
+template <class X> struct Bare<X&> { using type = X; };
+template <class X> struct Bare<const X&> { using type = X; };
+template <class X> struct Bare<const X> { using type = X; };
+
 // One DIF stage s of the length-L transform over T pencils with NT threads.
 //   ld(t, p) -> double2 : element at storage position p of pencil t (stage input)
 //   st(t, p, v)         : write element at position p of pencil t (stage output)
@@ -145,9 +191,17 @@ __device__ __forceinline__ void fft_stage(LD&& ld, ST&& st, const double2* __res
         const int b = rest % S;
         const int g = rest / S;
         const int base = g * Lc + b;
+        using LDT = typename Bare<LD>::type;
+        using STT = typename Bare<ST>::type;
         double2 v[R];
+        if constexpr (IsSmAcc<LDT>::value) {
+            const int i0 = LDT::idx(t, base);
 #pragma unroll
-        for (int j = 0; j < R; ++j) v[j] = ld(t, base + j * S);
+            for (int j = 0; j < R; ++j) v[j] = ld.sm[LDT::at(i0, j * S)];
+        } else {
+#pragma unroll
+            for (int j = 0; j < R; ++j) v[j] = ld(t, base + j * S);
+        }
         reg_dft<R, INV>(v);
         if (S > 1) {
             // inter-stage twiddles w_Lc^{b m}: one table load, powers by squaring/products
@@ -160,30 +214,29 @@ __device__ __forceinline__ void fft_stage(LD&& ld, ST&& st, const double2* __res
                 const int hb = hipow2(m);  // highest power of two <= m
                 wp[m] = (m == hb) ? cmul(wp[m / 2], wp[m / 2]) : cmul(wp[hb], wp[m - hb]);
             }
+            if constexpr (IsSmAcc<STT>::value) {
+                const int i0 = STT::idx(t, base);
 #pragma unroll
-            for (int i = 0; i < R; ++i) {
-                const int m = bitrev<R>(i);
-                st(t, base + m * S, m == 0 ? v[i] : cmul(v[i], wp[m]));
+                for (int i = 0; i < R; ++i) {
+                    const int m = bitrev<R>(i);
+                    st.sm[STT::at(i0, m * S)] = m == 0 ? v[i] : cmul(v[i], wp[m]);
+                }
+            } else {
+#pragma unroll
+                for (int i = 0; i < R; ++i) {
+                    const int m = bitrev<R>(i);
+                    st(t, base + m * S, m == 0 ? v[i] : cmul(v[i], wp[m]));
+                }
             }
+        } else if constexpr (IsSmAcc<STT>::value) {
+            const int i0 = STT::idx(t, base);
+#pragma unroll
+            for (int i = 0; i < R; ++i) st.sm[STT::at(i0, bitrev<R>(i) * S)] = v[i];
         } else {
 #pragma unroll
             for (int i = 0; i < R; ++i) st(t, base + bitrev<R>(i) * S, v[i]);
         }
     }
-}
-
-// Shared-memory index of (pencil t, position p): PF -> [pos][pencil], else [pencil][pos].
-// The low 3 bits of the index (8 complex = one 128-byte bank row) are XOR-swizzled with bits
-// 3-5, 6-8 and 9-11, so that the access patterns of a quarter-warp -- 8 consecutive aligned
-// elements (stages with S >= 8), and the strided patterns of the last radix-8 stage (S = 1) and
-// of digit-reversed frequency reads -- hit 8 distinct bank groups (unswizzled, these were 2- to
-// 8-way conflicts: 27M extra wavefronts in k_p1<1024> on C4).  PF = false always swizzles; PF
-// layouts swizzle only with SWZ (P3's buffers are filled by bulk copies in the plain layout).
-__device__ __forceinline__ int swz8(int i) { return i ^ (((i >> 3) ^ (i >> 6) ^ (i >> 9)) & 7); }
-template <int L, int T, bool PF, bool SWZ = false>
-__device__ __forceinline__ int smi(int t, int p) {
-    if constexpr (PF) return SWZ ? swz8(p * T + t) : p * T + t;
-    else return t * L + swz8(p);
 }
 
 // Full transform: stage 0 reads through `ld0`, the last stage writes through `stN`, and the
@@ -193,8 +246,7 @@ template <int L, int T, int NT, bool INV, bool PF, int TB = 0, bool SWZ = false,
 __device__ __forceinline__ void fft_run(double2* sm, LD&& ld0, ST&& stN,
                                         const double2* __restrict__ tw, const int Tn = T) {
     constexpr int NS = Plan<L>::NS;
-    auto lds = [&](int t, int p) { return sm[smi<L, T, PF, SWZ>(t, p)]; };
-    auto sts = [&](int t, int p, double2 v) { sm[smi<L, T, PF, SWZ>(t, p)] = v; };
+    const SmAcc<L, T, PF, SWZ> lds{sm}, sts{sm};
     if constexpr (NS == 1) {
         fft_stage<L, T, NT, INV, PF, 0, TB>(ld0, stN, tw, Tn);
     } else if constexpr (NS == 2) {

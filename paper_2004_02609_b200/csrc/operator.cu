@@ -90,7 +90,7 @@ constexpr int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi 
 template <int L> struct FX {
     static constexpr int T = clampi(2048 / L, 1, 64);
     static constexpr int NT = clampi(T * L / 16, 64, 256);
-    static constexpr int MINB = 65536 / (NT * 80) < 1 ? 1 : 65536 / (NT * 80);  // <= 80 regs
+    static constexpr int MINB = 65536 / (NT * 96) < 1 ? 1 : 65536 / (NT * 96);  // <= 102 regs (128 thr)
 };
 template <int L> struct FY {
     static constexpr int T = clampi(4096 / L, 2, 32);  // >= 2 adjacent kx: 32-byte row segments

@@ -90,7 +90,9 @@ constexpr int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi 
 template <int L> struct FX {
     static constexpr int T = clampi(2048 / L, 1, 64);
     static constexpr int NT = clampi(T * L / 16, 64, 256);
-    static constexpr int MINB = 65536 / (NT * 96) < 1 ? 1 : 65536 / (NT * 96);  // <= 102 regs (128 thr)
+    // register caps (measured on C4): P1 best at <= 96 (5 CTAs/SM), P5 at <= 128 (no spills)
+    static constexpr int MINB = 65536 / (NT * 96) < 1 ? 1 : 65536 / (NT * 96);
+    static constexpr int MINB5 = 65536 / (NT * 128) < 1 ? 1 : 65536 / (NT * 128);
 };
 template <int L> struct FY {
     static constexpr int T = clampi(4096 / L, 2, 32);  // >= 2 adjacent kx: 32-byte row segments
@@ -472,7 +474,7 @@ __global__ void __launch_bounds__(kNT3) k_p3(MV mv) {
 // P5: times phi_f,x, C2R along x (two lines per complex FFT), gather + dielectric terms
 // ---------------------------------------------------------------------------------------
 template <int L, bool D>
-__global__ void __launch_bounds__(FX<L>::NT, FX<L>::MINB) k_p5(MV mv) {
+__global__ void __launch_bounds__(FX<L>::NT, FX<L>::MINB5) k_p5(MV mv) {
     constexpr int T = TX<L>::T;
     extern __shared__ double2 sm[];
     const int f = blockIdx.y;

@@ -194,6 +194,10 @@ __global__ void k_emit(Geo g, int64_t Ftot, const int64_t* __restrict__ tile_off
     const int64_t base = (int64_t)blockIdx.x * kTile;
     constexpr int PER = kTile / kNT;  // faces per thread, contiguous
     __shared__ int64_t warp_tot[kNT / 32];
+    // panel extents: reduced in shared memory, then one global atomic per value and block (a
+    // global atomic per panel serialised ~4.6M updates on 36 addresses: 3.2 ms on C4)
+    __shared__ int sext[36];
+    if (threadIdx.x < 36) sext[threadIdx.x] = (threadIdx.x % 6) < 3 ? INT32_MAX : INT32_MIN;
     int flag[PER];
     FaceInfo fi[PER];
     int a0 = 0, ii[PER], jj[PER], kk[PER], aa[PER];
@@ -243,7 +247,7 @@ __global__ void k_emit(Geo g, int64_t Ftot, const int64_t* __restrict__ tile_off
             o.ibar[p] = diel ? o.area_over_2eps0 * (fi[q].ed + fi[q].eb) / (fi[q].ed - fi[q].eb) : 0.0;
             o.fc[p] = diel ? 0.0 : fi[q].eb;
             o.slotmap[a][r] = (int32_t)p | (diel ? kSlotDiel : 0) | (diel && fi[q].sign < 0 ? kSlotNeg : 0);
-            int* e = o.ext + ((diel ? 1 : 0) * 3 + a) * 6;
+            int* e = sext + ((diel ? 1 : 0) * 3 + a) * 6;
             atomicMin(e + 0, ii[q]);
             atomicMin(e + 1, jj[q]);
             atomicMin(e + 2, kk[q]);
@@ -253,6 +257,15 @@ __global__ void k_emit(Geo g, int64_t Ftot, const int64_t* __restrict__ tile_off
             ++p;
         } else {
             o.slotmap[a][r] = -1;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < 36) {
+        const int v = sext[threadIdx.x];
+        if ((threadIdx.x % 6) < 3) {
+            if (v != INT32_MAX) atomicMin(o.ext + threadIdx.x, v);
+        } else if (v != INT32_MIN) {
+            atomicMax(o.ext + threadIdx.x, v);
         }
     }
 }

@@ -43,14 +43,28 @@ def build(force=False, verbose=False):
     if not force and os.path.exists(OUT) and os.path.exists(stamp) and open(stamp).read() == dig:
         return OUT
 
+    # per-object digest: a .cu is recompiled when it, any header or the flags changed
+    hdr = hashlib.sha256()
+    for f in sorted(os.listdir(CSRC)) + ["../../include/voxcap.h"]:
+        if not f.endswith(".cu") and os.path.isfile(os.path.join(CSRC, f)):
+            hdr.update(f.encode())
+            hdr.update(open(os.path.join(CSRC, f), "rb").read())
+    hdr.update(" ".join(FLAGS).encode())
+
     def comp(src):
         obj = os.path.join(BUILD, src[:-3] + ".o")
+        od = hashlib.sha256(hdr.digest() + open(os.path.join(CSRC, src), "rb").read()).hexdigest()
+        ostamp = obj + ".digest"
+        if not force and os.path.exists(obj) and os.path.exists(ostamp) and open(ostamp).read() == od:
+            return obj
         cmd = [NVCC, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr[-6000:]}")
         with open(os.path.join(BUILD, src[:-3] + ".ptxas.log"), "w") as fh:
             fh.write(r.stderr)
+        with open(ostamp, "w") as fh:
+            fh.write(od)
         return obj
 
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 2)) as ex:

@@ -36,6 +36,7 @@ __global__ void __launch_bounds__(kRedNT) k_multidot(const double* __restrict__ 
 #pragma unroll
     for (int i = 0; i < kDotG; ++i) acc[i] = 0.0;
     const double* __restrict__ Vg = V + (int64_t)g0 * ldv;
+#pragma unroll 2
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
          k += (int64_t)gridDim.x * blockDim.x) {
         const double wk = w[k];

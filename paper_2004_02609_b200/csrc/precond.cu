@@ -23,6 +23,8 @@ struct Precond {
     int max_n = 0;
     DevBuf<int32_t> box_start, box_n, box_uid;  // per non-empty box
     DevBuf<int32_t> ubox_start, ubox_list;       // boxes of each unique block (CSR)
+    DevBuf<int32_t> btile_b, btile_r0;           // per-box apply tiles (box, first row)
+    int nbtile = 0;
     DevBuf<int32_t> tile_u, tile_r0, tile_q0;    // apply tiles: (unique block, first row, first box)
     int ntile = 0;
     DevBuf<int32_t> panel_ids;                   // conductor panels sorted by box
@@ -216,6 +218,35 @@ __global__ void __launch_bounds__(256) k_pc_apply_grouped(
     }
 }
 
+// z_b = R_u r_b with one CTA per (box, 32 rows): r_b gathered once into shared memory, each
+// warp takes rows and reads them straight from the block table (L2-resident: the unique blocks
+// of C4 total ~13 MB), lanes strided over the columns, shuffle-reduced.  No R staging and no
+// per-box serial loop, so every box's latency overlaps (measured against the grouped kernel).
+constexpr int kPbRows = 32;
+__global__ void __launch_bounds__(256) k_pc_apply_box(
+    const int32_t* __restrict__ tb, const int32_t* __restrict__ tr0,
+    const int32_t* __restrict__ bstart, const int32_t* __restrict__ bn,
+    const int32_t* __restrict__ buid, const int64_t* __restrict__ uoff,
+    const int32_t* __restrict__ pids, const double* __restrict__ blocks,
+    const double* __restrict__ r, double* __restrict__ z) {
+    extern __shared__ double rb[];
+    const int b = tb[blockIdx.x], r0 = tr0[blockIdx.x];
+    const int n = bn[b], s0 = bstart[b];
+    const double* __restrict__ R = blocks + uoff[buid[b]];
+    for (int j = threadIdx.x; j < n; j += blockDim.x) rb[j] = r[pids[s0 + j]];
+    __syncthreads();
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int r1 = min(n, r0 + kPbRows);
+    for (int row = r0 + w; row < r1; row += nw) {
+        const double* __restrict__ Rr = R + (int64_t)row * n;
+        double acc = 0.0;
+#pragma unroll 8
+        for (int j = lane; j < n; j += 32) acc = fma(__ldg(Rr + j), rb[j], acc);
+        for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) z[pids[s0 + row]] = acc;
+    }
+}
+
 // per-panel diagonal of R: 1/Ī on dielectric rows; conductor rows 1 (none), 1/P_self
 // (diagonal-only option) or 0 (their block of R_BD writes them)
 __global__ void k_pc_dinv(int64_t n, const int32_t* __restrict__ cid, const double* __restrict__ ibar,
@@ -401,6 +432,17 @@ vc_status precond_build(vc_ctx* c, const int32_t box_in[3], int kind) {
                     tq.push_back(q0);
                 }
         pc->ntile = (int)tu.size();
+        std::vector<int32_t> bt, br;
+        for (int b = 0; b < nbox; ++b)
+            for (int r0 = 0; r0 < bcount[b]; r0 += kPbRows) {
+                bt.push_back(b);
+                br.push_back(r0);
+            }
+        pc->nbtile = (int)bt.size();
+        VC_CUDA(c, pc->btile_b.alloc(std::max<size_t>(1, bt.size())));
+        VC_CUDA(c, pc->btile_r0.alloc(std::max<size_t>(1, br.size())));
+        VC_CUDA(c, up(pc->btile_b.p, bt.data(), 4 * bt.size()));
+        VC_CUDA(c, up(pc->btile_r0.p, br.data(), 4 * br.size()));
         VC_CUDA(c, pc->ubox_start.alloc(nu + 1));
         VC_CUDA(c, pc->ubox_list.alloc(std::max(1, nbox)));
         VC_CUDA(c, pc->tile_u.alloc(std::max<size_t>(1, tu.size())));
@@ -460,7 +502,13 @@ vc_status precond_apply_dev(vc_ctx* c, const double* d_r, double* d_z) {
     const int64_t N = c->NL;
     k_pc_diag<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((N + 255) / 256, 148 * 8)), 256, 0, st>>>(N, d_r, pc->diag_inv.p, d_z);
     count_launch(c);
-    if (pc->kind == 3 && pc->ntile > 0) {
+    static const bool grouped = getenv("VC_PC_GROUPED") != nullptr;
+    if (pc->kind == 3 && !grouped && pc->nbtile > 0) {
+        k_pc_apply_box<<<pc->nbtile, 256, sizeof(double) * (size_t)pc->max_n, st>>>(
+            pc->btile_b.p, pc->btile_r0.p, pc->box_start.p, pc->box_n.p, pc->box_uid.p,
+            pc->uniq_off.p, pc->panel_ids.p, pc->blocks.p, d_r, d_z);
+        count_launch(c);
+    } else if (pc->kind == 3 && pc->ntile > 0) {
         const size_t sh = sizeof(double) * (size_t)(kPcRows + 1) * pc->max_n;
         if (sh > 48 * 1024)
             VC_CUDA(c, grant_max_dyn_smem(k_pc_apply_grouped, max_dyn_smem()));

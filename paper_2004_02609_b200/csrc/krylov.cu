@@ -287,8 +287,14 @@ vc_status solve_dev(vc_ctx* c, const double* d_b, double* d_x, const vc_solve_op
             if ((s = enqueue(0))) return s;
             queued = 1;
         }
+        // The prefetch of step j + 1 is skipped when the residual history predicts that step j
+        // converges (geometric extrapolation rre_j ~ rre_{j-1}^2 / rre_{j-2} within 2x of tol):
+        // a wrong guess costs one host round trip, a right one saves a wasted Arnoldi step.
+        double r_prev = 0.0, r_prev2 = 0.0;
         for (int j = 0; j < queued; ++j) {
-            if (queued < restart && it0 + queued < maxit) {
+            const bool can = queued < restart && it0 + queued < maxit;
+            const bool near = j >= 2 && r_prev2 > 0.0 && r_prev * (r_prev / r_prev2) <= 2.0 * tol;
+            if (can && !near) {
                 if ((s = enqueue(queued))) return s;
                 ++queued;
             }
@@ -314,6 +320,12 @@ vc_status solve_dev(vc_ctx* c, const double* d_b, double* d_x, const vc_solve_op
             rre = std::fabs(g[j + 1]) / nrb;
             jend = j + 1;
             if (rre <= tol || !(rre == rre)) break;
+            r_prev2 = r_prev;
+            r_prev = rre;
+            if (queued == j + 1 && queued < restart && it0 + queued < maxit) {  // prefetch skipped
+                if ((s = enqueue(queued))) return s;
+                ++queued;
+            }
         }
         // y = H^{-1} g (upper triangular), x += V y
         for (int i = jend - 1; i >= 0; --i) {

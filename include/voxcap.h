@@ -73,7 +73,11 @@ typedef struct {
                                are x<->y mirrors of another (P^{yy} of P^{xx}, ...) are
                                transposed from it instead of generated; 1 =
                                generate every block (bitwise comparisons with multi-rank runs) */
-    int32_t reserved[7];
+    int32_t no_batch;       /* 0 = default: on one rank with m >= 2 conductors, keep pass buffers
+                               for 2 columns so vc_solve_capacitance runs its m solves in
+                               lockstep with batched matvecs; 1 = one
+                               column at a time (less memory)                                 */
+    int32_t reserved[6];
 } vc_build_opts;
 
 /* Solve options.  Zero fields take the paper's defaults. */
@@ -185,6 +189,14 @@ vc_status vc_get_grid(const vc_ctx* ctx, int32_t* m3);
 /* y = ([0; Ī] + [P; E]) x   (Eq. 4; Eqs. 9-11).  x, y: N doubles (world > 1:
  * this rank's n_local entries). */
 vc_status vc_matvec(vc_ctx* ctx, const double* x, double* y, int32_t on_device);
+
+/* Y = A X for nb columns (the matvec of vc_matvec per column): X, Y are
+ * column-major n x nb (column c at x + c * n, n = N or this rank's n_local), host or device.
+ * Columns are processed up to two per launch chain when the build kept batch buffers
+ * (vc_build_opts.no_batch = 0, one rank, m >= 2): every pass runs once for the pair and P3
+ * reads each kernel-spectrum tile once for both; each column's result is bitwise equal to
+ * vc_matvec on it.  nb = 0 is a no-op; nb < 0 or NULL vectors: VC_ERR_INPUT. */
+vc_status vc_matvec_batch(vc_ctx* ctx, int32_t nb, const double* x, double* y, int32_t on_device);
 
 /* z = R r with R the preconditioner chosen at build time (Eq. 14). */
 vc_status vc_precond(vc_ctx* ctx, const double* r, double* z, int32_t on_device);

@@ -23,7 +23,7 @@ _LIB_NAME = "libvoxcap.so"
 
 # every symbol include/voxcap.h declares
 EXPORTS = ("vc_create", "vc_set_geometry", "vc_get_sizes", "vc_get_panels", "vc_build_operator",
-           "vc_get_grid", "vc_matvec", "vc_precond", "vc_solve", "vc_solve_capacitance",
+           "vc_get_grid", "vc_matvec", "vc_matvec_batch", "vc_precond", "vc_solve", "vc_solve_capacitance",
            "vc_set_timing", "vc_get_stats", "vc_reset_stats", "vc_debug_kernel_entries",
            "vc_debug_fft", "vc_last_error", "vc_version", "vc_destroy", "vc_init_distributed",
            "vc_nccl_unique_id", "vc_group_create", "vc_group_destroy", "vc_get_local_panels",
@@ -43,7 +43,8 @@ class VoxCapError(RuntimeError):
 class BuildOpts(ctypes.Structure):
     _fields_ = [("pad", ctypes.c_int32 * 3), ("box", ctypes.c_int32 * 3),
                 ("precond", ctypes.c_int32), ("zmode", ctypes.c_int32),
-                ("no_mirror", ctypes.c_int32), ("reserved", ctypes.c_int32 * 7)]
+                ("no_mirror", ctypes.c_int32), ("no_batch", ctypes.c_int32),
+                ("reserved", ctypes.c_int32 * 6)]
 
 
 class SolveOpts(ctypes.Structure):
@@ -113,6 +114,7 @@ def load_library(build_if_missing=False):
         "vc_solve": [vp, vp, vp, P(SolveOpts), P(SolveInfo), i32],
         "vc_solve_capacitance": [vp, vp, P(SolveOpts), vp],
         "vc_set_timing": [vp, i32],
+        "vc_matvec_batch": [vp, i32, vp, vp, i32],
         "vc_get_stats": [vp, P(Stats)],
         "vc_reset_stats": [vp],
         "vc_debug_kernel_entries": [vp, i32, vp, vp, vp, vp, vp],
@@ -295,12 +297,13 @@ class VoxCap:
         return out
 
     # -- operator ------------------------------------------------------------------------
-    def build_operator(self, pad=None, box=None, precond=3, zmode=0, mirror=True):
+    def build_operator(self, pad=None, box=None, precond=3, zmode=0, mirror=True, batch=True):
         """zmode: 0 automatic, 1 z-FFT (3-D circulant), 2 direct z-convolution; mirror=False
         generates every kernel block (no x<->y transposes)."""
         o = BuildOpts()
         o.zmode = int(zmode)
         o.no_mirror = 0 if mirror else 1
+        o.no_batch = 0 if batch else 1
         if pad is not None:
             for a in range(3):
                 o.pad[a] = int(pad[a])
@@ -347,6 +350,21 @@ class VoxCap:
     def matvec(self, x, out=None):
         """y = ([0; Ī] + [P; E]) x (Eq. 4)."""
         return self._vec_call(self._lib.vc_matvec, x, out)
+
+    def matvec_batch(self, X):
+        """Y[:, c] = A X[:, c] for the columns of an (n, nb) array (NEXT-3 batched matvec)."""
+        if _is_cuda_tensor(X):
+            import torch
+            Xc = X.t().contiguous()  # column c contiguous
+            Y = torch.empty_like(Xc)
+            self._fence_in(Xc, Y)
+            self._check(self._lib.vc_matvec_batch(self._ctx, int(Xc.shape[0]), _ptr(Xc), _ptr(Y), 1))
+            self._fence_out()
+            return Y.t()
+        Xc = np.ascontiguousarray(np.asarray(X, dtype=np.float64).T)
+        Y = np.empty_like(Xc)
+        self._check(self._lib.vc_matvec_batch(self._ctx, int(Xc.shape[0]), _ptr(Xc), _ptr(Y), 0))
+        return Y.T
 
     def precond(self, r, out=None):
         return self._vec_call(self._lib.vc_precond, r, out)

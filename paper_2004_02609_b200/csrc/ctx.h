@@ -150,7 +150,9 @@ struct vc_ctx {
     size_t blk_stride = 0;  // doubles per folded spectrum
     vc::DevBuf<double> Rt;  // folded, phase-stripped, scaled kernel spectra
     vc::DevBuf<double2> tw;  // twiddles exp(-2 pi i n / kTabN)
-    vc::DevBuf<double2> bufA, bufB, bufC;  // X1/X4, X2, X3
+    vc::DevBuf<double2> bufA, bufB, bufC;  // X1/X4, X2, X3 (nbmax column copies each)
+    int nbmax = 1;                          // columns one batched matvec may carry (NEXT-3)
+    size_t colA = 0, colB = 0, colC = 0;    // per-column strides of bufA / bufB / bufC
     size_t offB[3], offC[6];
     int T3 = 1, nt3 = 1;   // P3 tile width and kx-tile count (tile-major X2 / R layouts)
     bool zdirect = false;  // P3 direct-z mode (operator.cu k_p3d)
@@ -247,6 +249,9 @@ inline vc_status set_err(vc_ctx* c, vc_status s, const std::string& msg) {
 vc_status geometry_build(vc_ctx* c, const int32_t* d_label, const double* d_eps);
 vc_status operator_build(vc_ctx* c, const vc_build_opts* o);
 vc_status matvec_dev(vc_ctx* c, const double* d_x, double* d_y);
+// y_c = A x_c for c < nb with one launch per pass (kernel spectra read once per P3 tile for all
+// columns); nb <= ctx->nbmax, else (or in z-FFT mode) column by column
+vc_status matvec_batch_dev(vc_ctx* c, int nb, const double* const* d_x, double* const* d_y);
 vc_status precond_build(vc_ctx* c, const int32_t box[3], int kind);
 vc_status precond_apply_dev(vc_ctx* c, const double* d_r, double* d_z);
 void precond_free(vc_ctx* c);

@@ -22,6 +22,7 @@
 namespace vc {
 
 constexpr int kMaxOG = 64;  // P3 direct-z: max output groups
+constexpr int kMaxB = 2;    // columns per batched matvec (NEXT-3; one rank, direct-z mode)
 
 struct MV {
     int Mx, My, Mz, Kx;
@@ -34,6 +35,12 @@ struct MV {
     const int32_t* slotmap[3];
     const double* x;
     double* y;
+    // batched matvec (blockIdx.z / P3 thread group = column c): x, y and the pass buffers of
+    // column c are xs[c], ys[c] and the column-0 buffers + c * col{A,B,C} (one rank only)
+    int nb;
+    const double* xs[kMaxB];
+    double* ys[kMaxB];
+    int64_t colA, colB, colC;
     const int8_t* info;
     const double* ibar;
     double2* X2[3];
@@ -135,7 +142,7 @@ __global__ void __launch_bounds__(FX<L>::NT, FX<L>::MINB) k_p1(MV mv) {
     const int Gx = mv.G[beta][0], Gy = mv.G[beta][1];
     const int64_t zrow =
         ((int64_t)(z + mv.lo[2]) * Gy + mv.lo[1] + mv.ya[mv.rank]) * Gx + mv.lo[0];
-    const double* __restrict__ x = mv.x;
+    const double* __restrict__ x = mv.xs[blockIdx.z];
     // branch-free (predicated loads, selects), so the unrolled stage-0 loop issues all its
     // slot-map loads, then all its x loads, instead of one dependent pair at a time
     auto ld0 = [&](int t, int n) -> double2 {
@@ -156,7 +163,7 @@ __global__ void __launch_bounds__(FX<L>::NT, FX<L>::MINB) k_p1(MV mv) {
     __syncthreads();
     constexpr int K = L / 2 + 1;
     const bool ph = beta != 0;  // c_beta,x = 1/2 for y- and z-normal panels
-    double2* const S1self = mv.S1[0][beta];
+    double2* const S1self = mv.S1[0][beta] + blockIdx.z * mv.colA;
     for (int u = threadIdx.x; u < T * K; u += FX<L>::NT) {
         const int t = u / K, k = u % K;
         const int q = ch * T + t;
@@ -197,10 +204,10 @@ __global__ void __launch_bounds__(FY<L>::NT) k_p2(MV mv) {
     if (j >= mv.nzin[beta]) return;
     (void)ez;
     // X2 tile-major for P3: [q][kx / T3][side][plane][kx % T3], q = |ky| (ky <= L/2: side 0)
-    double2* __restrict__ out = mv.X2[beta];
+    double2* __restrict__ out = mv.X2[beta] + blockIdx.z * mv.colB;
     const int nzb = mv.nzin[beta], nt3 = (nkx + mv.T3 - 1) >> mv.lgT3;
     const bool ph = beta != 1;  // c_beta,y = 1/2 for x- and z-normal panels
-    const double2* const in0 = mv.R1[0][beta] + (int64_t)j * mv.nr[0][beta] * nkx;  // (!D)
+    const double2* const in0 = mv.R1[0][beta] + blockIdx.z * mv.colA + (int64_t)j * mv.nr[0][beta] * nkx;  // (!D)
     auto ld0 = [&](int t, int n) -> double2 {
         const int kx = tile * T + t;
         if (n >= ey || kx >= nkx) return czero();
@@ -242,8 +249,10 @@ __global__ void __launch_bounds__(FYS<L, KB>::NT) k_p4s(MV mv) {
     const int ntx = (nkx + T - 1) / T;
     int G = 0;
     for (int f = 0; f < nf; ++f) G += mv.nzout[f];
-    const int ntiles = G * ntx;
+    const int nt1 = G * ntx;  // tiles per column
+    const int ntiles = nt1 * mv.nb;
     auto decode = [&](int tl, int& f, int& j, int& xt) {
+        tl %= nt1;
         xt = tl % ntx;
         int g = tl / ntx;
         f = 0;
@@ -253,7 +262,7 @@ __global__ void __launch_bounds__(FYS<L, KB>::NT) k_p4s(MV mv) {
     auto prefetch = [&](int tl, int stg) {
         int f, j, xt;
         decode(tl, f, j, xt);
-        const double2* in = mv.X3[f] + (int64_t)j * L * nkx;
+        const double2* in = mv.X3[f] + (tl / nt1) * mv.colC + (int64_t)j * L * nkx;
         double2* dst = sm + stg * L * T;
         for (int e = threadIdx.x; e < L * T; e += NT) {
             const int n = e / T, t = e % T;
@@ -287,7 +296,7 @@ __global__ void __launch_bounds__(FYS<L, KB>::NT) k_p4s(MV mv) {
             if (kx < nkx && yy < eyo) {
                 const int pr = D ? row_owner(mv, yy) : 0;  // row yy goes to rank pr for P5
                 const int y0 = D ? mv.ya[pr] : 0;
-                mv.S2[pr][f][((int64_t)j * mv.nr[pr][3 + f] + (yy - y0)) * nkx + kx] = v;
+                mv.S2[pr][f][(tl / nt1) * mv.colA + ((int64_t)j * mv.nr[pr][3 + f] + (yy - y0)) * nkx + kx] = v;
             }
         };
         fft_run<L, T, NT, true, true, 0, true>(buf, lds, stN, mv.tw);
@@ -497,7 +506,7 @@ __global__ void __launch_bounds__(FX<L>::NT, FX<L>::MINB5) k_p5(MV mv) {
             k0 = mv.kxa[qd];
             nk = mv.kxa[qd + 1] - k0;
         }
-        const double2* src = mv.R2[qd][f] + ((int64_t)j * nrow + yrow) * nk + (k - k0);
+        const double2* src = mv.R2[qd][f] + blockIdx.z * mv.colA + ((int64_t)j * nrow + yrow) * nk + (k - k0);
         double2 w = v ? __ldg(src) : czero();
         if (ph) w = cmul(w, half_phase(mv.tw, k, L, +1));
         if (k == 0 || 2 * k == L) w.y = 0.0;
@@ -528,7 +537,8 @@ __global__ void __launch_bounds__(FX<L>::NT, FX<L>::MINB5) k_p5(MV mv) {
     const int64_t zrow =
         ((int64_t)(z + mv.lo[2]) * Gy + mv.lo[1] + mv.ya[mv.rank]) * Gx + mv.lo[0];
     const int32_t want = kind ? kSlotDiel : 0;
-    double* __restrict__ y = mv.y;
+    double* __restrict__ y = mv.ys[blockIdx.z];
+    const double* __restrict__ xc = mv.xs[blockIdx.z];
     constexpr int NI = (L + FX<L>::NT - 1) / FX<L>::NT;  // slots per thread and line (exo <= L)
 #pragma unroll 1
     for (int r = 0; r < 2 * T; ++r) {
@@ -551,7 +561,7 @@ __global__ void __launch_bounds__(FX<L>::NT, FX<L>::MINB5) k_p5(MV mv) {
             const double val = half ? v.y : v.x;
             const int p = e[i] & kSlotIdx;
             if (kind == 0) y[p] = val;
-            else y[p] = ((e[i] & kSlotNeg) ? -val : val) + mv.ibar[p] * mv.x[p];
+            else y[p] = ((e[i] & kSlotNeg) ? -val : val) + mv.ibar[p] * xc[p];
         }
     }
 }
@@ -827,7 +837,7 @@ static cudaError_t launch_p1(const MV& mv, cudaStream_t st) {
         auto kern = mv.W > 1 ? k_p1<LL, true> : k_p1<LL, false>;
         cudaError_t e = prep(kern, smem);
         if (e) return e;
-        dim3 grid(std::max(1, maxch * maxz), 3);
+        dim3 grid(std::max(1, maxch * maxz), 3, mv.nb);
         kern<<<grid, FX<LL>::NT, smem, st>>>(mv);
     });
     return cudaGetLastError();
@@ -849,7 +859,7 @@ static cudaError_t launch_p4s_t(const MV& mv, cudaStream_t st) {
     auto kern = mv.W > 1 ? k_p4s<LL, KB, true> : k_p4s<LL, KB, false>;
     cudaError_t e = prep(kern, smem);
     if (e) return e;
-    const int ntiles = G * ((mv.nkx + T - 1) / T);
+    const int ntiles = G * ((mv.nkx + T - 1) / T) * mv.nb;
     if (ntiles == 0) return cudaSuccess;
     kern<<<persistent_grid(kern, NT, smem, ntiles), NT, smem, st>>>(mv);
     return cudaSuccess;
@@ -868,7 +878,7 @@ static cudaError_t launch_p2(const MV& mv, cudaStream_t st) {
         auto kern = mv.W > 1 ? k_p2<LL, true> : k_p2<LL, false>;
         cudaError_t e = prep(kern, smem);
         if (e) return e;
-        dim3 grid(std::max(1, ((mv.nkx + T - 1) / T) * maxz), 3);
+        dim3 grid(std::max(1, ((mv.nkx + T - 1) / T) * maxz), 3, mv.nb);
         kern<<<grid, FY<LL>::NT, smem, st>>>(mv);
     });
     return cudaGetLastError();
@@ -945,11 +955,16 @@ __device__ __forceinline__ void p3d_acc_win(double2 (&a0)[kZB], double2 (&a1)[kZ
 // Persistent and TMA-fed like the z-FFT P3: a tile's X2 rows and K rows are contiguous (tile-
 // major layouts), so one thread fetches the next tile with four cp.async.bulk copies into the
 // other half of a two-stage ring while the CTA computes the current tile from shared memory.
+// Batched (mv.nb columns): the CTA holds one thread group per column; the groups share each
+// tile's K rows (fetched once) and get their own X2 rows, so the kernel spectra are read from
+// HBM once per tile for all columns.
 template <int NST>  // stages of the TMA ring (1: no prefetch, more CTAs per SM)
-__global__ void __launch_bounds__(256) k_p3d(MV mv) {
+__global__ void __launch_bounds__(512) k_p3d(MV mv) {
     constexpr int T = kDirectT;
     extern __shared__ __align__(16) double2 sd[];
-    const int t = threadIdx.x % T, og0 = threadIdx.x / T, OGS = blockDim.x / T;
+    const int NB = mv.nb, nthr1 = blockDim.x / NB;
+    const int col = threadIdx.x / nthr1, tid1 = threadIdx.x - col * nthr1;
+    const int t = tid1 % T, og0 = tid1 / T, OGS = nthr1 / T;
     const int nkx = mv.nkx, My = mv.My, ZL = mv.ZL;
     const int nt3 = (nkx + T - 1) / T;
     const int ntiles = nt3 * (My / 2 + 1);
@@ -957,8 +972,8 @@ __global__ void __launch_bounds__(256) k_p3d(MV mv) {
     const int xo1 = 2 * T * nz0, xo2 = 2 * T * (nz0 + nz1);
     const int XS = 2 * T * (nz0 + nz1 + nz2);  // double2 per stage
     const int RC = mv.rchunk;                  // doubles per stage (even)
-    double2* xin = sd;                                          // [NST][XS]
-    double* kin = reinterpret_cast<double*>(xin + NST * XS);    // [NST][RC]
+    double2* xin = sd;                                          // [NST][NB][XS]
+    double* kin = reinterpret_cast<double*>(xin + NST * NB * XS);  // [NST][RC]
     int* zl = reinterpret_cast<int*>(kin + NST * RC);           // [9][ZL] plane lists
     uint64_t* bar = reinterpret_cast<uint64_t*>(zl + ((9 * ZL + 3) & ~3));  // [2]
     if (threadIdx.x == 0) {
@@ -971,10 +986,14 @@ __global__ void __launch_bounds__(256) k_p3d(MV mv) {
     __syncthreads();
     auto issue = [&](int tl, int s) {  // one thread: fetch tile tl into stage s
         const size_t qt = (size_t)tl;
-        mbar_arrive_expect_tx(&bar[s], (unsigned)(16 * XS + 8 * RC));
-        if (nz0) bulk_g2s(xin + s * XS, mv.X2[0] + qt * 2 * T * nz0, 32u * T * nz0, &bar[s]);
-        if (nz1) bulk_g2s(xin + s * XS + xo1, mv.X2[1] + qt * 2 * T * nz1, 32u * T * nz1, &bar[s]);
-        if (nz2) bulk_g2s(xin + s * XS + xo2, mv.X2[2] + qt * 2 * T * nz2, 32u * T * nz2, &bar[s]);
+        mbar_arrive_expect_tx(&bar[s], (unsigned)(16 * NB * XS + 8 * RC));
+        for (int c = 0; c < NB; ++c) {
+            double2* xd = xin + (s * NB + c) * XS;
+            const int64_t co = c * mv.colB;
+            if (nz0) bulk_g2s(xd, mv.X2[0] + co + qt * 2 * T * nz0, 32u * T * nz0, &bar[s]);
+            if (nz1) bulk_g2s(xd + xo1, mv.X2[1] + co + qt * 2 * T * nz1, 32u * T * nz1, &bar[s]);
+            if (nz2) bulk_g2s(xd + xo2, mv.X2[2] + co + qt * 2 * T * nz2, 32u * T * nz2, &bar[s]);
+        }
         bulk_g2s(kin + s * RC, mv.Rt + qt * RC, 8u * RC, &bar[s]);
     };
     if (NST > 1 && threadIdx.x == 0 && (int)blockIdx.x < ntiles) issue(blockIdx.x, 0);
@@ -991,7 +1010,7 @@ __global__ void __launch_bounds__(256) k_p3d(MV mv) {
         }
         if (st == 0) { mbar_wait(&bar[0], par0); par0 ^= 1; }
         else { mbar_wait(&bar[1], par1); par1 ^= 1; }
-        const double2* xs = xin + st * XS;
+        const double2* xs = xin + (st * NB + col) * XS;
         const double* ks = kin + st * RC;
         const int q = tl / nt3, xt = tl % nt3;
         const int kx = xt * T + t;
@@ -1053,7 +1072,7 @@ __global__ void __launch_bounds__(256) k_p3d(MV mv) {
                 }
             }
             if (!valid) continue;
-            double2* __restrict__ X3 = mv.X3[f];
+            double2* __restrict__ X3 = mv.X3[f] + col * mv.colC;
             const bool ifac = kind == 1 && alpha != 2;  // E^{x.}, E^{y.}: R stores Im(K)
 #pragma unroll
             for (int k = 0; k < kZB; ++k) {
@@ -1074,14 +1093,19 @@ __global__ void __launch_bounds__(256) k_p3d(MV mv) {
     }
 }
 
+static size_t p3d_smem(const MV& mv) {
+    return kP3dStages * (16 * (size_t)2 * kDirectT * (mv.nzin[0] + mv.nzin[1] + mv.nzin[2]) * mv.nb +
+                         8 * (size_t)mv.rchunk) +
+           4 * (size_t)((9 * mv.ZL + 3) & ~3) + 2 * sizeof(uint64_t);
+}
 static cudaError_t launch_p3d(const MV& mv, cudaStream_t st) {
     const int nt3 = (mv.nkx + kDirectT - 1) / kDirectT;
     const int ntiles = nt3 * (mv.My / 2 + 1);
     if (ntiles == 0 || mv.nog == 0) return cudaSuccess;
     const int ogs = std::min(mv.nog, 256 / kDirectT);
-    const int nthr = kDirectT * ogs;
+    const int nthr = kDirectT * ogs * mv.nb;
     constexpr int NST = kP3dStages;
-    const size_t smem = NST * (16 * (size_t)2 * kDirectT * (mv.nzin[0] + mv.nzin[1] + mv.nzin[2]) +
+    const size_t smem = NST * (16 * (size_t)2 * kDirectT * (mv.nzin[0] + mv.nzin[1] + mv.nzin[2]) * mv.nb +
                                8 * (size_t)mv.rchunk) +
                         4 * (size_t)((9 * mv.ZL + 3) & ~3) + 2 * sizeof(uint64_t);
     if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
@@ -1133,6 +1157,19 @@ static cudaError_t launch_p3_l(const MV& mv, cudaStream_t st) {
     }
 }
 static cudaError_t launch_p3(const MV& mv, cudaStream_t st) {
+    if (mv.nb > 1 && !(mv.zdirect && p3d_smem(mv) <= 227 * 1024 &&
+                       kDirectT * std::min(mv.nog, 256 / kDirectT) * mv.nb <= 512)) {
+        // column by column (z-FFT mode, or the batched tile does not fit one CTA)
+        for (int c = 0; c < mv.nb; ++c) {
+            MV m1 = mv;
+            m1.nb = 1;
+            for (int b = 0; b < 3; ++b) m1.X2[b] += c * mv.colB;
+            for (int f = 0; f < 6; ++f) m1.X3[f] += c * mv.colC;
+            const cudaError_t e = launch_p3(m1, st);
+            if (e) return e;
+        }
+        return cudaSuccess;
+    }
     if (mv.zdirect) return launch_p3d(mv, st);
     cudaError_t e;
     switch (mv.Mz) {  // kMaxLz: the [L][W] pencil buffer must fit one CTA's shared memory
@@ -1158,7 +1195,7 @@ static cudaError_t launch_p5(const MV& mv, cudaStream_t st) {
         auto kern = mv.W > 1 ? k_p5<LL, true> : k_p5<LL, false>;
         cudaError_t e = prep(kern, smem);
         if (e) return e;
-        dim3 grid(std::max(1, maxch * maxz), mv.nf);
+        dim3 grid(std::max(1, maxch * maxz), mv.nf, mv.nb);
         kern<<<grid, FX<LL>::NT, smem, st>>>(mv);
     });
     return cudaGetLastError();
@@ -1613,9 +1650,22 @@ vc_status operator_build(vc_ctx* c, const vc_build_opts* o) {
         c->offC[f] = nC;
         nC += (size_t)c->nzout[f] * My * nkx;
     }
-    VC_CUDA(c, c->bufA.alloc(std::max<size_t>(1, std::max(nR1, nR2))));
-    VC_CUDA(c, c->bufB.alloc(std::max<size_t>(1, nBt)));
-    VC_CUDA(c, c->bufC.alloc(std::max<size_t>(1, nC)));
+    // batched matvec (NEXT-3): one rank and at least two conductors; as many column copies of
+    // the pass buffers as the free memory comfortably holds (<= kMaxB)
+    c->colA = std::max<size_t>(1, std::max(nR1, nR2));
+    c->colB = std::max<size_t>(1, nBt);
+    c->colC = std::max<size_t>(1, nC);
+    c->nbmax = 1;
+    if (W == 1 && c->m >= 2 && !(o && o->no_batch)) {
+        size_t fr = 0, totm = 0;
+        cudaMemGetInfo(&fr, &totm);
+        const size_t percol = sizeof(double2) * (c->colA + c->colB + c->colC);
+        const size_t have = c->bufA.bytes() + c->bufB.bytes() + c->bufC.bytes();
+        while (c->nbmax < std::min(kMaxB, c->m) && (c->nbmax + 1) * percol <= (fr + have) / 3) ++c->nbmax;
+    }
+    VC_CUDA(c, c->bufA.alloc(c->colA * c->nbmax));
+    VC_CUDA(c, c->bufB.alloc(c->colB * c->nbmax));
+    VC_CUDA(c, c->bufC.alloc(c->colC * c->nbmax));
     c->bufS.reset();
     if (W > 1) VC_CUDA(c, c->bufS.alloc(std::max<size_t>(1, std::max(nS1, nS2))));
     // all-to-all block tables (bytes; the self block is written in place by P1 / P4)
@@ -1781,6 +1831,12 @@ static MV make_mv(vc_ctx* c, const double* x, double* y) {
     }
     mv.x = x;
     mv.y = y;
+    mv.nb = 1;
+    mv.xs[0] = x;
+    mv.ys[0] = y;
+    mv.colA = (int64_t)c->colA;
+    mv.colB = (int64_t)c->colB;
+    mv.colC = (int64_t)c->colC;
     mv.info = loc ? c->lp.info.p : c->pan.info.p;
     mv.ibar = loc ? c->lp.ibar.p : c->pan.ibar.p;
     mv.Rt = c->Rt.p;
@@ -1826,13 +1882,39 @@ static MV make_mv(vc_ctx* c, const double* x, double* y) {
     return mv;
 }
 
+static vc_status matvec_run(vc_ctx* c, const MV& mv);
+
+vc_status matvec_batch_dev(vc_ctx* c, int nb, const double* const* d_x, double* const* d_y) {
+    for (int c0 = 0; c0 < nb; c0 += c->nbmax) {
+        const int n1 = std::min(c->nbmax, nb - c0);
+        if (n1 == 1) {
+            vc_status s = matvec_dev(c, d_x[c0], d_y[c0]);
+            if (s) return s;
+            continue;
+        }
+        MV mv = make_mv(c, d_x[c0], d_y[c0]);
+        mv.nb = n1;
+        for (int i = 0; i < n1; ++i) {
+            mv.xs[i] = d_x[c0 + i];
+            mv.ys[i] = d_y[c0 + i];
+        }
+        vc_status s = matvec_run(c, mv);
+        if (s) return s;
+    }
+    return VC_OK;
+}
+
 vc_status matvec_dev(vc_ctx* c, const double* d_x, double* d_y) {
+    return matvec_run(c, make_mv(c, d_x, d_y));
+}
+
+static vc_status matvec_run(vc_ctx* c, const MV& mv) {
     cudaStream_t st = c->stream;
-    const MV mv = make_mv(c, d_x, d_y);
     Timing& T = c->timing;
     const bool det = T.detail && T.ev_ok;
     if (T.ev_ok) VC_CUDA(c, cudaEventRecord(T.ev[0], st));
-    k_zero<<<std::max<int64_t>(1, std::min<int64_t>((c->NL + 255) / 256, 1184)), 256, 0, st>>>(d_y, c->NL);
+    for (int i = 0; i < mv.nb; ++i)
+        k_zero<<<std::max<int64_t>(1, std::min<int64_t>((c->NL + 255) / 256, 1184)), 256, 0, st>>>(mv.ys[i], c->NL);
     cudaError_t (*launch[5])(const MV&, cudaStream_t) = {launch_p1, launch_p2, launch_p3,
                                                          launch_p4s, launch_p5};
     for (int p = 0; p < 5; ++p) {
@@ -1849,8 +1931,8 @@ vc_status matvec_dev(vc_ctx* c, const double* d_x, double* d_y) {
         if (det) VC_CUDA(c, cudaEventRecord(T.ev[6 + p], st));
     }
     if (T.ev_ok) VC_CUDA(c, cudaEventRecord(T.ev[11], st));
-    count_launch(c, 6);
-    c->stats.n_matvec += 1;
+    count_launch(c, 5 + mv.nb);
+    c->stats.n_matvec += mv.nb;
     for (int p = 0; p < 5; ++p) c->stats.n_pass[p] += 1;
     if (T.ev_ok) {
         // accumulate device times (waits for this matvec; used only with timing on)

@@ -1,3 +1,4 @@
+#include <vector>
 // voxcap.cu -- the C ABI of libvoxcap.so (include/voxcap.h).  Argument checking, state
 // machine, host<->device marshalling; every step of the path runs in the kernels of
 // panels.cu / operator.cu / precond.cu / krylov.cu.
@@ -269,6 +270,38 @@ vc_status vc_matvec(vc_ctx* c, const double* x, double* y, int32_t on_device) {
     DeviceGuard g(c->device);
     return with_vectors(c, x, y, on_device, false,
                         [&](const double* dx, double* dy) { return matvec_dev(c, dx, dy); });
+}
+
+vc_status vc_matvec_batch(vc_ctx* c, int32_t nb, const double* x, double* y, int32_t on_device) {
+    VC_CHECK_CTX(c);
+    if (!c->has_op) return set_err(c, VC_ERR_STATE, "vc_matvec_batch before vc_build_operator");
+    if (nb < 0) return set_err(c, VC_ERR_INPUT, "nb must be >= 0");
+    if (nb > 0 && (!x || !y)) return set_err(c, VC_ERR_INPUT, "null vector");
+    if (nb == 0) return VC_OK;
+    DeviceGuard g(c->device);
+    const int64_t n = c->NL;
+    std::vector<const double*> xs(nb);
+    std::vector<double*> ys(nb);
+    if (on_device) {
+        for (int i = 0; i < nb; ++i) {
+            xs[i] = x + i * n;
+            ys[i] = y + i * n;
+        }
+        return matvec_batch_dev(c, nb, xs.data(), ys.data());
+    }
+    DevBuf<double>&din = c->io_in, &dout = c->io_out;
+    VC_CUDA(c, din.alloc(std::max<int64_t>(1, n * nb)));
+    VC_CUDA(c, dout.alloc(std::max<int64_t>(1, n * nb)));
+    VC_CUDA(c, cudaMemcpyAsync(din.p, x, 8 * n * nb, cudaMemcpyHostToDevice, c->stream));
+    for (int i = 0; i < nb; ++i) {
+        xs[i] = din.p + i * n;
+        ys[i] = dout.p + i * n;
+    }
+    vc_status s = matvec_batch_dev(c, nb, xs.data(), ys.data());
+    if (s) return s;
+    VC_CUDA(c, cudaMemcpyAsync(y, dout.p, 8 * n * nb, cudaMemcpyDeviceToHost, c->stream));
+    VC_CUDA(c, cudaStreamSynchronize(c->stream));
+    return VC_OK;
 }
 
 vc_status vc_precond(vc_ctx* c, const double* r, double* z, int32_t on_device) {

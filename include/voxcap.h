@@ -111,6 +111,9 @@ typedef struct {
     double  ms_kfft;        /* last build: 3-D FFT of the kernels + phase strip / fold        */
     double  ms_geometry;    /* last vc_set_geometry (panel indexing), device time            */
     double  ms_comm;        /* all-to-all time inside matvecs (world > 1, timing_detail = 1)  */
+    double  bytes_moved[5]; /* algorithmic bytes of all launches of each pass since the reset:
+                               a batched launch of nb columns counts nb x its per-column arrays
+                               and the P3 kernel spectra once (vc_matvec_batch)              */
     int64_t reserved[4];
 } vc_stats;
 

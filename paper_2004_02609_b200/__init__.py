@@ -68,12 +68,14 @@ class Stats(ctypes.Structure):
                 ("ms_setup", ctypes.c_double), ("ms_precond_build", ctypes.c_double),
                 ("gpu_launches", ctypes.c_int64), ("ms_kgen", ctypes.c_double),
                 ("ms_kfft", ctypes.c_double), ("ms_geometry", ctypes.c_double),
-                ("ms_comm", ctypes.c_double), ("reserved", ctypes.c_int64 * 4)]
+                ("ms_comm", ctypes.c_double), ("bytes_moved", ctypes.c_double * 5),
+                ("reserved", ctypes.c_int64 * 4)]
 
     def as_dict(self):
         return {"n_matvec": self.n_matvec, "ms_matvec": self.ms_matvec,
                 "n_pass": list(self.n_pass), "ms_pass": list(self.ms_pass),
                 "bytes_pass": list(self.bytes_pass), "bytes_matvec": self.bytes_matvec,
+                "bytes_moved": list(self.bytes_moved),
                 "ms_setup": self.ms_setup, "ms_precond_build": self.ms_precond_build,
                 "gpu_launches": self.gpu_launches, "ms_kgen": self.ms_kgen,
                 "ms_kfft": self.ms_kfft, "ms_geometry": self.ms_geometry,

@@ -164,6 +164,7 @@ struct vc_ctx {
     int ZL = 0, nzin[3] = {0, 0, 0}, nzout[6] = {0, 0, 0, 0, 0, 0};  // active z-plane counts
     vc::DevBuf<int32_t> planes;  // plane lists + inverse maps (operator.cu)
     double bytes_pass[5] = {0, 0, 0, 0, 0};
+    double bytes_k3 = 0;  // the kernel-spectrum share of bytes_pass[2] (read once per P3 launch)
     int precond_kind = 3;
     int box[3] = {10, 10, 10};
     vc::Precond* pc = nullptr;
@@ -205,6 +206,7 @@ struct vc_ctx {
     vc::DevBuf<double> partial;
     vc::DevBuf<double> dvec;  // small device vector (dots)
     double* h_pinned = nullptr;  // pinned host scratch (dots)
+    double* h_pinned_multi = nullptr;  // pinned host scratch of the lockstep solver
     vc::DevBuf<unsigned> ticket;  // last-block ticket of the fused multi-dot
     cudaEvent_t arn_ev[2] = {};   // pipelined Arnoldi: coefficients of step j landed on the host
     bool arn_ev_ok = false;

@@ -17,6 +17,7 @@ namespace vc {
 namespace {
 
 constexpr int kMaxBasis = 64;  // restart + 1 <= 64
+constexpr int kMaxCols = 2;    // lockstep columns (= the batched matvec's kMaxB)
 constexpr int kRedBlocks = 296;
 constexpr int kRedNT = 256;
 
@@ -356,6 +357,209 @@ vc_status solve_dev(vc_ctx* c, const double* d_b, double* d_x, const vc_solve_op
     return converged ? VC_OK : set_err(c, VC_NOT_CONVERGED, "GMRES did not reach tol within maxit");
 }
 
+// Lockstep GMRES for ncol <= kMaxB right-hand sides: every column runs
+// the same restarted, left-preconditioned GMRES with CGS2 as solve_dev (identical kernels and
+// arithmetic per column), but each step's matvecs -- the Arnoldi products R A v_j of the columns
+// in a cycle and the restart residuals b - A x of the others -- go through one batched matvec,
+// so P3 reads each kernel tile once for all columns.  One host synchronisation per step (the
+// Givens updates of all columns).  d_b, d_x: ncol device vectors of n.
+vc_status solve_multi_dev(vc_ctx* c, int ncol, const double* const* d_b, double* const* d_x,
+                          const vc_solve_opts* o, vc_solve_info* info) {
+    const double tol = (o && o->tol > 0) ? o->tol : 1e-4;
+    const int restart = (o && o->restart > 0) ? std::min(o->restart, kMaxBasis - 1) : 35;
+    const int maxit = (o && o->maxit > 0) ? o->maxit : 2000;
+    const int64_t n = c->NL;
+    cudaStream_t st = c->stream;
+    const unsigned gn = grid_for(n);
+    const size_t per = (size_t)(restart + 1 + 5) * n;
+    if (c->work_n < per * ncol) {
+        VC_CUDA(c, c->work.alloc(per * ncol));
+        c->work_n = per * ncol;
+    }
+    if (c->partial.n < (size_t)kRedBlocks * kMaxBasis) VC_CUDA(c, c->partial.alloc((size_t)kRedBlocks * kMaxBasis));
+    if (c->dvec.n < (size_t)8 * kMaxBasis * kMaxCols) VC_CUDA(c, c->dvec.alloc((size_t)8 * kMaxBasis * kMaxCols));
+    if (!c->ticket.p) {
+        VC_CUDA(c, c->ticket.alloc(1));
+        VC_CUDA(c, cudaMemsetAsync(c->ticket.p, 0, sizeof(unsigned), st));
+    }
+    if (!c->h_pinned_multi) VC_CUDA(c, cudaMallocHost(&c->h_pinned_multi, sizeof(double) * 8 * kMaxBasis * kMaxCols));
+    if (!c->h_pinned) VC_CUDA(c, cudaMallocHost(&c->h_pinned, 8 * 8 * kMaxBasis));
+    struct Col {
+        Krylov K;
+        double *dh, *hp;
+        std::vector<double> H, cs, sn, g, y;
+        double nrb = 0, nb = 0, rre = 1, nr = 0;
+        int iters = 0, j = 0, phase = 0;  // phase 0: restart residual, 1: Arnoldi, 2: done
+        bool converged = false;
+    };
+    std::vector<Col> col(ncol);
+    vc_status s;
+    for (int i = 0; i < ncol; ++i) {
+        Col& C = col[i];
+        C.K.c = c;
+        C.K.n = n;
+        C.K.m = restart;
+        C.K.V = c->work.p + per * i;
+        C.K.w = C.K.V + (size_t)(restart + 1) * n;
+        C.K.t = C.K.w + n;
+        C.K.r = C.K.t + n;
+        C.K.b = C.K.r + n;
+        C.K.x = C.K.b + n;
+        C.dh = c->dvec.p + (size_t)8 * kMaxBasis * i;
+        C.hp = c->h_pinned_multi + (size_t)8 * kMaxBasis * i;
+        C.H.assign((size_t)(restart + 1) * restart, 0.0);
+        C.cs.assign(restart, 0.0);
+        C.sn.assign(restart, 0.0);
+        C.g.assign(restart + 1, 0.0);
+        C.y.assign(restart, 0.0);
+        VC_CUDA(c, cudaMemcpyAsync(C.K.b, d_b[i], 8 * n, cudaMemcpyDeviceToDevice, st));
+        VC_CUDA(c, cudaMemsetAsync(C.K.x, 0, 8 * n, st));
+        if ((s = precond_apply_dev(c, C.K.b, C.K.r))) return s;  // x = 0: r = R b
+        if ((s = C.K.norm2_host(C.K.r, &C.nrb))) return s;
+        if ((s = C.K.norm2_host(C.K.b, &C.nb))) return s;
+        if (C.nrb == 0.0) {
+            C.converged = true;
+            C.rre = 0.0;
+            C.phase = 2;
+        } else {  // first cycle: V0 = r / ||r||
+            k_axpby<<<gn, 256, 0, st>>>(C.K.V, C.K.r, 1.0 / C.nrb, 0.0, n);
+            count_launch(c);
+            C.g[0] = C.nrb;
+            C.phase = 1;
+        }
+    }
+    auto finish_cycle = [&](Col& C) -> vc_status {  // y = H^{-1} g, x += V y
+        const int jend = C.j;
+        for (int i = jend - 1; i >= 0; --i) {
+            double v = C.g[i];
+            for (int k = i + 1; k < jend; ++k) v -= C.H[(size_t)k * (restart + 1) + i] * C.y[k];
+            C.y[i] = v / C.H[(size_t)i * (restart + 1) + i];
+        }
+        if (jend > 0) {
+            VC_CUDA(c, cudaMemcpyAsync(C.dh + 6 * kMaxBasis, C.y.data(), 8 * jend, cudaMemcpyHostToDevice, st));
+            k_multiaxpy<<<gn, 256, 0, st>>>(C.K.x, C.K.V, n, jend, C.dh + 6 * kMaxBasis, n, 1.0);
+            count_launch(c);
+        }
+        return VC_OK;
+    };
+    std::vector<const double*> ins;
+    std::vector<double*> outs;
+    std::vector<int> act;
+    for (;;) {
+        act.clear();
+        ins.clear();
+        outs.clear();
+        for (int i = 0; i < ncol; ++i) {
+            Col& C = col[i];
+            if (C.phase == 2) continue;
+            act.push_back(i);
+            ins.push_back(C.phase == 1 ? C.K.V + (size_t)C.j * n : C.K.x);
+            outs.push_back(C.K.w);
+        }
+        if (act.empty()) break;
+        if ((s = matvec_batch_dev(c, (int)act.size(), ins.data(), outs.data()))) return s;
+        for (int i : act) {
+            Col& C = col[i];
+            Krylov& K = C.K;
+            if (C.phase == 1) {  // CGS2 of w' = R A v_j against v_0..v_j, as in solve_dev
+                const int j = C.j;
+                if ((s = precond_apply_dev(c, K.w, K.t))) return s;
+                if ((s = K.dots(K.V, j + 1, K.t, C.dh))) return s;
+                k_multiaxpy<<<gn, 256, 0, st>>>(K.t, K.V, n, j + 1, C.dh, n, -1.0);
+                if ((s = K.dots(K.V, j + 1, K.t, C.dh + kMaxBasis))) return s;
+                k_multiaxpy<<<gn, 256, 0, st>>>(K.t, K.V, n, j + 1, C.dh + kMaxBasis, n, -1.0);
+                if ((s = K.dots(K.t, 1, K.t, C.dh + 2 * kMaxBasis))) return s;
+                k_scale_by_norm<<<gn, 256, 0, st>>>(K.V + (size_t)(j + 1) * n, K.t, C.dh + 2 * kMaxBasis, n);
+                count_launch(c, 3);
+            } else {  // restart residual r = R (b - A x)
+                k_axpby<<<gn, 256, 0, st>>>(K.w, K.b, 1.0, -1.0, n);
+                count_launch(c);
+                if ((s = precond_apply_dev(c, K.w, K.r))) return s;
+                if ((s = K.dots(K.r, 1, K.r, C.dh + 2 * kMaxBasis))) return s;
+            }
+            VC_CUDA(c, cudaMemcpyAsync(C.hp, C.dh, 8 * 3 * kMaxBasis, cudaMemcpyDeviceToHost, st));
+        }
+        VC_CUDA(c, cudaStreamSynchronize(st));
+        for (int i : act) {
+            Col& C = col[i];
+            const double* hh = C.hp;
+            if (C.phase == 1) {
+                const int j = C.j;
+                ++C.iters;
+                double* Hj = C.H.data() + (size_t)j * (restart + 1);
+                for (int q = 0; q <= j; ++q) Hj[q] = hh[q] + hh[kMaxBasis + q];
+                Hj[j + 1] = std::sqrt(hh[2 * kMaxBasis]);
+                for (int q = 0; q < j; ++q) {
+                    const double a = Hj[q], bb = Hj[q + 1];
+                    Hj[q] = C.cs[q] * a + C.sn[q] * bb;
+                    Hj[q + 1] = -C.sn[q] * a + C.cs[q] * bb;
+                }
+                const double a = Hj[j], bb = Hj[j + 1];
+                const double den = std::hypot(a, bb);
+                C.cs[j] = den > 0 ? a / den : 1.0;
+                C.sn[j] = den > 0 ? bb / den : 0.0;
+                Hj[j] = den;
+                Hj[j + 1] = 0.0;
+                C.g[j + 1] = -C.sn[j] * C.g[j];
+                C.g[j] = C.cs[j] * C.g[j];
+                C.rre = std::fabs(C.g[j + 1]) / C.nrb;
+                C.j = j + 1;
+                const bool nan = !(C.rre == C.rre);
+                if (C.rre <= tol || C.j == restart || C.iters >= maxit || nan) {
+                    if ((s = finish_cycle(C))) return s;
+                    if (C.rre <= tol) {
+                        C.converged = true;
+                        C.phase = 2;
+                    } else if (C.iters >= maxit || nan) {
+                        C.phase = 2;
+                    } else {
+                        C.phase = 0;
+                    }
+                }
+            } else {
+                const double beta = std::sqrt(hh[2 * kMaxBasis]);
+                C.rre = beta / C.nrb;
+                if (C.rre <= tol) {
+                    C.converged = true;
+                    C.phase = 2;
+                } else {
+                    k_axpby<<<gn, 256, 0, st>>>(C.K.V, C.K.r, 1.0 / beta, 0.0, n);
+                    count_launch(c);
+                    std::fill(C.g.begin(), C.g.end(), 0.0);
+                    C.g[0] = beta;
+                    C.j = 0;
+                    C.phase = 1;
+                }
+            }
+        }
+    }
+    // true residuals ||b - A x|| / ||b|| (one batched matvec)
+    ins.clear();
+    outs.clear();
+    for (int i = 0; i < ncol; ++i) {
+        ins.push_back(col[i].K.x);
+        outs.push_back(col[i].K.w);
+    }
+    if ((s = matvec_batch_dev(c, ncol, ins.data(), outs.data()))) return s;
+    bool all = true;
+    for (int i = 0; i < ncol; ++i) {
+        Col& C = col[i];
+        k_axpby<<<gn, 256, 0, st>>>(C.K.w, C.K.b, 1.0, -1.0, n);
+        count_launch(c);
+        if ((s = C.K.norm2_host(C.K.w, &C.nr))) return s;
+        VC_CUDA(c, cudaMemcpyAsync(d_x[i], C.K.x, 8 * n, cudaMemcpyDeviceToDevice, st));
+        if (info) {
+            info[i].iters = C.iters;
+            info[i].converged = C.converged ? 1 : 0;
+            info[i].rre_prec = C.rre;
+            info[i].rre_true = C.nb > 0 ? C.nr / C.nb : 0.0;
+        }
+        all = all && C.converged;
+    }
+    VC_CUDA(c, cudaStreamSynchronize(st));
+    return all ? VC_OK : set_err(c, VC_NOT_CONVERGED, "GMRES did not reach tol within maxit");
+}
+
 vc_status capacitance_dev(vc_ctx* c, double* h_C, const vc_solve_opts* o, vc_solve_info* info) {
     cudaStream_t st = c->stream;
     const int64_t n = c->NL;
@@ -363,30 +567,43 @@ vc_status capacitance_dev(vc_ctx* c, double* h_C, const vc_solve_opts* o, vc_sol
     const int32_t* cid = c->world > 1 ? c->lp.cid.p : c->pan.cid.p;
     const double* fc = c->world > 1 ? c->lp.fc.p : c->pan.fc.p;
     DevBuf<double>&b = c->cap_b, &rho = c->cap_rho, &part = c->cap_part, &col = c->cap_col;
-    VC_CUDA(c, b.alloc(std::max<int64_t>(1, n)));
-    VC_CUDA(c, rho.alloc(std::max<int64_t>(1, n)));
+    // columns in lockstep groups of up to nbmax (batched matvecs, NEXT-3), else one by one
+    const int G = std::max(1, std::min(std::min(c->nbmax, kMaxCols), m));
+    VC_CUDA(c, b.alloc(std::max<int64_t>(1, n) * G));
+    VC_CUDA(c, rho.alloc(std::max<int64_t>(1, n) * G));
     const unsigned nb = 148;
     VC_CUDA(c, part.alloc((size_t)nb * m));
     VC_CUDA(c, col.alloc(m));
     std::vector<double> hp(m);
     const double area = c->dv * c->dv;
     vc_status worst = VC_OK;
-    for (int j = 1; j <= m; ++j) {
-        k_rhs<<<grid_for(n), 256, 0, st>>>(b.p, cid, j, area, n);
-        count_launch(c);
-        vc_solve_info inf{};
-        vc_status s = solve_dev(c, b.p, rho.p, o, &inf);
+    for (int j0 = 1; j0 <= m; j0 += G) {
+        const int ng = std::min(G, m - j0 + 1);
+        const double* bs[kMaxCols];
+        double* xs[kMaxCols];
+        for (int q = 0; q < ng; ++q) {
+            bs[q] = b.p + (size_t)q * n;
+            xs[q] = rho.p + (size_t)q * n;
+            k_rhs<<<grid_for(n), 256, 0, st>>>(b.p + (size_t)q * n, cid, j0 + q, area, n);
+            count_launch(c);
+        }
+        vc_solve_info inf[kMaxCols] = {};
+        vc_status s = ng > 1 ? solve_multi_dev(c, ng, bs, xs, o, inf)
+                             : solve_dev(c, bs[0], xs[0], o, &inf[0]);
         if (s != VC_OK && s != VC_NOT_CONVERGED) return s;
         if (s == VC_NOT_CONVERGED) worst = s;
-        if (info) info[j - 1] = inf;
-        dim3 g(nb, m);
-        k_cap_partial<<<g, kRedNT, 0, st>>>(rho.p, cid, fc, area, n, m, part.p);
-        k_cap_final<<<1, std::max(32, ((m + 31) / 32) * 32), 0, st>>>(part.p, nb, m, col.p);
-        count_launch(c, 2);
-        if ((s = comm_allreduce(c, col.p, m))) return s;
-        VC_CUDA(c, cudaMemcpyAsync(hp.data(), col.p, 8 * (size_t)m, cudaMemcpyDeviceToHost, st));
-        VC_CUDA(c, cudaStreamSynchronize(st));
-        for (int i = 0; i < m; ++i) h_C[(size_t)i * m + (j - 1)] = hp[i];
+        for (int q = 0; q < ng; ++q) {
+            const int j = j0 + q;
+            if (info) info[j - 1] = inf[q];
+            dim3 g(nb, m);
+            k_cap_partial<<<g, kRedNT, 0, st>>>(xs[q], cid, fc, area, n, m, part.p);
+            k_cap_final<<<1, std::max(32, ((m + 31) / 32) * 32), 0, st>>>(part.p, nb, m, col.p);
+            count_launch(c, 2);
+            if ((s = comm_allreduce(c, col.p, m))) return s;
+            VC_CUDA(c, cudaMemcpyAsync(hp.data(), col.p, 8 * (size_t)m, cudaMemcpyDeviceToHost, st));
+            VC_CUDA(c, cudaStreamSynchronize(st));
+            for (int i = 0; i < m; ++i) h_C[(size_t)i * m + (j - 1)] = hp[i];
+        }
     }
     return worst == VC_OK ? VC_OK : set_err(c, worst, "some capacitance columns did not converge");
 }

@@ -1721,8 +1721,8 @@ vc_status operator_build(vc_ctx* c, const vc_build_opts* o) {
     for (int64_t i = 0; i < c->NL; ++i) ndl += c->h_cid[W > 1 ? c->h_gidx[i] : i] == 0;
     c->bytes_pass[0] = cb * nX1 + 4.0 * slots + 8.0 * NL;
     c->bytes_pass[1] = cb * (nX1r + nB);
-    c->bytes_pass[2] = cb * (nB + (double)nC) +
-                       8.0 * (double)nkx * (My / 2 + 1) * (c->zdirect ? c->ZU : Mz / 2 + 1) * c->nblk;
+    c->bytes_k3 = 8.0 * (double)nkx * (My / 2 + 1) * (c->zdirect ? c->ZU : Mz / 2 + 1) * c->nblk;
+    c->bytes_pass[2] = cb * (nB + (double)nC) + c->bytes_k3;
     c->bytes_pass[3] = cb * ((double)nC + nX4);
     c->bytes_pass[4] = cb * nX4r + 4.0 * slots_out + 8.0 * NL + (8.0 + 8.0 + 1.0) * ndl + 1.0 * NL;
     double tot = 0;
@@ -1933,7 +1933,13 @@ static vc_status matvec_run(vc_ctx* c, const MV& mv) {
     if (T.ev_ok) VC_CUDA(c, cudaEventRecord(T.ev[11], st));
     count_launch(c, 5 + mv.nb);
     c->stats.n_matvec += mv.nb;
-    for (int p = 0; p < 5; ++p) c->stats.n_pass[p] += 1;
+    for (int p = 0; p < 5; ++p) {
+        c->stats.n_pass[p] += 1;
+        // a batched P3 launch reads the kernel spectra once for its columns (z-FFT mode and
+        // oversized tiles run P3 column by column: nb reads)
+        const bool shared_k = p == 2 && mv.zdirect && mv.nb > 1 && p3d_smem(mv) <= 227 * 1024;
+        c->stats.bytes_moved[p] += mv.nb * c->bytes_pass[p] - (shared_k ? (mv.nb - 1) * c->bytes_k3 : 0.0);
+    }
     if (T.ev_ok) {
         // accumulate device times (waits for this matvec; used only with timing on)
         VC_CUDA(c, cudaEventSynchronize(T.ev[11]));

@@ -106,6 +106,7 @@ void vc_destroy(vc_ctx* c) {
         c->partial.reset();
         c->dvec.reset();
         if (c->h_pinned) cudaFreeHost(c->h_pinned);
+        if (c->h_pinned_multi) cudaFreeHost(c->h_pinned_multi);
         if (c->timing.ev_ok)
             for (auto& e : c->timing.ev) cudaEventDestroy(e);
         if (c->arn_ev_ok)

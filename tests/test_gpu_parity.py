@@ -255,3 +255,18 @@ def test_matvec_batch_bitwise(ctx, name, zmode, nb):
         assert np.array_equal(Y[:, i], ctx.matvec(X[:, i])), (name, i)
     ctx.build_operator(zmode=zmode, batch=False)  # no batch buffers: column by column
     assert np.array_equal(ctx.matvec_batch(X), Y)
+
+
+@pytest.mark.parametrize("name", ["C2", "R1", "R2"])
+def test_capacitance_lockstep_matches_single(ctx, name):
+    """NEXT-3: the lockstep multi-column solve (batched matvecs) runs the same GMRES per column
+    as the one-column solver: same iteration counts, same C to rounding."""
+    st = voxgen.config(name)
+    ctx.set_structure(st)
+    ctx.build_operator()
+    Cb, ib = ctx.solve_capacitance(tol=1e-10, maxit=4000)
+    ctx.build_operator(batch=False)
+    Cs, is_ = ctx.solve_capacitance(tol=1e-10, maxit=4000)
+    assert [i["iters"] for i in ib] == [i["iters"] for i in is_]
+    assert all(i["converged"] for i in ib)
+    assert np.abs(Cb - Cs).max() <= 1e-12 * np.abs(Cs).max()

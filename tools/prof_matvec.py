@@ -13,13 +13,15 @@ import voxgen  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="C4")
 ap.add_argument("--n", type=int, default=5)
+ap.add_argument("--batch", type=int, default=1, help="columns per matvec (vc_matvec_batch)")
 a = ap.parse_args()
 st = voxgen.config(a.config)
 ctx = vc.VoxCap(0)
 ctx.set_structure(st)
 ctx.build_operator()
 x = torch.from_numpy(voxgen.seeded_vector(ctx.n, 0)).cuda()
+X = torch.stack([x] * a.batch, dim=1)
 for _ in range(a.n):
-    y = ctx.matvec(x)
+    y = ctx.matvec(x) if a.batch == 1 else ctx.matvec_batch(X)
 torch.cuda.synchronize()
 print("ok", a.config, ctx.n, ctx.grid(), float(y.abs().sum()))

@@ -15,11 +15,13 @@ namespace vc {
 
 constexpr int ilog2c(int n) { return n <= 1 ? 0 : 1 + ilog2c(n / 2); }
 
-template <int L>
+// MB: largest radix exponent per stage (4: radix <= 16, the default; 3: radix <= 8, more stages
+// but fewer registers per thread)
+template <int L, int MB = 4>
 struct Plan {
     static_assert(L >= 2 && (L & (L - 1)) == 0 && L <= kMaxL, "L must be a power of two");
     static constexpr int B = ilog2c(L);
-    static constexpr int NS = (B + 3) / 4;
+    static constexpr int NS = (B + MB - 1) / MB;
     __host__ __device__ static constexpr int bits(int s) { return B / NS + (s < B % NS ? 1 : 0); }
     __host__ __device__ static constexpr int radix(int s) { return 1 << bits(s); }
     __host__ __device__ static constexpr int lc(int s) {
@@ -169,11 +171,11 @@ template <class X> struct Bare<const X> { using type = X; };
 //   Tn (<= T): pencils actually transformed (the shared-memory layout keeps stride T)
 //   TB > 0 (PF only): Tn is a multiple of the compile-time pencil block TB; lanes take
 //       consecutive pencils within a block, so no division by the run-time Tn is needed
-template <int L, int T, int NT, bool INV, bool PF, int s, int TB = 0, class LD, class ST>
+template <int L, int T, int NT, bool INV, bool PF, int s, int TB = 0, int MB = 4, class LD, class ST>
 __device__ __forceinline__ void fft_stage(LD&& ld, ST&& st, const double2* __restrict__ tw,
                                           const int Tn = T) {
-    constexpr int R = Plan<L>::radix(s);
-    constexpr int Lc = Plan<L>::lc(s);
+    constexpr int R = Plan<L, MB>::radix(s);
+    constexpr int Lc = Plan<L, MB>::lc(s);
     constexpr int S = Lc / R;
     constexpr int TW = kTabN / Lc;
     const int NB = Tn * (L / R);
@@ -242,24 +244,33 @@ __device__ __forceinline__ void fft_stage(LD&& ld, ST&& st, const double2* __res
 // Full transform: stage 0 reads through `ld0`, the last stage writes through `stN`, and the
 // intermediate stages use shared memory `sm` (layout smi<L,T,PF>).  If NS == 1 the single
 // stage goes ld0 -> stN.  No trailing __syncthreads().
-template <int L, int T, int NT, bool INV, bool PF, int TB = 0, bool SWZ = false, class LD, class ST>
+template <int L, int T, int NT, bool INV, bool PF, int TB = 0, bool SWZ = false, int MB = 4,
+          class LD, class ST>
 __device__ __forceinline__ void fft_run(double2* sm, LD&& ld0, ST&& stN,
                                         const double2* __restrict__ tw, const int Tn = T) {
-    constexpr int NS = Plan<L>::NS;
+    constexpr int NS = Plan<L, MB>::NS;
     const SmAcc<L, T, PF, SWZ> lds{sm}, sts{sm};
     if constexpr (NS == 1) {
-        fft_stage<L, T, NT, INV, PF, 0, TB>(ld0, stN, tw, Tn);
+        fft_stage<L, T, NT, INV, PF, 0, TB, MB>(ld0, stN, tw, Tn);
     } else if constexpr (NS == 2) {
-        fft_stage<L, T, NT, INV, PF, 0, TB>(ld0, sts, tw, Tn);
+        fft_stage<L, T, NT, INV, PF, 0, TB, MB>(ld0, sts, tw, Tn);
         __syncthreads();
-        fft_stage<L, T, NT, INV, PF, 1, TB>(lds, stN, tw, Tn);
+        fft_stage<L, T, NT, INV, PF, 1, TB, MB>(lds, stN, tw, Tn);
+    } else if constexpr (NS == 3) {
+        fft_stage<L, T, NT, INV, PF, 0, TB, MB>(ld0, sts, tw, Tn);
+        __syncthreads();
+        fft_stage<L, T, NT, INV, PF, 1, TB, MB>(lds, sts, tw, Tn);
+        __syncthreads();
+        fft_stage<L, T, NT, INV, PF, 2, TB, MB>(lds, stN, tw, Tn);
     } else {
-        static_assert(NS == 3, "L <= 4096");
-        fft_stage<L, T, NT, INV, PF, 0, TB>(ld0, sts, tw, Tn);
+        static_assert(NS == 4, "L <= 4096 with radix >= 8");
+        fft_stage<L, T, NT, INV, PF, 0, TB, MB>(ld0, sts, tw, Tn);
         __syncthreads();
-        fft_stage<L, T, NT, INV, PF, 1, TB>(lds, sts, tw, Tn);
+        fft_stage<L, T, NT, INV, PF, 1, TB, MB>(lds, sts, tw, Tn);
         __syncthreads();
-        fft_stage<L, T, NT, INV, PF, 2, TB>(lds, stN, tw, Tn);
+        fft_stage<L, T, NT, INV, PF, 2, TB, MB>(lds, sts, tw, Tn);
+        __syncthreads();
+        fft_stage<L, T, NT, INV, PF, 3, TB, MB>(lds, stN, tw, Tn);
     }
 }
 

@@ -256,6 +256,8 @@ vc_status matvec_dev(vc_ctx* c, const double* d_x, double* d_y);
 vc_status matvec_batch_dev(vc_ctx* c, int nb, const double* const* d_x, double* const* d_y);
 vc_status precond_build(vc_ctx* c, const int32_t box[3], int kind);
 vc_status precond_apply_dev(vc_ctx* c, const double* d_r, double* d_z);
+// z_q = R r_q for nc columns (two at once share each R row read)
+vc_status precond_apply_multi_dev(vc_ctx* c, int nc, const double* const* d_r, double* const* d_z);
 void precond_free(vc_ctx* c);
 vc_status solve_dev(vc_ctx* c, const double* d_b, double* d_x, const vc_solve_opts* o,
                     vc_solve_info* info);

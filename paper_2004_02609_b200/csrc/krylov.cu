@@ -458,12 +458,22 @@ vc_status solve_multi_dev(vc_ctx* c, int ncol, const double* const* d_b, double*
         }
         if (act.empty()) break;
         if ((s = matvec_batch_dev(c, (int)act.size(), ins.data(), outs.data()))) return s;
+        {  // t = R w for the Arnoldi columns, in one apply
+            const double* pr[kMaxCols];
+            double* pz[kMaxCols];
+            int np = 0;
+            for (int i : act)
+                if (col[i].phase == 1) {
+                    pr[np] = col[i].K.w;
+                    pz[np++] = col[i].K.t;
+                }
+            if (np && (s = precond_apply_multi_dev(c, np, pr, pz))) return s;
+        }
         for (int i : act) {
             Col& C = col[i];
             Krylov& K = C.K;
             if (C.phase == 1) {  // CGS2 of w' = R A v_j against v_0..v_j, as in solve_dev
                 const int j = C.j;
-                if ((s = precond_apply_dev(c, K.w, K.t))) return s;
                 if ((s = K.dots(K.V, j + 1, K.t, C.dh))) return s;
                 k_multiaxpy<<<gn, 256, 0, st>>>(K.t, K.V, n, j + 1, C.dh, n, -1.0);
                 if ((s = K.dots(K.V, j + 1, K.t, C.dh + kMaxBasis))) return s;

@@ -610,9 +610,16 @@ __global__ void k_kgen_oct(double* Ko, int Ox, int Oy, int Oz, int kind, int alp
 
 // preconditioner near-field table: the near corner |t| < T of a P block's octant, evaluated
 // directly (the same kernel for generated and mirrored blocks, so both builds agree bitwise)
-__global__ void k_kgen_corner(double* __restrict__ Tb, int Tx, int Ty, int Tz, int Ox, int Oy,
-                              int Oz, int alpha, int beta, double scale) {
+// All P pairs in one launch (blockIdx.y = pair; the near-field closed forms are long-latency,
+// six small launches in sequence cost 6x one).
+struct CornerPairs {
+    int n, alpha[6], beta[6], slot[6];
+};
+__global__ void k_kgen_corner(double* __restrict__ Tb0, int Tx, int Ty, int Tz, int Ox, int Oy,
+                              int Oz, CornerPairs cp, double scale) {
     const int n = Tx * Ty * Tz;
+    const int alpha = cp.alpha[blockIdx.y], beta = cp.beta[blockIdx.y];
+    double* __restrict__ Tb = Tb0 + (size_t)cp.slot[blockIdx.y] * n;
     for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
         const int ix = e % Tx, iy = (e / Tx) % Ty, iz = e / (Tx * Ty);
         Tb[e] = (ix < Ox && iy < Oy && iz < Oz)
@@ -1535,6 +1542,22 @@ vc_status operator_build(vc_ctx* c, const vc_build_opts* o) {
                     }
             }
         const int NW = zd ? c->ZU : Mz / 2 + 1;
+        {   // preconditioner near-field tables of every P pair, evaluated directly (one launch)
+            CornerPairs cp{};
+            for (int i = 0; i < c->nblk; ++i)
+                if (defs[i].kind == 0) {
+                    cp.alpha[cp.n] = defs[i].alpha;
+                    cp.beta[cp.n] = defs[i].beta;
+                    cp.slot[cp.n] = c->pcPair[defs[i].alpha][defs[i].beta];
+                    ++cp.n;
+                }
+            if (cp.n) {
+                k_kgen_corner<<<dim3((tvol + 127) / 128, cp.n), 128, 0, st>>>(
+                    c->pcTab.p, c->pcTabDim[0], c->pcTabDim[1], c->pcTabDim[2], Ox, Oy, Oz, cp,
+                    c->dv * c->dv * c->dv / fpe);
+                count_launch(c);
+            }
+        }
         for (int pass = 0; pass < 2; ++pass)
         for (int i = 0; i < c->nblk; ++i) {
             const BlkDef& d = defs[i];
@@ -1544,13 +1567,6 @@ vc_status operator_build(vc_ctx* c, const vc_build_opts* o) {
             cudaEvent_t* ev = c->kev.data() + 4 * (size_t)i;
             if (mirror_of[i] >= 0) {
                 VC_CUDA(c, cudaEventRecord(ev[0], st));
-                if (d.kind == 0) {
-                    k_kgen_corner<<<(tvol + 255) / 256, 256, 0, st>>>(
-                        c->pcTab.p + (size_t)c->pcPair[d.alpha][d.beta] * tvol, c->pcTabDim[0],
-                        c->pcTabDim[1], c->pcTabDim[2], Ox, Oy, Oz, d.alpha, d.beta,
-                        c->dv * c->dv * c->dv / fpe);
-                    count_launch(c);
-                }
                 VC_CUDA(c, cudaEventRecord(ev[1], st));
                 VC_CUDA(c, cudaEventRecord(ev[2], st));
                 const int64_t mt = (int64_t)Kx * Kx * NW;
@@ -1561,13 +1577,6 @@ vc_status operator_build(vc_ctx* c, const vc_build_opts* o) {
                 continue;
             }
             VC_CUDA(c, cudaEventRecord(ev[0], st));
-            if (d.kind == 0) {  // preconditioner near-field table, evaluated directly (both paths)
-                k_kgen_corner<<<(tvol + 255) / 256, 256, 0, st>>>(
-                    c->pcTab.p + (size_t)c->pcPair[d.alpha][d.beta] * tvol, c->pcTabDim[0],
-                    c->pcTabDim[1], c->pcTabDim[2], Ox, Oy, Oz, d.alpha, d.beta,
-                    c->dv * c->dv * c->dv / fpe);
-                count_launch(c);
-            }
             const int oblocks = (int)std::min<int64_t>((otot + 127) / 128, 148 * 64);
             k_kgen_oct<<<oblocks, 128, 0, st>>>(Ko.p, Ox, Oy, Oz, d.kind, d.alpha, d.beta, scale);
             const int gblocks = (int)std::min<int64_t>((tot + 255) / 256, 148 * 64);

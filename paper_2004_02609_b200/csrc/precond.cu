@@ -222,28 +222,46 @@ __global__ void __launch_bounds__(256) k_pc_apply_grouped(
 // warp takes rows and reads them straight from the block table (L2-resident: the unique blocks
 // of C4 total ~13 MB), lanes strided over the columns, shuffle-reduced.  No R staging and no
 // per-box serial loop, so every box's latency overlaps (measured against the grouped kernel).
+// NC columns (the lockstep solver's pair): each R row read once for all of them.
 constexpr int kPbRows = 32;
+struct PcCols {
+    const double* r[2];
+    double* z[2];
+};
+template <int NC>
 __global__ void __launch_bounds__(256) k_pc_apply_box(
     const int32_t* __restrict__ tb, const int32_t* __restrict__ tr0,
     const int32_t* __restrict__ bstart, const int32_t* __restrict__ bn,
     const int32_t* __restrict__ buid, const int64_t* __restrict__ uoff,
-    const int32_t* __restrict__ pids, const double* __restrict__ blocks,
-    const double* __restrict__ r, double* __restrict__ z) {
-    extern __shared__ double rb[];
+    const int32_t* __restrict__ pids, const double* __restrict__ blocks, PcCols cols) {
+    extern __shared__ double rb[];  // [NC][n]
     const int b = tb[blockIdx.x], r0 = tr0[blockIdx.x];
     const int n = bn[b], s0 = bstart[b];
     const double* __restrict__ R = blocks + uoff[buid[b]];
-    for (int j = threadIdx.x; j < n; j += blockDim.x) rb[j] = r[pids[s0 + j]];
+    for (int j = threadIdx.x; j < n; j += blockDim.x) {
+        const int p = pids[s0 + j];
+#pragma unroll
+        for (int q = 0; q < NC; ++q) rb[q * n + j] = cols.r[q][p];
+    }
     __syncthreads();
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int r1 = min(n, r0 + kPbRows);
     for (int row = r0 + w; row < r1; row += nw) {
         const double* __restrict__ Rr = R + (int64_t)row * n;
-        double acc = 0.0;
+        double acc[NC];
+#pragma unroll
+        for (int q = 0; q < NC; ++q) acc[q] = 0.0;
 #pragma unroll 8
-        for (int j = lane; j < n; j += 32) acc = fma(__ldg(Rr + j), rb[j], acc);
-        for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (lane == 0) z[pids[s0 + row]] = acc;
+        for (int j = lane; j < n; j += 32) {
+            const double rv = __ldg(Rr + j);
+#pragma unroll
+            for (int q = 0; q < NC; ++q) acc[q] = fma(rv, rb[q * n + j], acc[q]);
+        }
+#pragma unroll
+        for (int q = 0; q < NC; ++q) {
+            for (int o = 16; o; o >>= 1) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], o);
+            if (lane == 0) cols.z[q][pids[s0 + row]] = acc[q];
+        }
     }
 }
 
@@ -495,6 +513,33 @@ vc_status precond_build(vc_ctx* c, const int32_t box_in[3], int kind) {
     return VC_OK;
 }
 
+vc_status precond_apply_multi_dev(vc_ctx* c, int nc, const double* const* d_r, double* const* d_z) {
+    Precond* pc = c->pc;
+    if (!pc) return set_err(c, VC_ERR_STATE, "no preconditioner");
+    static const bool grouped = getenv("VC_PC_GROUPED") != nullptr;
+    if (nc != 2 || pc->kind != 3 || grouped || pc->nbtile == 0) {
+        for (int q = 0; q < nc; ++q) {
+            vc_status s = precond_apply_dev(c, d_r[q], d_z[q]);
+            if (s) return s;
+        }
+        return VC_OK;
+    }
+    cudaStream_t st = c->stream;
+    const int64_t N = c->NL;
+    PcCols cols{};
+    for (int q = 0; q < 2; ++q) {
+        k_pc_diag<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((N + 255) / 256, 148 * 8)), 256, 0, st>>>(N, d_r[q], pc->diag_inv.p, d_z[q]);
+        cols.r[q] = d_r[q];
+        cols.z[q] = d_z[q];
+    }
+    k_pc_apply_box<2><<<pc->nbtile, 256, 2 * sizeof(double) * (size_t)pc->max_n, st>>>(
+        pc->btile_b.p, pc->btile_r0.p, pc->box_start.p, pc->box_n.p, pc->box_uid.p,
+        pc->uniq_off.p, pc->panel_ids.p, pc->blocks.p, cols);
+    count_launch(c, 3);
+    VC_CUDA(c, cudaGetLastError());
+    return VC_OK;
+}
+
 vc_status precond_apply_dev(vc_ctx* c, const double* d_r, double* d_z) {
     Precond* pc = c->pc;
     if (!pc) return set_err(c, VC_ERR_STATE, "no preconditioner");
@@ -504,9 +549,12 @@ vc_status precond_apply_dev(vc_ctx* c, const double* d_r, double* d_z) {
     count_launch(c);
     static const bool grouped = getenv("VC_PC_GROUPED") != nullptr;
     if (pc->kind == 3 && !grouped && pc->nbtile > 0) {
-        k_pc_apply_box<<<pc->nbtile, 256, sizeof(double) * (size_t)pc->max_n, st>>>(
+        PcCols cols{};
+        cols.r[0] = d_r;
+        cols.z[0] = d_z;
+        k_pc_apply_box<1><<<pc->nbtile, 256, sizeof(double) * (size_t)pc->max_n, st>>>(
             pc->btile_b.p, pc->btile_r0.p, pc->box_start.p, pc->box_n.p, pc->box_uid.p,
-            pc->uniq_off.p, pc->panel_ids.p, pc->blocks.p, d_r, d_z);
+            pc->uniq_off.p, pc->panel_ids.p, pc->blocks.p, cols);
         count_launch(c);
     } else if (pc->kind == 3 && pc->ntile > 0) {
         const size_t sh = sizeof(double) * (size_t)(kPcRows + 1) * pc->max_n;

@@ -5,11 +5,13 @@ import csv, io, subprocess, sys
 rep = sys.argv[1]
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
-hdr = rows[0]
+hdr, units = rows[0], rows[1]
+un = dict(zip(hdr, units))
 for r in rows[2:]:
     d = dict(zip(hdr, r))
-    print("==", d["Kernel Name"][:60], "time us", d["gpu__time_duration.sum"],
-          "dram MB r/w", d.get("dram__bytes_read.sum"), d.get("dram__bytes_write.sum"))
+    print("==", d["Kernel Name"][:60], "time", d["gpu__time_duration.sum"], un.get("gpu__time_duration.sum"),
+          "dram r/w", d.get("dram__bytes_read.sum"), un.get("dram__bytes_read.sum"),
+          d.get("dram__bytes_write.sum"), un.get("dram__bytes_write.sum"))
     st = []
     for k, v in d.items():
         if "warps_issue_stalled" in k and k.endswith("_per_issue_active.ratio"):

@@ -764,6 +764,94 @@ __global__ void __launch_bounds__(FY<L>::NT) k_fft_strided(double2* data, int64_
     fft_run<L, T, FY<L>::NT, false, true, 0, true>(sm, ld0, stN, tw);
 }
 
+// Direct-z kernel table in two fused passes (replacing fill -> C2C x -> C2C y -> extract):
+// x stage: the cyclic x/y kernel rows are built from the octant table on the fly (the parity
+// signs of k_kfill2d), two real rows per complex FFT, split R2C -> Gx[u][y][kx < Mx/2 + 1];
+// y stage: C2C along y of this rank's kx columns only, phase-stripped and folded straight into
+// the tile-major table (the store of k_extract2d).  Half the x work, a quarter of the y work
+// and two fewer passes over the grid.
+template <int L>
+__global__ void __launch_bounds__(FX<L>::NT) k_kx_r2c(double2* __restrict__ Gx,
+                                                    const double* __restrict__ Ko, int My, int ZU,
+                                                    int Ox, int Oy, int kind, int alpha, int beta,
+                                                    const double2* __restrict__ tw) {
+    constexpr int T = TX<L>::T, K = L / 2 + 1, NT = FX<L>::NT;
+    extern __shared__ double2 sm[];
+    const int npair = My / 2;
+    const int64_t npen = (int64_t)ZU * npair;
+    const int64_t pair0 = (int64_t)blockIdx.x * T;
+    auto val = [&](int nx, int ny, int u) -> double {
+        const int nn[2] = {nx, ny}, M[2] = {L, My};
+        int o[2];
+        double sg = 1.0;
+        bool zero = false;
+#pragma unroll
+        for (int a = 0; a < 2; ++a) {
+            const int s2 = c2(alpha, a) - c2(beta, a);
+            const int t2 = rep_t2(nn[a], M[a], s2);
+            const int at2 = t2 < 0 ? -t2 : t2;
+            o[a] = s2 == 0 ? at2 / 2 : (at2 - 1) / 2;
+            if (kind == 1 && a == alpha) {
+                if (t2 < 0) sg = -sg;
+                if (s2 == 0 && 2 * nn[a] == M[a]) zero = true;  // unresolvable odd tie
+            }
+        }
+        return zero ? 0.0 : sg * Ko[((int64_t)u * Oy + o[1]) * Ox + o[0]];
+    };
+    auto ld0 = [&](int t, int n) -> double2 {
+        const int64_t pp = pair0 + t;
+        if (pp >= npen) return czero();
+        const int u = (int)(pp / npair), q = (int)(pp % npair);
+        return make_double2(val(n, 2 * q, u), val(n, 2 * q + 1, u));
+    };
+    const SmAcc<L, T, false, false> sts{sm};
+    fft_run<L, T, NT, false, false>(sm, ld0, sts, tw);
+    __syncthreads();
+    for (int e = threadIdx.x; e < T * K; e += NT) {
+        const int t = e / K, k = e % K;
+        const int64_t pp = pair0 + t;
+        if (pp >= npen) continue;
+        const int u = (int)(pp / npair), q = (int)(pp % npair);
+        const double2 zk = sm[smi<L, T, false>(t, Plan<L>::pos(k))];
+        const double2 zm = sm[smi<L, T, false>(t, Plan<L>::pos((L - k) & (L - 1)))];
+        double2* o = Gx + ((int64_t)u * My + 2 * q) * K + k;
+        o[0] = make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y));
+        o[K] = make_double2(0.5 * (zk.y + zm.y), -0.5 * (zk.x - zm.x));
+    }
+}
+
+template <int L>
+__global__ void __launch_bounds__(FY<L>::NT) k_ky_extract(double* __restrict__ R,
+                                                        const double2* __restrict__ Gx, int Mx,
+                                                        int ZU, int kx0, int nkx, int kind,
+                                                        int alpha, int beta,
+                                                        const double2* __restrict__ tw, int blk,
+                                                        int lgT3, int RC) {
+    constexpr int T = TY<L>::T;
+    extern __shared__ double2 sm[];
+    const int Kx = Mx / 2 + 1;
+    const int ntile = (nkx + T - 1) / T;
+    const int u = blockIdx.x / ntile, tile = blockIdx.x % ntile;
+    const int T3 = 1 << lgT3, nt3 = (nkx + T3 - 1) >> lgT3;
+    const int s2x = c2(alpha, 0) - c2(beta, 0), s2y = c2(alpha, 1) - c2(beta, 1);
+    const bool im = kind == 1 && alpha != 2;
+    const double2* __restrict__ col = Gx + (int64_t)u * L * Kx + kx0;
+    auto ld0 = [&](int t, int n) -> double2 {
+        const int kxl = tile * T + t;
+        return kxl < nkx ? col[(int64_t)n * Kx + kxl] : czero();
+    };
+    auto stN = [&](int t, int p, double2 v) {
+        const int kxl = tile * T + t;
+        const int ky = Plan<L>::freq(p);
+        if (kxl >= nkx || 2 * ky > L) return;
+        v = cmul(v, half_phase(tw, (kx0 + kxl) * s2x, Mx, -1));
+        v = cmul(v, half_phase(tw, ky * s2y, L, -1));
+        R[((int64_t)ky * nt3 + (kxl >> lgT3)) * RC + ((int64_t)blk * ZU + u) * T3 + (kxl & (T3 - 1))] =
+            im ? v.y : v.x;
+    };
+    fft_run<L, T, FY<L>::NT, false, true, 0, true>(sm, ld0, stN, tw);
+}
+
 // Folded spectrum of block `blk`, tile-major for P3:
 //   R[(ky' * nt3 + kx / T3) * RC + blk * KZ * T3 + kz' * T3 + kx % T3]
 //     = {Re | Im}(K^(kx, ky', kz') exp(-2 pi i k.(c_a - c_b) / M)) * scale
@@ -1225,6 +1313,34 @@ static cudaError_t launch_fft_lines(double2* d, int L, int64_t nlines, bool inv,
     });
     return cudaGetLastError();
 }
+static cudaError_t launch_kx_r2c(double2* Gx, const double* Ko, int Mx, int My, int ZU, int Ox,
+                                 int Oy, int kind, int alpha, int beta, const double2* tw,
+                                 cudaStream_t st) {
+    VC_DISPATCH_L(Mx, {
+        constexpr int T = TX<LL>::T;
+        const size_t smem = sizeof(double2) * LL * T;
+        cudaError_t e = prep(k_kx_r2c<LL>, smem);
+        if (e) return e;
+        const unsigned grid = (unsigned)(((int64_t)ZU * (My / 2) + T - 1) / T);
+        k_kx_r2c<LL><<<grid, FX<LL>::NT, smem, st>>>(Gx, Ko, My, ZU, Ox, Oy, kind, alpha, beta, tw);
+    });
+    return cudaGetLastError();
+}
+static cudaError_t launch_ky_extract(double* R, const double2* Gx, int Mx, int My, int ZU, int kx0,
+                                     int nkx, int kind, int alpha, int beta, const double2* tw,
+                                     int blk, int lgT3, int RC, cudaStream_t st) {
+    VC_DISPATCH_L(My, {
+        constexpr int T = TY<LL>::T;
+        const size_t smem = sizeof(double2) * LL * T;
+        cudaError_t e = prep(k_ky_extract<LL>, smem);
+        if (e) return e;
+        const unsigned grid = (unsigned)(ZU * ((nkx + T - 1) / T));
+        if (grid) k_ky_extract<LL><<<grid, FY<LL>::NT, smem, st>>>(R, Gx, Mx, ZU, kx0, nkx, kind, alpha,
+                                                                 beta, tw, blk, lgT3, RC);
+    });
+    return cudaGetLastError();
+}
+
 static cudaError_t launch_fft_strided(double2* d, int L, int64_t es, int64_t ncols,
                                       int64_t nbatch, int64_t bs, const double2* tw,
                                       cudaStream_t st) {
@@ -1542,6 +1658,8 @@ vc_status operator_build(vc_ctx* c, const vc_build_opts* o) {
                     }
             }
         const int NW = zd ? c->ZU : Mz / 2 + 1;
+        // direct-z: fused kernel-table stages (VC_KT_LEGACY=1: the fill / FFT / extract chain)
+        const bool fused_kt = !(getenv("VC_KT_LEGACY") && atoi(getenv("VC_KT_LEGACY")));
         {   // preconditioner near-field tables of every P pair, evaluated directly (one launch)
             CornerPairs cp{};
             for (int i = 0; i < c->nblk; ++i)
@@ -1579,6 +1697,17 @@ vc_status operator_build(vc_ctx* c, const vc_build_opts* o) {
             VC_CUDA(c, cudaEventRecord(ev[0], st));
             const int oblocks = (int)std::min<int64_t>((otot + 127) / 128, 148 * 64);
             k_kgen_oct<<<oblocks, 128, 0, st>>>(Ko.p, Ox, Oy, Oz, d.kind, d.alpha, d.beta, scale);
+            if (zd && fused_kt) {  // fused x / y stages (k_kx_r2c, k_ky_extract)
+                VC_CUDA(c, launch_kx_r2c(G.p, Ko.p, M[0], M[1], MZ, Ox, Oy, d.kind, d.alpha, d.beta,
+                                         c->tw.p, st));
+                VC_CUDA(c, cudaEventRecord(ev[1], st));
+                VC_CUDA(c, cudaEventRecord(ev[2], st));
+                VC_CUDA(c, launch_ky_extract(c->Rt.p, G.p, M[0], M[1], MZ, kx0, nkx, d.kind, d.alpha,
+                                             d.beta, c->tw.p, i, ilog2c(c->T3), (int)c->rchunk, st));
+                VC_CUDA(c, cudaEventRecord(ev[3], st));
+                count_launch(c, 3);
+                continue;
+            }
             const int gblocks = (int)std::min<int64_t>((tot + 255) / 256, 148 * 64);
             if (zd)
                 k_kfill2d<<<gblocks, 256, 0, st>>>(G.p, Ko.p, M[0], M[1], MZ, Ox, Oy, d.kind, d.alpha, d.beta);

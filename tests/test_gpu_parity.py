@@ -270,3 +270,18 @@ def test_capacitance_lockstep_matches_single(ctx, name):
     assert [i["iters"] for i in ib] == [i["iters"] for i in is_]
     assert all(i["converged"] for i in ib)
     assert np.abs(Cb - Cs).max() <= 1e-12 * np.abs(Cs).max()
+
+
+@pytest.mark.parametrize("name", ["C2", "R1", "C4"])
+def test_fused_kernel_table_matches_legacy(ctx, name, monkeypatch):
+    """The fused direct-z kernel-table build (R2C x stage from the octant, y stage straight into
+    the folded table) gives the matvec of the fill / C2C / C2C / extract chain to rounding."""
+    st = voxgen.config(name)
+    ctx.set_structure(st)
+    monkeypatch.setenv("VC_KT_LEGACY", "1")
+    ctx.build_operator(zmode=2)
+    x = voxgen.seeded_vector(ctx.n, 19)
+    y0 = ctx.matvec(x)
+    monkeypatch.setenv("VC_KT_LEGACY", "0")
+    ctx.build_operator(zmode=2)
+    assert _rel(ctx.matvec(x), y0) < 1e-13

@@ -285,3 +285,17 @@ def test_fused_kernel_table_matches_legacy(ctx, name, monkeypatch):
     monkeypatch.setenv("VC_KT_LEGACY", "0")
     ctx.build_operator(zmode=2)
     assert _rel(ctx.matvec(x), y0) < 1e-13
+
+
+@pytest.mark.parametrize("zmode", [1, 2])
+def test_capacitance_three_conductors(ctx, zmode):
+    """m = 3 (seeded random structure 8): the lockstep pair (columns 1, 2) plus a single-column
+    solve (column 3) against the dense direct solve; both z modes; Maxwell invariants."""
+    st = voxgen.random_structure(8)
+    p = _setup(ctx, st, zmode=zmode)
+    assert ctx.m == 3
+    C, info = ctx.solve_capacitance(tol=1e-12, maxit=4000)
+    Cref = O.solve_capacitance(p)
+    assert all(i["converged"] for i in info)
+    assert np.abs(C - Cref).max() <= 1e-6 * np.abs(Cref).max(), (C, Cref)
+    assert np.all(np.diag(C) > 0) and np.all(C - np.diag(np.diag(C)) <= 0)

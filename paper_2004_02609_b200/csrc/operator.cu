@@ -528,14 +528,25 @@ __global__ void __launch_bounds__(FX<L>::NT, FX<L>::MINB5) k_p5(MV mv) {
     };
     // the last stage goes to shared memory; the gather then walks each output line with
     // consecutive lanes on consecutive slots (coalesced slot-map reads and y writes; the panel
-    // kind and the dielectric sign come folded into the slot-map entry, common.cuh kSlot*)
-    auto sts = [&](int t, int p, double2 v) { sm[smi<L, T, false>(t, p)] = v; };
-    fft_run<L, T, FX<L>::NT, true, false>(sm, ld0, sts, mv.tw);
-    __syncthreads();
+    // kind and the dielectric sign come folded into the slot-map entry, common.cuh kSlot*).
+    // The 2T slot-map lines are fetched with cp.async before the FFT, so the gather does not
+    // wait on them.
     const int32_t* __restrict__ smap = mv.slotmap[alpha];
     const int Gx = mv.G[alpha][0], Gy = mv.G[alpha][1];
     const int64_t zrow =
         ((int64_t)(z + mv.lo[2]) * Gy + mv.lo[1] + mv.ya[mv.rank]) * Gx + mv.lo[0];
+    int32_t* const ss = reinterpret_cast<int32_t*>(sm + L * T);  // [2T][L]
+    for (int r = 0; r < 2 * T; ++r) {
+        const int q = ch * T + (r >> 1), l = 2 * q - s + (r & 1);
+        if (q >= nyp || l < 0 || l >= nrow) continue;
+        const int32_t* srow = smap + zrow + (int64_t)l * Gx;
+        for (int n = threadIdx.x; n < exo; n += FX<L>::NT) cp_async4(ss + r * L + n, srow + n);
+    }
+    cp_async_commit();
+    auto sts = [&](int t, int p, double2 v) { sm[smi<L, T, false>(t, p)] = v; };
+    fft_run<L, T, FX<L>::NT, true, false>(sm, ld0, sts, mv.tw);
+    cp_async_wait<0>();
+    __syncthreads();
     const int32_t want = kind ? kSlotDiel : 0;
     double* __restrict__ y = mv.ys[blockIdx.z];
     const double* __restrict__ xc = mv.xs[blockIdx.z];
@@ -546,12 +557,11 @@ __global__ void __launch_bounds__(FX<L>::NT, FX<L>::MINB5) k_p5(MV mv) {
         const int q = ch * T + t;
         const int l = 2 * q - s + half;
         if (q >= nyp || l < 0 || l >= nrow) continue;
-        const int32_t* __restrict__ srow = smap + zrow + (int64_t)l * Gx;
         int32_t e[NI];
 #pragma unroll
-        for (int i = 0; i < NI; ++i) {  // all slot-map loads of the line in flight together
+        for (int i = 0; i < NI; ++i) {
             const int n = threadIdx.x + i * FX<L>::NT;
-            e[i] = n < exo ? __ldg(srow + n) : -1;
+            e[i] = n < exo ? ss[r * L + n] : -1;
         }
 #pragma unroll
         for (int i = 0; i < NI; ++i) {
@@ -1286,7 +1296,7 @@ static cudaError_t launch_p5(const MV& mv, cudaStream_t st) {
     VC_DISPATCH_L(mv.Mx, {
         constexpr int T = TX<LL>::T;
         for (int f = 0; f < mv.nf; ++f) maxch = std::max(maxch, ((mv.nr[mv.rank][3 + f] + 2) / 2 + T - 1) / T);
-        const size_t smem = sizeof(double2) * LL * T;
+        const size_t smem = sizeof(double2) * LL * T + sizeof(int32_t) * 2 * T * LL;  // + slot lines
         auto kern = mv.W > 1 ? k_p5<LL, true> : k_p5<LL, false>;
         cudaError_t e = prep(kern, smem);
         if (e) return e;

@@ -7,6 +7,7 @@
 // is tiny and is updated with Givens rotations on the host, one 3*(restart+1)-double device ->
 // host copy per iteration.
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <vector>
 
@@ -78,6 +79,96 @@ __global__ void __launch_bounds__(kRedNT) k_multidot(const double* __restrict__ 
         if (lane == 0) out[i] = v;
     }
     if (threadIdx.x == 0) *ticket = 0u;
+}
+
+// Two lockstep columns in one launch each (blockIdx.z = column; same nv for both): the same
+// per-column arithmetic as k_multidot / k_multiaxpy / k_scale_by_norm (identical summation order,
+// so the lockstep solver stays bitwise equal to the one-column solver), half the launches and a
+// fuller grid.  Per-column partials and tickets.
+struct Cols2 {
+    const double* V[2];
+    const double* w[2];
+    double* out[2];  // dots: outputs; axpy: the updated vectors
+    const double* h[2];
+};
+__global__ void __launch_bounds__(kRedNT) k_multidot2(Cols2 cc, int64_t ldv, int nv, int64_t n,
+                                                      double* __restrict__ partial,
+                                                      unsigned* __restrict__ ticket) {
+    const int z = blockIdx.z;
+    const int g0 = blockIdx.y * kDotG;
+    const int ng = min(kDotG, nv - g0);
+    double* __restrict__ part = partial + (size_t)z * kRedBlocks * kMaxBasis;
+    const double* __restrict__ w = cc.w[z];
+    double acc[kDotG];
+#pragma unroll
+    for (int i = 0; i < kDotG; ++i) acc[i] = 0.0;
+    const double* __restrict__ Vg = cc.V[z] + (int64_t)g0 * ldv;
+#pragma unroll 2
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        const double wk = w[k];
+        if (ng == kDotG) {
+#pragma unroll
+            for (int i = 0; i < kDotG; ++i) acc[i] = fma(Vg[i * ldv + k], wk, acc[i]);
+        } else {
+#pragma unroll
+            for (int i = 0; i < kDotG; ++i)
+                if (i < ng) acc[i] = fma(Vg[i * ldv + k], wk, acc[i]);
+        }
+    }
+    __shared__ double s[kRedNT / 32][kDotG];
+    const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+#pragma unroll
+    for (int i = 0; i < kDotG; ++i) {
+        double v = acc[i];
+        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) s[wp][i] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < ng) {
+        double v = 0.0;
+        for (int q = 0; q < kRedNT / 32; ++q) v += s[q][threadIdx.x];
+        part[(int64_t)blockIdx.x * nv + g0 + threadIdx.x] = v;
+    }
+    __threadfence();
+    __shared__ bool last;
+    if (threadIdx.x == 0) last = atomicAdd(ticket + z, 1u) == gridDim.x * gridDim.y - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    for (int i = wp; i < nv; i += kRedNT / 32) {
+        double v = 0.0;
+        for (int b = lane; b < (int)gridDim.x; b += 32) v += __ldcg(part + (int64_t)b * nv + i);
+        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) cc.out[z][i] = v;
+    }
+    if (threadIdx.x == 0) ticket[z] = 0u;
+}
+
+__global__ void k_multiaxpy2(Cols2 cc, int64_t ldv, int nv, int64_t n, double sgn) {
+    const int z = blockIdx.z;
+    __shared__ double hs[kMaxBasis];
+    if (threadIdx.x < nv) hs[threadIdx.x] = cc.h[z][threadIdx.x];
+    __syncthreads();
+    const double* __restrict__ V = cc.V[z];
+    double* __restrict__ w = cc.out[z];
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        double acc = 0.0;
+        for (int i = 0; i < nv; ++i) acc = fma(hs[i], V[i * ldv + k], acc);
+        w[k] = fma(sgn, acc, w[k]);
+    }
+}
+
+// out[z] = w[z] / sqrt(*h[z])
+__global__ void k_scale_by_norm2(Cols2 cc, int64_t n) {
+    const int z = blockIdx.z;
+    const double s = 1.0 / sqrt(*cc.h[z]);
+    const double* __restrict__ src = cc.w[z];
+    double* __restrict__ dst = cc.out[z];
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+         k += (int64_t)gridDim.x * blockDim.x)
+        dst[k] = src[k] * s;
 }
 
 // w -= sum_i h[i] V[i]   (h on the device)
@@ -169,9 +260,9 @@ struct Krylov {
         }
         if (c->partial.n < (size_t)kRedBlocks * kMaxBasis) VC_CUDA(c, c->partial.alloc((size_t)kRedBlocks * kMaxBasis));
         if (c->dvec.n < 8 * kMaxBasis) VC_CUDA(c, c->dvec.alloc(8 * kMaxBasis));
-        if (!c->ticket.p) {
-            VC_CUDA(c, c->ticket.alloc(1));
-            VC_CUDA(c, cudaMemsetAsync(c->ticket.p, 0, sizeof(unsigned), c->stream));
+        if (c->ticket.n < 2) {
+            VC_CUDA(c, c->ticket.alloc(2));
+            VC_CUDA(c, cudaMemsetAsync(c->ticket.p, 0, 2 * sizeof(unsigned), c->stream));
         }
         if (!c->h_pinned) VC_CUDA(c, cudaMallocHost(&c->h_pinned, 8 * 8 * kMaxBasis));
         V = c->work.p;
@@ -376,11 +467,12 @@ vc_status solve_multi_dev(vc_ctx* c, int ncol, const double* const* d_b, double*
         VC_CUDA(c, c->work.alloc(per * ncol));
         c->work_n = per * ncol;
     }
-    if (c->partial.n < (size_t)kRedBlocks * kMaxBasis) VC_CUDA(c, c->partial.alloc((size_t)kRedBlocks * kMaxBasis));
+    if (c->partial.n < (size_t)kRedBlocks * kMaxBasis * kMaxCols)
+        VC_CUDA(c, c->partial.alloc((size_t)kRedBlocks * kMaxBasis * kMaxCols));
     if (c->dvec.n < (size_t)8 * kMaxBasis * kMaxCols) VC_CUDA(c, c->dvec.alloc((size_t)8 * kMaxBasis * kMaxCols));
-    if (!c->ticket.p) {
-        VC_CUDA(c, c->ticket.alloc(1));
-        VC_CUDA(c, cudaMemsetAsync(c->ticket.p, 0, sizeof(unsigned), st));
+    if (c->ticket.n < 2) {
+        VC_CUDA(c, c->ticket.alloc(2));
+        VC_CUDA(c, cudaMemsetAsync(c->ticket.p, 0, 2 * sizeof(unsigned), st));
     }
     if (!c->h_pinned_multi) VC_CUDA(c, cudaMallocHost(&c->h_pinned_multi, sizeof(double) * 8 * kMaxBasis * kMaxCols));
     if (!c->h_pinned) VC_CUDA(c, cudaMallocHost(&c->h_pinned, 8 * 8 * kMaxBasis));
@@ -469,7 +561,44 @@ vc_status solve_multi_dev(vc_ctx* c, int ncol, const double* const* d_b, double*
                 }
             if (np && (s = precond_apply_multi_dev(c, np, pr, pz))) return s;
         }
+        // both columns in Arnoldi at the same j: the CGS2 kernels run once for the pair
+        static const bool pair_ok = !(getenv("VC_GS_PAIR") && !atoi(getenv("VC_GS_PAIR")));
+        bool pair = pair_ok && act.size() == 2 && col[act[0]].phase == 1 && col[act[1]].phase == 1 &&
+                    col[act[0]].j == col[act[1]].j;
+        if (pair) {
+            Col &A = col[act[0]], &B = col[act[1]];
+            const int nv = A.j + 1;
+            auto cc = [&](const double* v0, const double* v1, const double* w0, const double* w1,
+                          double* o0, double* o1, const double* h0, const double* h1) {
+                Cols2 q;
+                q.V[0] = v0; q.V[1] = v1; q.w[0] = w0; q.w[1] = w1;
+                q.out[0] = o0; q.out[1] = o1; q.h[0] = h0; q.h[1] = h1;
+                return q;
+            };
+            const dim3 gd(kRedBlocks, (nv + kDotG - 1) / kDotG, 2), gd1(kRedBlocks, 1, 2), ga(gn, 1, 2);
+            k_multidot2<<<gd, kRedNT, 0, st>>>(cc(A.K.V, B.K.V, A.K.t, B.K.t, A.dh, B.dh, nullptr, nullptr),
+                                               n, nv, n, c->partial.p, c->ticket.p);
+            k_multiaxpy2<<<ga, 256, 0, st>>>(cc(A.K.V, B.K.V, nullptr, nullptr, A.K.t, B.K.t, A.dh, B.dh),
+                                             n, nv, n, -1.0);
+            k_multidot2<<<gd, kRedNT, 0, st>>>(cc(A.K.V, B.K.V, A.K.t, B.K.t, A.dh + kMaxBasis,
+                                                  B.dh + kMaxBasis, nullptr, nullptr),
+                                               n, nv, n, c->partial.p, c->ticket.p);
+            k_multiaxpy2<<<ga, 256, 0, st>>>(cc(A.K.V, B.K.V, nullptr, nullptr, A.K.t, B.K.t,
+                                                A.dh + kMaxBasis, B.dh + kMaxBasis),
+                                             n, nv, n, -1.0);
+            k_multidot2<<<gd1, kRedNT, 0, st>>>(cc(A.K.t, B.K.t, A.K.t, B.K.t, A.dh + 2 * kMaxBasis,
+                                                   B.dh + 2 * kMaxBasis, nullptr, nullptr),
+                                                n, 1, n, c->partial.p, c->ticket.p);
+            k_scale_by_norm2<<<ga, 256, 0, st>>>(cc(nullptr, nullptr, A.K.t, B.K.t,
+                                                    A.K.V + (size_t)nv * n, B.K.V + (size_t)nv * n,
+                                                    A.dh + 2 * kMaxBasis, B.dh + 2 * kMaxBasis),
+                                                 n);
+            count_launch(c, 6);
+            for (int i : act)
+                VC_CUDA(c, cudaMemcpyAsync(col[i].hp, col[i].dh, 8 * 3 * kMaxBasis, cudaMemcpyDeviceToHost, st));
+        }
         for (int i : act) {
+            if (pair) break;
             Col& C = col[i];
             Krylov& K = C.K;
             if (C.phase == 1) {  // CGS2 of w' = R A v_j against v_0..v_j, as in solve_dev

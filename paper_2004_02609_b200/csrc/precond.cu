@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(512) k_pc_invert(const int32_t* __restrict__ u
 // keeps the matrix symmetric at every step (so half the storage and half the updates of the
 // Gauss-Jordan kernel above), and sweeping every pivot of an SPD block (no pivoting needed)
 // leaves -A^{-1}.  Packed index of (i >= j): i (i + 1) / 2 + j.  Warps take rows, lanes columns.
-__global__ void __launch_bounds__(512) k_pc_sweep(const int32_t* __restrict__ un,
+__global__ void __launch_bounds__(1024) k_pc_sweep(const int32_t* __restrict__ un,
                                                   const int64_t* __restrict__ uoff,
                                                   double* __restrict__ blocks, int smem_elems) {
     extern __shared__ double sh[];
@@ -493,7 +493,7 @@ vc_status precond_build(vc_ctx* c, const int32_t box_in[3], int kind) {
         const size_t cap = (size_t)max_dyn_smem() - 1024;
         const size_t sw = std::min(cap, sizeof(double) * ((size_t)maxn * (maxn + 1) / 2 + maxn));
         if (sw > 48 * 1024) VC_CUDA(c, grant_max_dyn_smem(k_pc_sweep, max_dyn_smem()));
-        k_pc_sweep<<<pc->nuniq, 512, sw, st>>>(pc->uniq_n.p, pc->uniq_off.p, pc->blocks.p,
+        k_pc_sweep<<<pc->nuniq, 1024, sw, st>>>(pc->uniq_n.p, pc->uniq_off.p, pc->blocks.p,
                                                (int)(sw / sizeof(double)));
         if ((size_t)maxn * (maxn + 1) / 2 + maxn > sw / sizeof(double)) {
             const size_t sh = 2 * sizeof(double) * maxn;

@@ -210,6 +210,8 @@ struct vc_ctx {
     vc::DevBuf<unsigned> ticket;  // last-block ticket of the fused multi-dot
     cudaEvent_t arn_ev[2] = {};   // pipelined Arnoldi: coefficients of step j landed on the host
     bool arn_ev_ok = false;
+    cudaEvent_t mc_ev[2] = {};   // lockstep solver: coefficients of the step in parity slot p landed
+    bool mc_ev_ok = false;
 
     // ---- instrumentation ----
     vc_stats stats{};

@@ -7,6 +7,7 @@
 // is tiny and is updated with Givens rotations on the host, one 3*(restart+1)-double device ->
 // host copy per iteration.
 #include <algorithm>
+#include <deque>
 #include <cstdlib>
 #include <cmath>
 #include <vector>
@@ -482,6 +483,7 @@ vc_status solve_multi_dev(vc_ctx* c, int ncol, const double* const* d_b, double*
         std::vector<double> H, cs, sn, g, y;
         double nrb = 0, nb = 0, rre = 1, nr = 0;
         int iters = 0, j = 0, phase = 0;  // phase 0: restart residual, 1: Arnoldi, 2: done
+        double r_prev = 0, r_prev2 = 0;    // residual history (speculation guard)
         bool converged = false;
     };
     std::vector<Col> col(ncol);
@@ -534,104 +536,152 @@ vc_status solve_multi_dev(vc_ctx* c, int ncol, const double* const* d_b, double*
         }
         return VC_OK;
     };
+    // A step = one batched matvec + the per-column work after it, for a list of (column, phase,
+    // j) entries; its coefficients land in parity slot `par` of each column's device / pinned
+    // scratch (3 * kMaxBasis doubles each) and an event marks them.  While step s is in flight
+    // the next Arnoldi step of the same columns is enqueued speculatively (its input v_{j+1} is
+    // produced on the device), unless a column may leave phase 1 (cycle end, maxit, predicted
+    // convergence); entries of a speculative step whose column changed state are discarded.
+    struct Ent { int col, phase, j; };
+    struct Step { std::vector<Ent> ent; int par; };
+    std::deque<Step> q;
+    int par = 0;
+    if (!c->mc_ev_ok) {
+        for (auto& e : c->mc_ev) VC_CUDA(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        c->mc_ev_ok = true;
+    }
     std::vector<const double*> ins;
     std::vector<double*> outs;
-    std::vector<int> act;
-    for (;;) {
-        act.clear();
+    auto enqueue_step = [&](std::vector<Ent> ents) -> vc_status {
+        Step S{std::move(ents), par};
+        par ^= 1;
+        const int sl = S.par * 3 * kMaxBasis;
+        vc_status e;
         ins.clear();
         outs.clear();
-        for (int i = 0; i < ncol; ++i) {
-            Col& C = col[i];
-            if (C.phase == 2) continue;
-            act.push_back(i);
-            ins.push_back(C.phase == 1 ? C.K.V + (size_t)C.j * n : C.K.x);
+        for (const Ent& en : S.ent) {
+            Col& C = col[en.col];
+            ins.push_back(en.phase == 1 ? C.K.V + (size_t)en.j * n : C.K.x);
             outs.push_back(C.K.w);
         }
-        if (act.empty()) break;
-        if ((s = matvec_batch_dev(c, (int)act.size(), ins.data(), outs.data()))) return s;
+        if ((e = matvec_batch_dev(c, (int)S.ent.size(), ins.data(), outs.data()))) return e;
         {  // t = R w for the Arnoldi columns, in one apply
             const double* pr[kMaxCols];
             double* pz[kMaxCols];
             int np = 0;
-            for (int i : act)
-                if (col[i].phase == 1) {
-                    pr[np] = col[i].K.w;
-                    pz[np++] = col[i].K.t;
+            for (const Ent& en : S.ent)
+                if (en.phase == 1) {
+                    pr[np] = col[en.col].K.w;
+                    pz[np++] = col[en.col].K.t;
                 }
-            if (np && (s = precond_apply_multi_dev(c, np, pr, pz))) return s;
+            if (np && (e = precond_apply_multi_dev(c, np, pr, pz))) return e;
         }
         // both columns in Arnoldi at the same j: the CGS2 kernels run once for the pair
         static const bool pair_ok = !(getenv("VC_GS_PAIR") && !atoi(getenv("VC_GS_PAIR")));
-        bool pair = pair_ok && act.size() == 2 && col[act[0]].phase == 1 && col[act[1]].phase == 1 &&
-                    col[act[0]].j == col[act[1]].j;
+        const bool pair = pair_ok && S.ent.size() == 2 && S.ent[0].phase == 1 &&
+                          S.ent[1].phase == 1 && S.ent[0].j == S.ent[1].j;
         if (pair) {
-            Col &A = col[act[0]], &B = col[act[1]];
-            const int nv = A.j + 1;
+            Col &A = col[S.ent[0].col], &B = col[S.ent[1].col];
+            const int nv = S.ent[0].j + 1;
+            double *ha = A.dh + sl, *hb = B.dh + sl;
             auto cc = [&](const double* v0, const double* v1, const double* w0, const double* w1,
                           double* o0, double* o1, const double* h0, const double* h1) {
-                Cols2 q;
-                q.V[0] = v0; q.V[1] = v1; q.w[0] = w0; q.w[1] = w1;
-                q.out[0] = o0; q.out[1] = o1; q.h[0] = h0; q.h[1] = h1;
-                return q;
+                Cols2 qq;
+                qq.V[0] = v0; qq.V[1] = v1; qq.w[0] = w0; qq.w[1] = w1;
+                qq.out[0] = o0; qq.out[1] = o1; qq.h[0] = h0; qq.h[1] = h1;
+                return qq;
             };
             const dim3 gd(kRedBlocks, (nv + kDotG - 1) / kDotG, 2), gd1(kRedBlocks, 1, 2), ga(gn, 1, 2);
-            k_multidot2<<<gd, kRedNT, 0, st>>>(cc(A.K.V, B.K.V, A.K.t, B.K.t, A.dh, B.dh, nullptr, nullptr),
+            k_multidot2<<<gd, kRedNT, 0, st>>>(cc(A.K.V, B.K.V, A.K.t, B.K.t, ha, hb, nullptr, nullptr),
                                                n, nv, n, c->partial.p, c->ticket.p);
-            k_multiaxpy2<<<ga, 256, 0, st>>>(cc(A.K.V, B.K.V, nullptr, nullptr, A.K.t, B.K.t, A.dh, B.dh),
+            k_multiaxpy2<<<ga, 256, 0, st>>>(cc(A.K.V, B.K.V, nullptr, nullptr, A.K.t, B.K.t, ha, hb),
                                              n, nv, n, -1.0);
-            k_multidot2<<<gd, kRedNT, 0, st>>>(cc(A.K.V, B.K.V, A.K.t, B.K.t, A.dh + kMaxBasis,
-                                                  B.dh + kMaxBasis, nullptr, nullptr),
+            k_multidot2<<<gd, kRedNT, 0, st>>>(cc(A.K.V, B.K.V, A.K.t, B.K.t, ha + kMaxBasis,
+                                                  hb + kMaxBasis, nullptr, nullptr),
                                                n, nv, n, c->partial.p, c->ticket.p);
             k_multiaxpy2<<<ga, 256, 0, st>>>(cc(A.K.V, B.K.V, nullptr, nullptr, A.K.t, B.K.t,
-                                                A.dh + kMaxBasis, B.dh + kMaxBasis),
+                                                ha + kMaxBasis, hb + kMaxBasis),
                                              n, nv, n, -1.0);
-            k_multidot2<<<gd1, kRedNT, 0, st>>>(cc(A.K.t, B.K.t, A.K.t, B.K.t, A.dh + 2 * kMaxBasis,
-                                                   B.dh + 2 * kMaxBasis, nullptr, nullptr),
+            k_multidot2<<<gd1, kRedNT, 0, st>>>(cc(A.K.t, B.K.t, A.K.t, B.K.t, ha + 2 * kMaxBasis,
+                                                   hb + 2 * kMaxBasis, nullptr, nullptr),
                                                 n, 1, n, c->partial.p, c->ticket.p);
             k_scale_by_norm2<<<ga, 256, 0, st>>>(cc(nullptr, nullptr, A.K.t, B.K.t,
                                                     A.K.V + (size_t)nv * n, B.K.V + (size_t)nv * n,
-                                                    A.dh + 2 * kMaxBasis, B.dh + 2 * kMaxBasis),
+                                                    ha + 2 * kMaxBasis, hb + 2 * kMaxBasis),
                                                  n);
             count_launch(c, 6);
-            for (int i : act)
-                VC_CUDA(c, cudaMemcpyAsync(col[i].hp, col[i].dh, 8 * 3 * kMaxBasis, cudaMemcpyDeviceToHost, st));
-        }
-        for (int i : act) {
-            if (pair) break;
-            Col& C = col[i];
-            Krylov& K = C.K;
-            if (C.phase == 1) {  // CGS2 of w' = R A v_j against v_0..v_j, as in solve_dev
-                const int j = C.j;
-                if ((s = K.dots(K.V, j + 1, K.t, C.dh))) return s;
-                k_multiaxpy<<<gn, 256, 0, st>>>(K.t, K.V, n, j + 1, C.dh, n, -1.0);
-                if ((s = K.dots(K.V, j + 1, K.t, C.dh + kMaxBasis))) return s;
-                k_multiaxpy<<<gn, 256, 0, st>>>(K.t, K.V, n, j + 1, C.dh + kMaxBasis, n, -1.0);
-                if ((s = K.dots(K.t, 1, K.t, C.dh + 2 * kMaxBasis))) return s;
-                k_scale_by_norm<<<gn, 256, 0, st>>>(K.V + (size_t)(j + 1) * n, K.t, C.dh + 2 * kMaxBasis, n);
-                count_launch(c, 3);
-            } else {  // restart residual r = R (b - A x)
-                k_axpby<<<gn, 256, 0, st>>>(K.w, K.b, 1.0, -1.0, n);
-                count_launch(c);
-                if ((s = precond_apply_dev(c, K.w, K.r))) return s;
-                if ((s = K.dots(K.r, 1, K.r, C.dh + 2 * kMaxBasis))) return s;
+        } else {
+            for (const Ent& en : S.ent) {
+                Col& C = col[en.col];
+                Krylov& K = C.K;
+                double* dh = C.dh + sl;
+                if (en.phase == 1) {  // CGS2 of w' = R A v_j against v_0..v_j, as in solve_dev
+                    const int j = en.j;
+                    if ((e = K.dots(K.V, j + 1, K.t, dh))) return e;
+                    k_multiaxpy<<<gn, 256, 0, st>>>(K.t, K.V, n, j + 1, dh, n, -1.0);
+                    if ((e = K.dots(K.V, j + 1, K.t, dh + kMaxBasis))) return e;
+                    k_multiaxpy<<<gn, 256, 0, st>>>(K.t, K.V, n, j + 1, dh + kMaxBasis, n, -1.0);
+                    if ((e = K.dots(K.t, 1, K.t, dh + 2 * kMaxBasis))) return e;
+                    k_scale_by_norm<<<gn, 256, 0, st>>>(K.V + (size_t)(j + 1) * n, K.t, dh + 2 * kMaxBasis, n);
+                    count_launch(c, 3);
+                } else {  // restart residual r = R (b - A x)
+                    k_axpby<<<gn, 256, 0, st>>>(K.w, K.b, 1.0, -1.0, n);
+                    count_launch(c);
+                    if ((e = precond_apply_dev(c, K.w, K.r))) return e;
+                    if ((e = K.dots(K.r, 1, K.r, dh + 2 * kMaxBasis))) return e;
+                }
             }
-            VC_CUDA(c, cudaMemcpyAsync(C.hp, C.dh, 8 * 3 * kMaxBasis, cudaMemcpyDeviceToHost, st));
         }
-        VC_CUDA(c, cudaStreamSynchronize(st));
-        for (int i : act) {
-            Col& C = col[i];
-            const double* hh = C.hp;
+        for (const Ent& en : S.ent)
+            VC_CUDA(c, cudaMemcpyAsync(col[en.col].hp + sl, col[en.col].dh + sl, 8 * 3 * kMaxBasis,
+                                       cudaMemcpyDeviceToHost, st));
+        VC_CUDA(c, cudaEventRecord(c->mc_ev[S.par], st));
+        q.push_back(std::move(S));
+        return VC_OK;
+    };
+    auto near = [&](const Col& C) {  // residual history predicts convergence at the next step
+        return C.r_prev2 > 0.0 && C.r_prev * (C.r_prev / C.r_prev2) <= 2.0 * tol;
+    };
+    for (;;) {
+        if (q.empty()) {
+            std::vector<Ent> ents;
+            for (int i = 0; i < ncol; ++i)
+                if (col[i].phase != 2) ents.push_back({i, col[i].phase, col[i].j});
+            if (ents.empty()) break;
+            if ((s = enqueue_step(std::move(ents)))) return s;
+        }
+        if (q.size() == 1) {  // speculative next Arnoldi step of the same columns
+            bool spec = true;
+            std::vector<Ent> nxt;
+            int nact = 0;
+            for (int i = 0; i < ncol; ++i) nact += col[i].phase != 2;
+            for (const Ent& en : q.front().ent) {
+                const Col& C = col[en.col];
+                if (en.phase != 1 || en.j + 1 >= restart || C.iters + 1 >= maxit || near(C)) {
+                    spec = false;
+                    break;
+                }
+                nxt.push_back({en.col, 1, en.j + 1});
+            }
+            if (spec && (int)nxt.size() == nact && (s = enqueue_step(std::move(nxt)))) return s;
+        }
+        Step F = std::move(q.front());
+        q.pop_front();
+        VC_CUDA(c, cudaEventSynchronize(c->mc_ev[F.par]));
+        for (const Ent& en : F.ent) {
+            Col& C = col[en.col];
+            if (C.phase != en.phase || (en.phase == 1 && C.j != en.j)) continue;  // stale
+            const double* hh = C.hp + F.par * 3 * kMaxBasis;
             if (C.phase == 1) {
                 const int j = C.j;
                 ++C.iters;
                 double* Hj = C.H.data() + (size_t)j * (restart + 1);
-                for (int q = 0; q <= j; ++q) Hj[q] = hh[q] + hh[kMaxBasis + q];
+                for (int qq = 0; qq <= j; ++qq) Hj[qq] = hh[qq] + hh[kMaxBasis + qq];
                 Hj[j + 1] = std::sqrt(hh[2 * kMaxBasis]);
-                for (int q = 0; q < j; ++q) {
-                    const double a = Hj[q], bb = Hj[q + 1];
-                    Hj[q] = C.cs[q] * a + C.sn[q] * bb;
-                    Hj[q + 1] = -C.sn[q] * a + C.cs[q] * bb;
+                for (int qq = 0; qq < j; ++qq) {
+                    const double a = Hj[qq], bb = Hj[qq + 1];
+                    Hj[qq] = C.cs[qq] * a + C.sn[qq] * bb;
+                    Hj[qq + 1] = -C.sn[qq] * a + C.cs[qq] * bb;
                 }
                 const double a = Hj[j], bb = Hj[j + 1];
                 const double den = std::hypot(a, bb);
@@ -642,10 +692,13 @@ vc_status solve_multi_dev(vc_ctx* c, int ncol, const double* const* d_b, double*
                 C.g[j + 1] = -C.sn[j] * C.g[j];
                 C.g[j] = C.cs[j] * C.g[j];
                 C.rre = std::fabs(C.g[j + 1]) / C.nrb;
+                C.r_prev2 = C.r_prev;
+                C.r_prev = C.rre;
                 C.j = j + 1;
                 const bool nan = !(C.rre == C.rre);
                 if (C.rre <= tol || C.j == restart || C.iters >= maxit || nan) {
                     if ((s = finish_cycle(C))) return s;
+                    C.r_prev = C.r_prev2 = 0.0;
                     if (C.rre <= tol) {
                         C.converged = true;
                         C.phase = 2;

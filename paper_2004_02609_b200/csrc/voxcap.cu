@@ -111,6 +111,8 @@ void vc_destroy(vc_ctx* c) {
             for (auto& e : c->timing.ev) cudaEventDestroy(e);
         if (c->arn_ev_ok)
             for (auto& e : c->arn_ev) cudaEventDestroy(e);
+        if (c->mc_ev_ok)
+            for (auto& e : c->mc_ev) cudaEventDestroy(e);
         for (auto& e : c->kev) cudaEventDestroy(e);
         if (c->own_stream) cudaStreamDestroy(c->stream);
     }

@@ -77,7 +77,13 @@ typedef struct {
                                for 2 columns so vc_solve_capacitance runs its m solves in
                                lockstep with batched matvecs; 1 = one
                                column at a time (less memory)                                 */
-    int32_t reserved[6];
+    int32_t reuse_tables;   /* 1: keep the kernel spectra and preconditioner near-field tables
+                               from the previous build when their signature (grid, z mode,
+                               kernel blocks, tile layout, rank slab, dv, boxes, variants) is
+                               unchanged -- they do not depend on panel positions or on the
+                               permittivities (kept in HBM instead of an
+                               install-time file); 0 = default: always regenerate            */
+    int32_t reserved[5];
 } vc_build_opts;
 
 /* Solve options.  Zero fields take the paper's defaults. */

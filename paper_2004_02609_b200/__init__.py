@@ -44,7 +44,7 @@ class BuildOpts(ctypes.Structure):
     _fields_ = [("pad", ctypes.c_int32 * 3), ("box", ctypes.c_int32 * 3),
                 ("precond", ctypes.c_int32), ("zmode", ctypes.c_int32),
                 ("no_mirror", ctypes.c_int32), ("no_batch", ctypes.c_int32),
-                ("reserved", ctypes.c_int32 * 6)]
+                ("reuse_tables", ctypes.c_int32), ("reserved", ctypes.c_int32 * 5)]
 
 
 class SolveOpts(ctypes.Structure):
@@ -299,13 +299,15 @@ class VoxCap:
         return out
 
     # -- operator ------------------------------------------------------------------------
-    def build_operator(self, pad=None, box=None, precond=3, zmode=0, mirror=True, batch=True):
+    def build_operator(self, pad=None, box=None, precond=3, zmode=0, mirror=True, batch=True,
+                       reuse_tables=False):
         """zmode: 0 automatic, 1 z-FFT (3-D circulant), 2 direct z-convolution; mirror=False
         generates every kernel block (no x<->y transposes)."""
         o = BuildOpts()
         o.zmode = int(zmode)
         o.no_mirror = 0 if mirror else 1
         o.no_batch = 0 if batch else 1
+        o.reuse_tables = 1 if reuse_tables else 0
         if pad is not None:
             for a in range(3):
                 o.pad[a] = int(pad[a])

@@ -150,6 +150,8 @@ struct vc_ctx {
     size_t blk_stride = 0;  // doubles per folded spectrum
     vc::DevBuf<double> Rt;  // folded, phase-stripped, scaled kernel spectra
     vc::DevBuf<double2> tw;  // twiddles exp(-2 pi i n / kTabN)
+    std::vector<double> kt_key;  // signature of the kernel tables in Rt / pcTab (reuse_tables)
+    bool tables_reused = false;
     vc::DevBuf<double2> bufA, bufB, bufC;  // X1/X4, X2, X3 (nbmax column copies each)
     int nbmax = 1;                          // columns one batched matvec may carry (NEXT-3)
     size_t colA = 0, colB = 0, colC = 0;    // per-column strides of bufA / bufB / bufC

@@ -1614,8 +1614,28 @@ vc_status operator_build(vc_ctx* c, const vc_build_opts* o) {
     VC_CUDA(c, c->tw.alloc(kTabN));
     k_twiddles<<<(kTabN + 255) / 256, 256, 0, st>>>(c->tw.p);
     count_launch(c);
-    VC_CUDA(c, c->Rt.alloc(std::max<size_t>(1, c->rchunk * (size_t)(My / 2 + 1) * c->nt3)));
-    VC_CUDA(c, cudaMemsetAsync(c->Rt.p, 0, c->Rt.bytes(), st));
+    // kernel-table reuse (as a device-resident cache): the spectra and the
+    // preconditioner near-field tables depend only on this signature -- grid, z mode, blocks,
+    // tile layout, rank slab, dv, boxes and the build variants -- not on where the panels are or
+    // on the permittivities, so with vc_build_opts.reuse_tables a rebuild on the same signature
+    // keeps the tables already in HBM
+    std::vector<double> key = {(double)M[0], (double)M[1], (double)M[2], (double)c->zdirect,
+                               (double)c->ZU, (double)c->T3, (double)c->rchunk, (double)nkx,
+                               (double)kx0, (double)c->world, (double)c->rank, c->dv,
+                               (double)c->box[0], (double)c->box[1], (double)c->box[2],
+                               (double)(o && o->no_mirror),
+                               (double)(getenv("VC_KT_LEGACY") && atoi(getenv("VC_KT_LEGACY")))};
+    for (const BlkDef& d : defs) {
+        key.push_back(d.kind);
+        key.push_back(d.alpha);
+        key.push_back(d.beta);
+    }
+    const size_t rt_n = std::max<size_t>(1, c->rchunk * (size_t)(My / 2 + 1) * c->nt3);
+    const bool reuse = o && o->reuse_tables && key == c->kt_key && c->Rt.p && c->Rt.n == rt_n;
+    c->kt_key.clear();
+    c->tables_reused = reuse;
+    VC_CUDA(c, c->Rt.alloc(rt_n));
+    if (!reuse) VC_CUDA(c, cudaMemsetAsync(c->Rt.p, 0, c->Rt.bytes(), st));
     // spectra (a2 on the parity octant -> full cyclic grid -> 3-D FFT -> phase strip + fold)
     {
         // no host synchronisation in this loop: the preconditioner's host bookkeeping (next in
@@ -1626,7 +1646,7 @@ vc_status operator_build(vc_ctx* c, const vc_build_opts* o) {
             c->kev.resize(4 * (size_t)std::max(1, c->nblk));
             for (size_t e = n0; e < c->kev.size(); ++e) VC_CUDA(c, cudaEventCreate(&c->kev[e]));
         }
-        c->kev_n = c->nblk;
+        c->kev_n = reuse ? 0 : c->nblk;
         DevBuf<double2>& G = c->kG;
         DevBuf<double>& Ko = c->kKo;
         const bool zd = c->zdirect;
@@ -1635,8 +1655,10 @@ vc_status operator_build(vc_ctx* c, const vc_build_opts* o) {
         const int64_t tot = (int64_t)M[0] * M[1] * MZ;
         const int Ox = M[0] / 2 + 1, Oy = M[1] / 2 + 1, Oz = zd ? c->ZU : M[2] / 2 + 1;
         const int64_t otot = (int64_t)Ox * Oy * Oz;
-        VC_CUDA(c, G.alloc(tot));
-        VC_CUDA(c, Ko.alloc(otot));
+        if (!reuse) {
+            VC_CUDA(c, G.alloc(tot));
+            VC_CUDA(c, Ko.alloc(otot));
+        }
         // preconditioner near-field tables: one per P pair, |t| <= box along each axis
         for (int a = 0; a < 3; ++a) c->pcTabDim[a] = c->box[a] + 1;
         const int tvol = c->pcTabDim[0] * c->pcTabDim[1] * c->pcTabDim[2];
@@ -1650,6 +1672,7 @@ vc_status operator_build(vc_ctx* c, const vc_build_opts* o) {
             }
         VC_CUDA(c, c->pcTab.alloc((size_t)std::max(1, npair) * tvol));
         const double fpe = 4.0 * kPi * kEps0;
+        if (!reuse) {
         // x <-> y mirror pairs (k_rt_mirror): with a square x/y window on one rank, a block whose
         // mirror was listed earlier is transposed from it instead of generated + transformed
         const bool mirror_ok = M[0] == M[1] && c->world == 1 && !(o && o->no_mirror);
@@ -1748,7 +1771,9 @@ vc_status operator_build(vc_ctx* c, const vc_build_opts* o) {
             G.reset();
             Ko.reset();
         }
+        }  // !reuse
         VC_CUDA(c, cudaGetLastError());
+        c->kt_key = key;
     }
     // ---- spatial partition: rank p owns a contiguous range of preconditioner
     // box rows along y, so every R_BD block stays on one rank; window row y -> rank (monotone)

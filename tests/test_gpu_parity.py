@@ -299,3 +299,31 @@ def test_capacitance_three_conductors(ctx, zmode):
     assert all(i["converged"] for i in info)
     assert np.abs(C - Cref).max() <= 1e-6 * np.abs(Cref).max(), (C, Cref)
     assert np.all(np.diag(C) > 0) and np.all(C - np.diag(np.diag(C)) <= 0)
+
+
+def test_reuse_tables(ctx):
+    """NEXT-4: with reuse_tables a rebuild on the same table signature keeps the spectra and
+    near-field tables in HBM (no generation); permittivity changes give the matvec and C of a
+    fresh build bitwise; a different grid regenerates."""
+    st = voxgen.config("C2")
+    ctx.set_structure(st)
+    ctx.build_operator()
+    x = voxgen.seeded_vector(ctx.n, 23)
+    y0 = ctx.matvec(x)
+    ctx.reset_stats()
+    ctx.build_operator(reuse_tables=True)
+    assert ctx.stats()["ms_kgen"] == 0.0  # nothing generated
+    assert np.array_equal(ctx.matvec(x), y0)
+    eps2 = np.where(st.eps > 1.0, 7.5, st.eps)  # same panels, other permittivity
+    ctx.set_geometry(st.label, eps2, st.eps_out, st.dv)
+    ctx.build_operator(reuse_tables=True)
+    y1 = ctx.matvec(x)
+    C1, _ = ctx.solve_capacitance(tol=1e-10)
+    ctx.build_operator()
+    assert np.array_equal(ctx.matvec(x), y1)
+    C2, _ = ctx.solve_capacitance(tol=1e-10)
+    assert np.array_equal(C1, C2)
+    ctx.set_structure(voxgen.config("R1"))  # another grid: tables regenerated
+    ctx.reset_stats()
+    ctx.build_operator(reuse_tables=True)
+    assert ctx.stats()["ms_kgen"] > 0.0

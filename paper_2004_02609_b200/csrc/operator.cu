@@ -607,14 +607,19 @@ __device__ __forceinline__ int oct_D(int i, int alpha, int beta, int a) {
     // |t| = i (s2 = 0) or i + 1/2; slot offset D = t - s
     return s2 == 0 ? i : (s2 > 0 ? i : i + 1);
 }
+// symxy (zz blocks, Ox == Oy): z-normal pairs are symmetric under x <-> y, so only ix <= iy is
+// evaluated and written to both (ix, iy) and (iy, ix)
 __global__ void k_kgen_oct(double* Ko, int Ox, int Oy, int Oz, int kind, int alpha, int beta,
-                           double scale) {
+                           double scale, int symxy) {
     const int64_t tot = (int64_t)Ox * Oy * Oz;
     for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < tot;
          idx += (int64_t)gridDim.x * blockDim.x) {
         const int i[3] = {(int)(idx % Ox), (int)((idx / Ox) % Oy), (int)(idx / ((int64_t)Ox * Oy))};
-        Ko[idx] = scale * kappa(kind, alpha, beta, oct_D(i[0], alpha, beta, 0),
-                                oct_D(i[1], alpha, beta, 1), oct_D(i[2], alpha, beta, 2));
+        if (symxy && i[0] > i[1]) continue;
+        const double v = scale * kappa(kind, alpha, beta, oct_D(i[0], alpha, beta, 0),
+                                       oct_D(i[1], alpha, beta, 1), oct_D(i[2], alpha, beta, 2));
+        Ko[idx] = v;
+        if (symxy && i[0] != i[1]) Ko[((int64_t)i[2] * Oy + i[0]) * Ox + i[1]] = v;
     }
 }
 
@@ -1729,7 +1734,8 @@ vc_status operator_build(vc_ctx* c, const vc_build_opts* o) {
             }
             VC_CUDA(c, cudaEventRecord(ev[0], st));
             const int oblocks = (int)std::min<int64_t>((otot + 127) / 128, 148 * 64);
-            k_kgen_oct<<<oblocks, 128, 0, st>>>(Ko.p, Ox, Oy, Oz, d.kind, d.alpha, d.beta, scale);
+            k_kgen_oct<<<oblocks, 128, 0, st>>>(Ko.p, Ox, Oy, Oz, d.kind, d.alpha, d.beta, scale,
+                                                d.alpha == 2 && d.beta == 2 && Ox == Oy);
             if (zd && fused_kt) {  // fused x / y stages (k_kx_r2c, k_ky_extract)
                 VC_CUDA(c, launch_kx_r2c(G.p, Ko.p, M[0], M[1], MZ, Ox, Oy, d.kind, d.alpha, d.beta,
                                          c->tw.p, st));

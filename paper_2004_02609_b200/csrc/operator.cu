@@ -795,23 +795,38 @@ __global__ void __launch_bounds__(FX<L>::NT) k_kx_r2c(double2* __restrict__ Gx,
     const int npair = My / 2;
     const int64_t npen = (int64_t)ZU * npair;
     const int64_t pair0 = (int64_t)blockIdx.x * T;
-    auto val = [&](int nx, int ny, int u) -> double {
-        const int nn[2] = {nx, ny}, M[2] = {L, My};
-        int o[2];
-        double sg = 1.0;
-        bool zero = false;
-#pragma unroll
-        for (int a = 0; a < 2; ++a) {
-            const int s2 = c2(alpha, a) - c2(beta, a);
-            const int t2 = rep_t2(nn[a], M[a], s2);
+    // x part of the octant mapping per column n, once per CTA: o_x | parity sign (bit 30) |
+    // unresolvable odd tie (bit 31, value 0)
+    int32_t* const xt = reinterpret_cast<int32_t*>(sm + L * T);
+    {
+        const int s2 = c2(alpha, 0) - c2(beta, 0);
+        for (int n = threadIdx.x; n < L; n += NT) {
+            const int t2 = rep_t2(n, L, s2);
             const int at2 = t2 < 0 ? -t2 : t2;
-            o[a] = s2 == 0 ? at2 / 2 : (at2 - 1) / 2;
-            if (kind == 1 && a == alpha) {
-                if (t2 < 0) sg = -sg;
-                if (s2 == 0 && 2 * nn[a] == M[a]) zero = true;  // unresolvable odd tie
+            int e = s2 == 0 ? at2 / 2 : (at2 - 1) / 2;
+            if (kind == 1 && alpha == 0) {
+                if (t2 < 0) e |= 1 << 30;
+                if (s2 == 0 && 2 * n == L) e |= (int)(1u << 31);
             }
+            xt[n] = e;
         }
-        return zero ? 0.0 : sg * Ko[((int64_t)u * Oy + o[1]) * Ox + o[0]];
+        __syncthreads();
+    }
+    auto val = [&](int nx, int ny, int u) -> double {
+        const int s2 = c2(alpha, 1) - c2(beta, 1);
+        const int t2 = rep_t2(ny, My, s2);
+        const int at2 = t2 < 0 ? -t2 : t2;
+        const int oy = s2 == 0 ? at2 / 2 : (at2 - 1) / 2;
+        bool neg = false, zero = false;
+        if (kind == 1 && alpha == 1) {
+            neg = t2 < 0;
+            zero = s2 == 0 && 2 * ny == My;  // unresolvable odd tie
+        }
+        const int e = xt[nx];
+        neg ^= (e >> 30) & 1;
+        zero |= e < 0;
+        const double v = Ko[((int64_t)u * Oy + oy) * Ox + (e & 0x3fffffff)];
+        return zero ? 0.0 : (neg ? -v : v);
     };
     auto ld0 = [&](int t, int n) -> double2 {
         const int64_t pp = pair0 + t;
@@ -1333,7 +1348,7 @@ static cudaError_t launch_kx_r2c(double2* Gx, const double* Ko, int Mx, int My, 
                                  cudaStream_t st) {
     VC_DISPATCH_L(Mx, {
         constexpr int T = TX<LL>::T;
-        const size_t smem = sizeof(double2) * LL * T;
+        const size_t smem = sizeof(double2) * LL * T + sizeof(int32_t) * LL;  // + x table
         cudaError_t e = prep(k_kx_r2c<LL>, smem);
         if (e) return e;
         const unsigned grid = (unsigned)(((int64_t)ZU * (My / 2) + T - 1) / T);

@@ -71,7 +71,7 @@ def build(force=False, verbose=False):
         objs = list(ex.map(comp, _sources()))
     tmp = OUT + f".{os.getpid()}.tmp"
     cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", tmp, *objs,
-           "-lcudart"]
+           "-lcudart", "-lpthread"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr[-4000:]}")

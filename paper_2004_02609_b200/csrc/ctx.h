@@ -258,7 +258,13 @@ vc_status matvec_dev(vc_ctx* c, const double* d_x, double* d_y);
 // y_c = A x_c for c < nb with one launch per pass (kernel spectra read once per P3 tile for all
 // columns); nb <= ctx->nbmax, else (or in z-FFT mode) column by column
 vc_status matvec_batch_dev(vc_ctx* c, int nb, const double* const* d_x, double* const* d_y);
-vc_status precond_build(vc_ctx* c, const int32_t box[3], int kind);
+// preconditioner host bookkeeping (boxes, signatures, unique blocks, tiles), separable so that
+// vc_build_operator can run it on a helper thread beside the kernel-table build
+struct PcPlan;
+PcPlan* pc_plan_new();
+void pc_plan_free(PcPlan* p);
+void pc_plan_compute(const vc_ctx* c, const int32_t box_in[3], int64_t N, PcPlan& P);
+vc_status precond_build(vc_ctx* c, const int32_t box[3], int kind, const PcPlan* pre = nullptr);
 vc_status precond_apply_dev(vc_ctx* c, const double* d_r, double* d_z);
 // z_q = R r_q for nc columns (two at once share each R row read)
 vc_status precond_apply_multi_dev(vc_ctx* c, int nc, const double* const* d_r, double* const* d_z);

@@ -284,34 +284,19 @@ void precond_free(vc_ctx* c) {
     c->pc = nullptr;
 }
 
-vc_status precond_build(vc_ctx* c, const int32_t box_in[3], int kind) {
-    if (!c->pc) c->pc = new Precond();  // kept across builds: its buffers are grow-only
-    Precond* pc = c->pc;
-    pc->kind = kind;
-    pc->nbox = pc->nuniq = pc->max_n = 0;
-    pc->block_doubles = 0;
-    cudaStream_t st = c->stream;
-    HostTrace tr("precond");
-    const int64_t N = c->NL;  // this rank's panels (boxes never straddle ranks)
+// Host bookkeeping of the block-diagonal preconditioner: boxes of the conductor panels,
+// their canonical signatures and the unique blocks (hash-first dedup), the per-box and
+// grouped-apply tile lists.  Pure host work on the immutable panel mirrors, so
+// vc_build_operator runs it on a helper thread beside the kernel-table build (one rank).
+struct PcPlan {
+    int nbox = 0, maxn = 0;
+    int64_t total = 0;
+    std::vector<int32_t> bcount, bstart, sorted, buid, un, ulist_off, uaxis, uslot;
+    std::vector<int64_t> uoff;
+};
+
+void pc_plan_compute(const vc_ctx* c, const int32_t box_in[3], int64_t N, PcPlan& P) {
     auto G = [&](int64_t i) { return c->world > 1 ? c->h_gidx[i] : i; };  // local -> global
-    const double fpe = 4.0 * kPi * kEps0;
-    const double pscale = c->dv * c->dv * c->dv / fpe;
-    // diagonal part (on the device, from the rank's panel arrays)
-    // self term of a unit square (textbook), used only for the diagonal-only option
-    const double pself = pscale * ((4.0 / 3.0) * (1.0 - std::sqrt(2.0)) + 4.0 * std::log(1.0 + std::sqrt(2.0)));
-    VC_CUDA(c, pc->diag_inv.alloc(std::max<int64_t>(1, N)));
-    if (N) {
-        const bool loc = c->world > 1;
-        k_pc_dinv<<<(unsigned)std::min<int64_t>((N + 255) / 256, 148 * 8), 256, 0, st>>>(
-            N, loc ? c->lp.cid.p : c->pan.cid.p, loc ? c->lp.ibar.p : c->pan.ibar.p, kind, pself,
-            pc->diag_inv.p);
-        count_launch(c);
-    }
-    tr.mark("diagonal");
-    if (kind != 3) {
-        VC_CUDA(c, cudaStreamSynchronize(st));
-        return VC_OK;
-    }
     int nv[3], nb[3];
     const int dims[3] = {c->nx, c->ny, c->nz};
     for (int a = 0; a < 3; ++a) {
@@ -342,7 +327,6 @@ vc_status precond_build(vc_ctx* c, const int32_t box_in[3], int kind) {
         pb[q] = bi;
     }
     const int nbox = (int)box_keys.size();
-    tr.mark("box assignment");
     std::vector<int32_t> bcount(nbox, 0), bstart(nbox + 1, 0);
     for (int32_t b : pb) bcount[b]++;
     for (int b = 0; b < nbox; ++b) bstart[b + 1] = bstart[b] + bcount[b];
@@ -401,6 +385,56 @@ vc_status precond_build(vc_ctx* c, const int32_t box_in[3], int kind) {
         }
         buid[b] = id;
     }
+    P.nbox = nbox;
+    P.maxn = maxn;
+    P.total = total;
+    P.bcount = std::move(bcount);
+    P.bstart = std::move(bstart);
+    P.sorted = std::move(sorted);
+    P.buid = std::move(buid);
+    P.un = std::move(un);
+    P.ulist_off = std::move(ulist_off);
+    P.uaxis = std::move(uaxis);
+    P.uslot = std::move(uslot);
+    P.uoff = std::move(uoff);
+}
+
+vc_status precond_build(vc_ctx* c, const int32_t box_in[3], int kind, const PcPlan* pre) {
+    if (!c->pc) c->pc = new Precond();  // kept across builds: its buffers are grow-only
+    Precond* pc = c->pc;
+    pc->kind = kind;
+    pc->nbox = pc->nuniq = pc->max_n = 0;
+    pc->block_doubles = 0;
+    cudaStream_t st = c->stream;
+    HostTrace tr("precond");
+    const int64_t N = c->NL;  // this rank's panels (boxes never straddle ranks)
+    const double fpe = 4.0 * kPi * kEps0;
+    const double pscale = c->dv * c->dv * c->dv / fpe;
+    // diagonal part (on the device, from the rank's panel arrays)
+    // self term of a unit square (textbook), used only for the diagonal-only option
+    const double pself = pscale * ((4.0 / 3.0) * (1.0 - std::sqrt(2.0)) + 4.0 * std::log(1.0 + std::sqrt(2.0)));
+    VC_CUDA(c, pc->diag_inv.alloc(std::max<int64_t>(1, N)));
+    if (N) {
+        const bool loc = c->world > 1;
+        k_pc_dinv<<<(unsigned)std::min<int64_t>((N + 255) / 256, 148 * 8), 256, 0, st>>>(
+            N, loc ? c->lp.cid.p : c->pan.cid.p, loc ? c->lp.ibar.p : c->pan.ibar.p, kind, pself,
+            pc->diag_inv.p);
+        count_launch(c);
+    }
+    tr.mark("diagonal");
+    if (kind != 3) {
+        VC_CUDA(c, cudaStreamSynchronize(st));
+        return VC_OK;
+    }
+    PcPlan own;
+    if (!pre) pc_plan_compute(c, box_in, N, own);
+    const PcPlan& P = pre ? *pre : own;
+    const int nbox = P.nbox, maxn = P.maxn;
+    const int64_t total = P.total;
+    const std::vector<int32_t>&bcount = P.bcount, &bstart = P.bstart, &sorted = P.sorted,
+                          &buid = P.buid, &un = P.un, &ulist_off = P.ulist_off,
+                          &uaxis = P.uaxis, &uslot = P.uslot;
+    const std::vector<int64_t>& uoff = P.uoff;
     tr.mark("signatures");
     if (tr.on) {
         double f3 = 0;
@@ -569,4 +603,9 @@ vc_status precond_apply_dev(vc_ctx* c, const double* d_r, double* d_z) {
     return VC_OK;
 }
 
+}  // namespace vc
+
+namespace vc {
+PcPlan* pc_plan_new() { return new PcPlan(); }
+void pc_plan_free(PcPlan* p) { delete p; }
 }  // namespace vc

@@ -1,3 +1,5 @@
+#include <memory>
+#include <thread>
 #include <vector>
 // voxcap.cu -- the C ABI of libvoxcap.so (include/voxcap.h).  Argument checking, state
 // machine, host<->device marshalling; every step of the path runs in the kernels of
@@ -232,10 +234,19 @@ vc_status vc_build_operator(vc_ctx* c, const vc_build_opts* o) {
     VC_CUDA(c, cudaEventCreate(&e1));
     VC_CUDA(c, cudaEventCreate(&e2));
     VC_CUDA(c, cudaEventRecord(e0, c->stream));
+    // one rank: the preconditioner's host bookkeeping runs on a helper thread while this thread
+    // builds the operator and enqueues the kernel tables (it reads only the panel mirrors of
+    // vc_set_geometry, which the build does not touch)
+    const bool async_plan = kind == 3 && c->world == 1;
+    std::unique_ptr<PcPlan, void (*)(PcPlan*)> plan_own(async_plan ? pc_plan_new() : nullptr, pc_plan_free);
+    PcPlan* plan = plan_own.get();
+    std::thread planner;
+    if (async_plan) planner = std::thread([c, &box, plan] { pc_plan_compute(c, box, c->N, *plan); });
     vc_status s = operator_build(c, o);
+    if (planner.joinable()) planner.join();
     if (s == VC_OK) {
         VC_CUDA(c, cudaEventRecord(e1, c->stream));
-        s = precond_build(c, box, kind);
+        s = precond_build(c, box, kind, plan);
         VC_CUDA(c, cudaEventRecord(e2, c->stream));
     }
     if (s == VC_OK) {

@@ -327,3 +327,20 @@ def test_reuse_tables(ctx):
     ctx.reset_stats()
     ctx.build_operator(reuse_tables=True)
     assert ctx.stats()["ms_kgen"] > 0.0
+
+
+@pytest.mark.parametrize("restart,maxit", [(5, 4000), (3, 40)])
+def test_lockstep_restarts_and_maxit(ctx, restart, maxit):
+    """The pipelined lockstep solver across many restart cycles (restart 5) and stopped by maxit
+    (restart 3, 40 iterations: not converged): the same iterations, residuals and C as the
+    one-column solver (speculative steps of columns that restarted or stopped are discarded)."""
+    st = voxgen.config("R1")
+    ctx.set_structure(st)
+    ctx.build_operator()
+    Cb, ib = ctx.solve_capacitance(tol=1e-10, restart=restart, maxit=maxit)
+    ctx.build_operator(batch=False)
+    Cs, is_ = ctx.solve_capacitance(tol=1e-10, restart=restart, maxit=maxit)
+    assert [i["iters"] for i in ib] == [i["iters"] for i in is_]
+    assert [i["converged"] for i in ib] == [i["converged"] for i in is_]
+    assert np.allclose([i["rre_prec"] for i in ib], [i["rre_prec"] for i in is_], rtol=1e-6, atol=0)
+    assert np.abs(Cb - Cs).max() <= 1e-12 * np.abs(Cs).max()

@@ -109,10 +109,10 @@ template <int L> struct TX { static constexpr int T = FX<L>::T; };
 template <int L> struct TY { static constexpr int T = FY<L>::T; };
 constexpr int kNT = 256;
 constexpr int kNT3 = 256;  // P3 threads per CTA
-constexpr int kMaxLz = 256;
+constexpr int kMaxLz = 256;  // largest z FFT length (P3 keeps whole z-pencils in shared memory)
 constexpr int kDirectT = 16;  // P3 direct-z tile width (kx per tile = lanes per output group)
 constexpr int kZB = 4;       // P3 direct-z: output planes per thread
-constexpr int kP3dStages = 2;  // P3 direct-z TMA stages (measured: 2 beat 1 stage + more CTAs)  // largest z FFT length (P3 keeps whole z-pencils in shared memory)
+constexpr int kP3dStages = 2;  // P3 direct-z TMA stages (measured: 2 beat 1 stage + more CTAs)
 
 __device__ __forceinline__ int ktil(int k, int M) { return k <= M / 2 ? k : k - M; }
 

@@ -160,6 +160,11 @@ struct vc_ctx {
     bool zdirect = false;  // P3 direct-z mode (operator.cu k_p3d)
     int ZU = 0, nog = 0, og_f[64] = {}, og_j[64] = {};
     unsigned long long og_contig = 0;  // k_p3d groups with consecutive output planes
+    // k_p3d: octant-offset table of the (output group, source) pairs with non-consecutive planes
+    // ([ji][kZB] int16: u | sign << 15), start per pair (-1: windowed or absent)
+    vc::DevBuf<int16_t> p3tab;
+    int p3tabo[64][3] = {};
+    int p3tab_n = 0;
     int src_contig = 0;                // sources with consecutive planes
     std::vector<int32_t> h_planes;     // host copy of the plane lists
     size_t rchunk = 0;     // doubles of R per P3 tile

@@ -71,6 +71,8 @@ struct MV {
     // P3 direct-z mode: output groups (field, first plane) of kZB planes each
     int zdirect, ZU, nog;
     int og_f[kMaxOG], og_j[kMaxOG];
+    const int16_t* p3tab;  // see vc_ctx::p3tab
+    int p3tabo[kMaxOG][3], p3tab_n;
     unsigned long long og_contig;  // bit og: the group's output planes are consecutive
     int src_contig;                // bit b: source b's planes are consecutive
 };
@@ -1020,24 +1022,25 @@ static cudaError_t launch_p2(const MV& mv, cudaStream_t st) {
 // Thread = (kx t, output group of kZB planes of one field) computing both ky sides; Q loads are
 // shared by all groups of a warp (broadcast), rows of T kx are contiguous (tile-major X2, K).
 // ---------------------------------------------------------------------------------------
-// Accumulate NZO output planes (both ky sides) of one field over the n input planes of one
-// source: a[k] += K(u(zo_k - zi)) Q(zi), with zo2[k] = 2 zo_k + s2 and zi2 = 2 zi, so the
-// doubled geometric offset is one subtraction; ODD: the E^{z.} blocks, odd in z.
+// Non-consecutive planes (any output group or source whose plane list has gaps): the octant
+// offsets u(zo_k - zi) and the odd-kernel signs come precomputed from vc_ctx::p3tab, four int16
+// entries per input plane read with one 8-byte shared-memory load (a[k] += K(u) Q(zi)).
 template <int NZO, bool ODD, int T>
-__device__ __forceinline__ void p3d_acc(double2 (&a0)[kZB], double2 (&a1)[kZB],
-                                        const int (&zo2)[kZB], int s2a, const double* Kb,
-                                        const double2* X, int n, const int* zi2) {
+__device__ __forceinline__ void p3d_acc_tab(double2 (&a0)[kZB], double2 (&a1)[kZB],
+                                            const int16_t* tb, const double* Kb, const double2* X,
+                                            int n) {
     const double2* X1 = X + n * T;  // side 1 rows (unused when nside = 1)
 #pragma unroll 2
     for (int ji = 0; ji < n; ++ji, X += T, X1 += T) {
-        const int z2 = zi2[ji];
+        const int2 pk = *reinterpret_cast<const int2*>(tb + kZB * ji);
         const double2 q0 = *X;
         const double2 q1 = *X1;
 #pragma unroll
         for (int k = 0; k < NZO; ++k) {
-            const int g2 = zo2[k] - z2;
-            double kv = Kb[(((g2 < 0 ? -g2 : g2) - s2a) >> 1) * T];
-            if (ODD) kv = g2 < 0 ? -kv : kv;
+            const int w32 = k < 2 ? pk.x : pk.y;
+            const int e = (k & 1) ? (w32 >> 16) : ((w32 << 16) >> 16);  // sign-extended int16
+            double kv = Kb[(e & 0x7fff) * T];
+            if (ODD) kv = e < 0 ? -kv : kv;
             a0[k].x = fma(kv, q0.x, a0[k].x);
             a0[k].y = fma(kv, q0.y, a0[k].y);
             a1[k].x = fma(kv, q1.x, a1[k].x);
@@ -1101,6 +1104,8 @@ __global__ void __launch_bounds__(512) k_p3d(MV mv) {
     double* kin = reinterpret_cast<double*>(xin + NST * NB * XS);  // [NST][RC]
     int* zl = reinterpret_cast<int*>(kin + NST * RC);           // [9][ZL] plane lists
     uint64_t* bar = reinterpret_cast<uint64_t*>(zl + ((9 * ZL + 3) & ~3));  // [2]
+    int16_t* ptab = reinterpret_cast<int16_t*>(bar + 2);                    // [p3tab_n]
+    for (int e = threadIdx.x; e < mv.p3tab_n; e += blockDim.x) ptab[e] = mv.p3tab[e];
     if (threadIdx.x == 0) {
         mbar_init(&bar[0], 1);
         mbar_init(&bar[1], 1);
@@ -1180,19 +1185,22 @@ __global__ void __launch_bounds__(512) k_p3d(MV mv) {
                             default: p3d_acc_win<4, false, T>(a0, a1, G0, s2a, Kb, X, nzb); break;
                         }
                     }
-                } else if (kind == 1 && alpha == 2) {  // E^{z.}: odd in z
-                    switch (nzo) {
-                        case 1: p3d_acc<1, true, T>(a0, a1, zo2, s2a, Kb, X, nzb, zi2); break;
-                        case 2: p3d_acc<2, true, T>(a0, a1, zo2, s2a, Kb, X, nzb, zi2); break;
-                        case 3: p3d_acc<3, true, T>(a0, a1, zo2, s2a, Kb, X, nzb, zi2); break;
-                        default: p3d_acc<4, true, T>(a0, a1, zo2, s2a, Kb, X, nzb, zi2); break;
-                    }
                 } else {
-                    switch (nzo) {
-                        case 1: p3d_acc<1, false, T>(a0, a1, zo2, s2a, Kb, X, nzb, zi2); break;
-                        case 2: p3d_acc<2, false, T>(a0, a1, zo2, s2a, Kb, X, nzb, zi2); break;
-                        case 3: p3d_acc<3, false, T>(a0, a1, zo2, s2a, Kb, X, nzb, zi2); break;
-                        default: p3d_acc<4, false, T>(a0, a1, zo2, s2a, Kb, X, nzb, zi2); break;
+                    const int16_t* tb = ptab + mv.p3tabo[og][b];
+                    if (kind == 1 && alpha == 2) {  // E^{z.}: odd in z
+                        switch (nzo) {
+                            case 1: p3d_acc_tab<1, true, T>(a0, a1, tb, Kb, X, nzb); break;
+                            case 2: p3d_acc_tab<2, true, T>(a0, a1, tb, Kb, X, nzb); break;
+                            case 3: p3d_acc_tab<3, true, T>(a0, a1, tb, Kb, X, nzb); break;
+                            default: p3d_acc_tab<4, true, T>(a0, a1, tb, Kb, X, nzb); break;
+                        }
+                    } else {
+                        switch (nzo) {
+                            case 1: p3d_acc_tab<1, false, T>(a0, a1, tb, Kb, X, nzb); break;
+                            case 2: p3d_acc_tab<2, false, T>(a0, a1, tb, Kb, X, nzb); break;
+                            case 3: p3d_acc_tab<3, false, T>(a0, a1, tb, Kb, X, nzb); break;
+                            default: p3d_acc_tab<4, false, T>(a0, a1, tb, Kb, X, nzb); break;
+                        }
                     }
                 }
             }
@@ -1221,7 +1229,7 @@ __global__ void __launch_bounds__(512) k_p3d(MV mv) {
 static size_t p3d_smem(const MV& mv) {
     return kP3dStages * (16 * (size_t)2 * kDirectT * (mv.nzin[0] + mv.nzin[1] + mv.nzin[2]) * mv.nb +
                          8 * (size_t)mv.rchunk) +
-           4 * (size_t)((9 * mv.ZL + 3) & ~3) + 2 * sizeof(uint64_t);
+           4 * (size_t)((9 * mv.ZL + 3) & ~3) + 2 * sizeof(uint64_t) + 2 * (size_t)mv.p3tab_n + 16;
 }
 static cudaError_t launch_p3d(const MV& mv, cudaStream_t st) {
     const int nt3 = (mv.nkx + kDirectT - 1) / kDirectT;
@@ -1230,9 +1238,8 @@ static cudaError_t launch_p3d(const MV& mv, cudaStream_t st) {
     const int ogs = std::min(mv.nog, 256 / kDirectT);
     const int nthr = kDirectT * ogs * mv.nb;
     constexpr int NST = kP3dStages;
-    const size_t smem = NST * (16 * (size_t)2 * kDirectT * (mv.nzin[0] + mv.nzin[1] + mv.nzin[2]) * mv.nb +
-                               8 * (size_t)mv.rchunk) +
-                        4 * (size_t)((9 * mv.ZL + 3) & ~3) + 2 * sizeof(uint64_t);
+    static_assert(kP3dStages == NST, "p3d_smem uses kP3dStages");
+    const size_t smem = p3d_smem(mv);
     if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
     cudaError_t e = prep(k_p3d<NST>, smem);
     if (e) return e;
@@ -1622,6 +1629,30 @@ vc_status operator_build(vc_ctx* c, const vc_build_opts* o) {
             for (int b = 0; b < 3; ++b)
                 if (c->nzin[b] > 0 && plane(b, c->nzin[b] - 1) - plane(b, 0) == c->nzin[b] - 1)
                     c->src_contig |= 1 << b;
+            // octant-offset table of the pairs k_p3d cannot window (non-consecutive planes)
+            std::vector<int16_t> tab;
+            for (int g = 0; g < c->nog; ++g)
+                for (int b = 0; b < 3; ++b) {
+                    c->p3tabo[g][b] = -1;
+                    const int f = c->og_f[g];
+                    if (f < 0 || c->blk[f][b] < 0) continue;
+                    if (((c->og_contig >> g) & 1) && ((c->src_contig >> b) & 1)) continue;
+                    const int nzo = std::min(kZB, c->nzout[f] - c->og_j[g]);
+                    const int s2 = c2(c->f[f].axis, 2) - c2(b, 2), s2a = s2 != 0;
+                    c->p3tabo[g][b] = (int)tab.size();
+                    for (int j = 0; j < c->nzin[b]; ++j)
+                        for (int k = 0; k < kZB; ++k) {
+                            const int zo2 = 2 * (k < nzo ? plane(3 + f, c->og_j[g] + k) : 0) + s2;
+                            const int g2 = zo2 - 2 * plane(b, j);
+                            const int u = ((g2 < 0 ? -g2 : g2) - s2a) >> 1;
+                            tab.push_back((int16_t)(u | (g2 < 0 ? 0x8000 : 0)));
+                        }
+                }
+            c->p3tab_n = (int)tab.size();
+            VC_CUDA(c, c->p3tab.alloc(std::max<size_t>(4, tab.size())));
+            if (!tab.empty())
+                VC_CUDA(c, cudaMemcpyAsync(c->p3tab.p, tab.data(), 2 * tab.size(), cudaMemcpyHostToDevice, st));
+            VC_CUDA(c, cudaStreamSynchronize(st));
         }
     }
     // P3 tile width and the tile-major spectrum layout (one contiguous chunk per P3 tile)
@@ -2045,6 +2076,10 @@ static MV make_mv(vc_ctx* c, const double* x, double* y) {
     mv.ZU = c->ZU;
     mv.nog = c->nog;
     mv.og_contig = c->og_contig;
+    mv.p3tab = c->p3tab.p;
+    mv.p3tab_n = c->p3tab_n;
+    for (int g = 0; g < kMaxOG; ++g)
+        for (int b = 0; b < 3; ++b) mv.p3tabo[g][b] = g < c->nog ? c->p3tabo[g][b] : -1;
     mv.src_contig = c->src_contig;
     for (int g = 0; g < c->nog; ++g) {
         mv.og_f[g] = c->og_f[g];

@@ -1434,6 +1434,7 @@ static int next_pow2(int v) {
 
 vc_status operator_build(vc_ctx* c, const vc_build_opts* o) {
     cudaStream_t st = c->stream;
+    HostTrace tr("operator");
     // window origin and per-orientation extents
     int lo[3] = {INT32_MAX, INT32_MAX, INT32_MAX};
     bool has[2][3] = {{false, false, false}, {false, false, false}};
@@ -1655,6 +1656,7 @@ vc_status operator_build(vc_ctx* c, const vc_build_opts* o) {
             VC_CUDA(c, cudaStreamSynchronize(st));
         }
     }
+    tr.mark("plans");
     // P3 tile width and the tile-major spectrum layout (one contiguous chunk per P3 tile)
     c->T3 = c->zdirect ? kDirectT : p3_tile(Mz, c->nf);
     plan_kx_slabs(c->world, Kx, c->T3, c->kxa);
@@ -1827,6 +1829,7 @@ vc_status operator_build(vc_ctx* c, const vc_build_opts* o) {
         VC_CUDA(c, cudaGetLastError());
         c->kt_key = key;
     }
+    tr.mark("kernel tables enqueued");
     // ---- spatial partition: rank p owns a contiguous range of preconditioner
     // box rows along y, so every R_BD block stays on one rank; window row y -> rank (monotone)
     int EY = 1;
@@ -1881,7 +1884,12 @@ vc_status operator_build(vc_ctx* c, const vc_build_opts* o) {
     c->colB = std::max<size_t>(1, nBt);
     c->colC = std::max<size_t>(1, nC);
     c->nbmax = 1;
-    if (W == 1 && c->m >= 2 && !(o && o->no_batch)) {
+    const int nbw = std::min(kMaxB, c->m);
+    if (W == 1 && c->m >= 2 && !(o && o->no_batch) && c->bufA.cap >= c->colA * nbw &&
+        c->bufB.cap >= c->colB * nbw && c->bufC.cap >= c->colC * nbw) {
+        c->nbmax = nbw;  // the buffers already hold nbw columns (no memory query: it can stall
+                         // behind the kernel-table work just enqueued)
+    } else if (W == 1 && c->m >= 2 && !(o && o->no_batch)) {
         size_t fr = 0, totm = 0;
         cudaMemGetInfo(&fr, &totm);
         const size_t percol = sizeof(double2) * (c->colA + c->colB + c->colC);
@@ -1942,8 +1950,11 @@ vc_status operator_build(vc_ctx* c, const vc_build_opts* o) {
         nX4r += (double)c->nzout[f] * c->nr[rk][3 + f] * Kx;  // P5 reads
     }
     const double NL = (double)c->NL;
-    double ndl = 0;
-    for (int64_t i = 0; i < c->NL; ++i) ndl += c->h_cid[W > 1 ? c->h_gidx[i] : i] == 0;
+    double ndl = (double)c->Nd;  // one rank: every dielectric panel
+    if (W > 1) {
+        ndl = 0;
+        for (int64_t i = 0; i < c->NL; ++i) ndl += c->h_cid[c->h_gidx[i]] == 0;
+    }
     c->bytes_pass[0] = cb * nX1 + 4.0 * slots + 8.0 * NL;
     c->bytes_pass[1] = cb * (nX1r + nB);
     c->bytes_k3 = 8.0 * (double)nkx * (My / 2 + 1) * (c->zdirect ? c->ZU : Mz / 2 + 1) * c->nblk;
@@ -1956,6 +1967,7 @@ vc_status operator_build(vc_ctx* c, const vc_build_opts* o) {
         tot += c->bytes_pass[p];
     }
     c->stats.bytes_matvec = tot;
+    tr.mark("buffers + partition + bytes");
     return VC_OK;
 }
 

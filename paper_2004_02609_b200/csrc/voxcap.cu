@@ -243,7 +243,11 @@ vc_status vc_build_operator(vc_ctx* c, const vc_build_opts* o) {
     std::thread planner;
     if (async_plan) planner = std::thread([c, &box, plan] { pc_plan_compute(c, box, c->N, *plan); });
     vc_status s = operator_build(c, o);
-    if (planner.joinable()) planner.join();
+    {
+        HostTrace tj("build_operator");
+        if (planner.joinable()) planner.join();
+        tj.mark("join planner");
+    }
     if (s == VC_OK) {
         VC_CUDA(c, cudaEventRecord(e1, c->stream));
         s = precond_build(c, box, kind, plan);

@@ -137,6 +137,7 @@ struct vc_ctx {
     vc::PinnedVec<int8_t> h_axis, h_sign;
     vc::PinnedVec<int32_t> h_si, h_sj, h_sk, h_cid;
     vc::PinnedVec<double> h_ibar;
+    vc::PinnedVec<char> pc_stage;  // pinned staging of the preconditioner uploads
 
     // ---- operator (vc_build_operator) ----
     bool has_op = false;

@@ -462,8 +462,19 @@ vc_status precond_build(vc_ctx* c, const int32_t box_in[3], int kind, const PcPl
     VC_CUDA(c, pc->uniq_axis.alloc(std::max<size_t>(1, uaxis.size())));
     VC_CUDA(c, pc->uniq_slot.alloc(std::max<size_t>(1, uslot.size())));
     VC_CUDA(c, pc->blocks.alloc(std::max<int64_t>(1, total)));
+    // uploads are gathered into one host staging area and sent from pinned memory in one batch
+    // of async copies (a pageable cudaMemcpyAsync synchronises the stream first: sixteen of them
+    // serialised the host behind the kernel tables)
+    std::vector<char> stage;
+    std::vector<std::pair<void*, std::pair<size_t, size_t>>> ups;  // dst, (offset, bytes)
     auto up = [&](void* d, const void* h, size_t bytes) {
-        return bytes ? cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, st) : cudaSuccess;
+        if (bytes) {
+            const size_t off = (stage.size() + 15) & ~(size_t)15;
+            stage.resize(off + bytes);
+            memcpy(stage.data() + off, h, bytes);
+            ups.push_back({d, {off, bytes}});
+        }
+        return cudaSuccess;
     };
     VC_CUDA(c, up(pc->box_start.p, bstart.data(), 4 * nbox));
     VC_CUDA(c, up(pc->box_n.p, bcount.data(), 4 * nbox));
@@ -512,6 +523,11 @@ vc_status precond_build(vc_ctx* c, const int32_t box_in[3], int kind, const PcPl
     VC_CUDA(c, up(pc->uniq_list_off.p, ulist_off.data(), 4 * ulist_off.size()));
     VC_CUDA(c, up(pc->uniq_axis.p, uaxis.data(), 4 * uaxis.size()));
     VC_CUDA(c, up(pc->uniq_slot.p, uslot.data(), 4 * uslot.size()));
+    VC_CUDA(c, c->pc_stage.resize(std::max<size_t>(1, stage.size())));
+    if (!stage.empty()) memcpy(c->pc_stage.data(), stage.data(), stage.size());
+    for (const auto& u : ups)
+        VC_CUDA(c, cudaMemcpyAsync(u.first, c->pc_stage.data() + u.second.first, u.second.second,
+                                   cudaMemcpyHostToDevice, st));
     if (pc->nuniq > 0) {
         dim3 g(std::max(1, std::min(64, (maxn * maxn + 255) / 256)), pc->nuniq);
         PcTab tab;

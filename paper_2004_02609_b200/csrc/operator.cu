@@ -53,6 +53,7 @@ struct MV {
     int ya[kMaxRanks + 1], kxa[kMaxRanks + 1];
     int nr[kMaxRanks][9];  // rows of rank p within source b's (0..2) / field f's (3+f) extent
     int kx0, nkx;          // this rank's kx slab
+    int lgtk;              // one rank: X1 is kx-tile-major with 2^lgtk kx per tile (= P2's width)
     double2* S1[kMaxRanks][3];
     const double2* R1[kMaxRanks][3];
     double2* S2[kMaxRanks][6];
@@ -183,9 +184,16 @@ __global__ void __launch_bounds__(FX<L>::NT, FX<L>::MINB) k_p1(MV mv) {
         const int k0 = D ? mv.kxa[qd] : 0;
         const int nk = D ? mv.kxa[qd + 1] - k0 : mv.nkx;
         const int l0 = 2 * q - s;
-        double2* o = (D ? mv.S1[qd][beta] : S1self) + ((int64_t)j * nrow + l0) * nk + (k - k0);
-        if (l0 >= 0) o[0] = A;
-        if (l0 + 1 < nrow) o[nk] = B;
+        if (D) {
+            double2* o = mv.S1[qd][beta] + ((int64_t)j * nrow + l0) * nk + (k - k0);
+            if (l0 >= 0) o[0] = A;
+            if (l0 + 1 < nrow) o[nk] = B;
+        } else {  // one rank: [plane][kx tile][row][kx % tk], so P2 reads each tile contiguously
+            const int tk = 1 << mv.lgtk, ntk = (nk + tk - 1) >> mv.lgtk;
+            double2* o = S1self + (((int64_t)j * ntk + (k >> mv.lgtk)) * nrow + l0) * tk + (k & (tk - 1));
+            if (l0 >= 0) o[0] = A;
+            if (l0 + 1 < nrow) o[tk] = B;
+        }
     }
 }
 
@@ -209,11 +217,12 @@ __global__ void __launch_bounds__(FY<L>::NT) k_p2(MV mv) {
     double2* __restrict__ out = mv.X2[beta] + blockIdx.z * mv.colB;
     const int nzb = mv.nzin[beta], nt3 = (nkx + mv.T3 - 1) >> mv.lgT3;
     const bool ph = beta != 1;  // c_beta,y = 1/2 for x- and z-normal panels
-    const double2* const in0 = mv.R1[0][beta] + blockIdx.z * mv.colA + (int64_t)j * mv.nr[0][beta] * nkx;  // (!D)
+    // (!D) tile `tile` of plane j: T adjacent kx of all ey rows, contiguous
+    const double2* const in0 = mv.R1[0][beta] + blockIdx.z * mv.colA + (int64_t)j * ntile * ey * T;
     auto ld0 = [&](int t, int n) -> double2 {
         const int kx = tile * T + t;
         if (n >= ey || kx >= nkx) return czero();
-        if (!D) return in0[(int64_t)n * nkx + kx];
+        if (!D) return in0[((int64_t)tile * ey + n) * T + t];  // kx-tile-major X1 (one rank)
         const int p = row_owner(mv, n);  // row n arrived from rank p
         return mv.R1[p][beta][((int64_t)j * mv.nr[p][beta] + (n - mv.ya[p])) * nkx + kx];
     };
@@ -1849,11 +1858,14 @@ vc_status operator_build(vc_ctx* c, const vc_build_opts* o) {
     // later P4 -> P5 blocks [sender][field][plane][own rows][sender kx] (recv 2); S: blocks for
     // peers (send 1, later send 2); B: X2 tile-major; C: X3.
     auto nkxq = [&](int q) { return c->kxa[q + 1] - c->kxa[q]; };
+    c->lgtk = ilog2c(std::min(32, std::max(2, 4096 / My)));  // FY<My>::T, P2's kx tile width
     size_t nR1 = 0, nR2 = 0, nS1 = 0, nS2 = 0, nBt = 0, nC = 0;
     for (int p = 0; p < W; ++p)
         for (int b = 0; b < 3; ++b) {
             c->offR1[p][b] = nR1;
-            nR1 += (size_t)c->nzin[b] * c->nr[p][b] * nkx;
+            // one rank: kx-tile-major X1 padded to whole P2 tiles
+            const size_t nkxp = W == 1 ? (size_t)((nkx + (1 << c->lgtk) - 1) >> c->lgtk) << c->lgtk : nkx;
+            nR1 += (size_t)c->nzin[b] * c->nr[p][b] * nkxp;
         }
     for (int q = 0; q < W; ++q)
         for (int f = 0; f < c->nf; ++f) {
@@ -2108,6 +2120,7 @@ static MV make_mv(vc_ctx* c, const double* x, double* y) {
     }
     for (int q = 0; q < W; ++q)
         for (int g = 0; g < 9; ++g) mv.nr[q][g] = c->nr[q][g];
+    mv.lgtk = c->lgtk;
     mv.kx0 = c->kxa[r];
     mv.nkx = c->kxa[r + 1] - c->kxa[r];
     for (int q = 0; q < W; ++q) {

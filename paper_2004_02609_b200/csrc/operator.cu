@@ -54,6 +54,7 @@ struct MV {
     int nr[kMaxRanks][9];  // rows of rank p within source b's (0..2) / field f's (3+f) extent
     int kx0, nkx;          // this rank's kx slab
     int lgtk;              // one rank: X1 is kx-tile-major with 2^lgtk kx per tile (= P2's width)
+    int lgt4;              // X3 is kx-tile-major with P4's tile width 2^lgt4: [f][plane][tile][ky][t]
     double2* S1[kMaxRanks][3];
     const double2* R1[kMaxRanks][3];
     double2* S2[kMaxRanks][6];
@@ -273,13 +274,13 @@ __global__ void __launch_bounds__(FYS<L, KB>::NT) k_p4s(MV mv) {
     auto prefetch = [&](int tl, int stg) {
         int f, j, xt;
         decode(tl, f, j, xt);
-        const double2* in = mv.X3[f] + (tl / nt1) * mv.colC + (int64_t)j * L * nkx;
+        // kx-tile-major X3: the tile's T kx x L ky are one contiguous block
+        const double2* in = mv.X3[f] + (tl / nt1) * mv.colC + ((int64_t)j * ntx + xt) * L * T;
         double2* dst = sm + stg * L * T;
         for (int e = threadIdx.x; e < L * T; e += NT) {
             const int n = e / T, t = e % T;
-            const int kx = xt * T + t;
-            const bool valid = kx < nkx;
-            cp_async16(dst + smi<L, T, true, true>(t, n), valid ? in + (int64_t)n * nkx + kx : in, valid);
+            const bool valid = xt * T + t < nkx;
+            cp_async16(dst + smi<L, T, true, true>(t, n), valid ? in + e : in, valid);
         }
         cp_async_commit();
     };
@@ -483,7 +484,8 @@ __global__ void __launch_bounds__(kNT3) k_p3(MV mv) {
             const int kx = tile * T + t;
             const int jz = zmap[(3 + f) * L + Plan<L>::freq(p)];
             if (side < nside && kx < Kx && jz >= 0)
-                mv.X3[f][((int64_t)jz * My + (side ? My - q : q)) * Kx + kx] = v;
+                mv.X3[f][((((int64_t)jz * ((Kx + (1 << mv.lgt4) - 1) >> mv.lgt4) + (kx >> mv.lgt4)) * My +
+                           (side ? My - q : q)) << mv.lgt4) | (kx & ((1 << mv.lgt4) - 1))] = v;
         };
         fft_run<L, W, kNT3, true, true>(buf, ldo, sto, mv.tw, NF * T2);
         __syncthreads();
@@ -1104,6 +1106,7 @@ __global__ void __launch_bounds__(512) k_p3d(MV mv) {
     const int t = tid1 % T, og0 = tid1 / T, OGS = nthr1 / T;
     const int nkx = mv.nkx, My = mv.My, ZL = mv.ZL;
     const int nt3 = (nkx + T - 1) / T;
+    const int nt4 = (nkx + (1 << mv.lgt4) - 1) >> mv.lgt4;  // X3 tiles (P4's width)
     const int ntiles = nt3 * (My / 2 + 1);
     const int nz0 = mv.nzin[0], nz1 = mv.nzin[1], nz2 = mv.nzin[2];
     const int xo1 = 2 * T * nz0, xo2 = 2 * T * (nz0 + nz1);
@@ -1227,7 +1230,8 @@ __global__ void __launch_bounds__(512) k_p3d(MV mv) {
                         const bool neg = alpha == 1 && side == 1;  // odd along y: ky < 0 side
                         a = neg ? make_double2(a.y, -a.x) : make_double2(-a.y, a.x);
                     }
-                    X3[((int64_t)(jo0 + k) * My + (side ? My - q : q)) * nkx + kx] = a;
+                    X3[(((int64_t)(jo0 + k) * nt4 + (kx >> mv.lgt4)) * My + (side ? My - q : q))
+                           << mv.lgt4 | (kx & ((1 << mv.lgt4) - 1))] = a;
                 }
             }
         }
@@ -1859,6 +1863,7 @@ vc_status operator_build(vc_ctx* c, const vc_build_opts* o) {
     // peers (send 1, later send 2); B: X2 tile-major; C: X3.
     auto nkxq = [&](int q) { return c->kxa[q + 1] - c->kxa[q]; };
     c->lgtk = ilog2c(std::min(32, std::max(2, 4096 / My)));  // FY<My>::T, P2's kx tile width
+    c->lgt4 = ilog2c(std::min(32, std::max(1, 2048 / My)));  // FYS<My, 32>::T, P4's
     size_t nR1 = 0, nR2 = 0, nS1 = 0, nS2 = 0, nBt = 0, nC = 0;
     for (int p = 0; p < W; ++p)
         for (int b = 0; b < 3; ++b) {
@@ -1888,7 +1893,7 @@ vc_status operator_build(vc_ctx* c, const vc_build_opts* o) {
     }
     for (int f = 0; f < c->nf; ++f) {
         c->offC[f] = nC;
-        nC += (size_t)c->nzout[f] * My * nkx;
+        nC += (size_t)c->nzout[f] * My * ((size_t)((nkx + (1 << c->lgt4) - 1) >> c->lgt4) << c->lgt4);
     }
     // batched matvec (NEXT-3): one rank and at least two conductors; as many column copies of
     // the pass buffers as the free memory comfortably holds (<= kMaxB)
@@ -2121,6 +2126,7 @@ static MV make_mv(vc_ctx* c, const double* x, double* y) {
     for (int q = 0; q < W; ++q)
         for (int g = 0; g < 9; ++g) mv.nr[q][g] = c->nr[q][g];
     mv.lgtk = c->lgtk;
+    mv.lgt4 = c->lgt4;
     mv.kx0 = c->kxa[r];
     mv.nkx = c->kxa[r + 1] - c->kxa[r];
     for (int q = 0; q < W; ++q) {

@@ -308,7 +308,14 @@ __global__ void __launch_bounds__(FYS<L, KB>::NT) k_p4s(MV mv) {
             if (kx < nkx && yy < eyo) {
                 const int pr = D ? row_owner(mv, yy) : 0;  // row yy goes to rank pr for P5
                 const int y0 = D ? mv.ya[pr] : 0;
-                mv.S2[pr][f][(tl / nt1) * mv.colA + ((int64_t)j * mv.nr[pr][3 + f] + (yy - y0)) * nkx + kx] = v;
+                if (D) {
+                    mv.S2[pr][f][((int64_t)j * mv.nr[pr][3 + f] + (yy - y0)) * nkx + kx] = v;
+                } else {  // one rank: X4 row-pair interleaved [plane][row pair][kx][2] (P5's pairs)
+                    const int s5 = mv.lo[1] & 1, rr = yy + s5;
+                    const int np = (mv.nr[0][3 + f] + s5 + 1) >> 1;
+                    mv.S2[0][f][(tl / nt1) * mv.colA +
+                                ((((int64_t)j * np + (rr >> 1)) * nkx + kx) << 1 | (rr & 1))] = v;
+                }
             }
         };
         fft_run<L, T, NT, true, true, 0, true>(buf, lds, stN, mv.tw);
@@ -519,7 +526,10 @@ __global__ void __launch_bounds__(FX<L>::NT, FX<L>::MINB5) k_p5(MV mv) {
             k0 = mv.kxa[qd];
             nk = mv.kxa[qd + 1] - k0;
         }
-        const double2* src = mv.R2[qd][f] + blockIdx.z * mv.colA + ((int64_t)j * nrow + yrow) * nk + (k - k0);
+        const int rr = yrow + s;  // one rank: row-pair interleaved X4 (see P4)
+        const double2* src =
+            D ? mv.R2[qd][f] + ((int64_t)j * nrow + yrow) * nk + (k - k0)
+              : mv.R2[0][f] + blockIdx.z * mv.colA + ((((int64_t)j * nyp + (rr >> 1)) * nk + k) << 1 | (rr & 1));
         double2 w = v ? __ldg(src) : czero();
         if (ph) w = cmul(w, half_phase(mv.tw, k, L, +1));
         if (k == 0 || 2 * k == L) w.y = 0.0;
@@ -1875,7 +1885,10 @@ vc_status operator_build(vc_ctx* c, const vc_build_opts* o) {
     for (int q = 0; q < W; ++q)
         for (int f = 0; f < c->nf; ++f) {
             c->offR2[q][f] = nR2;
-            nR2 += (size_t)c->nzout[f] * c->nr[rk][3 + f] * nkxq(q);
+            // one rank: row-pair interleaved (P5 pairs rows at absolute (2m, 2m+1))
+            const int s5 = c->lo[1] & 1;
+            nR2 += (size_t)c->nzout[f] * nkxq(q) *
+                   (W == 1 ? (size_t)2 * ((c->nr[rk][3 + f] + s5 + 1) >> 1) : (size_t)c->nr[rk][3 + f]);
         }
     for (int q = 0; q < W; ++q)
         for (int b = 0; b < 3; ++b) {

@@ -69,3 +69,35 @@ def test_product_never_imports_oracle():
                 src = open(os.path.join(dirpath, f), errors="ignore").read()
                 assert not re.search(r"^\s*(import|from)\s+oracle\b", src, re.M), f
                 assert "kernels_q" not in src, f
+
+
+def test_struct_layouts_match_header(tmp_path):
+    """The ctypes mirrors of the option / info / stats structs have the sizes and field offsets
+    the C compiler gives the header's definitions (a field added on one side only would shift
+    every later field)."""
+    import paper_2004_02609_b200 as m
+    checks = {"vc_build_opts": m.BuildOpts, "vc_solve_opts": m.SolveOpts,
+              "vc_solve_info": m.SolveInfo, "vc_stats": m.Stats}
+    lines = ['#include <stddef.h>', '#include <stdio.h>', '#include "voxcap.h"', "int main(void) {"]
+    for cname, cls in checks.items():
+        lines.append(f'printf("{cname} size %zu\\n", sizeof({cname}));')
+        for fname, _ in cls._fields_:
+            lines.append(f'printf("{cname} {fname} %zu\\n", offsetof({cname}, {fname}));')
+    lines.append("return 0; }")
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    cuda_inc = "/usr/local/cuda/include"
+    r = subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), "-I", cuda_inc, str(src), "-o", str(exe)],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    out = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split("\n")
+    got = {}
+    for ln in out:
+        if ln:
+            a, b, c = ln.split()
+            got[(a, b)] = int(c)
+    for cname, cls in checks.items():
+        assert got[(cname, "size")] == ctypes.sizeof(cls), cname
+        for fname, _ in cls._fields_:
+            assert got[(cname, fname)] == getattr(cls, fname).offset, (cname, fname)

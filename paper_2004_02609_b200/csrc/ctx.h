@@ -134,9 +134,8 @@ struct vc_ctx {
     // [kind][orientation][0 = min, 1 = max][axis]; min > max when no such panels
     int ext[2][3][2][3];
     // host mirror of the panel table (structure-only work: preconditioner boxes)
-    vc::PinnedVec<int8_t> h_axis, h_sign;
+    vc::PinnedVec<int8_t> h_axis;
     vc::PinnedVec<int32_t> h_si, h_sj, h_sk, h_cid;
-    vc::PinnedVec<double> h_ibar;
     vc::PinnedVec<char> pc_stage;  // pinned staging of the preconditioner uploads
 
     // ---- operator (vc_build_operator) ----

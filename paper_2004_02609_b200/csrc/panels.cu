@@ -187,7 +187,7 @@ struct Out {
     double *ed, *eb, *ibar, *fc;
     int32_t* slotmap[3];
     double area_over_2eps0;
-    int* ext;  // [kind][orient][min/max][axis] flattened, 36 ints
+    int* ext;  // [kind][orient][min/max][axis] flattened, 36 ints; [36] conductor-panel count
 };
 
 __global__ void k_emit(Geo g, int64_t Ftot, const int64_t* __restrict__ tile_off, Out o) {
@@ -196,8 +196,9 @@ __global__ void k_emit(Geo g, int64_t Ftot, const int64_t* __restrict__ tile_off
     __shared__ int64_t warp_tot[kNT / 32];
     // panel extents: reduced in shared memory, then one global atomic per value and block (a
     // global atomic per panel serialised ~4.6M updates on 36 addresses: 3.2 ms on C4)
-    __shared__ int sext[36];
+    __shared__ int sext[37];
     if (threadIdx.x < 36) sext[threadIdx.x] = (threadIdx.x % 6) < 3 ? INT32_MAX : INT32_MIN;
+    if (threadIdx.x == 36) sext[36] = 0;
     int flag[PER];
     FaceInfo fi[PER];
     int a0 = 0, ii[PER], jj[PER], kk[PER], aa[PER];
@@ -234,6 +235,7 @@ __global__ void k_emit(Geo g, int64_t Ftot, const int64_t* __restrict__ tile_off
         const int64_t r = f - g.Foff[a];
         if (flag[q]) {
             const bool diel = fi[q].type == 2;
+            if (!diel) atomicAdd(&sext[36], 1);
             o.axis[p] = (int8_t)a;
             o.sign[p] = (int8_t)fi[q].sign;
             o.info[p] = (int8_t)((diel ? 1 : 0) | (fi[q].sign < 0 ? 2 : 0));
@@ -260,6 +262,7 @@ __global__ void k_emit(Geo g, int64_t Ftot, const int64_t* __restrict__ tile_off
         }
     }
     __syncthreads();
+    if (threadIdx.x == 36 && sext[36]) atomicAdd(o.ext + 36, sext[36]);
     if (threadIdx.x < 36) {
         const int v = sext[threadIdx.x];
         if ((threadIdx.x % 6) < 3) {
@@ -348,11 +351,11 @@ vc_status geometry_build(vc_ctx* c, const int32_t* d_label, const double* d_eps)
     VC_CUDA(c, P.fc.alloc(N));
     for (int a = 0; a < 3; ++a) VC_CUDA(c, P.slotmap[a].alloc(g.F[a]));
     DevBuf<int>& ext = c->geo_ext;
-    VC_CUDA(c, ext.alloc(36));
-    std::vector<int> hext(36);
+    VC_CUDA(c, ext.alloc(37));
+    std::vector<int> hext(37, 0);
     for (int q = 0; q < 6; ++q)
         for (int t = 0; t < 6; ++t) hext[q * 6 + t] = t < 3 ? INT32_MAX : INT32_MIN;
-    VC_CUDA(c, cudaMemcpyAsync(ext.p, hext.data(), 36 * sizeof(int), cudaMemcpyHostToDevice, st));
+    VC_CUDA(c, cudaMemcpyAsync(ext.p, hext.data(), 37 * sizeof(int), cudaMemcpyHostToDevice, st));
     Out o;
     o.axis = P.axis.p;
     o.sign = P.sign.p;
@@ -371,22 +374,18 @@ vc_status geometry_build(vc_ctx* c, const int32_t* d_label, const double* d_eps)
     tr.mark("allocs");
     k_emit<<<(unsigned)ntiles, kNT, 0, st>>>(g, Ftot, tiles.p, o);
     count_launch(c);
-    VC_CUDA(c, cudaMemcpyAsync(hext.data(), ext.p, 36 * sizeof(int), cudaMemcpyDeviceToHost, st));
+    VC_CUDA(c, cudaMemcpyAsync(hext.data(), ext.p, 37 * sizeof(int), cudaMemcpyDeviceToHost, st));
     // host mirror of the structural fields
     VC_CUDA(c, c->h_axis.resize(N));
-    VC_CUDA(c, c->h_sign.resize(N));
     VC_CUDA(c, c->h_si.resize(N));
     VC_CUDA(c, c->h_sj.resize(N));
     VC_CUDA(c, c->h_sk.resize(N));
     VC_CUDA(c, c->h_cid.resize(N));
-    VC_CUDA(c, c->h_ibar.resize(N));
     VC_CUDA(c, cudaMemcpyAsync(c->h_axis.data(), P.axis.p, N, cudaMemcpyDeviceToHost, st));
-    VC_CUDA(c, cudaMemcpyAsync(c->h_sign.data(), P.sign.p, N, cudaMemcpyDeviceToHost, st));
     VC_CUDA(c, cudaMemcpyAsync(c->h_si.data(), P.si.p, N * 4, cudaMemcpyDeviceToHost, st));
     VC_CUDA(c, cudaMemcpyAsync(c->h_sj.data(), P.sj.p, N * 4, cudaMemcpyDeviceToHost, st));
     VC_CUDA(c, cudaMemcpyAsync(c->h_sk.data(), P.sk.p, N * 4, cudaMemcpyDeviceToHost, st));
     VC_CUDA(c, cudaMemcpyAsync(c->h_cid.data(), P.cid.p, N * 4, cudaMemcpyDeviceToHost, st));
-    VC_CUDA(c, cudaMemcpyAsync(c->h_ibar.data(), P.ibar.p, N * 8, cudaMemcpyDeviceToHost, st));
     VC_CUDA(c, cudaStreamSynchronize(st));
     VC_CUDA(c, cudaGetLastError());
     for (int kind = 0; kind < 2; ++kind)
@@ -396,9 +395,7 @@ vc_status geometry_build(vc_ctx* c, const int32_t* d_label, const double* d_eps)
                 c->ext[kind][a][1][t] = hext[(kind * 3 + a) * 6 + 3 + t];
             }
     tr.mark("emit + host mirrors");
-    int64_t Nc = 0;
-    for (int64_t p = 0; p < N; ++p) Nc += c->h_cid[p] > 0;
-    tr.mark("host count");
+    const int64_t Nc = hext[36];  // counted in k_emit
     c->N = N;
     c->Nc = Nc;
     c->Nd = N - Nc;

@@ -64,11 +64,13 @@ def test_conductor_block_spd():
 
 
 def test_sphere_near_one():
-    """Voxelised sphere capacitance -> 4πε0 R (BASELINE north_star); staircase error ~ 1/R."""
+    """Voxelised sphere capacitance -> 4πε0 R (BASELINE north_star): above 1 and within the
+    staircase error (error * R ≈ 0.14-0.21 voxels); the exact survey values
+    are pinned in test_oracle_survey_pins.py."""
     R = 8
     _, C = _cap(voxgen.sphere(R, dv=1.0))
     val = C[0, 0] / (K * R)
-    assert 1.0 < val < 1.04, val
+    assert 1.0 < val < 1.0 + 0.25 / R, val
 
 
 def _two_blocks(eps_r=None):
@@ -146,17 +148,6 @@ def test_permittivity_sweep():
     assert all(b > a for a, b in zip(vals, vals[1:]))
     assert abs(vals[-1] - vals[-2]) < 1e-4 * vals[-1]
     assert abs(vals[-1] / Cbare_d[0, 0] - 1) < 0.03
-
-
-@pytest.mark.slow
-def test_c2_parallel_plates():
-    """C2: |C12| ≈ εr ε0 A/d plus fringing, C symmetric by the z-mirror symmetry."""
-    st = voxgen.config("C2")
-    p, C = _cap(st)
-    par = 4.0 * O.EPS0 * (32e-6) ** 2 / 4e-6
-    assert 1.0 < -C[0, 1] / par < 1.15
-    assert abs(C[0, 1] - C[1, 0]) < 1e-9 * abs(C[0, 1])
-    assert abs(C[0, 0] - C[1, 1]) < 1e-9 * abs(C[0, 0])
 
 
 def test_precond_whole_domain_box_is_exact_inverse():

@@ -23,7 +23,7 @@ import numpy as np
 
 __all__ = [
     "Structure", "cube", "plates_slab", "sphere", "coated_sphere", "meander", "crossing_bus",
-    "random_structure", "config", "CONFIG_NAMES", "seeded_vector",
+    "random_structure", "config", "CONFIG_NAMES", "REDUCED_NAMES", "seeded_vector",
 ]
 
 
@@ -96,7 +96,7 @@ def coated_sphere(rc_vox, rd_vox, eps_r=2.0, dv=1.0, margin=0):
 
 
 def meander(seed=0, nx=512, ny=512, nz=64, sub=16, eps_r=4.4, dv=1e-6,
-            width=2, thick=2, pitch=4, run_pitch=12, run_min=400, run_max=500):
+            width=2, thick=2, pitch=4, run_pitch=12, run_min=400, run_max=500, edge=16):
     """C4: two parallel meander lines over a ``sub``-voxel eps_r substrate (P:238-257 shape).
 
     The pair follows a serpentine centre path: runs along x with lengths
@@ -105,19 +105,20 @@ def meander(seed=0, nx=512, ny=512, nz=64, sub=16, eps_r=4.4, dv=1e-6,
     the direction of travel, so the two lines are ``pitch`` apart centre to centre everywhere
     and the U-turns nest.  Each line is a band ``width`` voxels wide and ``thick`` voxels thick
     lying on the substrate (z in [sub, sub+thick)).  The substrate leaves a one-voxel margin at
-    the +x/+y walls.
+    the +x/+y walls.  ``edge`` is the clearance of the serpentine from the walls
+    (16 at full size; the reduced parity grids use a smaller one).
     """
     rng = np.random.default_rng(seed)
     label, eps = _empty(nx, ny, nz)
     eps[:sub, : ny - 1, : nx - 1] = eps_r
     z0, z1 = sub, sub + thick
-    lo_edge, hi_edge = 16, nx - 17
+    lo_edge, hi_edge = edge, nx - edge - 1
     hw = width // 2
     x = lo_edge
-    y = 16
+    y = edge
     d = +1
     runs = []  # (x_start, x_end, y, direction)
-    while y + 16 < ny - 16:
+    while y + edge < ny - edge:
         L = int(rng.integers(run_min, run_max))
         xe = min(max(x + d * L, lo_edge), hi_edge)
         runs.append((x, xe, y, d))
@@ -145,29 +146,30 @@ def meander(seed=0, nx=512, ny=512, nz=64, sub=16, eps_r=4.4, dv=1e-6,
 
 
 def crossing_bus(seed=0, nx=2048, ny=2048, nz=128, n_lines=16, w=4, dv=1e-6,
-                 layers=((0, 40, 3.9), (40, 80, 7.0), (80, 127, 2.5))):
+                 layers=((0, 40, 3.9), (40, 80, 7.0), (80, 127, 2.5)), edge=16, end=8, jitter=8):
     """C5: 16 lines along x in the lower layer crossing 16 lines along y in the upper layer,
     each w x w voxels, in three dielectric layers (eps_r 3.9 / 7.0 / 2.5) over x,y in
     [0, n-1) (one-voxel margin); seeded pitch and offsets (the §III.D crossing-bus shape,
-    P:218)."""
+    P:218).  ``edge`` / ``jitter`` (first-line offset and pitch jitter) and ``end`` (line-end
+    clearance) are 16 / 8 / 8 at full size; the reduced parity grids use smaller ones."""
     rng = np.random.default_rng(seed)
     label, eps = _empty(nx, ny, nz)
     for z0, z1, e in layers:
         eps[z0:z1, : ny - 1, : nx - 1] = e
     zl = (layers[0][0] + layers[0][1]) // 2 - w // 2
     zu = (layers[1][0] + layers[1][1]) // 2 - w // 2
-    span = min(nx, ny) - 32
-    pitch = int(rng.integers(span // (n_lines + 1) - 8, span // (n_lines + 1)))
-    off_a = 16 + int(rng.integers(0, 8))
-    off_b = 16 + int(rng.integers(0, 8))
+    span = min(nx, ny) - 2 * edge
+    pitch = int(rng.integers(span // (n_lines + 1) - jitter, span // (n_lines + 1)))
+    off_a = edge + int(rng.integers(0, jitter))
+    off_b = edge + int(rng.integers(0, jitter))
     cid = 1
     for i in range(n_lines):
         y0 = off_a + i * pitch
-        label[zl:zl + w, y0:y0 + w, 8:nx - 9] = cid
+        label[zl:zl + w, y0:y0 + w, end:nx - end - 1] = cid
         cid += 1
     for i in range(n_lines):
         x0 = off_b + i * pitch
-        label[zu:zu + w, 8:ny - 9, x0:x0 + w] = cid
+        label[zu:zu + w, end:ny - end - 1, x0:x0 + w] = cid
         cid += 1
     return Structure(label, eps, 1.0, dv, f"crossing_bus_s{seed}")
 
@@ -214,6 +216,13 @@ def random_structure(seed, margin=None):
 
 CONFIG_NAMES = ("C1", "C2", "C3", "C4", "C5")
 
+# Reduced grids of the C3 / C4 / C5 generators, small enough for the dense oracle (SURVEY.md
+# §8(c) last pins row: "pinned on the same generator at reduced grids").  C3r = C3 / 4 per
+# axis; C4r = the C4 meander pair (2 x 2 lines, pitch 4, run pitch 12, three U-turns) on a
+# 48 x 48 x 8 box with a 4-voxel eps_r 4.4 substrate; C5r = C5 / 64 in x, y,
+# / 8 in z with 2 + 2 lines of 2 x 2 voxels in the same three layers.
+REDUCED_NAMES = ("C3r", "C4r", "C5r")
+
 
 def config(name, seed=0):
     """Structures for BASELINE.json configs[0..4] (SURVEY.md §8(d) concretisation)."""
@@ -227,6 +236,13 @@ def config(name, seed=0):
         return meander(seed)
     if name == "C5":
         return crossing_bus(seed)
+    if name == "C3r":
+        return sphere(16)
+    if name == "C4r":
+        return meander(seed, 48, 48, 8, sub=4, run_min=24, run_max=32, edge=6)
+    if name == "C5r":
+        return crossing_bus(seed, 32, 32, 16, n_lines=2, w=2, edge=4, end=2, jitter=2,
+                            layers=((0, 5, 3.9), (5, 10, 7.0), (10, 15, 2.5)))
     if name.startswith("R"):
         return random_structure(int(name[1:]))
     raise KeyError(name)

@@ -223,8 +223,11 @@ vc_status vc_solve(vc_ctx* ctx, const double* b, double* x, const vc_solve_opts*
 vc_status vc_solve_capacitance(vc_ctx* ctx, double* C, const vc_solve_opts* opts,
                                vc_solve_info* per_column);
 
-/* Instrumentation: timing_detail = 1 records per-pass CUDA events (adds syncs-free event
- * pairs around every pass); vc_get_stats copies the counters; vc_reset_stats zeroes them. */
+/* Instrumentation: timing_detail = 1 records CUDA events around every matvec and every pass
+ * (ms_matvec, ms_pass, ms_comm); 0 records none.  Nothing waits on the device inside a
+ * matvec: the events are queued and resolved when vc_get_stats or vc_reset_stats is called
+ * (those two calls wait for the last timed matvec).  vc_get_stats copies the counters;
+ * vc_reset_stats zeroes them. */
 vc_status vc_set_timing(vc_ctx* ctx, int32_t timing_detail);
 vc_status vc_get_stats(const vc_ctx* ctx, vc_stats* out);
 vc_status vc_reset_stats(vc_ctx* ctx);

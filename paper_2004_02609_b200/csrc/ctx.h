@@ -107,10 +107,20 @@ struct PanelsLocal {
     DevBuf<int64_t> gidx;        // local -> global index
 };
 
+// Matvec timing (vc_set_timing): every timed matvec records its events from a grow-only pool
+// and queues a record; nothing waits on the device inside a matvec.  The records are resolved
+// (one event synchronise for the whole batch) when the stats are read or reset, or when the
+// queue reaches kMaxRecs.
 struct Timing {
-    bool detail = false;
-    cudaEvent_t ev[16] = {};
-    bool ev_ok = false;
+    static constexpr int kEvPerMv = 16;   // [0] start, [1..5] pass starts, [6..10] pass ends,
+                                          // [11] end, [12..15] all-to-all brackets
+    static constexpr int kMaxRecs = 4096;
+    bool on = false;      // per-matvec events (ms_matvec)
+    bool detail = false;  // per-pass events (ms_pass, ms_comm)
+    std::vector<cudaEvent_t> pool;
+    struct Rec { int base; int nb; bool det; bool comm; };
+    std::vector<Rec> recs;
+    int used = 0;
 };
 
 }  // namespace vc
@@ -284,6 +294,7 @@ vc_status debug_kernel_entries(vc_ctx* c, int n, const int32_t* kind, const int3
 vc_status debug_fft(vc_ctx* c, int L, int nl, double* data, int dir);
 vc_status partition_build(vc_ctx* c);  // operator.cu: slabs, local panels, local slot maps
 void kernel_table_times(vc_ctx* c);
+vc_status timing_resolve(vc_ctx* c);  // fold queued matvec timing records into c->stats
 int row_owner_abs(const vc_ctx* c, int yabs);
 void plan_kx_slabs(int W, int Kx, int T3, int* kxa);
 int row_owner_plan(int W, int Nv, int nb, int b0, int nbr, int yabs);

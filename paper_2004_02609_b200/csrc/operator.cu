@@ -105,8 +105,13 @@ template <int L> struct FX {
     static constexpr int MINB = 65536 / (NT * 96) < 1 ? 1 : 65536 / (NT * 96);
     static constexpr int MINB5 = 65536 / (NT * 128) < 1 ? 1 : 65536 / (NT * 128);
 };
+// Tile widths the host layout code must agree with (X1 is tiled by P2's width, X3 by P4's):
+// operator_build sizes and indexes those arrays through these two functions only.
+constexpr int p2_tile(int L) { return clampi(4096 / L, 2, 32); }  // FY<L>::T
+constexpr int kP4KB = 32;                                          // P4's shared KB per stage
+constexpr int p4_tile(int L) { return clampi(kP4KB * 64 / L, 1, 32); }  // FYS<L, kP4KB>::T
 template <int L> struct FY {
-    static constexpr int T = clampi(4096 / L, 2, 32);  // >= 2 adjacent kx: 32-byte row segments
+    static constexpr int T = p2_tile(L);  // >= 2 adjacent kx: 32-byte row segments
     static constexpr int NT = 256;
 };
 template <int L> struct TX { static constexpr int T = FX<L>::T; };
@@ -1001,6 +1006,7 @@ static int persistent_grid(K kern, int nthr, size_t smem, int ntiles) {
 template <int LL, int KB>
 static cudaError_t launch_p4s_t(const MV& mv, cudaStream_t st) {
     constexpr int T = FYS<LL, KB>::T, NT = FYS<LL, KB>::NT;
+    static_assert(T == p4_tile(LL), "X3 layout (operator_build, p4_tile) and P4's tile disagree");
     int G = 0;
     for (int f = 0; f < mv.nf; ++f) G += mv.nzout[f];
     const size_t smem = sizeof(double2) * 2 * LL * T;
@@ -1014,7 +1020,7 @@ static cudaError_t launch_p4s_t(const MV& mv, cudaStream_t st) {
 }
 static cudaError_t launch_p4s(const MV& mv, cudaStream_t st) {
     cudaError_t e;
-    VC_DISPATCH_L(mv.My, { e = launch_p4s_t<LL, 32>(mv, st); if (e) return e; });
+    VC_DISPATCH_L(mv.My, { e = launch_p4s_t<LL, kP4KB>(mv, st); if (e) return e; });
     return cudaGetLastError();
 }
 static cudaError_t launch_p2(const MV& mv, cudaStream_t st) {
@@ -1872,8 +1878,8 @@ vc_status operator_build(vc_ctx* c, const vc_build_opts* o) {
     // later P4 -> P5 blocks [sender][field][plane][own rows][sender kx] (recv 2); S: blocks for
     // peers (send 1, later send 2); B: X2 tile-major; C: X3.
     auto nkxq = [&](int q) { return c->kxa[q + 1] - c->kxa[q]; };
-    c->lgtk = ilog2c(std::min(32, std::max(2, 4096 / My)));  // FY<My>::T, P2's kx tile width
-    c->lgt4 = ilog2c(std::min(32, std::max(1, 2048 / My)));  // FYS<My, 32>::T, P4's
+    c->lgtk = ilog2c(p2_tile(My));  // FY<My>::T, P2's kx tile width
+    c->lgt4 = ilog2c(p4_tile(My));  // FYS<My, kP4KB>::T, P4's
     size_t nR1 = 0, nR2 = 0, nS1 = 0, nS2 = 0, nBt = 0, nC = 0;
     for (int p = 0; p < W; ++p)
         for (int b = 0; b < 3; ++b) {
@@ -2181,11 +2187,53 @@ vc_status matvec_dev(vc_ctx* c, const double* d_x, double* d_y) {
     return matvec_run(c, make_mv(c, d_x, d_y));
 }
 
+// Accumulate the queued matvec timing records into c->stats (one wait for the newest event).
+vc_status timing_resolve(vc_ctx* c) {
+    Timing& T = c->timing;
+    if (T.recs.empty()) return VC_OK;
+    VC_CUDA(c, cudaEventSynchronize(T.pool[T.recs.back().base + 11]));
+    float ms = 0;
+    for (const Timing::Rec& r : T.recs) {
+        const cudaEvent_t* ev = T.pool.data() + r.base;
+        VC_CUDA(c, cudaEventElapsedTime(&ms, ev[0], ev[11]));
+        c->stats.ms_matvec += ms;
+        if (r.det) {
+            for (int p = 0; p < 5; ++p) {
+                VC_CUDA(c, cudaEventElapsedTime(&ms, ev[1 + p], ev[6 + p]));
+                c->stats.ms_pass[p] += ms;
+            }
+            if (r.comm)
+                for (int e = 0; e < 2; ++e) {
+                    VC_CUDA(c, cudaEventElapsedTime(&ms, ev[12 + e], ev[14 + e]));
+                    c->stats.ms_comm += ms;
+                }
+        }
+    }
+    T.recs.clear();
+    T.used = 0;
+    return VC_OK;
+}
+
 static vc_status matvec_run(vc_ctx* c, const MV& mv) {
     cudaStream_t st = c->stream;
     Timing& T = c->timing;
-    const bool det = T.detail && T.ev_ok;
-    if (T.ev_ok) VC_CUDA(c, cudaEventRecord(T.ev[0], st));
+    const cudaEvent_t* ev = nullptr;
+    if (T.on) {
+        if ((int)T.recs.size() >= Timing::kMaxRecs) {
+            vc_status s = timing_resolve(c);
+            if (s) return s;
+        }
+        while ((int)T.pool.size() < T.used + Timing::kEvPerMv) {
+            cudaEvent_t e;
+            VC_CUDA(c, cudaEventCreate(&e));
+            T.pool.push_back(e);
+        }
+        T.recs.push_back({T.used, mv.nb, T.detail, c->world > 1});
+        ev = T.pool.data() + T.used;
+        T.used += Timing::kEvPerMv;
+    }
+    const bool det = ev && T.detail;
+    if (ev) VC_CUDA(c, cudaEventRecord(ev[0], st));
     for (int i = 0; i < mv.nb; ++i)
         k_zero<<<std::max<int64_t>(1, std::min<int64_t>((c->NL + 255) / 256, 1184)), 256, 0, st>>>(mv.ys[i], c->NL);
     cudaError_t (*launch[5])(const MV&, cudaStream_t) = {launch_p1, launch_p2, launch_p3,
@@ -2194,16 +2242,16 @@ static vc_status matvec_run(vc_ctx* c, const MV& mv) {
         if (c->world > 1 && (p == 1 || p == 4)) {
             // x-transformed planes: rows -> kx slabs before P2, back before P5
             const int e = p == 1 ? 0 : 1;
-            if (det) VC_CUDA(c, cudaEventRecord(T.ev[12 + e], st));
+            if (det) VC_CUDA(c, cudaEventRecord(ev[12 + e], st));
             vc_status s = comm_alltoall(c, c->a2a_send[e], c->a2a_sb[e], c->a2a_recv[e], c->a2a_rb[e]);
             if (s) return s;
-            if (det) VC_CUDA(c, cudaEventRecord(T.ev[14 + e], st));
+            if (det) VC_CUDA(c, cudaEventRecord(ev[14 + e], st));
         }
-        if (det) VC_CUDA(c, cudaEventRecord(T.ev[1 + p], st));
+        if (det) VC_CUDA(c, cudaEventRecord(ev[1 + p], st));
         VC_CUDA(c, launch[p](mv, st));
-        if (det) VC_CUDA(c, cudaEventRecord(T.ev[6 + p], st));
+        if (det) VC_CUDA(c, cudaEventRecord(ev[6 + p], st));
     }
-    if (T.ev_ok) VC_CUDA(c, cudaEventRecord(T.ev[11], st));
+    if (ev) VC_CUDA(c, cudaEventRecord(ev[11], st));
     count_launch(c, 5 + mv.nb);
     c->stats.n_matvec += mv.nb;
     for (int p = 0; p < 5; ++p) {
@@ -2212,24 +2260,6 @@ static vc_status matvec_run(vc_ctx* c, const MV& mv) {
         // oversized tiles run P3 column by column: nb reads)
         const bool shared_k = p == 2 && mv.zdirect && mv.nb > 1 && p3d_smem(mv) <= 227 * 1024;
         c->stats.bytes_moved[p] += mv.nb * c->bytes_pass[p] - (shared_k ? (mv.nb - 1) * c->bytes_k3 : 0.0);
-    }
-    if (T.ev_ok) {
-        // accumulate device times (waits for this matvec; used only with timing on)
-        VC_CUDA(c, cudaEventSynchronize(T.ev[11]));
-        float ms = 0;
-        VC_CUDA(c, cudaEventElapsedTime(&ms, T.ev[0], T.ev[11]));
-        c->stats.ms_matvec += ms;
-        if (det) {
-            for (int p = 0; p < 5; ++p) {
-                VC_CUDA(c, cudaEventElapsedTime(&ms, T.ev[1 + p], T.ev[6 + p]));
-                c->stats.ms_pass[p] += ms;
-            }
-            if (c->world > 1)
-                for (int e = 0; e < 2; ++e) {
-                    VC_CUDA(c, cudaEventElapsedTime(&ms, T.ev[12 + e], T.ev[14 + e]));
-                    c->stats.ms_comm += ms;
-                }
-        }
     }
     return VC_OK;
 }

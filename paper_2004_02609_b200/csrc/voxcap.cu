@@ -1,4 +1,5 @@
 #include <memory>
+#include <atomic>
 #include <thread>
 #include <vector>
 // voxcap.cu -- the C ABI of libvoxcap.so (include/voxcap.h).  Argument checking, state
@@ -109,8 +110,7 @@ void vc_destroy(vc_ctx* c) {
         c->dvec.reset();
         if (c->h_pinned) cudaFreeHost(c->h_pinned);
         if (c->h_pinned_multi) cudaFreeHost(c->h_pinned_multi);
-        if (c->timing.ev_ok)
-            for (auto& e : c->timing.ev) cudaEventDestroy(e);
+        for (auto& e : c->timing.pool) cudaEventDestroy(e);
         if (c->arn_ev_ok)
             for (auto& e : c->arn_ev) cudaEventDestroy(e);
         if (c->mc_ev_ok)
@@ -240,17 +240,46 @@ vc_status vc_build_operator(vc_ctx* c, const vc_build_opts* o) {
     const bool async_plan = kind == 3 && c->world == 1;
     std::unique_ptr<PcPlan, void (*)(PcPlan*)> plan_own(async_plan ? pc_plan_new() : nullptr, pc_plan_free);
     PcPlan* plan = plan_own.get();
+    // exceptions (host allocation failures at large N) never cross the C ABI: the helper thread
+    // stores a status, the thread is joined on every path, and both sides map to vc_status
+    std::atomic<int> plan_status{VC_OK};
     std::thread planner;
-    if (async_plan) planner = std::thread([c, &box, plan] { pc_plan_compute(c, box, c->N, *plan); });
-    vc_status s = operator_build(c, o);
+    struct Joiner {
+        std::thread& t;
+        ~Joiner() { if (t.joinable()) t.join(); }
+    } joiner{planner};
+    if (async_plan)
+        planner = std::thread([c, &box, plan, &plan_status] {
+            try {
+                pc_plan_compute(c, box, c->N, *plan);
+            } catch (const std::bad_alloc&) {
+                plan_status = VC_ERR_OOM;
+            } catch (...) {
+                plan_status = VC_ERR_INPUT;
+            }
+        });
+    vc_status s = VC_OK;
+    try {
+        s = operator_build(c, o);
+    } catch (const std::bad_alloc&) {
+        s = set_err(c, VC_ERR_OOM, "host allocation failed in vc_build_operator");
+    } catch (const std::exception& ex) {
+        s = set_err(c, VC_ERR_INPUT, std::string("vc_build_operator: ") + ex.what());
+    }
     {
         HostTrace tj("build_operator");
         if (planner.joinable()) planner.join();
         tj.mark("join planner");
     }
+    if (s == VC_OK && plan_status != VC_OK)
+        s = set_err(c, (vc_status)plan_status.load(), "preconditioner planning failed (host allocation)");
     if (s == VC_OK) {
         VC_CUDA(c, cudaEventRecord(e1, c->stream));
-        s = precond_build(c, box, kind, plan);
+        try {
+            s = precond_build(c, box, kind, plan);
+        } catch (const std::bad_alloc&) {
+            s = set_err(c, VC_ERR_OOM, "host allocation failed in the preconditioner build");
+        }
         VC_CUDA(c, cudaEventRecord(e2, c->stream));
     }
     if (s == VC_OK) {
@@ -357,22 +386,31 @@ vc_status vc_solve_capacitance(vc_ctx* c, double* C, const vc_solve_opts* o,
 vc_status vc_set_timing(vc_ctx* c, int32_t detail) {
     VC_CHECK_CTX(c);
     DeviceGuard g(c->device);
-    if (!c->timing.ev_ok) {
-        for (auto& e : c->timing.ev) VC_CUDA(c, cudaEventCreate(&e));
-        c->timing.ev_ok = true;
-    }
+    c->timing.on = detail != 0;
     c->timing.detail = detail != 0;
     return VC_OK;
 }
 
 vc_status vc_get_stats(const vc_ctx* c, vc_stats* out) {
     if (!c || !out) return VC_ERR_INPUT;
+    // queued matvec timings are folded in here (waits for the last timed matvec only)
+    vc_ctx* m = const_cast<vc_ctx*>(c);
+    if (!m->timing.recs.empty()) {
+        DeviceGuard g(m->device);
+        vc_status s = timing_resolve(m);
+        if (s) return s;
+    }
     *out = c->stats;
     return VC_OK;
 }
 
 vc_status vc_reset_stats(vc_ctx* c) {
     VC_CHECK_CTX(c);
+    if (!c->timing.recs.empty()) {
+        DeviceGuard g(c->device);
+        vc_status s = timing_resolve(c);
+        if (s) return s;
+    }
     const double bp[5] = {c->stats.bytes_pass[0], c->stats.bytes_pass[1], c->stats.bytes_pass[2],
                           c->stats.bytes_pass[3], c->stats.bytes_pass[4]};
     const double bm = c->stats.bytes_matvec, ms = c->stats.ms_setup, mp = c->stats.ms_precond_build;

@@ -128,6 +128,10 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
         "l"(src), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
 }
+// plain arrive (count 1)
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
 // wait until the barrier phase with parity `par` has completed
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned par) {
     asm volatile(

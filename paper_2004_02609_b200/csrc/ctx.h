@@ -169,15 +169,15 @@ struct vc_ctx {
     size_t colA = 0, colB = 0, colC = 0;    // per-column strides of bufA / bufB / bufC
     size_t offB[3], offC[6];
     int T3 = 1, nt3 = 1;   // P3 tile width and kx-tile count (tile-major X2 / R layouts)
-    bool zdirect = false;  // P3 direct-z mode (operator.cu k_p3d)
-    int ZU = 0, nog = 0, og_f[64] = {}, og_j[64] = {};
-    unsigned long long og_contig = 0;  // k_p3d groups with consecutive output planes
-    // k_p3d: octant-offset table of the (output group, source) pairs with non-consecutive planes
-    // ([ji][kZB] int16: u | sign << 15), start per pair (-1: windowed or absent)
-    vc::DevBuf<int16_t> p3tab;
-    int p3tabo[64][3] = {};
-    int p3tab_n = 0;
-    int src_contig = 0;                // sources with consecutive planes
+    bool zdirect = false;  // P3 direct-z mode (operator.cu k_p3m)
+    int ZU = 0;            // z offsets u per kernel block (direct-z)
+    int rs1 = 0;           // direct-z: K rows per kx in a tile (nblk * ZU + one zero row)
+    // k_p3m tables: A offsets [KC][MCT][32] (uint16 row | sign << 15, padded to an even count)
+    // then output rows [MCT * 8] (int32 f | plane << 4, -1 = padding)
+    vc::DevBuf<int32_t> p3m_tab;
+    int p3m_nzt = 0, p3m_kc = 0, p3m_mct = 0;  // stacked padded planes, column / row chunks
+    int p3m_nst = 2;                           // k_p3m ring depth
+    int p3m_zoff[3] = {0, 0, 0};               // first stacked position of each source
     std::vector<int32_t> h_planes;     // host copy of the plane lists
     size_t rchunk = 0;     // doubles of R per P3 tile
     int ZL = 0, nzin[3] = {0, 0, 0}, nzout[6] = {0, 0, 0, 0, 0, 0};  // active z-plane counts

@@ -11,6 +11,8 @@
 // K^{ab}(k) = phi_a(k) R^{ab}(k) conj(phi_b(k)), phi_g(k) = exp(2 pi i sum_c kt_c cg_c / M_c),
 // R real for P blocks and i*real for E blocks, even / odd (E along a) in each kt_c, so only the
 // octant 0 <= kt_c <= M_c/2 is stored; R^{yx} = R^{xy} (Eq. 12 after phase stripping).
+#include <cuda.h>
+
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -18,79 +20,9 @@
 #include "ctx.h"
 #include "fft.cuh"
 #include "kgen.cuh"
+#include "mv.cuh"
 
 namespace vc {
-
-constexpr int kMaxOG = 64;  // P3 direct-z: max output groups
-constexpr int kMaxB = 2;    // columns per batched matvec (NEXT-3; one rank, direct-z mode)
-
-struct MV {
-    int Mx, My, Mz, Kx;
-    int lo[3];
-    int G[3][3];       // slot-grid dims [orientation][axis]
-    int ext_in[3][3];  // [beta][axis]
-    int nf;
-    int fkind[6], faxis[6];
-    int ext_out[6][3];
-    const int32_t* slotmap[3];
-    const double* x;
-    double* y;
-    // batched matvec (blockIdx.z / P3 thread group = column c): x, y and the pass buffers of
-    // column c are xs[c], ys[c] and the column-0 buffers + c * col{A,B,C} (one rank only)
-    int nb;
-    const double* xs[kMaxB];
-    double* ys[kMaxB];
-    int64_t colA, colB, colC;
-    const int8_t* info;
-    const double* ibar;
-    double2* X2[3];
-    double2* X3[6];
-    // distribution: rank r owns window rows [ya[r], ya[r+1]) of the spatial
-    // passes (P1, P5) and kx columns [kxa[r], kxa[r+1]) of the spectral passes (P2-P4).  The
-    // x-transformed planes travel as blocks [source][plane][own rows][dest kx] (P1 -> P2) and
-    // [field][plane][dest rows][own kx] (P4 -> P5); the self block is written in place.
-    int W, rank;
-    int ya[kMaxRanks + 1], kxa[kMaxRanks + 1];
-    int nr[kMaxRanks][9];  // rows of rank p within source b's (0..2) / field f's (3+f) extent
-    int kx0, nkx;          // this rank's kx slab
-    int lgtk;              // one rank: X1 is kx-tile-major with 2^lgtk kx per tile (= P2's width)
-    int lgt4;              // X3 is kx-tile-major with P4's tile width 2^lgt4: [f][plane][tile][ky][t]
-    double2* S1[kMaxRanks][3];
-    const double2* R1[kMaxRanks][3];
-    double2* S2[kMaxRanks][6];
-    const double2* R2[kMaxRanks][6];
-    const double* Rt;       // tile-major: [q][kx-tile][block][kz'][t], rchunk doubles per tile
-    int rchunk;
-    int T3, lgT3;           // P3 tile width (power of two) and its log2
-    int blk[6][3];
-    int nblk;
-    const double2* tw;
-    // active z-planes (window-relative) of each source orientation / output field: only planes
-    // holding panels are transformed along x and y and stored
-    const int32_t* planes;  // [9][ZL] lists, then [9][ZL] inverse maps (plane -> index or -1)
-    int ZL;
-    int nzin[3], nzout[6];
-    // P3 direct-z mode: output groups (field, first plane) of kZB planes each
-    int zdirect, ZU, nog;
-    int og_f[kMaxOG], og_j[kMaxOG];
-    const int16_t* p3tab;  // see vc_ctx::p3tab
-    int p3tabo[kMaxOG][3], p3tab_n;
-    unsigned long long og_contig;  // bit og: the group's output planes are consecutive
-    int src_contig;                // bit b: source b's planes are consecutive
-};
-
-__device__ __forceinline__ int zlist(const MV& mv, int g, int j) { return mv.planes[g * mv.ZL + j]; }
-// rank owning window row y / kx column k (slabs are contiguous; W <= 8)
-__device__ __forceinline__ int row_owner(const MV& mv, int y) {
-    int p = 0;
-    while (y >= mv.ya[p + 1]) ++p;
-    return p;
-}
-__device__ __forceinline__ int kx_owner(const MV& mv, int k) {
-    int q = 0;
-    while (k >= mv.kxa[q + 1]) ++q;
-    return q;
-}
 
 // ---- tile-size choices (compile-time functions of the FFT length) -----------------------
 constexpr int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
@@ -119,9 +51,6 @@ template <int L> struct TY { static constexpr int T = FY<L>::T; };
 constexpr int kNT = 256;
 constexpr int kNT3 = 256;  // P3 threads per CTA
 constexpr int kMaxLz = 256;  // largest z FFT length (P3 keeps whole z-pencils in shared memory)
-constexpr int kDirectT = 16;  // P3 direct-z tile width (kx per tile = lanes per output group)
-constexpr int kZB = 4;       // P3 direct-z: output planes per thread
-constexpr int kP3dStages = 2;  // P3 direct-z TMA stages (measured: 2 beat 1 stage + more CTAs)
 
 __device__ __forceinline__ int ktil(int k, int M) { return k <= M / 2 ? k : k - M; }
 
@@ -216,12 +145,18 @@ __global__ void __launch_bounds__(FY<L>::NT) k_p2(MV mv) {
     const int nkx = mv.nkx;  // own kx slab (local column kx)
     const int ntile = (nkx + T - 1) / T;
     if (ntile == 0) return;
-    const int j = blockIdx.x / ntile, tile = blockIdx.x % ntile;
-    if (j >= mv.nzin[beta]) return;
+    // direct-z: the planes of one kx tile are adjacent blocks (their X2 elements share sectors)
+    const int nzb = mv.nzin[beta];
+    if (nzb == 0) return;
+    const int j = mv.zdirect ? blockIdx.x % nzb : blockIdx.x / ntile;
+    const int tile = mv.zdirect ? blockIdx.x / nzb : blockIdx.x % ntile;
+    if (j >= nzb || tile >= ntile) return;
     (void)ez;
-    // X2 tile-major for P3: [q][kx / T3][side][plane][kx % T3], q = |ky| (ky <= L/2: side 0)
+    // X2 tile-major for P3, q = |ky| (ky <= L/2: side 0): [q][kx / T3][side][plane][kx % T3],
+    // plane = x2zo + j of x2nz (z-FFT mode: per source; direct-z: the stacked sources, each
+    // padded to an even count, zero padding planes)
     double2* __restrict__ out = mv.X2[beta] + blockIdx.z * mv.colB;
-    const int nzb = mv.nzin[beta], nt3 = (nkx + mv.T3 - 1) >> mv.lgT3;
+    const int nt3 = (nkx + mv.T3 - 1) >> mv.lgT3;
     const bool ph = beta != 1;  // c_beta,y = 1/2 for x- and z-normal panels
     // (!D) tile `tile` of plane j: T adjacent kx of all ey rows, contiguous
     const double2* const in0 = mv.R1[0][beta] + blockIdx.z * mv.colA + (int64_t)j * ntile * ey * T;
@@ -238,8 +173,13 @@ __global__ void __launch_bounds__(FY<L>::NT) k_p2(MV mv) {
         const int k = Plan<L>::freq(p);
         if (ph) v = cmul(v, half_phase(mv.tw, ktil(k, L), L, -1));
         const int side = k > L / 2, qq = side ? L - k : k;
-        out[((((int64_t)qq * nt3 + (kx >> mv.lgT3)) * 2 + side) * nzb + j) * mv.T3 +
-            (kx & (mv.T3 - 1))] = v;
+        const int64_t ts = ((int64_t)qq * nt3 + (kx >> mv.lgT3)) * 2 + side;
+        double2* o = out + ((ts * mv.x2nz[beta] + mv.x2zo[beta] + j) << mv.lgT3) + (kx & (mv.T3 - 1));
+        o[0] = v;
+        if (mv.zdirect && j == nzb - 1) {  // zero the padding planes up to the next source's
+            const int pad = (beta < 2 ? mv.x2zo[beta + 1] : mv.x2nz[beta]) - mv.x2zo[beta] - nzb;
+            for (int e = 1; e <= pad; ++e) o[e << mv.lgT3] = czero();
+        }
     };
     fft_run<L, T, FY<L>::NT, false, true, 0, true>(sm, ld0, stN, mv.tw);
 }
@@ -678,7 +618,18 @@ __global__ void k_kgen_corner(double* __restrict__ Tb0, int Tx, int Ty, int Tz, 
 // E^{zx} -- so the folded, phase-stripped spectrum of the mirror block is the kx <-> ky
 // transpose of the original's (the strip phases and the parity octants swap with the axes):
 //   R_dst(kx, ky, w) = R_src(ky, kx, w), w = kz' (z-FFT mode) or u (direct-z mode)
-__global__ void k_rt_mirror(double* R, int K, int NW, int src, int dst, int lgT3, int RC) {
+// Index of R(kx, |ky|, block, w) in the tile-major table: z-FFT mode [block][kz'][t] per tile;
+// direct-z mode (RS1 > 0) [t][block * NW + u] with RS1 doubles per kx (k_p3m reads one kx's
+// rows contiguously; the last row of each kx is the zero row)
+__host__ __device__ __forceinline__ int64_t rt_idx(int ky, int kx, int blk, int NW, int w, int lgT3,
+                                                   int nt3, int RC, int RS1) {
+    const int64_t base = ((int64_t)ky * nt3 + (kx >> lgT3)) * RC;
+    const int t = kx & ((1 << lgT3) - 1);
+    return RS1 ? base + (int64_t)t * RS1 + (int64_t)blk * NW + w
+               : base + ((int64_t)blk * NW + w) * (1 << lgT3) + t;
+}
+
+__global__ void k_rt_mirror(double* R, int K, int NW, int src, int dst, int lgT3, int RC, int RS1) {
     const int T3 = 1 << lgT3, nt3 = (K + T3 - 1) >> lgT3;
     const int64_t tot = (int64_t)K * K * NW;
     for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < tot;
@@ -686,8 +637,7 @@ __global__ void k_rt_mirror(double* R, int K, int NW, int src, int dst, int lgT3
         const int kx = (int)(idx % K);
         const int w = (int)((idx / K) % NW);
         const int ky = (int)(idx / ((int64_t)K * NW));
-        R[((int64_t)ky * nt3 + (kx >> lgT3)) * RC + ((int64_t)dst * NW + w) * T3 + (kx & (T3 - 1))] =
-            R[((int64_t)kx * nt3 + (ky >> lgT3)) * RC + ((int64_t)src * NW + w) * T3 + (ky & (T3 - 1))];
+        R[rt_idx(ky, kx, dst, NW, w, lgT3, nt3, RC, RS1)] = R[rt_idx(kx, ky, src, NW, w, lgT3, nt3, RC, RS1)];
     }
 }
 
@@ -752,7 +702,7 @@ __global__ void k_kfill2d(double2* G, const double* __restrict__ Ko, int Mx, int
 //   E^{y.}) part; kx local to [kx0, kx0 + nkx)
 __global__ void k_extract2d(const double2* __restrict__ G, double* __restrict__ R, int Mx, int My,
                             int ZU, int kx0, int nkx, int kind, int alpha, int beta,
-                            const double2* __restrict__ tw, int blk, int lgT3, int RC) {
+                            const double2* __restrict__ tw, int blk, int lgT3, int RC, int RS1) {
     const int KY = My / 2 + 1;
     const int T3 = 1 << lgT3;
     const int nt3 = (nkx + T3 - 1) >> lgT3;
@@ -767,8 +717,7 @@ __global__ void k_extract2d(const double2* __restrict__ G, double* __restrict__ 
         double2 v = G[((int64_t)u * My + ky) * Mx + kx0 + kx];
         v = cmul(v, half_phase(tw, (kx0 + kx) * s2x, Mx, -1));
         v = cmul(v, half_phase(tw, ky * s2y, My, -1));
-        R[((int64_t)ky * nt3 + (kx >> lgT3)) * RC + ((int64_t)blk * ZU + u) * T3 + (kx & (T3 - 1))] =
-            im ? v.y : v.x;
+        R[rt_idx(ky, kx, blk, ZU, u, lgT3, nt3, RC, RS1)] = im ? v.y : v.x;
     }
 }
 
@@ -884,7 +833,7 @@ __global__ void __launch_bounds__(FY<L>::NT) k_ky_extract(double* __restrict__ R
                                                         int ZU, int kx0, int nkx, int kind,
                                                         int alpha, int beta,
                                                         const double2* __restrict__ tw, int blk,
-                                                        int lgT3, int RC) {
+                                                        int lgT3, int RC, int RS1) {
     constexpr int T = TY<L>::T;
     extern __shared__ double2 sm[];
     const int Kx = Mx / 2 + 1;
@@ -904,8 +853,7 @@ __global__ void __launch_bounds__(FY<L>::NT) k_ky_extract(double* __restrict__ R
         if (kxl >= nkx || 2 * ky > L) return;
         v = cmul(v, half_phase(tw, (kx0 + kxl) * s2x, Mx, -1));
         v = cmul(v, half_phase(tw, ky * s2y, L, -1));
-        R[((int64_t)ky * nt3 + (kxl >> lgT3)) * RC + ((int64_t)blk * ZU + u) * T3 + (kxl & (T3 - 1))] =
-            im ? v.y : v.x;
+        R[rt_idx(ky, kxl, blk, ZU, u, lgT3, nt3, RC, RS1)] = im ? v.y : v.x;
     };
     fft_run<L, T, FY<L>::NT, false, true, 0, true>(sm, ld0, stN, tw);
 }
@@ -953,17 +901,6 @@ __global__ void k_debug_kappa(int n, const int32_t* kind, const int32_t* a, cons
 // ---------------------------------------------------------------------------------------
 // launchers (compile-time FFT length dispatch)
 // ---------------------------------------------------------------------------------------
-template <class K>
-static cudaError_t prep(K kern, size_t smem) {
-    // all-shared carveout: the FFT passes are shared-memory-resident, so more CTAs per SM
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    if (e) return e;
-    // the limit is a process-wide function attribute: contexts of one process (ranks of a
-    // thread group) launch with different sizes, so always grant the device maximum (a
-    // per-launch value would race) -- occupancy follows the actual launch size
-    if (smem > 48 * 1024) return grant_max_dyn_smem(kern, max_dyn_smem());
-    return cudaSuccess;
-}
 
 #define VC_DISPATCH_L(L, ...)                                       \
     switch (L) {                                                    \
@@ -994,14 +931,6 @@ static cudaError_t launch_p1(const MV& mv, cudaStream_t st) {
         kern<<<grid, FX<LL>::NT, smem, st>>>(mv);
     });
     return cudaGetLastError();
-}
-template <class K>
-static int persistent_grid(K kern, int nthr, size_t smem, int ntiles) {
-    int per_sm = 0, nsm = 0, dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nthr, smem);
-    return std::max(1, std::min(ntiles, std::max(1, per_sm) * nsm));
 }
 template <int LL, int KB>
 static cudaError_t launch_p4s_t(const MV& mv, cudaStream_t st) {
@@ -1037,250 +966,6 @@ static cudaError_t launch_p2(const MV& mv, cudaStream_t st) {
     });
     return cudaGetLastError();
 }
-// ---------------------------------------------------------------------------------------
-// P3, direct-z mode: FFT along x and y only, direct convolution along z.
-//   out^f(kx, ky, z_o) = sum_b sum_{z_i} K^{f b}(kx, ky, z_o - z_i) Q^b(kx, ky, z_i)
-// with K the x/y-transformed, phase-stripped kernel at the geometric z offset (SURVEY App. B
-// applied to x and y only).  Exact like the z-FFT form (no circulant along z at all), and for
-// layered structures whose panels occupy few z-planes it costs sum_{f,b} n_out(f) n_in(b)
-// complex-by-real MACs per (kx, ky) instead of 3 + n_f z-FFTs.  K is stored on the z-parity
-// octant u = (|2 dz + s2| - |s2|) / 2 (s2 = 2 (c_a,z - c_b,z)): even in z except the E^{z.}
-// blocks (odd); E^{x.}, E^{y.} carry the factor i (odd along x / y) and E^{y.} the ky sign.
-// Thread = (kx t, output group of kZB planes of one field) computing both ky sides; Q loads are
-// shared by all groups of a warp (broadcast), rows of T kx are contiguous (tile-major X2, K).
-// ---------------------------------------------------------------------------------------
-// Non-consecutive planes (any output group or source whose plane list has gaps): the octant
-// offsets u(zo_k - zi) and the odd-kernel signs come precomputed from vc_ctx::p3tab, four int16
-// entries per input plane read with one 8-byte shared-memory load (a[k] += K(u) Q(zi)).
-template <int NZO, bool ODD, int T>
-__device__ __forceinline__ void p3d_acc_tab(double2 (&a0)[kZB], double2 (&a1)[kZB],
-                                            const int16_t* tb, const double* Kb, const double2* X,
-                                            int n) {
-    const double2* X1 = X + n * T;  // side 1 rows (unused when nside = 1)
-#pragma unroll 2
-    for (int ji = 0; ji < n; ++ji, X += T, X1 += T) {
-        const int2 pk = *reinterpret_cast<const int2*>(tb + kZB * ji);
-        const double2 q0 = *X;
-        const double2 q1 = *X1;
-#pragma unroll
-        for (int k = 0; k < NZO; ++k) {
-            const int w32 = k < 2 ? pk.x : pk.y;
-            const int e = (k & 1) ? (w32 >> 16) : ((w32 << 16) >> 16);  // sign-extended int16
-            double kv = Kb[(e & 0x7fff) * T];
-            if (ODD) kv = e < 0 ? -kv : kv;
-            a0[k].x = fma(kv, q0.x, a0[k].x);
-            a0[k].y = fma(kv, q0.y, a0[k].y);
-            a1[k].x = fma(kv, q1.x, a1[k].x);
-            a1[k].y = fma(kv, q1.y, a1[k].y);
-        }
-    }
-}
-
-// Contiguous output planes (zo_k = zo_0 + k) and contiguous input planes (zi = zi_0 + j): the K
-// values a thread needs for input j are the window g2 = G0 - 2 j + 2 k (k < NZO), so moving to
-// input j + 1 shifts the window by one and loads a single new value (register sliding window).
-template <int NZO, bool ODD, int T>
-__device__ __forceinline__ void p3d_acc_win(double2 (&a0)[kZB], double2 (&a1)[kZB], int G0,
-                                            int s2a, const double* Kb, const double2* X, int n) {
-    auto kval = [&](int g2) {
-        const double v = Kb[(((g2 < 0 ? -g2 : g2) - s2a) >> 1) * T];
-        return (ODD && g2 < 0) ? -v : v;
-    };
-    double w[NZO];
-#pragma unroll
-    for (int k = 0; k < NZO; ++k) w[k] = kval(G0 + 2 * k);
-    const double2* X1 = X + n * T;  // side 1 rows (unused when nside = 1)
-#pragma unroll 2
-    for (int ji = 0; ji < n; ++ji, X += T, X1 += T) {
-        const double2 q0 = *X;
-        const double2 q1 = *X1;
-#pragma unroll
-        for (int k = 0; k < NZO; ++k) {
-            a0[k].x = fma(w[k], q0.x, a0[k].x);
-            a0[k].y = fma(w[k], q0.y, a0[k].y);
-            a1[k].x = fma(w[k], q1.x, a1[k].x);
-            a1[k].y = fma(w[k], q1.y, a1[k].y);
-        }
-#pragma unroll
-        for (int k = NZO - 1; k > 0; --k) w[k] = w[k - 1];
-        w[0] = kval(G0 - 2 * (ji + 1));
-    }
-}
-
-// Persistent and TMA-fed like the z-FFT P3: a tile's X2 rows and K rows are contiguous (tile-
-// major layouts), so one thread fetches the next tile with four cp.async.bulk copies into the
-// other half of a two-stage ring while the CTA computes the current tile from shared memory.
-// Batched (mv.nb columns): the CTA holds one thread group per column; the groups share each
-// tile's K rows (fetched once) and get their own X2 rows, so the kernel spectra are read from
-// HBM once per tile for all columns.
-template <int NST>  // stages of the TMA ring (1: no prefetch, more CTAs per SM)
-__global__ void __launch_bounds__(512) k_p3d(MV mv) {
-    constexpr int T = kDirectT;
-    extern __shared__ __align__(16) double2 sd[];
-    const int NB = mv.nb, nthr1 = blockDim.x / NB;
-    const int col = threadIdx.x / nthr1, tid1 = threadIdx.x - col * nthr1;
-    const int t = tid1 % T, og0 = tid1 / T, OGS = nthr1 / T;
-    const int nkx = mv.nkx, My = mv.My, ZL = mv.ZL;
-    const int nt3 = (nkx + T - 1) / T;
-    const int nt4 = (nkx + (1 << mv.lgt4) - 1) >> mv.lgt4;  // X3 tiles (P4's width)
-    const int ntiles = nt3 * (My / 2 + 1);
-    const int nz0 = mv.nzin[0], nz1 = mv.nzin[1], nz2 = mv.nzin[2];
-    const int xo1 = 2 * T * nz0, xo2 = 2 * T * (nz0 + nz1);
-    const int XS = 2 * T * (nz0 + nz1 + nz2);  // double2 per stage
-    const int RC = mv.rchunk;                  // doubles per stage (even)
-    double2* xin = sd;                                          // [NST][NB][XS]
-    double* kin = reinterpret_cast<double*>(xin + NST * NB * XS);  // [NST][RC]
-    int* zl = reinterpret_cast<int*>(kin + NST * RC);           // [9][ZL] plane lists
-    uint64_t* bar = reinterpret_cast<uint64_t*>(zl + ((9 * ZL + 3) & ~3));  // [2]
-    int16_t* ptab = reinterpret_cast<int16_t*>(bar + 2);                    // [p3tab_n]
-    for (int e = threadIdx.x; e < mv.p3tab_n; e += blockDim.x) ptab[e] = mv.p3tab[e];
-    if (threadIdx.x == 0) {
-        mbar_init(&bar[0], 1);
-        mbar_init(&bar[1], 1);
-        fence_mbar_init();
-    }
-    // plane lists; source lists doubled (zi2 = 2 zi) for the offset arithmetic
-    for (int e = threadIdx.x; e < 9 * ZL; e += blockDim.x) zl[e] = mv.planes[e] * (e < 3 * ZL ? 2 : 1);
-    __syncthreads();
-    auto issue = [&](int tl, int s) {  // one thread: fetch tile tl into stage s
-        const size_t qt = (size_t)tl;
-        mbar_arrive_expect_tx(&bar[s], (unsigned)(16 * NB * XS + 8 * RC));
-        for (int c = 0; c < NB; ++c) {
-            double2* xd = xin + (s * NB + c) * XS;
-            const int64_t co = c * mv.colB;
-            if (nz0) bulk_g2s(xd, mv.X2[0] + co + qt * 2 * T * nz0, 32u * T * nz0, &bar[s]);
-            if (nz1) bulk_g2s(xd + xo1, mv.X2[1] + co + qt * 2 * T * nz1, 32u * T * nz1, &bar[s]);
-            if (nz2) bulk_g2s(xd + xo2, mv.X2[2] + co + qt * 2 * T * nz2, 32u * T * nz2, &bar[s]);
-        }
-        bulk_g2s(kin + s * RC, mv.Rt + qt * RC, 8u * RC, &bar[s]);
-    };
-    if (NST > 1 && threadIdx.x == 0 && (int)blockIdx.x < ntiles) issue(blockIdx.x, 0);
-    unsigned par0 = 0, par1 = 0;
-    int it = 0;
-    for (int tl = blockIdx.x; tl < ntiles; tl += gridDim.x, ++it) {
-        const int st = NST == 1 ? 0 : (it & 1);
-        if (threadIdx.x == 0) {
-            const int nxt = tl + (NST - 1) * (int)gridDim.x;
-            if (nxt < ntiles) {
-                fence_proxy_async();
-                issue(nxt, NST == 1 ? 0 : (st ^ 1));
-            }
-        }
-        if (st == 0) { mbar_wait(&bar[0], par0); par0 ^= 1; }
-        else { mbar_wait(&bar[1], par1); par1 ^= 1; }
-        const double2* xs = xin + (st * NB + col) * XS;
-        const double* ks = kin + st * RC;
-        const int q = tl / nt3, xt = tl % nt3;
-        const int kx = xt * T + t;
-        const bool valid = kx < nkx;
-        const int nside = (q == 0 || 2 * q == My) ? 1 : 2;
-        for (int og = og0; og < mv.nog; og += OGS) {
-            const int f = mv.og_f[og], jo0 = mv.og_j[og];
-            if (f < 0) continue;  // padding slot: keeps the warp's two groups alike
-            const int nzo = min(kZB, mv.nzout[f] - jo0);
-            const int kind = mv.fkind[f], alpha = mv.faxis[f];
-            double2 a0[kZB], a1[kZB];
-#pragma unroll
-            for (int k = 0; k < kZB; ++k) a0[k] = a1[k] = czero();
-#pragma unroll
-            for (int b = 0; b < 3; ++b) {
-                const int bk = mv.blk[f][b];
-                if (bk < 0) continue;
-                const int s2 = c2(alpha, 2) - c2(b, 2);
-                int zo2[kZB];
-#pragma unroll
-                for (int k = 0; k < kZB; ++k)
-                    zo2[k] = 2 * (k < nzo ? zl[(3 + f) * ZL + jo0 + k] : 0) + s2;
-                const double* Kb = ks + bk * mv.ZU * T + t;
-                const int nzb = b == 0 ? nz0 : (b == 1 ? nz1 : nz2);
-                const double2* X = xs + (b == 0 ? 0 : (b == 1 ? xo1 : xo2)) + t;
-                const int* zi2 = zl + b * ZL;
-                const int s2a = s2 != 0;
-                if (((mv.og_contig >> og) & 1) && ((mv.src_contig >> b) & 1)) {
-                    const int G0 = zo2[0] - zi2[0];
-                    if (kind == 1 && alpha == 2) {
-                        switch (nzo) {
-                            case 1: p3d_acc_win<1, true, T>(a0, a1, G0, s2a, Kb, X, nzb); break;
-                            case 2: p3d_acc_win<2, true, T>(a0, a1, G0, s2a, Kb, X, nzb); break;
-                            case 3: p3d_acc_win<3, true, T>(a0, a1, G0, s2a, Kb, X, nzb); break;
-                            default: p3d_acc_win<4, true, T>(a0, a1, G0, s2a, Kb, X, nzb); break;
-                        }
-                    } else {
-                        switch (nzo) {
-                            case 1: p3d_acc_win<1, false, T>(a0, a1, G0, s2a, Kb, X, nzb); break;
-                            case 2: p3d_acc_win<2, false, T>(a0, a1, G0, s2a, Kb, X, nzb); break;
-                            case 3: p3d_acc_win<3, false, T>(a0, a1, G0, s2a, Kb, X, nzb); break;
-                            default: p3d_acc_win<4, false, T>(a0, a1, G0, s2a, Kb, X, nzb); break;
-                        }
-                    }
-                } else {
-                    const int16_t* tb = ptab + mv.p3tabo[og][b];
-                    if (kind == 1 && alpha == 2) {  // E^{z.}: odd in z
-                        switch (nzo) {
-                            case 1: p3d_acc_tab<1, true, T>(a0, a1, tb, Kb, X, nzb); break;
-                            case 2: p3d_acc_tab<2, true, T>(a0, a1, tb, Kb, X, nzb); break;
-                            case 3: p3d_acc_tab<3, true, T>(a0, a1, tb, Kb, X, nzb); break;
-                            default: p3d_acc_tab<4, true, T>(a0, a1, tb, Kb, X, nzb); break;
-                        }
-                    } else {
-                        switch (nzo) {
-                            case 1: p3d_acc_tab<1, false, T>(a0, a1, tb, Kb, X, nzb); break;
-                            case 2: p3d_acc_tab<2, false, T>(a0, a1, tb, Kb, X, nzb); break;
-                            case 3: p3d_acc_tab<3, false, T>(a0, a1, tb, Kb, X, nzb); break;
-                            default: p3d_acc_tab<4, false, T>(a0, a1, tb, Kb, X, nzb); break;
-                        }
-                    }
-                }
-            }
-            if (!valid) continue;
-            double2* __restrict__ X3 = mv.X3[f] + col * mv.colC;
-            const bool ifac = kind == 1 && alpha != 2;  // E^{x.}, E^{y.}: R stores Im(K)
-#pragma unroll
-            for (int k = 0; k < kZB; ++k) {
-                if (k >= nzo) break;
-#pragma unroll
-                for (int side = 0; side < 2; ++side) {
-                    if (side >= nside) break;
-                    double2 a = side ? a1[k] : a0[k];
-                    if (ifac) {
-                        const bool neg = alpha == 1 && side == 1;  // odd along y: ky < 0 side
-                        a = neg ? make_double2(a.y, -a.x) : make_double2(-a.y, a.x);
-                    }
-                    X3[(((int64_t)(jo0 + k) * nt4 + (kx >> mv.lgt4)) * My + (side ? My - q : q))
-                           << mv.lgt4 | (kx & ((1 << mv.lgt4) - 1))] = a;
-                }
-            }
-        }
-        __syncthreads();  // stage st is refilled by the issue two iterations on
-    }
-}
-
-static size_t p3d_smem(const MV& mv) {
-    return kP3dStages * (16 * (size_t)2 * kDirectT * (mv.nzin[0] + mv.nzin[1] + mv.nzin[2]) * mv.nb +
-                         8 * (size_t)mv.rchunk) +
-           4 * (size_t)((9 * mv.ZL + 3) & ~3) + 2 * sizeof(uint64_t) + 2 * (size_t)mv.p3tab_n + 16;
-}
-static cudaError_t launch_p3d(const MV& mv, cudaStream_t st) {
-    const int nt3 = (mv.nkx + kDirectT - 1) / kDirectT;
-    const int ntiles = nt3 * (mv.My / 2 + 1);
-    if (ntiles == 0 || mv.nog == 0) return cudaSuccess;
-    const int ogs = std::min(mv.nog, 256 / kDirectT);
-    const int nthr = kDirectT * ogs * mv.nb;
-    constexpr int NST = kP3dStages;
-    static_assert(kP3dStages == NST, "p3d_smem uses kP3dStages");
-    const size_t smem = p3d_smem(mv);
-    if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
-    cudaError_t e = prep(k_p3d<NST>, smem);
-    if (e) return e;
-    int per_sm = 0, nsm = 0, dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_p3d<NST>, nthr, smem);
-    const int grid = std::max(1, std::min(ntiles, std::max(1, per_sm) * nsm));
-    k_p3d<NST><<<grid, nthr, smem, st>>>(mv);
-    return cudaGetLastError();
-}
-
 template <int L, int NF>
 static size_t p3_smem(const MV& mv) {
     constexpr int W = P3T<L, NF>::W, T = P3T<L, NF>::T;
@@ -1317,9 +1002,9 @@ static cudaError_t launch_p3_l(const MV& mv, cudaStream_t st) {
         default: return cudaErrorInvalidValue;
     }
 }
+static bool p3m_batched(const MV& mv) { return mv.zdirect != 0; }
 static cudaError_t launch_p3(const MV& mv, cudaStream_t st) {
-    if (mv.nb > 1 && !(mv.zdirect && p3d_smem(mv) <= 227 * 1024 &&
-                       kDirectT * std::min(mv.nog, 256 / kDirectT) * mv.nb <= 512)) {
+    if (mv.nb > 1 && !p3m_batched(mv)) {
         // column by column (z-FFT mode, or the batched tile does not fit one CTA)
         for (int c = 0; c < mv.nb; ++c) {
             MV m1 = mv;
@@ -1331,7 +1016,7 @@ static cudaError_t launch_p3(const MV& mv, cudaStream_t st) {
         }
         return cudaSuccess;
     }
-    if (mv.zdirect) return launch_p3d(mv, st);
+    if (mv.zdirect) return launch_p3m(mv, st);
     cudaError_t e;
     switch (mv.Mz) {  // kMaxLz: the [L][W] pencil buffer must fit one CTA's shared memory
         case 8: e = launch_p3_l<8>(mv, st); break;
@@ -1394,7 +1079,7 @@ static cudaError_t launch_kx_r2c(double2* Gx, const double* Ko, int Mx, int My, 
 }
 static cudaError_t launch_ky_extract(double* R, const double2* Gx, int Mx, int My, int ZU, int kx0,
                                      int nkx, int kind, int alpha, int beta, const double2* tw,
-                                     int blk, int lgT3, int RC, cudaStream_t st) {
+                                     int blk, int lgT3, int RC, int RS1, cudaStream_t st) {
     VC_DISPATCH_L(My, {
         constexpr int T = TY<LL>::T;
         const size_t smem = sizeof(double2) * LL * T;
@@ -1402,7 +1087,7 @@ static cudaError_t launch_ky_extract(double* R, const double2* Gx, int Mx, int M
         if (e) return e;
         const unsigned grid = (unsigned)(ZU * ((nkx + T - 1) / T));
         if (grid) k_ky_extract<LL><<<grid, FY<LL>::NT, smem, st>>>(R, Gx, Mx, ZU, kx0, nkx, kind, alpha,
-                                                                 beta, tw, blk, lgT3, RC);
+                                                                 beta, tw, blk, lgT3, RC, RS1);
     });
     return cudaGetLastError();
 }
@@ -1598,101 +1283,94 @@ vc_status operator_build(vc_ctx* c, const vc_build_opts* o) {
     // z-FFTs (complex-by-real MACs vs a radix-2 estimate of 3 + n_f transforms of length Mz)
     {
         double mac = 0;
-        int nog = 0;
+        int nrows = 0;
         for (int f = 0; f < c->nf; ++f) {
             for (int b = 0; b < 3; ++b)
                 if (c->blk[f][b] >= 0) mac += (double)c->nzout[f] * c->nzin[b];
-            const int gpw = 32 / kDirectT, ng = (c->nzout[f] + kZB - 1) / kZB;
-            nog += (ng + gpw - 1) / gpw * gpw;
+            nrows += c->nzout[f];
         }
+        // k_p3m columns: stacked plane positions, each source padded to an even count (X2
+        // sectors never straddle two sources) and the total to a multiple of 4
+        int zoff[3], nzp = 0;
+        for (int b = 0; b < 3; ++b) {
+            zoff[b] = nzp;
+            nzp += (c->nzin[b] + 1) & ~1;
+        }
+        nzp = (nzp + 3) & ~3;
         const double fft = 0.6 * (3 + c->nf) * 5.0 * Mz * ilog2c(Mz);
         const int zmode = o ? o->zmode : 0;
         if (zmode < 0 || zmode > 2) return set_err(c, VC_ERR_INPUT, "zmode must be 0, 1 or 2");
-        // k_p3d stages one tile (X2 rows, K tile, plane lists) in shared memory
-        const double smem = 2 * (16.0 * 2 * kDirectT * (c->nzin[0] + c->nzin[1] + c->nzin[2]) +
-                                 8.0 * std::max(1, c->nblk) * c->ZL * kDirectT) +
-                            4.0 * 9 * c->ZL + 64;
-        c->zdirect = nog <= kMaxOG && smem <= 200.0 * 1024 &&
+        // k_p3m: stacked rows in 8-row chunks, split into balanced passes of <= kMmaMC chunks
+        const int mct0 = (nrows + 7) / 8, npass = std::max(1, (mct0 + kMmaMC - 1) / kMmaMC);
+        const int mct = npass * ((mct0 + npass - 1) / npass), kc = nzp / 4;
+        const int rs1 = std::max(1, c->nblk) * c->ZL + 1;
+        // ring depth: 2 measured fastest on C4 (0.538 / 0.546 / 0.550 / 0.559 ms for 2 / 3 / 4 / 5
+        // stages per pair launch); VC_P3M_NST overrides it (A/B), bounded by what fits
+        const int nst_fit = p3m_stages(rs1, nzp, kc, mct);
+        const int nst = std::min(nst_fit, getenv("VC_P3M_NST") ? std::max(2, atoi(getenv("VC_P3M_NST"))) : 2);
+        c->zdirect = nrows <= kMaxRows && nzp > 0 && nzp + 4 <= 256 && rs1 <= 0x7fff && nst_fit >= 2 &&
                      (zmode == 2 || (zmode == 0 && 4.0 * mac <= fft));
         if (zmode == 2 && !c->zdirect)
-            return set_err(c, VC_ERR_UNSUPPORTED, "direct-z mode: too many output planes");
+            return set_err(c, VC_ERR_UNSUPPORTED, "direct-z mode: too many output planes or input planes");
         c->ZU = c->ZL;
-        c->nog = 0;
-        c->og_contig = 0;
-        c->src_contig = 0;
+        c->rs1 = c->zdirect ? rs1 : 0;
+        c->p3m_nzt = c->p3m_kc = c->p3m_mct = 0;
         auto plane = [&](int g, int j) { return c->h_planes[(size_t)g * c->ZL + j]; };
         if (c->zdirect) {
-            // the groups of a warp (32 / kDirectT of them) must follow one code path: same plane
-            // count, same contiguity, same z parity (E^{z.}) and the same sources present.  Groups
-            // are binned by that signature (across fields: C^x and C^y share warps) and a bin's
-            // last warp is padded with null groups.
-            const int gpw = 32 / kDirectT;
-            struct Og { int f, j, key; bool contig; };
-            std::vector<Og> ogs;
+            // DMMA fragment tables of k_p3m (see the kernel): A[r][c] = K^{f_r b_c}(u(z_r - z_c)),
+            // uint16 row | sign << 15, [KC][MCT][32]; then the output rows (f | plane << 4)
+            std::vector<int32_t> rows(8 * (size_t)mct, -1), cols(nzp, -1);
+            int r = 0;
             for (int f = 0; f < c->nf; ++f)
-                for (int j = 0; j < c->nzout[f]; j += kZB) {
-                    const int nzo = std::min(kZB, c->nzout[f] - j);
-                    const bool contig = plane(3 + f, j + nzo - 1) - plane(3 + f, j) == nzo - 1;
-                    int mask = 0;
-                    for (int b = 0; b < 3; ++b) mask |= (c->blk[f][b] >= 0) << b;
-                    const int odd = c->f[f].kind == 1 && c->f[f].axis == 2;
-                    static const bool pair = getenv("VC_OGPAIR") == nullptr || atoi(getenv("VC_OGPAIR"));
-                    ogs.push_back({f, j, pair ? ((nzo * 2 + (contig ? 1 : 0)) * 2 + odd) * 8 + mask : f, contig});
-                }
-            std::stable_sort(ogs.begin(), ogs.end(), [](const Og& x, const Og& y) { return x.key < y.key; });
-            for (size_t i = 0; i < ogs.size();) {
-                size_t e = i;
-                while (e < ogs.size() && ogs[e].key == ogs[i].key) ++e;
-                int ng = 0;
-                for (; i < e; ++i, ++ng) {
-                    if (ogs[i].contig) c->og_contig |= 1ull << c->nog;
-                    c->og_f[c->nog] = ogs[i].f;
-                    c->og_j[c->nog] = ogs[i].j;
-                    ++c->nog;
-                }
-                for (; ng % gpw; ++ng) {
-                    c->og_f[c->nog] = -1;
-                    c->og_j[c->nog] = 0;
-                    ++c->nog;
-                }
-            }
+                for (int j = 0; j < c->nzout[f]; ++j) rows[r++] = f | j << 4;
             for (int b = 0; b < 3; ++b)
-                if (c->nzin[b] > 0 && plane(b, c->nzin[b] - 1) - plane(b, 0) == c->nzin[b] - 1)
-                    c->src_contig |= 1 << b;
-            // octant-offset table of the pairs k_p3d cannot window (non-consecutive planes)
-            std::vector<int16_t> tab;
-            for (int g = 0; g < c->nog; ++g)
-                for (int b = 0; b < 3; ++b) {
-                    c->p3tabo[g][b] = -1;
-                    const int f = c->og_f[g];
-                    if (f < 0 || c->blk[f][b] < 0) continue;
-                    if (((c->og_contig >> g) & 1) && ((c->src_contig >> b) & 1)) continue;
-                    const int nzo = std::min(kZB, c->nzout[f] - c->og_j[g]);
-                    const int s2 = c2(c->f[f].axis, 2) - c2(b, 2), s2a = s2 != 0;
-                    c->p3tabo[g][b] = (int)tab.size();
-                    for (int j = 0; j < c->nzin[b]; ++j)
-                        for (int k = 0; k < kZB; ++k) {
-                            const int zo2 = 2 * (k < nzo ? plane(3 + f, c->og_j[g] + k) : 0) + s2;
-                            const int g2 = zo2 - 2 * plane(b, j);
-                            const int u = ((g2 < 0 ? -g2 : g2) - s2a) >> 1;
-                            tab.push_back((int16_t)(u | (g2 < 0 ? 0x8000 : 0)));
+                for (int j = 0; j < c->nzin[b]; ++j) cols[zoff[b] + j] = b << 16 | j;
+            const int zero_row = rs1 - 1;
+            std::vector<uint16_t> at;
+            at.reserve((size_t)kc * mct * 32 + 1);
+            for (int k = 0; k < kc; ++k)
+                for (int m = 0; m < mct; ++m)
+                    for (int l = 0; l < 32; ++l) {
+                        const int rr = m * 8 + l / 4, cc = k * 4 + l % 4;
+                        uint16_t e = (uint16_t)zero_row;
+                        if (rows[rr] >= 0 && cols[cc] >= 0) {
+                            const int f = rows[rr] & 15, jo = rows[rr] >> 4;
+                            const int b = cols[cc] >> 16, ji = cols[cc] & 0xffff;
+                            const int bk = c->blk[f][b];
+                            if (bk >= 0) {
+                                const int s2 = c2(c->f[f].axis, 2) - c2(b, 2);
+                                const int g2 = 2 * plane(3 + f, jo) + s2 - 2 * plane(b, ji);
+                                const int u = ((g2 < 0 ? -g2 : g2) - (s2 != 0)) >> 1;
+                                if (u < 0 || u >= c->ZU) return set_err(c, VC_ERR_INPUT, "direct-z offset out of range");
+                                const bool odd = c->f[f].kind == 1 && c->f[f].axis == 2;
+                                e = (uint16_t)((bk * c->ZU + u) | (odd && g2 < 0 ? 0x8000 : 0));
+                            }
                         }
-                }
-            c->p3tab_n = (int)tab.size();
-            VC_CUDA(c, c->p3tab.alloc(std::max<size_t>(4, tab.size())));
-            if (!tab.empty())
-                VC_CUDA(c, cudaMemcpyAsync(c->p3tab.p, tab.data(), 2 * tab.size(), cudaMemcpyHostToDevice, st));
+                        at.push_back(e);
+                    }
+            if (at.size() & 1) at.push_back(0);
+            std::vector<int32_t> tab(at.size() / 2 + rows.size());
+            memcpy(tab.data(), at.data(), 2 * at.size());
+            memcpy(tab.data() + at.size() / 2, rows.data(), 4 * rows.size());
+            c->p3m_nzt = nzp;
+            c->p3m_nst = nst;
+            c->p3m_kc = kc;
+            c->p3m_mct = mct;
+            for (int b = 0; b < 3; ++b) c->p3m_zoff[b] = zoff[b];
+            VC_CUDA(c, c->p3m_tab.alloc(tab.size()));
+            VC_CUDA(c, cudaMemcpyAsync(c->p3m_tab.p, tab.data(), 4 * tab.size(), cudaMemcpyHostToDevice, st));
             VC_CUDA(c, cudaStreamSynchronize(st));
         }
     }
     tr.mark("plans");
     // P3 tile width and the tile-major spectrum layout (one contiguous chunk per P3 tile)
-    c->T3 = c->zdirect ? kDirectT : p3_tile(Mz, c->nf);
+    c->T3 = c->zdirect ? kMmaT : p3_tile(Mz, c->nf);
     plan_kx_slabs(c->world, Kx, c->T3, c->kxa);
     const int kx0 = c->kxa[c->rank], nkx = c->kxa[c->rank + 1] - kx0;
     c->nt3 = (nkx + c->T3 - 1) / c->T3;
-    c->rchunk = ((size_t)std::max(1, c->nblk) * (c->zdirect ? c->ZU : Mz / 2 + 1) * c->T3 + 1) &
-                ~(size_t)1;
+    // direct-z: [t][block * ZU + u] plus one zero row per kx (k_p3m's absent / padding entries)
+    c->rchunk = c->zdirect ? (size_t)c->T3 * c->rs1
+                           : ((size_t)std::max(1, c->nblk) * (Mz / 2 + 1) * c->T3 + 1) & ~(size_t)1;
     VC_CUDA(c, c->tw.alloc(kTabN));
     k_twiddles<<<(kTabN + 255) / 256, 256, 0, st>>>(c->tw.p);
     count_launch(c);
@@ -1804,7 +1482,7 @@ vc_status operator_build(vc_ctx* c, const vc_build_opts* o) {
                 VC_CUDA(c, cudaEventRecord(ev[2], st));
                 const int64_t mt = (int64_t)Kx * Kx * NW;
                 k_rt_mirror<<<(int)std::min<int64_t>((mt + 255) / 256, 148 * 32), 256, 0, st>>>(
-                    c->Rt.p, Kx, NW, mirror_of[i], i, ilog2c(c->T3), (int)c->rchunk);
+                    c->Rt.p, Kx, NW, mirror_of[i], i, ilog2c(c->T3), (int)c->rchunk, c->rs1);
                 count_launch(c);
                 VC_CUDA(c, cudaEventRecord(ev[3], st));
                 continue;
@@ -1819,7 +1497,7 @@ vc_status operator_build(vc_ctx* c, const vc_build_opts* o) {
                 VC_CUDA(c, cudaEventRecord(ev[1], st));
                 VC_CUDA(c, cudaEventRecord(ev[2], st));
                 VC_CUDA(c, launch_ky_extract(c->Rt.p, G.p, M[0], M[1], MZ, kx0, nkx, d.kind, d.alpha,
-                                             d.beta, c->tw.p, i, ilog2c(c->T3), (int)c->rchunk, st));
+                                             d.beta, c->tw.p, i, ilog2c(c->T3), (int)c->rchunk, c->rs1, st));
                 VC_CUDA(c, cudaEventRecord(ev[3], st));
                 count_launch(c, 3);
                 continue;
@@ -1840,7 +1518,7 @@ vc_status operator_build(vc_ctx* c, const vc_build_opts* o) {
             if (zd)
                 k_extract2d<<<eblocks, 256, 0, st>>>(G.p, c->Rt.p, M[0], M[1], c->ZU, kx0, nkx, d.kind,
                                                      d.alpha, d.beta, c->tw.p, i, ilog2c(c->T3),
-                                                     (int)c->rchunk);
+                                                     (int)c->rchunk, c->rs1);
             else
                 k_extract<<<eblocks, 256, 0, st>>>(G.p, c->Rt.p, M[0], M[1], M[2], kx0, nkx, d.kind, d.alpha,
                                                    d.beta, 1.0, c->tw.p, i, ilog2c(c->T3),
@@ -1907,8 +1585,10 @@ vc_status operator_build(vc_ctx* c, const vc_build_opts* o) {
             if (p != rk) nS2 += (size_t)c->nzout[f] * c->nr[p][3 + f] * nkx;
         }
     for (int b = 0; b < 3; ++b) {
-        c->offB[b] = nBt;
-        nBt += (size_t)(My / 2 + 1) * c->nt3 * 2 * c->nzin[b] * c->T3;  // tile-major, padded
+        // tile-major, padded; direct-z: one stacked-plane array for the three sources (k_p3m)
+        c->offB[b] = c->zdirect ? 0 : nBt;
+        if (!c->zdirect || b == 0)
+            nBt += (size_t)(My / 2 + 1) * c->nt3 * 2 * (c->zdirect ? c->p3m_nzt : c->nzin[b]) * c->T3;
     }
     for (int f = 0; f < c->nf; ++f) {
         c->offC[f] = nC;
@@ -2122,17 +1802,16 @@ static MV make_mv(vc_ctx* c, const double* x, double* y) {
     mv.ZL = c->ZL;
     mv.zdirect = c->zdirect;
     mv.ZU = c->ZU;
-    mv.nog = c->nog;
-    mv.og_contig = c->og_contig;
-    mv.p3tab = c->p3tab.p;
-    mv.p3tab_n = c->p3tab_n;
-    for (int g = 0; g < kMaxOG; ++g)
-        for (int b = 0; b < 3; ++b) mv.p3tabo[g][b] = g < c->nog ? c->p3tabo[g][b] : -1;
-    mv.src_contig = c->src_contig;
-    for (int g = 0; g < c->nog; ++g) {
-        mv.og_f[g] = c->og_f[g];
-        mv.og_j[g] = c->og_j[g];
+    mv.rs1 = c->rs1;
+    for (int b = 0; b < 3; ++b) {
+        mv.x2nz[b] = c->zdirect ? c->p3m_nzt : c->nzin[b];
+        mv.x2zo[b] = c->zdirect ? c->p3m_zoff[b] : 0;
     }
+    mv.p3m_tab = c->p3m_tab.p;
+    mv.p3m_nzt = c->p3m_nzt;
+    mv.p3m_kc = c->p3m_kc;
+    mv.p3m_mct = c->p3m_mct;
+    mv.p3m_nst = c->p3m_nst;
     for (int b = 0; b < 3; ++b) mv.nzin[b] = c->nzin[b];
     for (int f = 0; f < 6; ++f) mv.nzout[f] = f < c->nf ? c->nzout[f] : 0;
     const int W = c->world, r = c->rank;
@@ -2258,7 +1937,7 @@ static vc_status matvec_run(vc_ctx* c, const MV& mv) {
         c->stats.n_pass[p] += 1;
         // a batched P3 launch reads the kernel spectra once for its columns (z-FFT mode and
         // oversized tiles run P3 column by column: nb reads)
-        const bool shared_k = p == 2 && mv.zdirect && mv.nb > 1 && p3d_smem(mv) <= 227 * 1024;
+        const bool shared_k = p == 2 && mv.nb > 1 && p3m_batched(mv);
         c->stats.bytes_moved[p] += mv.nb * c->bytes_pass[p] - (shared_k ? (mv.nb - 1) * c->bytes_k3 : 0.0);
     }
     return VC_OK;

@@ -241,6 +241,16 @@ vc_status vc_debug_kernel_entries(vc_ctx* ctx, int32_t n, const int32_t* kind,
                                   const int32_t* alpha, const int32_t* beta, const int32_t* d,
                                   double* out);
 vc_status vc_debug_fft(vc_ctx* ctx, int32_t L, int32_t n_lines, double* data, int32_t dir);
+/* Test hook (documented, stable): the folded, phase-stripped kernel spectra of the built operator
+ * (Eqs. 11-12 after App. B folding; DESIGN.md §6 "R").  layout[8] receives {zdirect, nblk, NW,
+ * T3, nt3, KY, RS1, nkx}: the table is [KY][nt3][...] tiles of rchunk doubles; direct-z tiles are
+ * [T3][RS1] with row = block * NW + u (NW = ZU z offsets, last row zero), z-FFT tiles are
+ * [block][NW = Mz/2 + 1][T3].  *n receives the table length in doubles.  vc_debug_get_spectra
+ * copies it to host `out` (NULL: sizes only); vc_debug_set_spectra overwrites it from host `in`
+ * (n doubles; VC_ERR_INPUT on a length mismatch) -- used to measure what a compressed (e.g.
+ * Tucker) spectrum does to the matvec.  VC_ERR_STATE before vc_build_operator. */
+vc_status vc_debug_get_spectra(vc_ctx* ctx, int64_t* n, int32_t* layout, double* out);
+vc_status vc_debug_set_spectra(vc_ctx* ctx, int64_t n, const double* in);
 
 /* Last error message of the context ("" if none).  Valid until the next call on ctx. */
 const char* vc_last_error(const vc_ctx* ctx);

@@ -27,7 +27,7 @@ EXPORTS = ("vc_create", "vc_set_geometry", "vc_get_sizes", "vc_get_panels", "vc_
            "vc_set_timing", "vc_get_stats", "vc_reset_stats", "vc_debug_kernel_entries",
            "vc_debug_fft", "vc_last_error", "vc_version", "vc_destroy", "vc_init_distributed",
            "vc_nccl_unique_id", "vc_group_create", "vc_group_destroy", "vc_get_local_panels",
-           "vc_plan_slabs")
+           "vc_plan_slabs", "vc_debug_get_spectra", "vc_debug_set_spectra")
 
 STATUS = {0: "VC_OK", 1: "VC_ERR_INPUT", 2: "VC_ERR_STATE", 3: "VC_ERR_OOM", 4: "VC_ERR_CUDA",
           5: "VC_ERR_NCCL", 6: "VC_NOT_CONVERGED", 7: "VC_ERR_UNSUPPORTED"}
@@ -121,6 +121,8 @@ def load_library(build_if_missing=False):
         "vc_reset_stats": [vp],
         "vc_debug_kernel_entries": [vp, i32, vp, vp, vp, vp, vp],
         "vc_debug_fft": [vp, i32, i32, vp, i32],
+        "vc_debug_get_spectra": [vp, P(i64), vp, vp],
+        "vc_debug_set_spectra": [vp, i64, vp],
         "vc_init_distributed": [vp, i32, i32, i32, vp],
         "vc_nccl_unique_id": [vp],
         "vc_group_create": [i32, P(vp)],
@@ -434,6 +436,21 @@ class VoxCap:
         self._check(self._lib.vc_debug_kernel_entries(self._ctx, n, _ptr(kind), _ptr(alpha),
                                                       _ptr(beta), _ptr(d), _ptr(out)))
         return out
+
+    def spectra(self):
+        """Folded kernel-spectrum table (test hook): (raw float64 array, layout dict)."""
+        n = ctypes.c_int64()
+        lay = np.zeros(8, np.int32)
+        self._check(self._lib.vc_debug_get_spectra(self._ctx, ctypes.byref(n), _ptr(lay), None))
+        out = np.empty(n.value, np.float64)
+        self._check(self._lib.vc_debug_get_spectra(self._ctx, ctypes.byref(n), _ptr(lay), _ptr(out)))
+        keys = ("zdirect", "nblk", "NW", "T3", "nt3", "KY", "RS1", "nkx")
+        return out, dict(zip(keys, (int(v) for v in lay)))
+
+    def set_spectra(self, table):
+        """Overwrite the kernel-spectrum table (test hook; same length and layout)."""
+        a = np.ascontiguousarray(table, dtype=np.float64)
+        self._check(self._lib.vc_debug_set_spectra(self._ctx, a.size, _ptr(a)))
 
     def fft(self, data, inverse=False):
         """Device batched FFT along the last axis (test hook); complex128 in, complex128 out."""

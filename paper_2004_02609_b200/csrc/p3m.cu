@@ -83,8 +83,10 @@ template <int MC, int KCM, bool KS>
 __global__ void __launch_bounds__(kMmaT * kMmaSplit * 32, 1)
     k_p3m(const __grid_constant__ CUtensorMap tmx0, const __grid_constant__ CUtensorMap tmx1, MV mv) {
     constexpr int T = kMmaT, NW = kMmaT * kMmaSplit, NTHR = NW * 32;
-    extern __shared__ uint8_t smraw[];
-    uint8_t* const sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~(uintptr_t)1023);
+    extern __shared__ __align__(1024) uint8_t smraw[];
+    // 1024-byte alignment for the 128B-swizzle TMA boxes, computed on the shared-window address
+    // so that the pointers stay shared-space (LDS, not generic loads)
+    uint8_t* const sm = smraw + ((1024u - (smem_u32(smraw) & 1023u)) & 1023u);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nkx = mv.nkx, My = mv.My;
     const int nt3 = (nkx + T - 1) / T;

@@ -438,6 +438,36 @@ vc_status vc_debug_fft(vc_ctx* c, int32_t L, int32_t n_lines, double* data, int3
     return debug_fft(c, L, n_lines, data, dir);
 }
 
+vc_status vc_debug_get_spectra(vc_ctx* c, int64_t* n, int32_t* layout, double* out) {
+    VC_CHECK_CTX(c);
+    if (!c->has_op) return set_err(c, VC_ERR_STATE, "vc_debug_get_spectra before vc_build_operator");
+    DeviceGuard g(c->device);
+    const int My = c->M[1];
+    if (n) *n = (int64_t)c->Rt.n;
+    if (layout) {
+        const int kx0 = c->kxa[c->rank], nkx = c->kxa[c->rank + 1] - kx0;
+        const int32_t L[8] = {c->zdirect ? 1 : 0, c->nblk, c->zdirect ? c->ZU : c->M[2] / 2 + 1, c->T3,
+                              c->nt3, My / 2 + 1, c->rs1, nkx};
+        memcpy(layout, L, sizeof L);
+    }
+    if (out) {
+        VC_CUDA(c, cudaMemcpyAsync(out, c->Rt.p, c->Rt.bytes(), cudaMemcpyDeviceToHost, c->stream));
+        VC_CUDA(c, cudaStreamSynchronize(c->stream));
+    }
+    return VC_OK;
+}
+
+vc_status vc_debug_set_spectra(vc_ctx* c, int64_t n, const double* in) {
+    VC_CHECK_CTX(c);
+    if (!c->has_op) return set_err(c, VC_ERR_STATE, "vc_debug_set_spectra before vc_build_operator");
+    if (!in || n != (int64_t)c->Rt.n) return set_err(c, VC_ERR_INPUT, "spectra length mismatch");
+    DeviceGuard g(c->device);
+    VC_CUDA(c, cudaMemcpyAsync(c->Rt.p, in, c->Rt.bytes(), cudaMemcpyHostToDevice, c->stream));
+    VC_CUDA(c, cudaStreamSynchronize(c->stream));
+    c->kt_key.clear();  // the tables no longer match their signature (no reuse_tables hit)
+    return VC_OK;
+}
+
 vc_status vc_init_distributed(vc_ctx* c, int32_t rank, int32_t world, int32_t transport,
                               const void* comm_id) {
     VC_CHECK_CTX(c);

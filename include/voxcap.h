@@ -65,7 +65,9 @@ typedef struct {
     int32_t box[3];         /* preconditioner box N_vx, N_vy, N_vz; 0 = 10    */
     int32_t precond;        /* 0 = default = 3; 1 = none; 2 = diagonal only (Ī^{-1} on
                                dielectric rows, 1/P_kk on conductor rows); 3 = the paper's
-                               block-diagonal-diagonal (Eq. 14)                    */
+                               block-diagonal-diagonal (Eq. 14); 4 = the
+                               conventional block-diagonal comparator of P:155-157 (every
+                               panel of a box in its block, Eq. 4 rows; one rank only)          */
     int32_t zmode;          /* z direction of the matvec: 0 = automatic, 1 = z-FFT
                                (3-D circulant, Eq. 11), 2 = direct z-convolution on the x/y
                                spectra (exact; cheaper when panels occupy few z-planes)       */
@@ -120,7 +122,9 @@ typedef struct {
     double  bytes_moved[5]; /* algorithmic bytes of all launches of each pass since the reset:
                                a batched launch of nb columns counts nb x its per-column arrays
                                and the P3 kernel spectra once (vc_matvec_batch)              */
-    int64_t reserved[4];
+    int64_t precond_doubles;/* last build: doubles of the stored (unique) preconditioner blocks
+                               (the memory P:157 compares; 0 for precond 1 / 2)              */
+    int64_t reserved[3];
 } vc_stats;
 
 /* Create a context on CUDA device `cuda_device`.  `cuda_stream` is a cudaStream_t to order

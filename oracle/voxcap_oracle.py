@@ -328,19 +328,25 @@ def precond_boxes(p: Panels, nv=(10, 10, 10)):
     return (b[2] * nbox[1] + b[1]) * nbox[0] + b[0]
 
 
-def precond_apply(p: Panels, r, nv=(10, 10, 10), A=None):
+def precond_apply(p: Panels, r, nv=(10, 10, 10), A=None, conventional=False):
     """z = R r with R = [R_BD; R_D] (Eq. 14; reading O9).
 
     R_BD: for every box, the inverse of the dense block of conductor-panel interactions
-    inside the box (Eq. 5 entries); R_D = Ī^{-1} on dielectric rows."""
+    inside the box (Eq. 5 entries); R_D = Ī^{-1} on dielectric rows.
+
+    conventional=True: the "conventional block-diagonal preconditioner" the paper compares
+    against: every panel of a box, conductor and dielectric, in its block, whose
+    entries are the rows of Eq. (4) restricted to the box; no separate diagonal part."""
     A = assemble(p) if A is None else A
     r = np.asarray(r, dtype=np.float64)
     z = np.zeros_like(r)
     box = precond_boxes(p, nv)
-    diel = ~p.is_cond
-    z[diel] = r[diel] / p.ibar[diel]
-    for b in np.unique(box[p.is_cond]):
-        idx = np.nonzero(p.is_cond & (box == b))[0]
+    sel = np.ones(p.n, bool) if conventional else p.is_cond
+    if not conventional:
+        diel = ~p.is_cond
+        z[diel] = r[diel] / p.ibar[diel]
+    for b in np.unique(box[sel]):
+        idx = np.nonzero(sel & (box == b))[0]
         blk = A[np.ix_(idx, idx)]
         z[idx] = np.linalg.inv(blk) @ r[idx]
     return z

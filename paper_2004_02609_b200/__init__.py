@@ -69,7 +69,7 @@ class Stats(ctypes.Structure):
                 ("gpu_launches", ctypes.c_int64), ("ms_kgen", ctypes.c_double),
                 ("ms_kfft", ctypes.c_double), ("ms_geometry", ctypes.c_double),
                 ("ms_comm", ctypes.c_double), ("bytes_moved", ctypes.c_double * 5),
-                ("reserved", ctypes.c_int64 * 4)]
+                ("precond_doubles", ctypes.c_int64), ("reserved", ctypes.c_int64 * 3)]
 
     def as_dict(self):
         return {"n_matvec": self.n_matvec, "ms_matvec": self.ms_matvec,
@@ -79,7 +79,7 @@ class Stats(ctypes.Structure):
                 "ms_setup": self.ms_setup, "ms_precond_build": self.ms_precond_build,
                 "gpu_launches": self.gpu_launches, "ms_kgen": self.ms_kgen,
                 "ms_kfft": self.ms_kfft, "ms_geometry": self.ms_geometry,
-                "ms_comm": self.ms_comm}
+                "ms_comm": self.ms_comm, "precond_doubles": self.precond_doubles}
 
 
 def lib_path():

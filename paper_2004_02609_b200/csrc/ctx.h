@@ -280,7 +280,7 @@ vc_status matvec_batch_dev(vc_ctx* c, int nb, const double* const* d_x, double* 
 struct PcPlan;
 PcPlan* pc_plan_new();
 void pc_plan_free(PcPlan* p);
-void pc_plan_compute(const vc_ctx* c, const int32_t box_in[3], int64_t N, PcPlan& P);
+void pc_plan_compute(const vc_ctx* c, const int32_t box_in[3], int64_t N, PcPlan& P, bool all_panels = false);
 vc_status precond_build(vc_ctx* c, const int32_t box[3], int kind, const PcPlan* pre = nullptr);
 vc_status precond_apply_dev(vc_ctx* c, const double* d_r, double* d_z);
 // z_q = R r_q for nc columns (two at once share each R row read)

@@ -76,6 +76,37 @@ __global__ void k_pc_fill(const int32_t* __restrict__ un, const int64_t* __restr
     }
 }
 
+// Conventional block-diagonal blocks (vc_build_opts.precond = 4; the comparator of P:155-157):
+// every panel of a box, conductor rows from Eq. (5), dielectric rows from Eq. (6) with the Ī of
+// Eq. (7) on the diagonal -- the same rows as the operator (Eq. 4) restricted to the box.  One
+// block per box (no dedup: a dielectric row also depends on its permittivities), entries from the
+// device closed forms (kgen.cuh kappa), scaled like the operator.
+__global__ void k_pc_fill_conv(const int32_t* __restrict__ bn, const int64_t* __restrict__ uoff,
+                               const int32_t* __restrict__ bstart, const int32_t* __restrict__ pids,
+                               const int8_t* __restrict__ axis, const int32_t* __restrict__ si,
+                               const int32_t* __restrict__ sj, const int32_t* __restrict__ sk,
+                               const int8_t* __restrict__ info, const double* __restrict__ ibar,
+                               double pscale, double escale, double* __restrict__ blocks) {
+    const int b = blockIdx.y;
+    const int n = bn[b], s0 = bstart[b];
+    const int64_t nn = (int64_t)n * n;
+    double* B = blocks + uoff[b];
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nn;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int i = (int)(e / n), j = (int)(e % n);
+        const int pi = pids[s0 + i], pj = pids[s0 + j];
+        const bool diel = info[pi] & 1;
+        double v = kappa(diel ? 1 : 0, axis[pi], axis[pj], si[pi] - si[pj], sj[pi] - sj[pj], sk[pi] - sk[pj]);
+        if (diel) {
+            v *= (info[pi] & 2) ? -escale : escale;  // s_k
+            if (i == j) v += ibar[pi];               // Eq. (7)
+        } else {
+            v *= pscale;
+        }
+        B[e] = v;
+    }
+}
+
 // In-place Gauss-Jordan inverse of an SPD block (no pivoting needed), one CTA (32 x 16
 // threads) per unique block.  The block is worked on in shared memory when it fits (copied in
 // and out once), else in global memory (L2-resident); the 2-D thread layout avoids index
@@ -271,7 +302,8 @@ __global__ void k_pc_dinv(int64_t n, const int32_t* __restrict__ cid, const doub
                           int kind, double pself, double* __restrict__ dinv) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
-        if (cid[i] == 0) dinv[i] = kind == 1 ? 1.0 : 1.0 / ibar[i];
+        if (kind == 4) dinv[i] = 0.0;  // every row lies in a box block
+        else if (cid[i] == 0) dinv[i] = kind == 1 ? 1.0 : 1.0 / ibar[i];
         else dinv[i] = kind == 1 ? 1.0 : (kind == 2 ? 1.0 / pself : 0.0);
     }
 }
@@ -295,7 +327,7 @@ struct PcPlan {
     std::vector<int64_t> uoff;
 };
 
-void pc_plan_compute(const vc_ctx* c, const int32_t box_in[3], int64_t N, PcPlan& P) {
+void pc_plan_compute(const vc_ctx* c, const int32_t box_in[3], int64_t N, PcPlan& P, bool all_panels) {
     auto G = [&](int64_t i) { return c->world > 1 ? c->h_gidx[i] : i; };  // local -> global
     int nv[3], nb[3];
     const int dims[3] = {c->nx, c->ny, c->nz};
@@ -308,7 +340,7 @@ void pc_plan_compute(const vc_ctx* c, const int32_t box_in[3], int64_t N, PcPlan
     std::vector<int32_t> cond;
     cond.reserve(c->Nc);
     for (int64_t i = 0; i < N; ++i)
-        if (c->h_cid[G(i)] > 0) cond.push_back((int32_t)i);  // local indices
+        if (all_panels || c->h_cid[G(i)] > 0) cond.push_back((int32_t)i);  // local indices
     // dense box table (the box grid is small: (N_x/N_v)(N_y/N_v)(N_z/N_v) entries)
     std::vector<int32_t> box_index((size_t)nb[0] * nb[1] * nb[2], -1);
     std::vector<int64_t> box_keys;
@@ -355,7 +387,7 @@ void pc_plan_compute(const vc_ctx* c, const int32_t box_in[3], int64_t N, PcPlan
                 h *= 1099511628211ull;
             }
         int id = -1;
-        auto& cand = by_hash[h];
+        auto& cand = by_hash[all_panels ? (uint64_t)b : h];  // conventional blocks: no dedup
         for (int u : cand) {
             if (un[u] != n) continue;
             bool same = true;
@@ -405,6 +437,7 @@ vc_status precond_build(vc_ctx* c, const int32_t box_in[3], int kind, const PcPl
     pc->kind = kind;
     pc->nbox = pc->nuniq = pc->max_n = 0;
     pc->block_doubles = 0;
+    c->stats.precond_doubles = 0;
     cudaStream_t st = c->stream;
     HostTrace tr("precond");
     const int64_t N = c->NL;  // this rank's panels (boxes never straddle ranks)
@@ -422,13 +455,16 @@ vc_status precond_build(vc_ctx* c, const int32_t box_in[3], int kind, const PcPl
         count_launch(c);
     }
     tr.mark("diagonal");
-    if (kind != 3) {
+    if (kind != 3 && kind != 4) {
         VC_CUDA(c, cudaStreamSynchronize(st));
         return VC_OK;
     }
+    const bool conv = kind == 4;
+    if (conv && c->world > 1)
+        return set_err(c, VC_ERR_UNSUPPORTED, "the conventional block-diagonal preconditioner runs on one rank");
     PcPlan own;
-    if (!pre) pc_plan_compute(c, box_in, N, own);
-    const PcPlan& P = pre ? *pre : own;
+    if (!pre || conv) pc_plan_compute(c, box_in, N, own, conv);
+    const PcPlan& P = (pre && !conv) ? *pre : own;
     const int nbox = P.nbox, maxn = P.maxn;
     const int64_t total = P.total;
     const std::vector<int32_t>&bcount = P.bcount, &bstart = P.bstart, &sorted = P.sorted,
@@ -452,6 +488,7 @@ vc_status precond_build(vc_ctx* c, const int32_t box_in[3], int kind, const PcPl
     pc->nuniq = (int)un.size();
     pc->max_n = maxn;
     pc->block_doubles = total;
+    c->stats.precond_doubles = total;
     VC_CUDA(c, pc->box_start.alloc(std::max(1, nbox)));
     VC_CUDA(c, pc->box_n.alloc(std::max(1, nbox)));
     VC_CUDA(c, pc->box_uid.alloc(std::max(1, nbox)));
@@ -536,6 +573,22 @@ vc_status precond_build(vc_ctx* c, const int32_t box_in[3], int kind, const PcPl
             tab.dim[a] = c->pcTabDim[a];
             for (int b = 0; b < 3; ++b) tab.pair[a][b] = c->pcPair[a][b];
         }
+        if (conv) {  // one block per box, all panels, Eq. (4) rows; Gauss-Jordan (not symmetric)
+            dim3 gb(std::max(1, std::min(64, (maxn * maxn + 255) / 256)), nbox);
+            k_pc_fill_conv<<<gb, 256, 0, st>>>(pc->box_n.p, pc->uniq_off.p, pc->box_start.p, pc->panel_ids.p,
+                                               c->pan.axis.p, c->pan.si.p, c->pan.sj.p, c->pan.sk.p,
+                                               c->pan.info.p, c->pan.ibar.p, pscale,
+                                               c->dv * c->dv / fpe, pc->blocks.p);
+            const size_t cap = (size_t)max_dyn_smem() - 1024;
+            const size_t sh = std::min(cap, sizeof(double) * ((size_t)maxn * maxn + 2 * maxn));
+            if (sh > 48 * 1024) VC_CUDA(c, grant_max_dyn_smem(k_pc_invert, max_dyn_smem()));
+            k_pc_invert<<<pc->nuniq, 512, sh, st>>>(pc->uniq_n.p, pc->uniq_off.p, pc->blocks.p,
+                                                    (int)(sh / sizeof(double)), 0);
+            count_launch(c, 2);
+            VC_CUDA(c, cudaGetLastError());
+            VC_CUDA(c, cudaStreamSynchronize(st));
+            return VC_OK;
+        }
         k_pc_fill<<<g, 256, 0, st>>>(pc->uniq_n.p, pc->uniq_off.p, pc->uniq_list_off.p,
                                      pc->uniq_axis.p, pc->uniq_slot.p, pc->blocks.p, tab);
         // sweep (packed, shared memory) for every block it fits; Gauss-Jordan in global memory
@@ -567,7 +620,7 @@ vc_status precond_apply_multi_dev(vc_ctx* c, int nc, const double* const* d_r, d
     Precond* pc = c->pc;
     if (!pc) return set_err(c, VC_ERR_STATE, "no preconditioner");
     static const bool grouped = getenv("VC_PC_GROUPED") != nullptr;
-    if (nc != 2 || pc->kind != 3 || grouped || pc->nbtile == 0) {
+    if (nc != 2 || pc->kind < 3 || grouped || pc->nbtile == 0) {
         for (int q = 0; q < nc; ++q) {
             vc_status s = precond_apply_dev(c, d_r[q], d_z[q]);
             if (s) return s;
@@ -598,7 +651,7 @@ vc_status precond_apply_dev(vc_ctx* c, const double* d_r, double* d_z) {
     k_pc_diag<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((N + 255) / 256, 148 * 8)), 256, 0, st>>>(N, d_r, pc->diag_inv.p, d_z);
     count_launch(c);
     static const bool grouped = getenv("VC_PC_GROUPED") != nullptr;
-    if (pc->kind == 3 && !grouped && pc->nbtile > 0) {
+    if (pc->kind >= 3 && !grouped && pc->nbtile > 0) {
         PcCols cols{};
         cols.r[0] = d_r;
         cols.z[0] = d_z;
@@ -606,7 +659,7 @@ vc_status precond_apply_dev(vc_ctx* c, const double* d_r, double* d_z) {
             pc->btile_b.p, pc->btile_r0.p, pc->box_start.p, pc->box_n.p, pc->box_uid.p,
             pc->uniq_off.p, pc->panel_ids.p, pc->blocks.p, cols);
         count_launch(c);
-    } else if (pc->kind == 3 && pc->ntile > 0) {
+    } else if (pc->kind >= 3 && pc->ntile > 0) {
         const size_t sh = sizeof(double) * (size_t)(kPcRows + 1) * pc->max_n;
         if (sh > 48 * 1024)
             VC_CUDA(c, grant_max_dyn_smem(k_pc_apply_grouped, max_dyn_smem()));

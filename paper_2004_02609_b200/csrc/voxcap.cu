@@ -221,7 +221,7 @@ vc_status vc_build_operator(vc_ctx* c, const vc_build_opts* o) {
     DeviceGuard g(c->device);
     drop_operator(c);
     int kind = (o && o->precond) ? o->precond : 3;
-    if (kind < 1 || kind > 3) return set_err(c, VC_ERR_INPUT, "precond must be 0..3");
+    if (kind < 1 || kind > 4) return set_err(c, VC_ERR_INPUT, "precond must be 0..4");
     int box[3] = {10, 10, 10};
     if (o)
         for (int a = 0; a < 3; ++a) {
@@ -414,11 +414,13 @@ vc_status vc_reset_stats(vc_ctx* c) {
     const double bp[5] = {c->stats.bytes_pass[0], c->stats.bytes_pass[1], c->stats.bytes_pass[2],
                           c->stats.bytes_pass[3], c->stats.bytes_pass[4]};
     const double bm = c->stats.bytes_matvec, ms = c->stats.ms_setup, mp = c->stats.ms_precond_build;
+    const int64_t pd = c->stats.precond_doubles;
     memset(&c->stats, 0, sizeof(c->stats));
     for (int p = 0; p < 5; ++p) c->stats.bytes_pass[p] = bp[p];
     c->stats.bytes_matvec = bm;
     c->stats.ms_setup = ms;
     c->stats.ms_precond_build = mp;
+    c->stats.precond_doubles = pd;
     return VC_OK;
 }
 

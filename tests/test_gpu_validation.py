@@ -49,8 +49,12 @@ def test_coated_sphere_counts_and_analytic(ctx, dv):
     ctx.set_structure(st)
     assert ctx.n == pin["N"][pin["dv_m"].index(dv)]
     ctx.build_operator()
+    C4, info4 = ctx.solve_capacitance(tol=1e-4, maxit=3000)  # the paper's RRE
     C, info = ctx.solve_capacitance(tol=1e-8, maxit=3000)
-    assert info[0]["converged"]
+    assert info[0]["converged"] and info4[0]["converged"]
+    paper_it = {0.05: 7, 0.025: 7, 0.02: 10, 0.01: 10}[dv]  # VoxCap iterations
+    print(f"dv={dv} iterations at RRE 1e-4: {info4[0]['iters']} (paper {paper_it})")
+    assert info4[0]["iters"] <= 2 * paper_it
     err = abs(C[0, 0] / _analytic(2.0) - 1)
     print(f"dv={dv} N={ctx.n} C={C[0, 0]:.6e} F analytic={_analytic(2.0):.6e} err={err:.4f} "
           f"iters={info[0]['iters']}")
@@ -94,16 +98,45 @@ def test_permittivity_sweep(ctx):
 
 
 def test_preconditioner_ordering(ctx):
-    """P:157 (Fig. 3(d)): iterations to RRE 1e-8 order as proposed (block-diagonal-diagonal)
-    <= diagonal < none.  (The paper's conventional block-diagonal variant, which also blocks
-    dielectric panels, is not one of the library's options.)"""
-    st = _coated(0.025, 2.0)
-    it = {}
-    for kind, name in ((3, "proposed"), (2, "diagonal"), (1, "none")):
+    """P:155-157 (Fig. 3(d)) as the paper ran it: the coated sphere at dv = 0.01 m (N = 59,016,
+    P:153), eps_r = 2, boxes N_v = 10, RRE 1e-8.  Iterations with the proposed block-diagonal-
+    diagonal preconditioner (3), the conventional block-diagonal one (4: dielectric panels in the
+    blocks too), the diagonal one (2) and none (1) order as the paper's 22 < 27 < 41 < 142
+    (proposed <= conventional: they tie here), and the proposed blocks need less than a quarter
+    of the conventional blocks' memory (paper: 17.04 vs 70.26 MB)."""
+    st = _coated(0.01, 2.0)
+    it, mem = {}, {}
+    for kind, name in ((3, "proposed"), (4, "block_diagonal"), (2, "diagonal"), (1, "none")):
         ctx.set_structure(st)
-        ctx.build_operator(precond=kind)
+        ctx.build_operator(precond=kind, box=(10, 10, 10))
         C, info = ctx.solve_capacitance(tol=1e-8, maxit=5000)
-        assert info[0]["converged"]
+        assert info[0]["converged"], name
         it[name] = info[0]["iters"]
+        mem[name] = ctx.stats()["precond_doubles"] * 8 / 1e6
     print("iterations to RRE 1e-8:", it, "paper (P:157):", PINS["precond_iterations_rre1e-8"])
-    assert it["proposed"] <= it["diagonal"] < it["none"]
+    print("preconditioner block memory (MB):", mem, "paper: proposed 17.04, conventional 70.26")
+    # measured (r02): 28 / 28 / 35 / 161 -- the proposed preconditioner ties the conventional
+    # one here (the paper has 22 vs 27, DESIGN.md §13) while storing 5.5x less
+    assert it["proposed"] <= it["block_diagonal"] < it["diagonal"] < it["none"]
+    assert mem["proposed"] < mem["block_diagonal"] / 4
+
+
+@pytest.mark.parametrize("name,box", [("R5", (4, 4, 4)), ("C2", (8, 8, 6)), ("R3", (3, 3, 3))])
+def test_conventional_block_diagonal_parity(ctx, name, box):
+    """precond = 4 (every panel of a box in its block, Eq. 4 rows) against the oracle's
+    conventional block-diagonal preconditioner (oracle.precond_apply(conventional=True))."""
+    import oracle as O
+    st = voxgen.config(name)
+    ctx.set_structure(st)
+    ctx.build_operator(precond=4, box=box)
+    p = O.enumerate_panels(st.label, st.eps, st.eps_out, st.dv)
+    A = O.assemble(p)
+    r = voxgen.seeded_vector(p.n, 8)
+    z = ctx.precond(r)
+    ref = O.precond_apply(p, r, nv=box, A=A, conventional=True)
+    # Gauss-Jordan on the non-symmetric blocks (no pivoting; dielectric rows are Ī-dominant):
+    # rounding ~ cond(block) x eps, measured 1e-10 on C2 -> bar 1e-9 (the proposed SPD blocks
+    # are inverted by the symmetric sweep and meet 1e-12, test_precond_parity)
+    assert np.linalg.norm(z - ref) / np.linalg.norm(ref) <= 1e-9
+    x, info = ctx.solve(A @ voxgen.seeded_vector(p.n, 9), tol=1e-12, maxit=500)
+    assert info["converged"]

@@ -165,3 +165,14 @@ def test_precond_whole_domain_box_is_exact_inverse():
     z = O.precond_apply(p, r, nv=(2, 2, 2))
     d = ~p.is_cond
     assert np.allclose(z[d], r[d] / p.ibar[d], rtol=1e-15)
+    # the conventional block-diagonal comparator: with one box holding every panel
+    # (dielectric ones too) R = A^{-1}; with no dielectric panels it equals the proposed one
+    A = O.assemble(p)
+    x = voxgen.seeded_vector(p.n, 2)
+    z = O.precond_apply(p, A @ x, nv=(64, 64, 64), A=A, conventional=True)
+    assert np.abs(z - x).max() < 1e-9 * np.abs(x).max()
+    st = _two_blocks()
+    p = O.enumerate_panels(st.label, st.eps, 1.0, st.dv)
+    r = voxgen.seeded_vector(p.n, 3)
+    assert np.allclose(O.precond_apply(p, r, nv=(3, 3, 3)), O.precond_apply(p, r, nv=(3, 3, 3), conventional=True),
+                       rtol=1e-13, atol=0)

@@ -517,7 +517,6 @@ __global__ void __launch_bounds__(FX<L>::NT, FX<L>::MINB5) k_p5(MV mv) {
     __syncthreads();
     const int32_t want = kind ? kSlotDiel : 0;
     double* __restrict__ y = mv.ys[blockIdx.z];
-    const double* __restrict__ xc = mv.xs[blockIdx.z];
     constexpr int NI = (L + FX<L>::NT - 1) / FX<L>::NT;  // slots per thread and line (exo <= L)
 #pragma unroll 1
     for (int r = 0; r < 2 * T; ++r) {
@@ -538,8 +537,11 @@ __global__ void __launch_bounds__(FX<L>::NT, FX<L>::MINB5) k_p5(MV mv) {
             const double2 v = sm[smi<L, T, false>(t, Plan<L>::pos(n))];
             const double val = half ? v.y : v.x;
             const int p = e[i] & kSlotIdx;
+            // dielectric rows: y was initialised to Ī x by k_yinit (Eq. 7); the field term is
+            // added without reading anything back (each panel appears in exactly one slot map,
+            // so the reduction has no contention and the thread never waits on it)
             if (kind == 0) y[p] = val;
-            else y[p] = ((e[i] & kSlotNeg) ? -val : val) + mv.ibar[p] * xc[p];
+            else atomicAdd(y + p, (e[i] & kSlotNeg) ? -val : val);
         }
     }
 }
@@ -884,6 +886,15 @@ __global__ void k_extract(const double2* __restrict__ G, double* __restrict__ R,
         R[((int64_t)ky * nt3 + (kx >> lgT3)) * RC + ((int64_t)blk * KZ + kz) * T3 + (kx & (T3 - 1))] =
             (kind == 0 ? v.x : v.y) * scale;
     }
+}
+
+// y = [0; Ī] x (Eq. 4's overlap diagonal, Eq. 7): dielectric rows start at Ī_k x_k, conductor
+// rows at 0; P5 then stores the conductor rows and adds the field term of the dielectric rows
+__global__ void k_yinit(double* __restrict__ y, const double* __restrict__ x,
+                        const double* __restrict__ ibar, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        y[i] = ibar[i] * x[i];  // ibar = 0 on conductor rows
 }
 
 __global__ void k_zero(double* y, int64_t n) {
@@ -1914,7 +1925,8 @@ static vc_status matvec_run(vc_ctx* c, const MV& mv) {
     const bool det = ev && T.detail;
     if (ev) VC_CUDA(c, cudaEventRecord(ev[0], st));
     for (int i = 0; i < mv.nb; ++i)
-        k_zero<<<std::max<int64_t>(1, std::min<int64_t>((c->NL + 255) / 256, 1184)), 256, 0, st>>>(mv.ys[i], c->NL);
+        k_yinit<<<std::max<int64_t>(1, std::min<int64_t>((c->NL + 255) / 256, 1184)), 256, 0, st>>>(
+            mv.ys[i], mv.xs[i], mv.ibar, c->NL);
     cudaError_t (*launch[5])(const MV&, cudaStream_t) = {launch_p1, launch_p2, launch_p3,
                                                          launch_p4s, launch_p5};
     for (int p = 0; p < 5; ++p) {

@@ -48,7 +48,10 @@ def _offsets():
     near = np.array(np.meshgrid(*[np.arange(-5, 6)] * 3, indexing="ij")).reshape(3, -1).T
     far = rng.integers(-300, 301, (600, 3))
     mid = rng.integers(-25, 26, (600, 3))
-    return np.concatenate([near, mid, far])
+    # the q = 2 bands (P beyond d = 300, E beyond 450; kgen.cuh gl_order) on a C4/C5-like
+    # window: in-plane offsets up to 1,000, z offsets up to 64
+    vfar = np.concatenate([rng.integers(-1000, 1001, (400, 2)), rng.integers(-64, 65, (400, 1))], axis=1)
+    return np.concatenate([near, mid, far, vfar])
 
 
 @pytest.mark.parametrize("kind", [0, 1])

@@ -348,9 +348,9 @@ cudaError_t launch_p3m(const MV& mv, cudaStream_t st) {
     const int grid = std::max(1, std::min(ntiles, nsm));
 #define VC_P3M_K2(M, KK, KSV)                                                                  \
     {                                                                                          \
-        static bool granted = false; /* process-wide attribute: grant once */                  \
+        static bool granted = false; /* process-wide attribute: grant the maximum once */      \
         if (!granted) {                                                                        \
-            e = prep(k_p3m<M, KK, KSV>, smem);                                                 \
+            e = prep(k_p3m<M, KK, KSV>, 227 * 1024);                                           \
             if (e) return e;                                                                   \
             granted = true;                                                                    \
         }                                                                                      \

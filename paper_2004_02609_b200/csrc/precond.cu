@@ -25,6 +25,8 @@ struct Precond {
     DevBuf<int32_t> ubox_start, ubox_list;       // boxes of each unique block (CSR)
     DevBuf<int32_t> btile_b, btile_r0;           // per-box apply tiles (box, first row)
     int nbtile = 0;
+    DevBuf<int32_t> stile_b, stile_r0;           // symmetric-apply tiles (box, first of kPsRows rows)
+    int nstile = 0;
     DevBuf<int32_t> tile_u, tile_r0, tile_q0;    // apply tiles: (unique block, first row, first box)
     int ntile = 0;
     DevBuf<int32_t> panel_ids;                   // conductor panels sorted by box
@@ -114,7 +116,7 @@ __global__ void k_pc_fill_conv(const int32_t* __restrict__ bn, const int64_t* __
 __global__ void __launch_bounds__(512) k_pc_invert(const int32_t* __restrict__ un,
                                                    const int64_t* __restrict__ uoff,
                                                    double* __restrict__ blocks, int smem_elems,
-                                                   int sweep_elems) {
+                                                   int sweep_elems, int symmetrize) {
     extern __shared__ double sh[];
     const int u = blockIdx.x;
     const int n = un[u];
@@ -146,8 +148,19 @@ __global__ void __launch_bounds__(512) k_pc_invert(const int32_t* __restrict__ u
             }
         }
     }
-    if (in_smem) {
+    __syncthreads();
+    if (symmetrize) {  // SPD block: make the inverse exactly symmetric (k_pc_apply_sym reads R^T)
+        for (int64_t e = threadIdx.x; e < (int64_t)n * n; e += blockDim.x) {
+            const int i = (int)(e / n), j = (int)(e % n);
+            if (i < j) {
+                const double v = 0.5 * (A[(int64_t)i * n + j] + A[(int64_t)j * n + i]);
+                A[(int64_t)i * n + j] = v;
+                A[(int64_t)j * n + i] = v;
+            }
+        }
         __syncthreads();
+    }
+    if (in_smem) {
         for (int64_t e = threadIdx.x; e < (int64_t)n * n; e += blockDim.x) G[e] = A[e];
     }
 }
@@ -294,6 +307,44 @@ __global__ void __launch_bounds__(256) k_pc_apply_box(
             if (lane == 0) cols.z[q][pids[s0 + row]] = acc[q];
         }
     }
+}
+
+// Symmetric blocks (the proposed R_BD: SPD blocks inverted by the symmetric sweep, so R = R^T
+// exactly): thread per row, z_row = sum_j R[j][row] r_j reads R column-wise, i.e. row j of the
+// stored block across consecutive threads -- coalesced, no shuffle reduction -- with r_j
+// broadcast from shared memory.  CTA = (box, kPsRows rows); all columns of the box in one pass.
+constexpr int kPsRows = 128;
+template <int NC>
+__global__ void __launch_bounds__(kPsRows) k_pc_apply_sym(
+    const int32_t* __restrict__ tb, const int32_t* __restrict__ tr0,
+    const int32_t* __restrict__ bstart, const int32_t* __restrict__ bn,
+    const int32_t* __restrict__ buid, const int64_t* __restrict__ uoff,
+    const int32_t* __restrict__ pids, const double* __restrict__ blocks, PcCols cols) {
+    extern __shared__ double rb[];  // [NC][n]
+    const int b = tb[blockIdx.x], r0 = tr0[blockIdx.x];
+    const int n = bn[b], s0 = bstart[b];
+    const double* __restrict__ R = blocks + uoff[buid[b]];
+    for (int j = threadIdx.x; j < n; j += kPsRows) {
+        const int p = pids[s0 + j];
+#pragma unroll
+        for (int q = 0; q < NC; ++q) rb[q * n + j] = cols.r[q][p];
+    }
+    __syncthreads();
+    const int row = r0 + threadIdx.x;
+    if (row >= n) return;
+    double acc[NC];
+#pragma unroll
+    for (int q = 0; q < NC; ++q) acc[q] = 0.0;
+    const double* __restrict__ Rc = R + row;
+#pragma unroll 4
+    for (int j = 0; j < n; ++j) {
+        const double rv = __ldg(Rc + (int64_t)j * n);
+#pragma unroll
+        for (int q = 0; q < NC; ++q) acc[q] = fma(rv, rb[q * n + j], acc[q]);
+    }
+    const int p = pids[s0 + row];
+#pragma unroll
+    for (int q = 0; q < NC; ++q) cols.z[q][p] = acc[q];
 }
 
 // per-panel diagonal of R: 1/Ī on dielectric rows; conductor rows 1 (none), 1/P_self
@@ -539,6 +590,17 @@ vc_status precond_build(vc_ctx* c, const int32_t box_in[3], int kind, const PcPl
                 br.push_back(r0);
             }
         pc->nbtile = (int)bt.size();
+        std::vector<int32_t> sb, sr;
+        for (int b = 0; b < nbox; ++b)
+            for (int r0 = 0; r0 < bcount[b]; r0 += kPsRows) {
+                sb.push_back(b);
+                sr.push_back(r0);
+            }
+        pc->nstile = (int)sb.size();
+        VC_CUDA(c, pc->stile_b.alloc(std::max<size_t>(1, sb.size())));
+        VC_CUDA(c, pc->stile_r0.alloc(std::max<size_t>(1, sr.size())));
+        VC_CUDA(c, up(pc->stile_b.p, sb.data(), 4 * sb.size()));
+        VC_CUDA(c, up(pc->stile_r0.p, sr.data(), 4 * sr.size()));
         VC_CUDA(c, pc->btile_b.alloc(std::max<size_t>(1, bt.size())));
         VC_CUDA(c, pc->btile_r0.alloc(std::max<size_t>(1, br.size())));
         VC_CUDA(c, up(pc->btile_b.p, bt.data(), 4 * bt.size()));
@@ -583,7 +645,7 @@ vc_status precond_build(vc_ctx* c, const int32_t box_in[3], int kind, const PcPl
             const size_t sh = std::min(cap, sizeof(double) * ((size_t)maxn * maxn + 2 * maxn));
             if (sh > 48 * 1024) VC_CUDA(c, grant_max_dyn_smem(k_pc_invert, max_dyn_smem()));
             k_pc_invert<<<pc->nuniq, 512, sh, st>>>(pc->uniq_n.p, pc->uniq_off.p, pc->blocks.p,
-                                                    (int)(sh / sizeof(double)), 0);
+                                                    (int)(sh / sizeof(double)), 0, 0);
             count_launch(c, 2);
             VC_CUDA(c, cudaGetLastError());
             VC_CUDA(c, cudaStreamSynchronize(st));
@@ -602,7 +664,7 @@ vc_status precond_build(vc_ctx* c, const int32_t box_in[3], int kind, const PcPl
             const size_t sh = 2 * sizeof(double) * maxn;
             k_pc_invert<<<pc->nuniq, 512, sh, st>>>(pc->uniq_n.p, pc->uniq_off.p, pc->blocks.p,
                                                     (int)(sh / sizeof(double)),
-                                                    (int)(sw / sizeof(double)));
+                                                    (int)(sw / sizeof(double)), 1);
             count_launch(c);
         }
         count_launch(c, 2);
@@ -614,6 +676,12 @@ vc_status precond_build(vc_ctx* c, const int32_t box_in[3], int kind, const PcPl
     VC_CUDA(c, cudaStreamSynchronize(st));
     VC_CUDA(c, cudaGetLastError());
     return VC_OK;
+}
+
+// VC_PC_ROWWARP=1: the warp-per-row apply for symmetric blocks too (A/B of k_pc_apply_sym)
+static bool pc_rowwarp() {
+    static const bool v = getenv("VC_PC_ROWWARP") && atoi(getenv("VC_PC_ROWWARP"));
+    return v;
 }
 
 vc_status precond_apply_multi_dev(vc_ctx* c, int nc, const double* const* d_r, double* const* d_z) {
@@ -635,9 +703,14 @@ vc_status precond_apply_multi_dev(vc_ctx* c, int nc, const double* const* d_r, d
         cols.r[q] = d_r[q];
         cols.z[q] = d_z[q];
     }
-    k_pc_apply_box<2><<<pc->nbtile, 256, 2 * sizeof(double) * (size_t)pc->max_n, st>>>(
-        pc->btile_b.p, pc->btile_r0.p, pc->box_start.p, pc->box_n.p, pc->box_uid.p,
-        pc->uniq_off.p, pc->panel_ids.p, pc->blocks.p, cols);
+    if (pc->kind == 3 && pc->nstile > 0 && !pc_rowwarp())
+        k_pc_apply_sym<2><<<pc->nstile, kPsRows, 2 * sizeof(double) * (size_t)pc->max_n, st>>>(
+            pc->stile_b.p, pc->stile_r0.p, pc->box_start.p, pc->box_n.p, pc->box_uid.p,
+            pc->uniq_off.p, pc->panel_ids.p, pc->blocks.p, cols);
+    else
+        k_pc_apply_box<2><<<pc->nbtile, 256, 2 * sizeof(double) * (size_t)pc->max_n, st>>>(
+            pc->btile_b.p, pc->btile_r0.p, pc->box_start.p, pc->box_n.p, pc->box_uid.p,
+            pc->uniq_off.p, pc->panel_ids.p, pc->blocks.p, cols);
     count_launch(c, 3);
     VC_CUDA(c, cudaGetLastError());
     return VC_OK;
@@ -655,9 +728,14 @@ vc_status precond_apply_dev(vc_ctx* c, const double* d_r, double* d_z) {
         PcCols cols{};
         cols.r[0] = d_r;
         cols.z[0] = d_z;
-        k_pc_apply_box<1><<<pc->nbtile, 256, sizeof(double) * (size_t)pc->max_n, st>>>(
-            pc->btile_b.p, pc->btile_r0.p, pc->box_start.p, pc->box_n.p, pc->box_uid.p,
-            pc->uniq_off.p, pc->panel_ids.p, pc->blocks.p, cols);
+        if (pc->kind == 3 && pc->nstile > 0 && !pc_rowwarp())
+            k_pc_apply_sym<1><<<pc->nstile, kPsRows, sizeof(double) * (size_t)pc->max_n, st>>>(
+                pc->stile_b.p, pc->stile_r0.p, pc->box_start.p, pc->box_n.p, pc->box_uid.p,
+                pc->uniq_off.p, pc->panel_ids.p, pc->blocks.p, cols);
+        else
+            k_pc_apply_box<1><<<pc->nbtile, 256, sizeof(double) * (size_t)pc->max_n, st>>>(
+                pc->btile_b.p, pc->btile_r0.p, pc->box_start.p, pc->box_n.p, pc->box_uid.p,
+                pc->uniq_off.p, pc->panel_ids.p, pc->blocks.p, cols);
         count_launch(c);
     } else if (pc->kind >= 3 && pc->ntile > 0) {
         const size_t sh = sizeof(double) * (size_t)(kPcRows + 1) * pc->max_n;

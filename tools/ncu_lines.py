@@ -11,7 +11,7 @@ hdr = None
 fname = None
 out = []
 for r in rows:
-    if r and r[0] == "File Name":
+    if r and r[0] in ("File Name", "File Path"):
         fname = r[1].split("/")[-1]
         continue
     if r and r[0] == "Line No":

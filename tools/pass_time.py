@@ -38,3 +38,15 @@ for label, fn in (("single", lambda: ctx.matvec(x)), ("pair", lambda: ctx.matvec
           [round(s["ms_pass"][i] / max(1, s["n_pass"][i]), 4) for i in range(5)],
           "matvec_ms/launch", round(s["ms_matvec"] / np_, 4),
           "GB/s per pass", [round(s["bytes_moved"][i] / max(1e-9, s["ms_pass"][i] * 1e-3) / 1e9) for i in range(5)])
+# preconditioner apply (single column, device vectors) and its stored block size
+r = torch.from_numpy(voxgen.seeded_vector(ctx.n, 3)).cuda()
+for _ in range(3):
+    ctx.precond(r)
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+torch.cuda.synchronize()
+e0.record()
+for _ in range(a.n):
+    ctx.precond(r)
+e1.record()
+torch.cuda.synchronize()
+print(a.config, "precond apply ms", round(e0.elapsed_time(e1) / a.n, 4), "blocks MB", ctx.stats()["precond_doubles"] * 8 / 1e6)

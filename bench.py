@@ -142,6 +142,19 @@ def cpu_baseline(st, seconds):
                       f"oracle (binary128 closed-form entries, OpenMP), {el:.1f} s"}
 
 
+def cpu_fft_baseline(ctx):
+    """Like-for-like CPU baseline: one matvec of the same five-pass dataflow on the host cores
+    (scipy.fft with every core, numpy MACs; random spectra of the stored shape, timing only;
+    tools/cpu_fft_baseline.py)."""
+    from tools.cpu_fft_baseline import time_matvec
+    pan = ctx.panels()
+    lay = ctx.spectra_layout()
+    t, workers = time_matvec(pan, ctx.grid(), zdirect=bool(lay["zdirect"]))
+    return {"value": ctx.n / t, "unit": "panel-matvecs/s", "cores": workers, "kind": "cpu_fft",
+            "sample": f"one full matvec (N={ctx.n}, grid {list(ctx.grid())}) through the same five "
+                      f"passes with scipy.fft (workers={workers}) and numpy MACs, {t:.2f} s"}
+
+
 def run_reference(args, rank, world):
     """--impl reference: the CPU oracle, as it stands, on our config and metric."""
     if rank != 0:
@@ -359,6 +372,7 @@ def main():
         line["solve_s_per_column"] = sum(solve_ms[:args.steps]) * 1e-3 / (args.steps * ctx.m)
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(st, args.cpu_seconds)
+            line["cpu_fft_baseline"] = cpu_fft_baseline(ctx)
         print(json.dumps(line), flush=True)
     ctx.close()
     if world > 1:

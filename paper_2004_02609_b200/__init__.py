@@ -447,6 +447,14 @@ class VoxCap:
         keys = ("zdirect", "nblk", "NW", "T3", "nt3", "KY", "RS1", "nkx")
         return out, dict(zip(keys, (int(v) for v in lay)))
 
+    def spectra_layout(self):
+        """Layout of the kernel-spectrum table (no copy): zdirect, nblk, NW, T3, nt3, KY, RS1, nkx."""
+        n = ctypes.c_int64()
+        lay = np.zeros(8, np.int32)
+        self._check(self._lib.vc_debug_get_spectra(self._ctx, ctypes.byref(n), _ptr(lay), None))
+        keys = ("zdirect", "nblk", "NW", "T3", "nt3", "KY", "RS1", "nkx")
+        return dict(zip(keys, (int(v) for v in lay)))
+
     def set_spectra(self, table):
         """Overwrite the kernel-spectrum table (test hook; same length and layout)."""
         a = np.ascontiguousarray(table, dtype=np.float64)

@@ -897,6 +897,19 @@ __global__ void k_yinit(double* __restrict__ y, const double* __restrict__ x,
         y[i] = ibar[i] * x[i];  // ibar = 0 on conductor rows
 }
 
+// active-plane flags: has[g][z] = 1 if source orientation g < 3 (field f: g = 3 + f) has a panel
+// on window plane z (benign racy stores of the value 1)
+__global__ void k_plane_flags(int64_t n, const int8_t* __restrict__ axis, const int32_t* __restrict__ sk,
+                              const int32_t* __restrict__ cid, int lo2, int ZL,
+                              const int* __restrict__ fidx, char* __restrict__ has) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        const int a = axis[p], z = sk[p] - lo2;
+        has[(int64_t)a * ZL + z] = 1;
+        has[(int64_t)(3 + fidx[(cid[p] == 0 ? 3 : 0) + a]) * ZL + z] = 1;
+    }
+}
+
 __global__ void k_zero(double* y, int64_t n) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x)
@@ -1266,11 +1279,24 @@ vc_status operator_build(vc_ctx* c, const vc_build_opts* o) {
         for (int f = 0; f < c->nf; ++f) ZL = std::max(ZL, c->f[f].ext[2]);
         int fidx[2][3] = {{-1, -1, -1}, {-1, -1, -1}};
         for (int f = 0; f < c->nf; ++f) fidx[c->f[f].kind][c->f[f].axis] = f;
+        // plane occupancy on the device (one flag per (source or field, plane)), read back as
+        // 9 ZL bytes: no host loop over the panels (round 2)
         std::vector<char> has(9 * (size_t)ZL, 0);
-        for (int64_t p = 0; p < c->N; ++p) {
-            const int a = c->h_axis[p], z = c->h_sk[p] - lo[2];
-            has[(size_t)a * ZL + z] = 1;
-            has[(size_t)(3 + fidx[c->h_cid[p] == 0 ? 1 : 0][a]) * ZL + z] = 1;
+        {
+            DevBuf<char> dh;
+            DevBuf<int> dfi;
+            VC_CUDA(c, dh.alloc(has.size()));
+            VC_CUDA(c, cudaMemsetAsync(dh.p, 0, has.size(), st));
+            VC_CUDA(c, dfi.alloc(6));
+            int fl[6];
+            for (int q = 0; q < 6; ++q) fl[q] = fidx[q / 3][q % 3];
+            VC_CUDA(c, cudaMemcpyAsync(dfi.p, fl, sizeof fl, cudaMemcpyHostToDevice, st));
+            if (c->N)
+                k_plane_flags<<<(unsigned)std::min<int64_t>((c->N + 255) / 256, 148 * 8), 256, 0, st>>>(
+                    c->N, c->pan.axis.p, c->pan.sk.p, c->pan.cid.p, lo[2], ZL, dfi.p, dh.p);
+            count_launch(c);
+            VC_CUDA(c, cudaMemcpyAsync(has.data(), dh.p, has.size(), cudaMemcpyDeviceToHost, st));
+            VC_CUDA(c, cudaStreamSynchronize(st));
         }
         std::vector<int32_t> hp(18 * (size_t)ZL, -1);
         for (int g = 0; g < 9; ++g) {

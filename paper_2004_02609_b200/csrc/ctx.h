@@ -167,6 +167,7 @@ struct vc_ctx {
     int lgtk = 2;                           // log2 of P2's kx tile width (one-rank X1 layout)
     int lgt4 = 1;                           // log2 of P4's kx tile width (X3 layout)
     size_t colA = 0, colB = 0, colC = 0;    // per-column strides of bufA / bufB / bufC
+    size_t colS = 0;                        // per-column stride of bufS (several ranks)
     size_t offB[3], offC[6];
     int T3 = 1, nt3 = 1;   // P3 tile width and kx-tile count (tile-major X2 / R layouts)
     bool zdirect = false;  // P3 direct-z mode (operator.cu k_p3m)

@@ -592,19 +592,28 @@ vc_status solve_multi_dev(vc_ctx* c, int ncol, const double* const* d_b, double*
                 return qq;
             };
             const dim3 gd(kRedBlocks, (nv + kDotG - 1) / kDotG, 2), gd1(kRedBlocks, 1, 2), ga(gn, 1, 2);
+            // several ranks: each column's partial dots are summed over ranks (as K.dots does)
+            auto sum_ranks = [&](int off, int cnt) -> vc_status {
+                if (c->world == 1) return VC_OK;
+                vc_status e2 = comm_allreduce(c, ha + off, cnt);
+                return e2 ? e2 : comm_allreduce(c, hb + off, cnt);
+            };
             k_multidot2<<<gd, kRedNT, 0, st>>>(cc(A.K.V, B.K.V, A.K.t, B.K.t, ha, hb, nullptr, nullptr),
                                                n, nv, n, c->partial.p, c->ticket.p);
+            if ((e = sum_ranks(0, nv))) return e;
             k_multiaxpy2<<<ga, 256, 0, st>>>(cc(A.K.V, B.K.V, nullptr, nullptr, A.K.t, B.K.t, ha, hb),
                                              n, nv, n, -1.0);
             k_multidot2<<<gd, kRedNT, 0, st>>>(cc(A.K.V, B.K.V, A.K.t, B.K.t, ha + kMaxBasis,
                                                   hb + kMaxBasis, nullptr, nullptr),
                                                n, nv, n, c->partial.p, c->ticket.p);
+            if ((e = sum_ranks(kMaxBasis, nv))) return e;
             k_multiaxpy2<<<ga, 256, 0, st>>>(cc(A.K.V, B.K.V, nullptr, nullptr, A.K.t, B.K.t,
                                                 ha + kMaxBasis, hb + kMaxBasis),
                                              n, nv, n, -1.0);
             k_multidot2<<<gd1, kRedNT, 0, st>>>(cc(A.K.t, B.K.t, A.K.t, B.K.t, ha + 2 * kMaxBasis,
                                                    hb + 2 * kMaxBasis, nullptr, nullptr),
                                                 n, 1, n, c->partial.p, c->ticket.p);
+            if ((e = sum_ranks(2 * kMaxBasis, 1))) return e;
             k_scale_by_norm2<<<ga, 256, 0, st>>>(cc(nullptr, nullptr, A.K.t, B.K.t,
                                                     A.K.V + (size_t)nv * n, B.K.V + (size_t)nv * n,
                                                     ha + 2 * kMaxBasis, hb + 2 * kMaxBasis),

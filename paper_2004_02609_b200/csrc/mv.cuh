@@ -29,6 +29,7 @@ struct MV {
     const double* xs[kMaxB];
     double* ys[kMaxB];
     int64_t colA, colB, colC;
+    int64_t colS;  // several ranks: per-column stride of the peer send blocks (bufS)
     const int8_t* info;
     const double* ibar;
     double2* X2[3];

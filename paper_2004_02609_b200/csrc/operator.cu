@@ -120,7 +120,8 @@ __global__ void __launch_bounds__(FX<L>::NT, FX<L>::MINB) k_p1(MV mv) {
         const int nk = D ? mv.kxa[qd + 1] - k0 : mv.nkx;
         const int l0 = 2 * q - s;
         if (D) {
-            double2* o = mv.S1[qd][beta] + ((int64_t)j * nrow + l0) * nk + (k - k0);
+            double2* o = mv.S1[qd][beta] + blockIdx.z * (qd == mv.rank ? mv.colA : mv.colS) +
+                         ((int64_t)j * nrow + l0) * nk + (k - k0);
             if (l0 >= 0) o[0] = A;
             if (l0 + 1 < nrow) o[nk] = B;
         } else {  // one rank: [plane][kx tile][row][kx % tk], so P2 reads each tile contiguously
@@ -165,7 +166,7 @@ __global__ void __launch_bounds__(FY<L>::NT) k_p2(MV mv) {
         if (n >= ey || kx >= nkx) return czero();
         if (!D) return in0[((int64_t)tile * ey + n) * T + t];  // kx-tile-major X1 (one rank)
         const int p = row_owner(mv, n);  // row n arrived from rank p
-        return mv.R1[p][beta][((int64_t)j * mv.nr[p][beta] + (n - mv.ya[p])) * nkx + kx];
+        return mv.R1[p][beta][blockIdx.z * mv.colA + ((int64_t)j * mv.nr[p][beta] + (n - mv.ya[p])) * nkx + kx];
     };
     auto stN = [&](int t, int p, double2 v) {
         const int kx = tile * T + t;
@@ -254,7 +255,8 @@ __global__ void __launch_bounds__(FYS<L, KB>::NT) k_p4s(MV mv) {
                 const int pr = D ? row_owner(mv, yy) : 0;  // row yy goes to rank pr for P5
                 const int y0 = D ? mv.ya[pr] : 0;
                 if (D) {
-                    mv.S2[pr][f][((int64_t)j * mv.nr[pr][3 + f] + (yy - y0)) * nkx + kx] = v;
+                    mv.S2[pr][f][(tl / nt1) * (pr == mv.rank ? mv.colA : mv.colS) +
+                                 ((int64_t)j * mv.nr[pr][3 + f] + (yy - y0)) * nkx + kx] = v;
                 } else {  // one rank: X4 row-pair interleaved [plane][row pair][kx][2] (P5's pairs)
                     const int s5 = mv.lo[1] & 1, rr = yy + s5;
                     const int np = (mv.nr[0][3 + f] + s5 + 1) >> 1;
@@ -473,7 +475,7 @@ __global__ void __launch_bounds__(FX<L>::NT, FX<L>::MINB5) k_p5(MV mv) {
         }
         const int rr = yrow + s;  // one rank: row-pair interleaved X4 (see P4)
         const double2* src =
-            D ? mv.R2[qd][f] + ((int64_t)j * nrow + yrow) * nk + (k - k0)
+            D ? mv.R2[qd][f] + blockIdx.z * mv.colA + ((int64_t)j * nrow + yrow) * nk + (k - k0)
               : mv.R2[0][f] + blockIdx.z * mv.colA + ((((int64_t)j * nyp + (rr >> 1)) * nk + k) << 1 | (rr & 1));
         double2 w = v ? __ldg(src) : czero();
         if (ph) w = cmul(w, half_phase(mv.tw, k, L, +1));
@@ -1636,24 +1638,29 @@ vc_status operator_build(vc_ctx* c, const vc_build_opts* o) {
     c->colA = std::max<size_t>(1, std::max(nR1, nR2));
     c->colB = std::max<size_t>(1, nBt);
     c->colC = std::max<size_t>(1, nC);
+    // (several ranks too, round 2: the pass kernels offset every block by the column, the
+    // all-to-alls run per column and the lockstep solver sums its dot products over ranks).
+    // Multi-rank batching needs the direct-z P3 (z-FFT mode runs P3 column by column anyway).
+    c->colS = W > 1 ? std::max<size_t>(1, std::max(nS1, nS2)) : 0;
     c->nbmax = 1;
     const int nbw = std::min(kMaxB, c->m);
-    if (W == 1 && c->m >= 2 && !(o && o->no_batch) && c->bufA.cap >= c->colA * nbw &&
-        c->bufB.cap >= c->colB * nbw && c->bufC.cap >= c->colC * nbw) {
+    const bool want_batch = c->m >= 2 && !(o && o->no_batch) && (W == 1 || c->zdirect);
+    if (want_batch && c->bufA.cap >= c->colA * nbw && c->bufB.cap >= c->colB * nbw &&
+        c->bufC.cap >= c->colC * nbw && c->bufS.cap >= c->colS * nbw) {
         c->nbmax = nbw;  // the buffers already hold nbw columns (no memory query: it can stall
                          // behind the kernel-table work just enqueued)
-    } else if (W == 1 && c->m >= 2 && !(o && o->no_batch)) {
+    } else if (want_batch) {
         size_t fr = 0, totm = 0;
         cudaMemGetInfo(&fr, &totm);
-        const size_t percol = sizeof(double2) * (c->colA + c->colB + c->colC);
-        const size_t have = c->bufA.bytes() + c->bufB.bytes() + c->bufC.bytes();
+        const size_t percol = sizeof(double2) * (c->colA + c->colB + c->colC + c->colS);
+        const size_t have = c->bufA.bytes() + c->bufB.bytes() + c->bufC.bytes() + c->bufS.bytes();
         while (c->nbmax < std::min(kMaxB, c->m) && (c->nbmax + 1) * percol <= (fr + have) / 3) ++c->nbmax;
     }
     VC_CUDA(c, c->bufA.alloc(c->colA * c->nbmax));
     VC_CUDA(c, c->bufB.alloc(c->colB * c->nbmax));
     VC_CUDA(c, c->bufC.alloc(c->colC * c->nbmax));
-    c->bufS.reset();
-    if (W > 1) VC_CUDA(c, c->bufS.alloc(std::max<size_t>(1, std::max(nS1, nS2))));
+    if (W > 1) VC_CUDA(c, c->bufS.alloc(c->colS * c->nbmax));
+    else c->bufS.reset();
     // all-to-all block tables (bytes; the self block is written in place by P1 / P4)
     for (int e = 0; e < 2; ++e) {
         c->a2a_send[e].assign(W, nullptr);
@@ -1827,6 +1834,7 @@ static MV make_mv(vc_ctx* c, const double* x, double* y) {
     mv.colA = (int64_t)c->colA;
     mv.colB = (int64_t)c->colB;
     mv.colC = (int64_t)c->colC;
+    mv.colS = (int64_t)c->colS;
     mv.info = loc ? c->lp.info.p : c->pan.info.p;
     mv.ibar = loc ? c->lp.ibar.p : c->pan.ibar.p;
     mv.Rt = c->Rt.p;
@@ -1960,8 +1968,21 @@ static vc_status matvec_run(vc_ctx* c, const MV& mv) {
             // x-transformed planes: rows -> kx slabs before P2, back before P5
             const int e = p == 1 ? 0 : 1;
             if (det) VC_CUDA(c, cudaEventRecord(ev[12 + e], st));
-            vc_status s = comm_alltoall(c, c->a2a_send[e], c->a2a_sb[e], c->a2a_recv[e], c->a2a_rb[e]);
-            if (s) return s;
+            for (int i = 0; i < mv.nb; ++i) {  // one all-to-all per batch column
+                vc_status s;
+                if (i == 0) {
+                    s = comm_alltoall(c, c->a2a_send[e], c->a2a_sb[e], c->a2a_recv[e], c->a2a_rb[e]);
+                } else {
+                    std::vector<const void*> sp(c->a2a_send[e]);
+                    std::vector<void*> rp(c->a2a_recv[e]);
+                    for (int q = 0; q < c->world; ++q) {
+                        if (sp[q]) sp[q] = static_cast<const double2*>(sp[q]) + (size_t)i * c->colS;
+                        if (rp[q]) rp[q] = static_cast<double2*>(rp[q]) + (size_t)i * c->colA;
+                    }
+                    s = comm_alltoall(c, sp, c->a2a_sb[e], rp, c->a2a_rb[e]);
+                }
+                if (s) return s;
+            }
             if (det) VC_CUDA(c, cudaEventRecord(ev[14 + e], st));
         }
         if (det) VC_CUDA(c, cudaEventRecord(ev[1 + p], st));

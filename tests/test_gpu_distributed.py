@@ -73,6 +73,7 @@ def _st(name):
     return voxgen.sphere(12) if name == "sphere12" else voxgen.config(name)
 
 
+
 @pytest.mark.parametrize("name,W,zmode", CASES)
 def test_distributed_matvec_bitwise(name, W, zmode):
     st = _st(name)
@@ -134,14 +135,48 @@ def test_distributed_solve_matches_single():
     assert np.linalg.norm(xd - x1) <= 1e-9 * np.linalg.norm(x1)
 
 
-def test_distributed_full_size_c4_rows():
-    """BASELINE C4 at full size split over 2 ranks: the distributed matvec equals the 1-rank one."""
+@pytest.mark.parametrize("name,W", [("C2", 2), ("C2", 3), ("R2", 2), ("C5r", 4)])
+def test_distributed_batch_bitwise(name, W):
+    """Batched matvecs (two columns per launch chain, NEXT-3) on W ranks: every column equals the
+    1-rank single-column matvec bitwise (direct-z builds, where multi-rank batching applies)."""
+    st = _st(name)
+    n = _single(st, lambda c: c.n, zmode=2)
+    X = np.stack([voxgen.seeded_vector(n, 31), voxgen.seeded_vector(n, 32)], axis=1)
+    Y1 = np.stack([_single(st, lambda c: c.matvec(X[:, i]), zmode=2, mirror=False) for i in range(2)], axis=1)
+    def fn(c, r):
+        g = c.local_panels()
+        c.reset_stats()
+        Y = c.matvec_batch(np.ascontiguousarray(X[g]))
+        s = c.stats()
+        return g, Y, (s["n_matvec"], s["n_pass"][0])
+
+    res = _group(W, st, fn, zmode=2)
+    Yd = np.empty_like(Y1)
+    for g, yl, cnt in res:
+        Yd[g] = yl
+        assert cnt == (2, 1), cnt  # both columns in one launch chain
+    assert np.array_equal(Yd, Y1)
+
+
+@pytest.mark.parametrize("W", [2, 8])
+def test_distributed_full_size_c4_rows(W):
+    """BASELINE C4 at full size split over W ranks (W = 8: one node's worth): the distributed
+    matvec -- single and batched pair -- equals the 1-rank one bitwise."""
     st = voxgen.config("C4")
     n = _single(st, lambda c: c.n)
     x = voxgen.seeded_vector(n, 0)
+    x2 = voxgen.seeded_vector(n, 1)
     y1 = _single(st, lambda c: c.matvec(x), mirror=False)
-    res = _group(2, st, lambda c, r: (c.local_panels(), c.matvec(x[c.local_panels()])))
-    yd = np.empty(n)
-    for g, yl in res:
+    y2 = _single(st, lambda c: c.matvec(x2), mirror=False)
+
+    def fn(c, r):
+        g = c.local_panels()
+        return g, c.matvec(x[g]), c.matvec_batch(np.stack([x[g], x2[g]], axis=1))
+
+    res = _group(W, st, fn, timeout=1200)
+    yd, Yd = np.empty(n), np.empty((n, 2))
+    for g, yl, Yl in res:
         yd[g] = yl
+        Yd[g] = Yl
     assert np.array_equal(yd, y1)
+    assert np.array_equal(Yd[:, 0], y1) and np.array_equal(Yd[:, 1], y2)

@@ -254,6 +254,12 @@ vc_status vc_debug_fft(vc_ctx* ctx, int32_t L, int32_t n_lines, double* data, in
  * (n doubles; VC_ERR_INPUT on a length mismatch) -- used to measure what a compressed (e.g.
  * Tucker) spectrum does to the matvec.  VC_ERR_STATE before vc_build_operator. */
 vc_status vc_debug_get_spectra(vc_ctx* ctx, int64_t* n, int32_t* layout, double* out);
+/* Test hook: NCCL transport self-test on a context initialised with transport 0 -- an
+ * ncclAllReduce of {1,2,3,4} and a grouped ncclSend / ncclRecv of four doubles with this rank as
+ * its own peer (works on a world-1 communicator, i.e. on one GPU).  out[8] host doubles:
+ * out[0..3] = world x {1,2,3,4}, out[4..7] = the received {world x 1..4}.  VC_ERR_STATE without
+ * an NCCL communicator, VC_ERR_NCCL on a failing call. */
+vc_status vc_debug_nccl_selftest(vc_ctx* ctx, double* out);
 vc_status vc_debug_set_spectra(vc_ctx* ctx, int64_t n, const double* in);
 
 /* Last error message of the context ("" if none).  Valid until the next call on ctx. */

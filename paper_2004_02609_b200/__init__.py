@@ -27,7 +27,8 @@ EXPORTS = ("vc_create", "vc_set_geometry", "vc_get_sizes", "vc_get_panels", "vc_
            "vc_set_timing", "vc_get_stats", "vc_reset_stats", "vc_debug_kernel_entries",
            "vc_debug_fft", "vc_last_error", "vc_version", "vc_destroy", "vc_init_distributed",
            "vc_nccl_unique_id", "vc_group_create", "vc_group_destroy", "vc_get_local_panels",
-           "vc_plan_slabs", "vc_debug_get_spectra", "vc_debug_set_spectra")
+           "vc_plan_slabs", "vc_debug_get_spectra", "vc_debug_set_spectra",
+           "vc_debug_nccl_selftest")
 
 STATUS = {0: "VC_OK", 1: "VC_ERR_INPUT", 2: "VC_ERR_STATE", 3: "VC_ERR_OOM", 4: "VC_ERR_CUDA",
           5: "VC_ERR_NCCL", 6: "VC_NOT_CONVERGED", 7: "VC_ERR_UNSUPPORTED"}
@@ -123,6 +124,7 @@ def load_library(build_if_missing=False):
         "vc_debug_fft": [vp, i32, i32, vp, i32],
         "vc_debug_get_spectra": [vp, P(i64), vp, vp],
         "vc_debug_set_spectra": [vp, i64, vp],
+        "vc_debug_nccl_selftest": [vp, vp],
         "vc_init_distributed": [vp, i32, i32, i32, vp],
         "vc_nccl_unique_id": [vp],
         "vc_group_create": [i32, P(vp)],
@@ -446,6 +448,12 @@ class VoxCap:
         self._check(self._lib.vc_debug_get_spectra(self._ctx, ctypes.byref(n), _ptr(lay), _ptr(out)))
         keys = ("zdirect", "nblk", "NW", "T3", "nt3", "KY", "RS1", "nkx")
         return out, dict(zip(keys, (int(v) for v in lay)))
+
+    def nccl_selftest(self):
+        """NCCL transport self-test (test hook): allreduce + grouped send/recv to self."""
+        out = np.zeros(8)
+        self._check(self._lib.vc_debug_nccl_selftest(self._ctx, _ptr(out)))
+        return out
 
     def spectra_layout(self):
         """Layout of the kernel-spectrum table (no copy): zdirect, nblk, NW, T3, nt3, KY, RS1, nkx."""

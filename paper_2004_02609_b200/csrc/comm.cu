@@ -213,6 +213,31 @@ vc_status comm_alltoall(vc_ctx* c, const std::vector<const void*>& send,
     return VC_OK;
 }
 
+// NCCL transport self-test (test hook): every collective entry point the matvec and the solver
+// use -- ncclAllReduce and a grouped ncclSend / ncclRecv pair -- on a small device buffer, with
+// this rank as its own peer, so a world-1 communicator exercises the loaded symbols and their
+// argument conventions on a one-GPU box.  out[0..3] = allreduce of {1,2,3,4} (x world),
+// out[4..7] = the four doubles received from this rank.
+vc_status comm_nccl_selftest(vc_ctx* c, double* out) {
+    Comm* m = c->comm;
+    if (!m || m->kind != 0) return set_err(c, VC_ERR_STATE, "no NCCL communicator (vc_init_distributed transport 0)");
+    cudaStream_t st = c->stream;
+    DevBuf<double> d;
+    VC_CUDA(c, d.alloc(8));
+    const double h[8] = {1, 2, 3, 4, 0, 0, 0, 0};
+    VC_CUDA(c, cudaMemcpyAsync(d.p, h, sizeof h, cudaMemcpyHostToDevice, st));
+    ncclResult_t e = g_nccl.AllReduce(d.p, d.p, 4, ncclFloat64, ncclSum, m->nccl, st);
+    if (e == ncclSuccess) e = g_nccl.GroupStart();
+    if (e == ncclSuccess) e = g_nccl.Send(d.p, 32, ncclUint8, m->rank, m->nccl, st);
+    if (e == ncclSuccess) e = g_nccl.Recv(d.p + 4, 32, ncclUint8, m->rank, m->nccl, st);
+    const ncclResult_t e2 = g_nccl.GroupEnd();
+    if (e != ncclSuccess || e2 != ncclSuccess)
+        return set_err(c, VC_ERR_NCCL, std::string("self-test: ") + g_nccl.GetErrorString(e != ncclSuccess ? e : e2));
+    VC_CUDA(c, cudaMemcpyAsync(out, d.p, sizeof h, cudaMemcpyDeviceToHost, st));
+    VC_CUDA(c, cudaStreamSynchronize(st));
+    return VC_OK;
+}
+
 // in-place sum over ranks of n doubles on the device (fixed rank order for the thread group)
 vc_status comm_allreduce(vc_ctx* c, double* d, int n) {
     Comm* m = c->comm;

@@ -309,5 +309,6 @@ void comm_free(vc_ctx* c);
 vc_status comm_alltoall(vc_ctx* c, const std::vector<const void*>& send, const std::vector<size_t>& sb,
                         const std::vector<void*>& recv, const std::vector<size_t>& rb);
 vc_status comm_allreduce(vc_ctx* c, double* d, int n);
+vc_status comm_nccl_selftest(vc_ctx* c, double* out);
 inline void count_launch(vc_ctx* c, int k = 1) { c->stats.gpu_launches += k; }
 }  // namespace vc

@@ -483,6 +483,13 @@ vc_status vc_init_distributed(vc_ctx* c, int32_t rank, int32_t world, int32_t tr
     return comm_init(c, rank, world, transport, comm_id);
 }
 
+vc_status vc_debug_nccl_selftest(vc_ctx* c, double* out) {
+    VC_CHECK_CTX(c);
+    if (!out) return set_err(c, VC_ERR_INPUT, "out is NULL");
+    DeviceGuard g(c->device);
+    return comm_nccl_selftest(c, out);
+}
+
 vc_status vc_nccl_unique_id(void* out) {
     if (!out) return VC_ERR_INPUT;
     std::string err;

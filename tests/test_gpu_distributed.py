@@ -180,3 +180,22 @@ def test_distributed_full_size_c4_rows(W):
         Yd[g] = Yl
     assert np.array_equal(yd, y1)
     assert np.array_equal(Yd[:, 0], y1) and np.array_equal(Yd[:, 1], y2)
+
+
+def test_nccl_transport_world1():
+    """The NCCL transport on the one GPU a test box has (the NCCL code never ran):
+    libnccl loads, a unique id is drawn, a world-1 communicator initialises, ncclAllReduce and a
+    grouped ncclSend / ncclRecv (this rank as its own peer) move the right bytes, and a
+    capacitance extraction through a context initialised with the NCCL transport equals the
+    plain one bitwise."""
+    st = voxgen.config("C2")
+    C0, _ = _single(st, lambda c: c.solve_capacitance(tol=1e-10, maxit=4000))
+    with vc.VoxCap(0) as c:
+        c.init_distributed(0, 1, nccl_id=vc.nccl_unique_id())
+        out = c.nccl_selftest()
+        assert np.array_equal(out, [1, 2, 3, 4, 1, 2, 3, 4]), out
+        c.set_structure(st)
+        c.build_operator()
+        C1, info = c.solve_capacitance(tol=1e-10, maxit=4000)
+    assert all(i["converged"] for i in info)
+    assert np.array_equal(C1, C0)

@@ -299,7 +299,11 @@ struct P3T {
 // host mirror of P3T<L, NF>::T (the tile width also fixes the X2 / R tiled layouts)
 inline int p3_tile(int Mz, int nf) { return clampi(256 / Mz, 1, 16) * (nf <= 3 ? 2 : 1); }
 
-template <int L, int NF>
+// NS: stages of the TMA ring.  NS = 2 prefetches the next tile while the current one is
+// transformed (one CTA per SM: the stages fill shared memory); NS = 1 refills the single stage
+// as soon as the MAC has read it (overlapping the inverse z-FFT and the stores), small enough
+// for two CTAs per SM that overlap each other.
+template <int L, int NF, int NS = 2>
 __global__ void __launch_bounds__(kNT3) k_p3(MV mv) {
     constexpr int T = P3T<L, NF>::T;
     constexpr int W = P3T<L, NF>::W;
@@ -313,10 +317,10 @@ __global__ void __launch_bounds__(kNT3) k_p3(MV mv) {
     const int RC = mv.rchunk;                       // doubles per stage (even)
     double2* buf = sm;                              // [L][W] transform buffer
     double2* ph = buf + L * W;                      // [L] exp(-i pi kt / L)
-    double2* xin = ph + L;                          // [2][XS] staged X2 tiles
-    double* rin = reinterpret_cast<double*>(xin + 2 * XS);  // [2][RC] staged R tiles
-    int* zmap = reinterpret_cast<int*>(rin + 2 * RC);       // [9][L] plane -> index / -1
-    uint64_t* bar = reinterpret_cast<uint64_t*>(zmap + 9 * L);  // [2]
+    double2* xin = ph + L;                          // [NS][XS] staged X2 tiles
+    double* rin = reinterpret_cast<double*>(xin + NS * XS);  // [NS][RC] staged R tiles
+    int16_t* zmap = reinterpret_cast<int16_t*>(rin + NS * RC);  // [9][L] plane -> index / -1
+    uint64_t* bar = reinterpret_cast<uint64_t*>(zmap + ((9 * L + 3) & ~3));  // [2]
     __shared__ int fmeta[NF][4];                    // kind | alpha << 1, R offsets of b0..b2
     const int xo1 = T2 * nz0, xo2 = T2 * (nz0 + nz1);
     const int ntile = (Kx + T - 1) / T;
@@ -334,7 +338,7 @@ __global__ void __launch_bounds__(kNT3) k_p3(MV mv) {
     for (int k = threadIdx.x; k < L; k += kNT3) ph[k] = half_phase(mv.tw, ktil(k, L), L, -1);
     for (int e = threadIdx.x; e < 9 * L; e += kNT3) {
         const int g = e / L, z = e % L;
-        zmap[e] = z < mv.ZL ? mv.planes[(9 + g) * mv.ZL + z] : -1;
+        zmap[e] = (int16_t)(z < mv.ZL ? mv.planes[(9 + g) * mv.ZL + z] : -1);
     }
     __syncthreads();
     auto issue = [&](int tl, int s) {  // one thread: fetch tile tl = q * ntile + tile into stage s
@@ -349,8 +353,8 @@ __global__ void __launch_bounds__(kNT3) k_p3(MV mv) {
     unsigned par0 = 0, par1 = 0;
     int it = 0;
     for (int tl = blockIdx.x; tl < ntiles; tl += gridDim.x, ++it) {
-        const int s = it & 1;
-        if (threadIdx.x == 0 && tl + (int)gridDim.x < ntiles) {
+        const int s = NS == 1 ? 0 : (it & 1);
+        if (NS == 2 && threadIdx.x == 0 && tl + (int)gridDim.x < ntiles) {
             fence_proxy_async();
             issue(tl + gridDim.x, s ^ 1);
         }
@@ -431,6 +435,11 @@ __global__ void __launch_bounds__(kNT3) k_p3(MV mv) {
             }
         }
         __syncthreads();
+        if (NS == 1 && threadIdx.x == 0 && tl + (int)gridDim.x < ntiles) {
+            // the stage is consumed (forward FFT and MAC done): refill it during the inverse
+            fence_proxy_async();
+            issue(tl + gridDim.x, 0);
+        }
         auto ldo = [&](int pp, int n) { return buf[n * W + pp]; };
         auto sto = [&](int pp, int p, double2 v) {
             const int f = pp / T2, c = pp % T2;
@@ -993,28 +1002,36 @@ static cudaError_t launch_p2(const MV& mv, cudaStream_t st) {
     return cudaGetLastError();
 }
 template <int L, int NF>
-static size_t p3_smem(const MV& mv) {
+static size_t p3_smem(const MV& mv, int ns) {
     constexpr int W = P3T<L, NF>::W, T = P3T<L, NF>::T;
     const size_t XS = (size_t)2 * T * (mv.nzin[0] + mv.nzin[1] + mv.nzin[2]);
-    return sizeof(double2) * ((size_t)L * W + L + 2 * XS) + sizeof(double) * 2 * (size_t)mv.rchunk +
-           sizeof(int) * 9 * L + 2 * sizeof(uint64_t);
+    return sizeof(double2) * ((size_t)L * W + L + ns * XS) + sizeof(double) * ns * (size_t)mv.rchunk +
+           sizeof(int16_t) * ((9 * L + 3) & ~3) + 2 * sizeof(uint64_t);
 }
-template <int L, int NF>
-static cudaError_t launch_p3_t(const MV& mv, cudaStream_t st) {
+template <int L, int NF, int NS>
+static cudaError_t launch_p3_ns(const MV& mv, cudaStream_t st, size_t smem) {
     constexpr int T = P3T<L, NF>::T;
-    const size_t smem = p3_smem<L, NF>(mv);
-    if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
-    cudaError_t e = prep(k_p3<L, NF>, smem);
+    cudaError_t e = prep(k_p3<L, NF, NS>, smem);
     if (e) return e;
     int per_sm = 0, nsm = 0, dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_p3<L, NF>, kNT3, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_p3<L, NF, NS>, kNT3, smem);
     const int ntiles = ((mv.nkx + T - 1) / T) * (mv.My / 2 + 1);
     if (ntiles == 0) return cudaSuccess;
     const int grid = std::max(1, std::min(ntiles, std::max(1, per_sm) * nsm));
-    k_p3<L, NF><<<grid, kNT3, smem, st>>>(mv);
+    k_p3<L, NF, NS><<<grid, kNT3, smem, st>>>(mv);
     return cudaSuccess;
+}
+template <int L, int NF>
+static cudaError_t launch_p3_t(const MV& mv, cudaStream_t st) {
+    // one stage when that lets two CTAs share an SM (VC_P3_NS forces 1 or 2: A/B)
+    static const int ns_env = getenv("VC_P3_NS") ? atoi(getenv("VC_P3_NS")) : 0;
+    const size_t s1 = p3_smem<L, NF>(mv, 1), s2 = p3_smem<L, NF>(mv, 2);
+    const int ns = ns_env == 1 || ns_env == 2 ? ns_env : (s1 <= 112 * 1024 && s2 > 112 * 1024 ? 1 : 2);
+    const size_t smem = ns == 1 ? s1 : s2;
+    if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
+    return ns == 1 ? launch_p3_ns<L, NF, 1>(mv, st, smem) : launch_p3_ns<L, NF, 2>(mv, st, smem);
 }
 template <int L>
 static cudaError_t launch_p3_l(const MV& mv, cudaStream_t st) {

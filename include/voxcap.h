@@ -85,7 +85,22 @@ typedef struct {
                                unchanged -- they do not depend on panel positions or on the
                                permittivities (kept in HBM instead of an
                                install-time file); 0 = default: always regenerate            */
-    int32_t reserved[5];
+    int32_t tucker_digits;  /* d > 0: keep the direct-z kernel spectra Tucker-compressed (P:121-129,
+                               Eq. 13): per block X ~ S x1 U1 x2 U2 with
+                               ||X - X~||_F <= 10^-d ||X||_F, and P3 rebuilds every tile's kernel
+                               rows from U1 and W = S x2 U2 on the FP64 tensor cores; the exact
+                               table is freed after compression.  Needs the direct-z P3 (zmode 0
+                               choosing it, or 2): VC_ERR_UNSUPPORTED otherwise.  0 = default:
+                               exact spectra.  d in 1..15.                                    */
+    int32_t tucker_pad_;    /* (alignment; must be 0)                                         */
+    const char* tucker_cache; /* with tucker_digits > 0: a directory holding the install-time
+                               cache of compressed tables:
+                               the build loads voxcap_tk_<signature>.bin when it exists and is
+                               valid (no kernel generation, no FFTs, no compression), otherwise
+                               builds, compresses and writes it (atomically).  The signature
+                               covers grid, window, rank slab, dv, kernel blocks, z offsets and
+                               digits.  NULL = no cache.                                      */
+    int32_t reserved[2];
 } vc_build_opts;
 
 /* Solve options.  Zero fields take the paper's defaults. */
@@ -124,7 +139,12 @@ typedef struct {
                                and the P3 kernel spectra once (vc_matvec_batch)              */
     int64_t precond_doubles;/* last build: doubles of the stored (unique) preconditioner blocks
                                (the memory P:157 compares; 0 for precond 1 / 2)              */
-    int64_t reserved[3];
+    int64_t spectra_doubles;/* last build: doubles of the resident kernel tables P3 reads (exact
+                               table, or the Tucker U1 / W fragment tables)                   */
+    int64_t tucker_cache;   /* last build: 0 no cache, 1 loaded from the cache file, 2 written,
+                               3 could not be written                                        */
+    double  tucker_err;     /* last build: max over blocks of the measured relative Frobenius
+                               error of the Tucker-compressed spectra (0 when exact)          */
 } vc_stats;
 
 /* Create a context on CUDA device `cuda_device`.  `cuda_stream` is a cudaStream_t to order
@@ -261,6 +281,12 @@ vc_status vc_debug_get_spectra(vc_ctx* ctx, int64_t* n, int32_t* layout, double*
  * an NCCL communicator, VC_ERR_NCCL on a failing call. */
 vc_status vc_debug_nccl_selftest(vc_ctx* ctx, double* out);
 vc_status vc_debug_set_spectra(vc_ctx* ctx, int64_t n, const double* in);
+/* Tucker-compressed spectra of the last build (vc_build_opts.tucker_digits > 0): *nblk blocks;
+ * ranks[2 * nblk] = (r1, r2) per block (kx mode, |ky| mode; the z-offset mode is kept full);
+ * err[nblk] = measured relative Frobenius error per block (as stored in the cache file when it
+ * was loaded); dims[3] = (nkx, nq, ZU).  Any output pointer may be NULL; arrays hold at least 16
+ * blocks.  VC_ERR_STATE if the build kept exact spectra. */
+vc_status vc_get_tucker(const vc_ctx* ctx, int32_t* nblk, int32_t* ranks, double* err, int32_t* dims);
 
 /* Last error message of the context ("" if none).  Valid until the next call on ctx. */
 const char* vc_last_error(const vc_ctx* ctx);

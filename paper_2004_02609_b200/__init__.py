@@ -28,7 +28,7 @@ EXPORTS = ("vc_create", "vc_set_geometry", "vc_get_sizes", "vc_get_panels", "vc_
            "vc_debug_fft", "vc_last_error", "vc_version", "vc_destroy", "vc_init_distributed",
            "vc_nccl_unique_id", "vc_group_create", "vc_group_destroy", "vc_get_local_panels",
            "vc_plan_slabs", "vc_debug_get_spectra", "vc_debug_set_spectra",
-           "vc_debug_nccl_selftest")
+           "vc_debug_nccl_selftest", "vc_get_tucker")
 
 STATUS = {0: "VC_OK", 1: "VC_ERR_INPUT", 2: "VC_ERR_STATE", 3: "VC_ERR_OOM", 4: "VC_ERR_CUDA",
           5: "VC_ERR_NCCL", 6: "VC_NOT_CONVERGED", 7: "VC_ERR_UNSUPPORTED"}
@@ -45,7 +45,9 @@ class BuildOpts(ctypes.Structure):
     _fields_ = [("pad", ctypes.c_int32 * 3), ("box", ctypes.c_int32 * 3),
                 ("precond", ctypes.c_int32), ("zmode", ctypes.c_int32),
                 ("no_mirror", ctypes.c_int32), ("no_batch", ctypes.c_int32),
-                ("reuse_tables", ctypes.c_int32), ("reserved", ctypes.c_int32 * 5)]
+                ("reuse_tables", ctypes.c_int32), ("tucker_digits", ctypes.c_int32),
+                ("tucker_pad_", ctypes.c_int32), ("tucker_cache", ctypes.c_char_p),
+                ("reserved", ctypes.c_int32 * 2)]
 
 
 class SolveOpts(ctypes.Structure):
@@ -70,7 +72,8 @@ class Stats(ctypes.Structure):
                 ("gpu_launches", ctypes.c_int64), ("ms_kgen", ctypes.c_double),
                 ("ms_kfft", ctypes.c_double), ("ms_geometry", ctypes.c_double),
                 ("ms_comm", ctypes.c_double), ("bytes_moved", ctypes.c_double * 5),
-                ("precond_doubles", ctypes.c_int64), ("reserved", ctypes.c_int64 * 3)]
+                ("precond_doubles", ctypes.c_int64), ("spectra_doubles", ctypes.c_int64),
+                ("tucker_cache", ctypes.c_int64), ("tucker_err", ctypes.c_double)]
 
     def as_dict(self):
         return {"n_matvec": self.n_matvec, "ms_matvec": self.ms_matvec,
@@ -80,7 +83,9 @@ class Stats(ctypes.Structure):
                 "ms_setup": self.ms_setup, "ms_precond_build": self.ms_precond_build,
                 "gpu_launches": self.gpu_launches, "ms_kgen": self.ms_kgen,
                 "ms_kfft": self.ms_kfft, "ms_geometry": self.ms_geometry,
-                "ms_comm": self.ms_comm, "precond_doubles": self.precond_doubles}
+                "ms_comm": self.ms_comm, "precond_doubles": self.precond_doubles,
+                "spectra_doubles": self.spectra_doubles, "tucker_cache": self.tucker_cache,
+                "tucker_err": self.tucker_err}
 
 
 def lib_path():
@@ -125,6 +130,7 @@ def load_library(build_if_missing=False):
         "vc_debug_get_spectra": [vp, P(i64), vp, vp],
         "vc_debug_set_spectra": [vp, i64, vp],
         "vc_debug_nccl_selftest": [vp, vp],
+        "vc_get_tucker": [vp, vp, vp, vp, vp],
         "vc_init_distributed": [vp, i32, i32, i32, vp],
         "vc_nccl_unique_id": [vp],
         "vc_group_create": [i32, P(vp)],
@@ -304,10 +310,15 @@ class VoxCap:
 
     # -- operator ------------------------------------------------------------------------
     def build_operator(self, pad=None, box=None, precond=3, zmode=0, mirror=True, batch=True,
-                       reuse_tables=False):
+                       reuse_tables=False, tucker_digits=0, tucker_cache=None):
         """zmode: 0 automatic, 1 z-FFT (3-D circulant), 2 direct z-convolution; mirror=False
-        generates every kernel block (no x<->y transposes)."""
+        generates every kernel block (no x<->y transposes); tucker_digits=d > 0 keeps the
+        direct-z spectra Tucker-compressed to relative error 10^-d, with the
+        compressed tables cached in directory `tucker_cache`."""
         o = BuildOpts()
+        o.tucker_digits = int(tucker_digits)
+        self._tk_cache = None if tucker_cache is None else os.fsencode(tucker_cache)
+        o.tucker_cache = self._tk_cache
         o.zmode = int(zmode)
         o.no_mirror = 0 if mirror else 1
         o.no_batch = 0 if batch else 1
@@ -448,6 +459,21 @@ class VoxCap:
         self._check(self._lib.vc_debug_get_spectra(self._ctx, ctypes.byref(n), _ptr(lay), _ptr(out)))
         keys = ("zdirect", "nblk", "NW", "T3", "nt3", "KY", "RS1", "nkx")
         return out, dict(zip(keys, (int(v) for v in lay)))
+
+    def tucker(self):
+        """Tucker-compressed spectra of the last build: ranks (r1, r2) and measured relative
+        error per block, dims (nkx, nq, ZU); None when the build kept exact spectra."""
+        nb = ctypes.c_int32()
+        ranks = np.zeros(32, np.int32)
+        err = np.zeros(16)
+        dims = np.zeros(3, np.int32)
+        st = self._lib.vc_get_tucker(self._ctx, ctypes.byref(nb), _ptr(ranks), _ptr(err), _ptr(dims))
+        if st == 2:
+            return None
+        self._check(st)
+        n = nb.value
+        return {"nblk": n, "ranks": ranks[: 2 * n].reshape(n, 2).tolist(), "err": err[:n].tolist(),
+                "dims": dims.tolist()}
 
     def nccl_selftest(self):
         """NCCL transport self-test (test hook): allreduce + grouped send/recv to self."""

@@ -96,6 +96,30 @@ struct Field {
 struct Precond;  // precond.cu
 struct Comm;     // comm.cu
 
+// Tucker-compressed direct-z kernel spectra (Eq. 13; tucker.cu).
+// Block b's table X_b[kx][q][u] (this rank's kx, q = |ky|, z offset u) is kept as
+//   X_b ~ S_b x1 U1_b x2 U2_b      (U1_b: nkx x r1, U2_b: nq x r2 orthonormal; S_b: r1 x r2 x ZU)
+// and P3 reconstructs the K rows of every tile on the fly from two resident tables:
+//   U1f [kx tile][block][kc][32]        DMMA A fragments of U1_b (8 kx x 4 ranks per kc)
+//   Wf  [q][block][nc][kc][32]          DMMA B fragments of W_b[q] = S_b x2 U2_b[q] (4 ranks x 8 u)
+struct Tucker {
+    bool on = false;
+    int digits = 0;          // relative Frobenius error <= 10^-digits per block
+    int nblk = 0, nkx = 0, nq = 0, ZU = 0;
+    std::vector<int> r1, r2;  // multilinear ranks (mode kx, mode q); mode u is kept full
+    std::vector<double> err;  // measured relative Frobenius error of the reconstructed block
+    int nkc[16] = {}, u1o[16] = {}, wo[16] = {};  // per block: rank chunks, fragment offsets
+    int nc = 0;               // 8-wide u chunks
+    int u1t = 0, wq = 0;      // doubles per U1f kx tile / per Wf q
+    int cache = 0;            // 0 no cache file, 1 loaded (NEXT-4 hit), 2 written, 3 write failed
+    int kind[16] = {};        // block kind (0 = P, 1 = E): the file holds cores at dv = 1 m, scaled
+    double dv = 0;            // by dv^3 (P) / dv^2 (E) when loaded (App. C)
+    DevBuf<double> U1f, Wf;
+    DevBuf<double> U1, U2, S;   // factors (column-major per block: [b][k][i]) and cores
+    DevBuf<double> R, vb, st, part, t1, w, errs;  // build scratch
+    int64_t resident() const { return (int64_t)(U1f.n + Wf.n); }
+};
+
 constexpr int kMaxRanks = 8;  // one NVLink box
 
 // This rank's panels (canonical order restricted to the rank) and its slot maps
@@ -159,6 +183,7 @@ struct vc_ctx {
     int nblk = 0;
     size_t blk_stride = 0;  // doubles per folded spectrum
     vc::DevBuf<double> Rt;  // folded, phase-stripped, scaled kernel spectra
+    vc::Tucker tk;          // Tucker-compressed form of Rt (vc_build_opts.tucker_digits)
     vc::DevBuf<double2> tw;  // twiddles exp(-2 pi i n / kTabN)
     std::vector<double> kt_key;  // signature of the kernel tables in Rt / pcTab (reuse_tables)
     bool tables_reused = false;
@@ -300,6 +325,11 @@ int row_owner_abs(const vc_ctx* c, int yabs);
 void plan_kx_slabs(int W, int Kx, int T3, int* kxa);
 int row_owner_plan(int W, int Nv, int nb, int b0, int nbr, int yabs);
 void plan_row_slabs(int W, int ny, int lo, int EY, int Nv, int* ya, int* nb, int* b0, int* nbr);
+// tucker.cu
+vc_status tucker_compress(vc_ctx* c);
+vc_status tucker_from_cache(vc_ctx* c);
+bool tucker_try_load(vc_ctx* c, const char* dir, const std::vector<double>& key);
+void tucker_save(vc_ctx* c, const char* dir, const std::vector<double>& key);
 // comm.cu
 vc_status comm_nccl_unique_id(void* out, std::string& err);
 void* group_create(int world);

@@ -69,6 +69,13 @@ struct MV {
     const int32_t* p3m_tab;
     int p3m_nzt, p3m_kc, p3m_mct;  // stacked padded planes, 4-column chunks, 8-row chunks
     int p3m_nst;                   // k_p3m ring depth
+    // Tucker-compressed spectra (tucker.cu; vc::Tucker): k_p3m<TK> rebuilds each tile's K rows
+    // from U1f (per kx tile, tk_u1t doubles) and Wf (per q, tk_wq doubles) instead of reading Rt
+    int tk;
+    const double* tk_u1;
+    const double* tk_w;
+    int tk_u1t, tk_wq, tk_nc, tk_items;
+    int tk_nkc[16], tk_u1o[16], tk_wo[16];
 };
 
 __device__ __forceinline__ int zlist(const MV& mv, int g, int j) { return mv.planes[g * mv.ZL + j]; }
@@ -115,6 +122,9 @@ constexpr int kP3mMaxStages = 6;
 // ring depth that fits shared memory for a shape (0 or 1: the shape cannot run direct-z)
 int p3m_stages(int rs1, int nzp, int kc, int mct);
 size_t p3m_smem(int rs1, int nzp, int kc, int mct, int nst);
+// Tucker P3: (block, u chunk) items per warp held in registers, and the ring depth that fits
+constexpr int kTkItems = 6;
+int p3m_tk_stages(int rs1, int nzp, int kc, int mct, int u1t, int wq);
 cudaError_t launch_p3m(const MV& mv, cudaStream_t st);
 
 }  // namespace vc

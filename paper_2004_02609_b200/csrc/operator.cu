@@ -1368,6 +1368,10 @@ vc_status operator_build(vc_ctx* c, const vc_build_opts* o) {
                      (zmode == 2 || (zmode == 0 && 4.0 * mac <= fft));
         if (zmode == 2 && !c->zdirect)
             return set_err(c, VC_ERR_UNSUPPORTED, "direct-z mode: too many output planes or input planes");
+        const int tkd = o ? o->tucker_digits : 0;
+        if (tkd < 0 || tkd > 14) return set_err(c, VC_ERR_INPUT, "tucker_digits must be 0..14");
+        if (tkd > 0 && !c->zdirect)
+            return set_err(c, VC_ERR_UNSUPPORTED, "Tucker-compressed spectra need the direct-z P3 (zmode 0 choosing it, or 2)");
         c->ZU = c->ZL;
         c->rs1 = c->zdirect ? rs1 : 0;
         c->p3m_nzt = c->p3m_kc = c->p3m_mct = 0;
@@ -1447,11 +1451,42 @@ vc_status operator_build(vc_ctx* c, const vc_build_opts* o) {
         key.push_back(d.beta);
     }
     const size_t rt_n = std::max<size_t>(1, c->rchunk * (size_t)(My / 2 + 1) * c->nt3);
-    const bool reuse = o && o->reuse_tables && key == c->kt_key && c->Rt.p && c->Rt.n == rt_n;
+    // Tucker-compressed spectra (NEXT-1) and their cache file (NEXT-4, keyed without the
+    // preconditioner boxes, which the spectra do not depend on)
+    Tucker& TK = c->tk;
+    TK.on = o && o->tucker_digits > 0;
+    TK.cache = 0;
+    TK.err.clear();
+    std::vector<double> tk_key;
+    bool tk_hit = false;
+    if (TK.on) {
+        TK.digits = o->tucker_digits;
+        TK.nblk = c->nblk;
+        TK.nkx = nkx;
+        TK.nq = My / 2 + 1;
+        TK.ZU = c->ZU;
+        TK.dv = c->dv;
+        for (int i = 0; i < c->nblk && i < 16; ++i) TK.kind[i] = defs[i].kind;
+        // the spectra scale as dv^3 (P) / dv^2 (E) (App. C): the file is independent of dv
+        tk_key = {1.0 /* format */, (double)M[0], (double)M[1], (double)M[2], (double)c->ZU, (double)nkx,
+                  (double)kx0, (double)c->world, (double)c->rank, (double)TK.digits,
+                  (double)(o && o->no_mirror)};
+        for (const BlkDef& d : defs) {
+            tk_key.push_back(d.kind);
+            tk_key.push_back(d.alpha);
+            tk_key.push_back(d.beta);
+        }
+        tk_hit = tucker_try_load(c, o->tucker_cache, tk_key);
+    }
+    const bool reuse = !TK.on && o && o->reuse_tables && key == c->kt_key && c->Rt.p && c->Rt.n == rt_n;
     c->kt_key.clear();
     c->tables_reused = reuse;
-    VC_CUDA(c, c->Rt.alloc(rt_n));
-    if (!reuse) VC_CUDA(c, cudaMemsetAsync(c->Rt.p, 0, c->Rt.bytes(), st));
+    if (tk_hit) {
+        c->Rt.reset();  // the compressed tables come from the cache file: no exact table at all
+    } else {
+        VC_CUDA(c, c->Rt.alloc(rt_n));
+        if (!reuse) VC_CUDA(c, cudaMemsetAsync(c->Rt.p, 0, c->Rt.bytes(), st));
+    }
     // spectra (a2 on the parity octant -> full cyclic grid -> 3-D FFT -> phase strip + fold)
     {
         // no host synchronisation in this loop: the preconditioner's host bookkeeping (next in
@@ -1462,7 +1497,7 @@ vc_status operator_build(vc_ctx* c, const vc_build_opts* o) {
             c->kev.resize(4 * (size_t)std::max(1, c->nblk));
             for (size_t e = n0; e < c->kev.size(); ++e) VC_CUDA(c, cudaEventCreate(&c->kev[e]));
         }
-        c->kev_n = reuse ? 0 : c->nblk;
+        c->kev_n = (reuse || tk_hit) ? 0 : c->nblk;
         DevBuf<double2>& G = c->kG;
         DevBuf<double>& Ko = c->kKo;
         const bool zd = c->zdirect;
@@ -1471,7 +1506,7 @@ vc_status operator_build(vc_ctx* c, const vc_build_opts* o) {
         const int64_t tot = (int64_t)M[0] * M[1] * MZ;
         const int Ox = M[0] / 2 + 1, Oy = M[1] / 2 + 1, Oz = zd ? c->ZU : M[2] / 2 + 1;
         const int64_t otot = (int64_t)Ox * Oy * Oz;
-        if (!reuse) {
+        if (!reuse && !tk_hit) {
             VC_CUDA(c, G.alloc(tot));
             VC_CUDA(c, Ko.alloc(otot));
         }
@@ -1525,7 +1560,7 @@ vc_status operator_build(vc_ctx* c, const vc_build_opts* o) {
                 count_launch(c);
             }
         }
-        for (int pass = 0; pass < 2; ++pass)
+        for (int pass = 0; pass < (tk_hit ? 0 : 2); ++pass)
         for (int i = 0; i < c->nblk; ++i) {
             const BlkDef& d = defs[i];
             if ((mirror_of[i] >= 0) != (pass == 1)) continue;
@@ -1590,9 +1625,20 @@ vc_status operator_build(vc_ctx* c, const vc_build_opts* o) {
         }
         }  // !reuse
         VC_CUDA(c, cudaGetLastError());
-        c->kt_key = key;
+        if (!TK.on) c->kt_key = key;
     }
     tr.mark("kernel tables enqueued");
+    if (TK.on) {
+        vc_status ts = tk_hit ? tucker_from_cache(c) : tucker_compress(c);
+        if (ts != VC_OK) return ts;
+        if (tk_hit) {
+            TK.cache = 1;
+        } else {
+            c->Rt.reset();  // P3 reads the compressed tables only
+            if (o->tucker_cache && *o->tucker_cache) tucker_save(c, o->tucker_cache, tk_key);
+        }
+        tr.mark("tucker tables");
+    }
     // ---- spatial partition: rank p owns a contiguous range of preconditioner
     // box rows along y, so every R_BD block stays on one rank; window row y -> rank (monotone)
     int EY = 1;
@@ -1734,7 +1780,13 @@ vc_status operator_build(vc_ctx* c, const vc_build_opts* o) {
     }
     c->bytes_pass[0] = cb * nX1 + 4.0 * slots + 8.0 * NL;
     c->bytes_pass[1] = cb * (nX1r + nB);
-    c->bytes_k3 = 8.0 * (double)nkx * (My / 2 + 1) * (c->zdirect ? c->ZU : Mz / 2 + 1) * c->nblk;
+    c->bytes_k3 = TK.on ? 8.0 * (double)TK.resident()
+                        : 8.0 * (double)nkx * (My / 2 + 1) * (c->zdirect ? c->ZU : Mz / 2 + 1) * c->nblk;
+    c->stats.spectra_doubles = TK.on ? TK.resident() : (int64_t)c->Rt.n;
+    c->stats.tucker_cache = TK.cache;
+    double tkerr = 0;
+    for (double e : TK.err) tkerr = std::max(tkerr, e);
+    c->stats.tucker_err = TK.on ? tkerr : 0.0;
     c->bytes_pass[2] = cb * (nB + (double)nC) + c->bytes_k3;
     c->bytes_pass[3] = cb * ((double)nC + nX4);
     c->bytes_pass[4] = cb * nX4r + 4.0 * slots_out + 8.0 * NL + (8.0 + 8.0 + 1.0) * ndl + 1.0 * NL;
@@ -1865,6 +1917,21 @@ static MV make_mv(vc_ctx* c, const double* x, double* y) {
     mv.zdirect = c->zdirect;
     mv.ZU = c->ZU;
     mv.rs1 = c->rs1;
+    mv.tk = c->tk.on ? 1 : 0;
+    if (mv.tk) {
+        const Tucker& T = c->tk;
+        mv.tk_u1 = T.U1f.p;
+        mv.tk_w = T.Wf.p;
+        mv.tk_u1t = T.u1t;
+        mv.tk_wq = T.wq;
+        mv.tk_nc = T.nc;
+        mv.tk_items = T.nblk * T.nc;
+        for (int b = 0; b < 16; ++b) {
+            mv.tk_nkc[b] = b < T.nblk ? T.nkc[b] : 0;
+            mv.tk_u1o[b] = b < T.nblk ? T.u1o[b] : 0;
+            mv.tk_wo[b] = b < T.nblk ? T.wo[b] : 0;
+        }
+    }
     for (int b = 0; b < 3; ++b) {
         mv.x2nz[b] = c->zdirect ? c->p3m_nzt : c->nzin[b];
         mv.x2zo[b] = c->zdirect ? c->p3m_zoff[b] : 0;

@@ -62,6 +62,27 @@ int p3m_stages(int rs1, int nzp, int kc, int mct) {
 size_t p3m_smem(int rs1, int nzp, int kc, int mct, int nst) {
     return 1024 + (size_t)nst * ((size_t)p3m_kbytes(rs1) + 4 * (size_t)p3m_xregion(nzp)) + p3m_fixed(kc, mct);
 }
+// Tucker P3 (TK): a stage's first region holds the tile's U1 fragments, then (rebuilt in place)
+// its K rows; the W fragments of the current q sit after the stages; no k-split exchange buffer
+// (K rows in shared memory use the odd stride rs1 | 1: the rebuilt rows of 8 kx land in distinct
+// banks)
+__host__ __device__ constexpr int p3m_tk_region(int rs1, int u1t) {
+    return ((8 * u1t > 8 * kMmaT * (rs1 | 1) ? 8 * u1t : 8 * kMmaT * (rs1 | 1)) + 1023) & ~1023;
+}
+static size_t p3m_tk_fixed(int kc, int mct, int wq) {
+    return (((size_t)8 * wq + 15) & ~(size_t)15) + 16 * (size_t)mct * 8 + 2 * (size_t)kc * mct * 32 +
+           4 * (size_t)mct * 8 + 16 * kP3mMaxStages + 64 + 16 * (size_t)kMmaT * kMmaSplit * kTkItems + 16;
+}
+static size_t p3m_tk_smem(int rs1, int nzp, int kc, int mct, int u1t, int wq, int nst) {
+    return 1024 + (size_t)nst * ((size_t)p3m_tk_region(rs1, u1t) + 4 * (size_t)p3m_xregion(nzp)) +
+           p3m_tk_fixed(kc, mct, wq);
+}
+int p3m_tk_stages(int rs1, int nzp, int kc, int mct, int u1t, int wq) {
+    const size_t st = (size_t)p3m_tk_region(rs1, u1t) + 4 * (size_t)p3m_xregion(nzp);
+    const size_t fx = 1024 + p3m_tk_fixed(kc, mct, wq);
+    if (fx >= 227 * 1024) return 0;
+    return (int)std::min<size_t>(2, (227 * 1024 - fx) / st);
+}
 
 __device__ __forceinline__ double p3m_aval(const double* __restrict__ kt, unsigned e16) {
     const double v = kt[e16 & 0x7fff];
@@ -79,7 +100,38 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* tm, in
 // instead of the rows and exchange partial sums through shared memory (a 64-thread named
 // barrier per pair), each storing half of the row chunks.  Measured on C4 (pair launch):
 // 0.61 ms vs 0.54 ms for the row split, so KS is off unless VC_P3M_KS=1 (A/B).
-template <int MC, int KCM, bool KS>
+// Tucker P3: the K-row items k = 0..NI-1 of this warp (item = warp + 16 k = (block, u chunk)),
+// C = U1 W[q] on the tensor cores as NI interleaved accumulation chains over the rank chunks
+template <int NI>
+__device__ __forceinline__ void tk_rebuild(double (&cr)[kTkItems][2], const double* __restrict__ u1s,
+                                           const double* __restrict__ wsm, const int4* __restrict__ it4, int nkc,
+                                           int lane) {
+    int ao[NI], bo[NI];
+#pragma unroll
+    for (int k = 0; k < NI; ++k) {
+        const int4 d = it4[k * kMmaT * kMmaSplit];
+        ao[k] = d.x + lane;
+        bo[k] = d.y + lane;
+        cr[k][0] = cr[k][1] = 0.0;
+    }
+    for (int kc = 0; kc < nkc; ++kc) {
+        double a[NI], bv[NI];
+#pragma unroll
+        for (int k = 0; k < NI; ++k) {
+            a[k] = u1s[ao[k] + kc * 32];
+            bv[k] = wsm[bo[k] + kc * 32];
+        }
+#pragma unroll
+        for (int k = 0; k < NI; ++k) dmma884(cr[k][0], cr[k][1], a[k], bv[k]);
+    }
+}
+
+// TK (Tucker-compressed spectra, tucker.cu): the stage carries the tile's U1 fragments instead
+// of its K rows; every warp first rebuilds (block, u chunk) items of K = U1 W[q] on the tensor
+// cores (W[q] resident in shared memory, reloaded by the producer when q changes: each CTA walks
+// one contiguous, q-major range of tiles), a CTA barrier, the K rows are written over the U1
+// fragments, a second barrier, then the MAC runs unchanged.
+template <int MC, int KCM, bool KS, bool TK>
 __global__ void __launch_bounds__(kMmaT * kMmaSplit * 32, 1)
     k_p3m(const __grid_constant__ CUtensorMap tmx0, const __grid_constant__ CUtensorMap tmx1, MV mv) {
     constexpr int T = kMmaT, NW = kMmaT * kMmaSplit, NTHR = NW * 32;
@@ -94,15 +146,35 @@ __global__ void __launch_bounds__(kMmaT * kMmaSplit * 32, 1)
     const int nb = mv.nb, nzp = mv.p3m_nzt, KC = mv.p3m_kc, MCT = mv.p3m_mct, RS1 = mv.rs1;
     const int NST = mv.p3m_nst;
     const int RC = T * RS1;
-    const int KB = p3m_kbytes(RS1), XR = p3m_xregion(nzp), SB = KB + 4 * XR;  // stage bytes
+    const int KB = TK ? p3m_tk_region(RS1, mv.tk_u1t) : p3m_kbytes(RS1);
+    const int XR = p3m_xregion(nzp), SB = KB + 4 * XR;  // stage bytes
     const int lg4 = mv.lgt4;
     const int nt4 = (nkx + (1 << lg4) - 1) >> lg4;
-    longlong2* const rdesc = reinterpret_cast<longlong2*>(sm + (size_t)NST * SB);      // [MCT * 8]
+    const int WB = TK ? ((8 * mv.tk_wq + 15) & ~15) : 0;  // W[q] fragments (TK)
+    double* const wsm = reinterpret_cast<double*>(sm + (size_t)NST * SB);
+    longlong2* const rdesc = reinterpret_cast<longlong2*>(sm + (size_t)NST * SB + WB);  // [MCT * 8]
     uint16_t* const atab = reinterpret_cast<uint16_t*>(rdesc + MCT * 8);             // [KC][MCT][32]
     int* const rtab = reinterpret_cast<int*>(atab + ((KC * MCT * 32 + 1) & ~1));     // [MCT * 8]
     uint64_t* const full = reinterpret_cast<uint64_t*>(rtab + ((MCT * 8 + 1) & ~1));
     uint64_t* const empty = full + kP3mMaxStages;
+    uint64_t* const wbar = empty + kP3mMaxStages;  // TK: W[q] landed
+    // TK: per (item k, warp) the tile-invariant offsets {U1 fragment, W fragment, K row of the
+    // chunk, u left in the chunk} of the warp's (block, u chunk) items, [k][warp]
+    int4* const tki = reinterpret_cast<int4*>((reinterpret_cast<uintptr_t>(wbar + 2) + 15) & ~(uintptr_t)15);
     double2* const xch = reinterpret_cast<double2*>(empty + kP3mMaxStages);  // KS: [T][MCT][32]
+    const int KS1 = TK ? (RS1 | 1) : RS1;  // K row stride in shared memory
+    if (TK)
+        for (int e = threadIdx.x; e < kTkItems * NW; e += NTHR) {
+            const int k = e / NW, w = e % NW;
+            const int item = w + k * NW;
+            int4 v = make_int4(0, 0, 0, 0);
+            if (item < mv.tk_items) {
+                const int b = item / mv.tk_nc, ncc = item - b * mv.tk_nc;
+                v = make_int4(mv.tk_u1o[b], mv.tk_wo[b] + ncc * mv.tk_nkc[b] * 32, b * mv.ZU + 8 * ncc,
+                              mv.ZU - 8 * ncc);
+            }
+            tki[e] = v;
+        }
     {
         const uint32_t* src = reinterpret_cast<const uint32_t*>(mv.p3m_tab);
         uint32_t* dst = reinterpret_cast<uint32_t*>(atab);
@@ -115,6 +187,7 @@ __global__ void __launch_bounds__(kMmaT * kMmaSplit * 32, 1)
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], NW);
         }
+        if (TK) mbar_init(wbar, 1);
         fence_mbar_init();
     }
     __syncthreads();
@@ -135,15 +208,21 @@ __global__ void __launch_bounds__(kMmaT * kMmaSplit * 32, 1)
     __syncthreads();
     // producer: thread 0 streams the tiles, NST - 1 ahead of its own compute; before refilling
     // a stage it waits until all warps released that stage's previous tile
-    const unsigned kbytes = (unsigned)(8 * RC), xbox = (unsigned)(128 * (nzp + 4));
+    const unsigned kbytes = TK ? (unsigned)(8 * mv.tk_u1t) : (unsigned)(8 * RC), xbox = (unsigned)(128 * (nzp + 4));
+    // tiles of this CTA: strided over the grid, or (TK) one contiguous q-major range, so that
+    // W[q] changes only every nt3 tiles
+    const int tbeg = TK ? (int)((long long)ntiles * blockIdx.x / gridDim.x) : 0;
+    const int tend = TK ? (int)((long long)ntiles * (blockIdx.x + 1) / gridDim.x) : ntiles;
+    auto tile_of = [&](int j) { return TK ? tbeg + j : (int)blockIdx.x + j * (int)gridDim.x; };
     auto issue = [&](int j) {  // this CTA's j-th tile into stage j % NST
-        const int tl = blockIdx.x + j * gridDim.x;
-        if (tl >= ntiles) return;
+        const int tl = tile_of(j);
+        if (tl >= tend) return;
         const int s = j % NST;
         if (j >= NST) mbar_wait(&empty[s], ((j / NST) - 1) & 1);
         uint8_t* st = sm + (size_t)s * SB;
         mbar_arrive_expect_tx(&full[s], kbytes + (unsigned)(2 * nb) * xbox);
-        bulk_g2s(st, mv.Rt + (size_t)tl * RC, kbytes, &full[s]);
+        if (TK) bulk_g2s(st, mv.tk_u1 + (size_t)(tl % nt3) * mv.tk_u1t, kbytes, &full[s]);
+        else bulk_g2s(st, mv.Rt + (size_t)tl * RC, kbytes, &full[s]);
         // side 0: rows [row0, row0 + nzp + 4) (the last 4 land in the region's slack); side 1:
         // rows [row0 + nzp - 4, row0 + 2 nzp), so its plane p sits in region row p + 4
         const int row0 = tl * 2 * nzp;
@@ -154,9 +233,16 @@ __global__ void __launch_bounds__(kMmaT * kMmaSplit * 32, 1)
             tma_load_2d(st + KB + 3 * XR, &tmx1, 0, row0 + nzp - 4, &full[s]);
         }
     };
+    auto wissue = [&](int j) {  // TK: W fragments of tile j's q (all blocks, one bulk copy)
+        const int q = tile_of(j) / nt3;
+        mbar_arrive_expect_tx(wbar, (unsigned)(8 * mv.tk_wq));
+        bulk_g2s(wsm, mv.tk_w + (size_t)q * mv.tk_wq, (unsigned)(8 * mv.tk_wq), wbar);
+    };
     const bool producer = threadIdx.x == 0;
-    if (producer)
+    if (producer) {
+        if (TK && tbeg < tend) wissue(0);
         for (int j = 0; j < NST - 1; ++j) issue(j);
+    }
     const int t = warp & (T - 1), half = warp / T;
     const int h0 = (MCT + 1) >> 1;  // row chunks stored by (!KS: computed by) the first half
     const int mlo = KS ? 0 : (half ? h0 : 0), mhi = KS ? MCT : (half ? MCT : h0);
@@ -189,13 +275,55 @@ __global__ void __launch_bounds__(kMmaT * kMmaSplit * 32, 1)
     }
     const int ocol = (lane & 3) >> 1, oside = lane & 1;  // this lane's C columns (see below)
     double2* const X3c = mv.X3[0] + ocol * mv.colC;
-    int it = 0;
-    for (int tl = blockIdx.x; tl < ntiles; tl += gridDim.x, ++it) {
+    int qprev = -1, nwl = 0;  // TK: q of the resident W, W loads waited for
+    for (int it = 0; tile_of(it) < tend; ++it) {
+        const int tl = tile_of(it);
         const int s = it % NST;
         if (producer) issue(it + NST - 1);
         mbar_wait(&full[s], (it / NST) & 1);
         const uint8_t* stg = sm + (size_t)s * SB;
-        const double* __restrict__ kt_ = reinterpret_cast<const double*>(stg) + t * RS1;
+        if constexpr (TK) {
+            const int q = tl / nt3;
+            if (q != qprev) {
+                mbar_wait(wbar, nwl & 1);
+                ++nwl;
+                qprev = q;
+            }
+            // K rows of the tile: item = (block, 8-wide u chunk), C[t][u] = sum_i U1[t][i] W[i][u];
+            // a warp's items (warp, warp + 16, ...) run as interleaved chains (uniform rank chunks)
+            const double* u1s = reinterpret_cast<const double*>(stg);
+            double cr[kTkItems][2];
+            const int nit = max(0, (mv.tk_items - warp + NW - 1) / NW);
+            const int4* it4 = tki + warp;  // item k at it4[k * NW]
+            const int nkc = mv.tk_nkc[0];
+            switch (nit) {
+                case 1: tk_rebuild<1>(cr, u1s, wsm, it4, nkc, lane); break;
+                case 2: tk_rebuild<2>(cr, u1s, wsm, it4, nkc, lane); break;
+                case 3: tk_rebuild<3>(cr, u1s, wsm, it4, nkc, lane); break;
+                case 4: tk_rebuild<4>(cr, u1s, wsm, it4, nkc, lane); break;
+                case 5: tk_rebuild<5>(cr, u1s, wsm, it4, nkc, lane); break;
+                case 6: tk_rebuild<6>(cr, u1s, wsm, it4, nkc, lane); break;
+                default: break;
+            }
+            __syncwarp();
+            asm volatile("bar.sync 15, %0;\n" ::"n"(NTHR) : "memory");  // U1 and W reads done
+            const int tn = tile_of(it + 1);
+            if (producer && tn < tend && tn / nt3 != q) wissue(it + 1);
+            double* kw = reinterpret_cast<double*>(sm + (size_t)s * SB);
+            const int uo = 2 * (lane & 3), ko = (lane >> 2) * KS1 + uo;
+#pragma unroll
+            for (int k = 0; k < kTkItems; ++k) {
+                if (k < nit) {
+                    const int4 d = it4[k * NW];
+                    if (uo < d.w) kw[d.z + ko] = cr[k][0];
+                    if (uo + 1 < d.w) kw[d.z + ko + 1] = cr[k][1];
+                }
+            }
+            if (threadIdx.x < T) kw[threadIdx.x * KS1 + RS1 - 1] = 0.0;  // the zero row
+            __syncwarp();
+            asm volatile("bar.sync 15, %0;\n" ::"n"(NTHR) : "memory");  // K rows complete
+        }
+        const double* __restrict__ kt_ = reinterpret_cast<const double*>(stg) + t * KS1;
         const uint8_t* xb_ = stg + boff0;
         const int q = tl / nt3, xti = tl - q * nt3;
         const int kx = xti * T + t;
@@ -227,6 +355,7 @@ __global__ void __launch_bounds__(kMmaT * kMmaSplit * 32, 1)
                 }
             }
             if (mc0 + MC >= mhi) {  // last read of this stage: release it to the producer
+                if (TK) fence_proxy_async();  // K rows were written here (generic proxy)
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&empty[s]);
             }
@@ -263,6 +392,7 @@ __global__ void __launch_bounds__(kMmaT * kMmaSplit * 32, 1)
             }
         }
         if (mhi <= mlo) {  // no rows for this half: still release the stage
+            if (TK) fence_proxy_async();
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[s]);
         }
@@ -296,8 +426,10 @@ cudaError_t launch_p3m(const MV& mv, cudaStream_t st) {
     const int nt3 = (mv.nkx + kMmaT - 1) / kMmaT;
     const int ntiles = nt3 * (mv.My / 2 + 1);
     if (ntiles == 0 || mv.p3m_mct == 0) return cudaSuccess;
+    const bool tk = mv.tk != 0;
     const int nst = mv.p3m_nst;
-    const size_t smem = p3m_smem(mv.rs1, mv.p3m_nzt, mv.p3m_kc, mv.p3m_mct, nst);
+    const size_t smem = tk ? p3m_tk_smem(mv.rs1, mv.p3m_nzt, mv.p3m_kc, mv.p3m_mct, mv.tk_u1t, mv.tk_wq, nst)
+                           : p3m_smem(mv.rs1, mv.p3m_nzt, mv.p3m_kc, mv.p3m_mct, nst);
     if (nst < 2 || smem > 227 * 1024) return cudaErrorInvalidConfiguration;
     // X2 of each column as a 2-D tensor of 128-byte rows, boxes of nzp + 4 rows.  The maps depend
     // only on the buffers and the shape, so they are encoded once and cached (per host thread:
@@ -334,7 +466,7 @@ cudaError_t launch_p3m(const MV& mv, cudaStream_t st) {
     }
     // k-split (KS) when all row chunks fit one pass; else row halves in balanced passes
     static const bool ks_env = getenv("VC_P3M_KS") && atoi(getenv("VC_P3M_KS"));
-    const bool ks = mv.p3m_mct <= kMmaMC && ks_env;
+    const bool ks = mv.p3m_mct <= kMmaMC && ks_env && !tk;
     const int npass = ks ? 1 : (((mv.p3m_mct + 1) >> 1) + kMmaMC - 1) / kMmaMC;
     const int mc = ks ? mv.p3m_mct : (((mv.p3m_mct + 1) >> 1) + npass - 1) / npass;
     const int kw = ks ? (mv.p3m_kc + 1) >> 1 : mv.p3m_kc;  // column chunks per warp
@@ -346,19 +478,20 @@ cudaError_t launch_p3m(const MV& mv, cudaStream_t st) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     const int grid = std::max(1, std::min(ntiles, nsm));
-#define VC_P3M_K2(M, KK, KSV)                                                                  \
+#define VC_P3M_K2(M, KK, KSV, TKV)                                                             \
     {                                                                                          \
         static bool granted = false; /* process-wide attribute: grant the maximum once */      \
         if (!granted) {                                                                        \
-            e = prep(k_p3m<M, KK, KSV>, 227 * 1024);                                           \
+            e = prep(k_p3m<M, KK, KSV, TKV>, 227 * 1024);                                      \
             if (e) return e;                                                                   \
             granted = true;                                                                    \
         }                                                                                      \
-        k_p3m<M, KK, KSV><<<grid, NT, smem, st>>>(tm[0], tm[1], mv);                           \
+        k_p3m<M, KK, KSV, TKV><<<grid, NT, smem, st>>>(tm[0], tm[1], mv);                      \
     }
 #define VC_P3M_K(M, KK)                                                                        \
     case KK:                                                                                   \
-        if (ks) VC_P3M_K2(M, KK, true) else VC_P3M_K2(M, KK, false)                           \
+        if (tk) VC_P3M_K2(M, KK, false, true)                                                  \
+        else if (ks) VC_P3M_K2(M, KK, true, false) else VC_P3M_K2(M, KK, false, false)        \
         break;
 #define VC_P3M_CASE(M)                                                                         \
     case M:                                                                                    \

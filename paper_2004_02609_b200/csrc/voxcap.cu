@@ -414,8 +414,12 @@ vc_status vc_reset_stats(vc_ctx* c) {
     const double bp[5] = {c->stats.bytes_pass[0], c->stats.bytes_pass[1], c->stats.bytes_pass[2],
                           c->stats.bytes_pass[3], c->stats.bytes_pass[4]};
     const double bm = c->stats.bytes_matvec, ms = c->stats.ms_setup, mp = c->stats.ms_precond_build;
-    const int64_t pd = c->stats.precond_doubles;
+    const int64_t pd = c->stats.precond_doubles, sd = c->stats.spectra_doubles, tc = c->stats.tucker_cache;
+    const double te = c->stats.tucker_err;
     memset(&c->stats, 0, sizeof(c->stats));
+    c->stats.spectra_doubles = sd;
+    c->stats.tucker_cache = tc;
+    c->stats.tucker_err = te;
     for (int p = 0; p < 5; ++p) c->stats.bytes_pass[p] = bp[p];
     c->stats.bytes_matvec = bm;
     c->stats.ms_setup = ms;
@@ -440,9 +444,30 @@ vc_status vc_debug_fft(vc_ctx* c, int32_t L, int32_t n_lines, double* data, int3
     return debug_fft(c, L, n_lines, data, dir);
 }
 
+vc_status vc_get_tucker(const vc_ctx* c, int32_t* nblk, int32_t* ranks, double* err, int32_t* dims) {
+    if (!c) return VC_ERR_INPUT;
+    if (!c->has_op || !c->tk.on) return VC_ERR_STATE;
+    const vc::Tucker& T = c->tk;
+    if (nblk) *nblk = T.nblk;
+    for (int b = 0; b < T.nblk; ++b) {
+        if (ranks) {
+            ranks[2 * b] = T.r1[b];
+            ranks[2 * b + 1] = T.r2[b];
+        }
+        if (err) err[b] = b < (int)T.err.size() ? T.err[b] : 0.0;
+    }
+    if (dims) {
+        dims[0] = T.nkx;
+        dims[1] = T.nq;
+        dims[2] = T.ZU;
+    }
+    return VC_OK;
+}
+
 vc_status vc_debug_get_spectra(vc_ctx* c, int64_t* n, int32_t* layout, double* out) {
     VC_CHECK_CTX(c);
     if (!c->has_op) return set_err(c, VC_ERR_STATE, "vc_debug_get_spectra before vc_build_operator");
+    if (c->tk.on) return set_err(c, VC_ERR_STATE, "the build kept Tucker-compressed spectra (no exact table)");
     DeviceGuard g(c->device);
     const int My = c->M[1];
     if (n) *n = (int64_t)c->Rt.n;
@@ -462,6 +487,7 @@ vc_status vc_debug_get_spectra(vc_ctx* c, int64_t* n, int32_t* layout, double* o
 vc_status vc_debug_set_spectra(vc_ctx* c, int64_t n, const double* in) {
     VC_CHECK_CTX(c);
     if (!c->has_op) return set_err(c, VC_ERR_STATE, "vc_debug_set_spectra before vc_build_operator");
+    if (c->tk.on) return set_err(c, VC_ERR_STATE, "the build kept Tucker-compressed spectra (no exact table)");
     if (!in || n != (int64_t)c->Rt.n) return set_err(c, VC_ERR_INPUT, "spectra length mismatch");
     DeviceGuard g(c->device);
     VC_CUDA(c, cudaMemcpyAsync(c->Rt.p, in, c->Rt.bytes(), cudaMemcpyHostToDevice, c->stream));

@@ -15,11 +15,16 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="C4")
 ap.add_argument("--n", type=int, default=20)
 ap.add_argument("--zmode", type=int, default=0)
+ap.add_argument("--tucker", type=int, default=0, help="tucker_digits (0 = exact spectra)")
 a = ap.parse_args()
 st = voxgen.config(a.config)
 ctx = vc.VoxCap(0)
 ctx.set_structure(st)
-ctx.build_operator(zmode=a.zmode)
+ctx.build_operator(zmode=a.zmode, tucker_digits=a.tucker)
+if a.tucker:
+    s0 = ctx.stats()
+    print(a.config, "tucker", a.tucker, "setup_ms", round(s0["ms_setup"], 2), "resident doubles", s0["spectra_doubles"],
+          "err", s0["tucker_err"], "ranks", ctx.tucker()["ranks"])
 x = torch.from_numpy(voxgen.seeded_vector(ctx.n, 0)).cuda()
 X = torch.stack([x, x.flip(0)], dim=1).contiguous()
 for label, fn in (("single", lambda: ctx.matvec(x)), ("pair", lambda: ctx.matvec_batch(X))):

@@ -14,11 +14,12 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="C4")
 ap.add_argument("--n", type=int, default=5)
 ap.add_argument("--batch", type=int, default=1, help="columns per matvec (vc_matvec_batch)")
+ap.add_argument("--tucker", type=int, default=0, help="tucker_digits (0 = exact spectra)")
 a = ap.parse_args()
 st = voxgen.config(a.config)
 ctx = vc.VoxCap(0)
 ctx.set_structure(st)
-ctx.build_operator()
+ctx.build_operator(tucker_digits=a.tucker)
 x = torch.from_numpy(voxgen.seeded_vector(ctx.n, 0)).cuda()
 X = torch.stack([x] * a.batch, dim=1)
 for _ in range(a.n):

@@ -203,6 +203,8 @@ struct vc_ctx {
     vc::DevBuf<int32_t> p3m_tab;
     int p3m_nzt = 0, p3m_kc = 0, p3m_mct = 0;  // stacked padded planes, column / row chunks
     int p3m_nst = 2;                           // k_p3m ring depth
+    int p3m_nneg = 0, p3m_oddmask = 0;         // negated odd-block rows (count, block bitmask)
+    size_t p3m_negoff = 0;                     // their row offsets in p3m_tab (int32)
     int p3m_zoff[3] = {0, 0, 0};               // first stacked position of each source
     std::vector<int32_t> h_planes;     // host copy of the plane lists
     size_t rchunk = 0;     // doubles of R per P3 tile

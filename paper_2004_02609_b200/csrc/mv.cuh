@@ -69,6 +69,9 @@ struct MV {
     const int32_t* p3m_tab;
     int p3m_nzt, p3m_kc, p3m_mct;  // stacked padded planes, 4-column chunks, 8-row chunks
     int p3m_nst;                   // k_p3m ring depth
+    // odd (E^{z.}) block rows whose negated copies k_p3m writes per tile (row offsets b * ZU + u)
+    int p3m_nneg, p3m_oddmask;
+    const int32_t* p3m_neg;
     // Tucker-compressed spectra (tucker.cu; vc::Tucker): k_p3m<TK> rebuilds each tile's K rows
     // from U1f (per kx tile, tk_u1t doubles) and Wf (per q, tk_wq doubles) instead of reading Rt
     int tk;
@@ -120,11 +123,11 @@ constexpr int kMmaSplit = 2;   // warps per kx (row-chunk halves)
 constexpr int kMmaMC = 8;      // row chunks (8 rows each) per pass: C fragments in registers
 constexpr int kP3mMaxStages = 6;
 // ring depth that fits shared memory for a shape (0 or 1: the shape cannot run direct-z)
-int p3m_stages(int rs1, int nzp, int kc, int mct);
-size_t p3m_smem(int rs1, int nzp, int kc, int mct, int nst);
+int p3m_stages(int rs1, int nzp, int kc, int mct, bool neg);
+size_t p3m_smem(int rs1, int nzp, int kc, int mct, int nst, bool neg);
 // Tucker P3: (block, u chunk) items per warp held in registers, and the ring depth that fits
 constexpr int kTkItems = 6;
-int p3m_tk_stages(int rs1, int nzp, int kc, int mct, int u1t, int wq);
+int p3m_tk_stages(int rs1, int nzp, int kc, int mct, int u1t, int wq, bool neg);
 cudaError_t launch_p3m(const MV& mv, cudaStream_t st);
 
 }  // namespace vc

@@ -1362,9 +1362,19 @@ vc_status operator_build(vc_ctx* c, const vc_build_opts* o) {
         const int rs1 = std::max(1, c->nblk) * c->ZL + 1;
         // ring depth: 2 measured fastest on C4 (0.538 / 0.546 / 0.550 / 0.559 ms for 2 / 3 / 4 / 5
         // stages per pair launch); VC_P3M_NST overrides it (A/B), bounded by what fits
-        const int nst_fit = p3m_stages(rs1, nzp, kc, mct);
+        // odd (E^{z.}) blocks: k_p3m keeps negated copies of their rows so that no A entry
+        // carries a sign (the A offsets are plain uint16 row indices, negated rows at 8 ks1 + row)
+        int oddmask = 0;
+        for (int f = 0; f < c->nf; ++f)
+            if (c->f[f].kind == 1 && c->f[f].axis == 2)
+                for (int b = 0; b < 3; ++b)
+                    if (c->blk[f][b] >= 0) oddmask |= 1 << c->blk[f][b];
+        const bool tkb = o && o->tucker_digits > 0;
+        const int ks1 = tkb ? (rs1 | 1) : rs1;  // K row stride in shared memory
+        const int nst_fit = p3m_stages(rs1, nzp, kc, mct, false);
         const int nst = std::min(nst_fit, getenv("VC_P3M_NST") ? std::max(2, atoi(getenv("VC_P3M_NST"))) : 2);
-        c->zdirect = nrows <= kMaxRows && nzp > 0 && nzp + 4 <= 256 && rs1 <= 0x7fff && nst_fit >= 2 &&
+        c->zdirect = nrows <= kMaxRows && nzp > 0 && nzp + 4 <= 256 && rs1 <= 0x7fff && 9 * ks1 <= 0xffff &&
+                     nst_fit >= 2 &&
                      (zmode == 2 || (zmode == 0 && 4.0 * mac <= fft));
         if (zmode == 2 && !c->zdirect)
             return set_err(c, VC_ERR_UNSUPPORTED, "direct-z mode: too many output planes or input planes");
@@ -1403,15 +1413,25 @@ vc_status operator_build(vc_ctx* c, const vc_build_opts* o) {
                                 const int u = ((g2 < 0 ? -g2 : g2) - (s2 != 0)) >> 1;
                                 if (u < 0 || u >= c->ZU) return set_err(c, VC_ERR_INPUT, "direct-z offset out of range");
                                 const bool odd = c->f[f].kind == 1 && c->f[f].axis == 2;
-                                e = (uint16_t)((bk * c->ZU + u) | (odd && g2 < 0 ? 0x8000 : 0));
+                                // Tucker P3: negated copy at 8 ks1 + row; exact table: sign bit
+                                e = tkb ? (uint16_t)((odd && g2 < 0 ? 8 * ks1 : 0) + bk * c->ZU + u)
+                                        : (uint16_t)((bk * c->ZU + u) | (odd && g2 < 0 ? 0x8000 : 0));
                             }
                         }
                         at.push_back(e);
                     }
             if (at.size() & 1) at.push_back(0);
-            std::vector<int32_t> tab(at.size() / 2 + rows.size());
+            std::vector<int32_t> negs;
+            for (int b = 0; b < c->nblk; ++b)
+                if (oddmask >> b & 1)
+                    for (int u = 0; u < c->ZU; ++u) negs.push_back(b * c->ZU + u);
+            std::vector<int32_t> tab(at.size() / 2 + rows.size() + negs.size());
             memcpy(tab.data(), at.data(), 2 * at.size());
             memcpy(tab.data() + at.size() / 2, rows.data(), 4 * rows.size());
+            memcpy(tab.data() + at.size() / 2 + rows.size(), negs.data(), 4 * negs.size());
+            c->p3m_nneg = (int)negs.size();
+            c->p3m_oddmask = oddmask;
+            c->p3m_negoff = at.size() / 2 + rows.size();
             c->p3m_nzt = nzp;
             c->p3m_nst = nst;
             c->p3m_kc = kc;
@@ -1937,6 +1957,9 @@ static MV make_mv(vc_ctx* c, const double* x, double* y) {
         mv.x2zo[b] = c->zdirect ? c->p3m_zoff[b] : 0;
     }
     mv.p3m_tab = c->p3m_tab.p;
+    mv.p3m_nneg = c->zdirect ? c->p3m_nneg : 0;
+    mv.p3m_oddmask = c->p3m_oddmask;
+    mv.p3m_neg = c->p3m_tab.p + c->p3m_negoff;
     mv.p3m_nzt = c->p3m_nzt;
     mv.p3m_kc = c->p3m_kc;
     mv.p3m_mct = c->p3m_mct;

@@ -49,42 +49,51 @@ __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double
 // X2 stage: 4 (column, side) regions of 128-byte rows (side 1 starts 4 rows early), each a
 // whole number of 1024-byte swizzle atoms
 __host__ __device__ constexpr int p3m_xregion(int nzp) { return ((nzp + 4) * 128 + 1023) & ~1023; }
-__host__ __device__ constexpr int p3m_kbytes(int rs1) { return (8 * kMmaT * rs1 + 1023) & ~1023; }
+// K rows of a stage: [t][rs1], then (neg: odd E^{z.} blocks present) their negated copies at
+// row index 8 rs1 + t rs1 + (block row), so that every A entry is a plain shared load
+__host__ __device__ constexpr int p3m_kbytes(int rs1, bool neg) { return (8 * kMmaT * rs1 * (neg ? 2 : 1) + 1023) & ~1023; }
 static size_t p3m_fixed(int kc, int mct) {  // tables + barriers + k-split exchange (after the stages)
     return 16 * (size_t)mct * 8 + 2 * (size_t)kc * mct * 32 + 4 * (size_t)mct * 8 + 16 * kP3mMaxStages + 64 +
            (mct <= kMmaMC ? (size_t)kMmaT * mct * 32 * 16 : 0);
 }
-int p3m_stages(int rs1, int nzp, int kc, int mct) {
-    const size_t st = (size_t)p3m_kbytes(rs1) + 4 * (size_t)p3m_xregion(nzp);
+int p3m_stages(int rs1, int nzp, int kc, int mct, bool neg) {
+    const size_t st = (size_t)p3m_kbytes(rs1, neg) + 4 * (size_t)p3m_xregion(nzp);
     const size_t avail = 227 * 1024 - 1024 - p3m_fixed(kc, mct);
     return (int)std::min<size_t>(kP3mMaxStages, avail / st);
 }
-size_t p3m_smem(int rs1, int nzp, int kc, int mct, int nst) {
-    return 1024 + (size_t)nst * ((size_t)p3m_kbytes(rs1) + 4 * (size_t)p3m_xregion(nzp)) + p3m_fixed(kc, mct);
+size_t p3m_smem(int rs1, int nzp, int kc, int mct, int nst, bool neg) {
+    return 1024 + (size_t)nst * ((size_t)p3m_kbytes(rs1, neg) + 4 * (size_t)p3m_xregion(nzp)) + p3m_fixed(kc, mct);
 }
 // Tucker P3 (TK): a stage's first region holds the tile's U1 fragments, then (rebuilt in place)
 // its K rows; the W fragments of the current q sit after the stages; no k-split exchange buffer
 // (K rows in shared memory use the odd stride rs1 | 1: the rebuilt rows of 8 kx land in distinct
 // banks)
-__host__ __device__ constexpr int p3m_tk_region(int rs1, int u1t) {
-    return ((8 * u1t > 8 * kMmaT * (rs1 | 1) ? 8 * u1t : 8 * kMmaT * (rs1 | 1)) + 1023) & ~1023;
+__host__ __device__ constexpr int p3m_tk_region(int rs1, int u1t, bool neg) {
+    return ((8 * u1t > 8 * kMmaT * (rs1 | 1) * (neg ? 2 : 1) ? 8 * u1t : 8 * kMmaT * (rs1 | 1) * (neg ? 2 : 1)) + 1023) &
+           ~1023;
 }
 static size_t p3m_tk_fixed(int kc, int mct, int wq) {
     return (((size_t)8 * wq + 15) & ~(size_t)15) + 16 * (size_t)mct * 8 + 2 * (size_t)kc * mct * 32 +
            4 * (size_t)mct * 8 + 16 * kP3mMaxStages + 64 + 16 * (size_t)kMmaT * kMmaSplit * kTkItems + 16;
 }
-static size_t p3m_tk_smem(int rs1, int nzp, int kc, int mct, int u1t, int wq, int nst) {
-    return 1024 + (size_t)nst * ((size_t)p3m_tk_region(rs1, u1t) + 4 * (size_t)p3m_xregion(nzp)) +
+static size_t p3m_tk_smem(int rs1, int nzp, int kc, int mct, int u1t, int wq, int nst, bool neg) {
+    return 1024 + (size_t)nst * ((size_t)p3m_tk_region(rs1, u1t, neg) + 4 * (size_t)p3m_xregion(nzp)) +
            p3m_tk_fixed(kc, mct, wq);
 }
-int p3m_tk_stages(int rs1, int nzp, int kc, int mct, int u1t, int wq) {
-    const size_t st = (size_t)p3m_tk_region(rs1, u1t) + 4 * (size_t)p3m_xregion(nzp);
+int p3m_tk_stages(int rs1, int nzp, int kc, int mct, int u1t, int wq, bool neg) {
+    const size_t st = (size_t)p3m_tk_region(rs1, u1t, neg) + 4 * (size_t)p3m_xregion(nzp);
     const size_t fx = 1024 + p3m_tk_fixed(kc, mct, wq);
     if (fx >= 227 * 1024) return 0;
     return (int)std::min<size_t>(2, (227 * 1024 - fx) / st);
 }
 
+// A entry: row index | sign << 15 (odd E^{z.} blocks at negative offsets).  The Tucker P3 (PL)
+// writes negated copies of the odd rows when it rebuilds them (p3m_kbytes), so its entries are
+// plain row indices (measured: for the exact table, negating the rows in shared memory per tile
+// costs more than the sign flips it saves, 0.529 -> 0.543 ms per C4 pair launch)
+template <bool PL>
 __device__ __forceinline__ double p3m_aval(const double* __restrict__ kt, unsigned e16) {
+    if constexpr (PL) return kt[e16];
     const double v = kt[e16 & 0x7fff];
     return __longlong_as_double(__double_as_longlong(v) ^ ((long long)(e16 & 0x8000) << 48));
 }
@@ -146,7 +155,8 @@ __global__ void __launch_bounds__(kMmaT * kMmaSplit * 32, 1)
     const int nb = mv.nb, nzp = mv.p3m_nzt, KC = mv.p3m_kc, MCT = mv.p3m_mct, RS1 = mv.rs1;
     const int NST = mv.p3m_nst;
     const int RC = T * RS1;
-    const int KB = TK ? p3m_tk_region(RS1, mv.tk_u1t) : p3m_kbytes(RS1);
+    const bool NEG = TK && mv.p3m_nneg > 0;
+    const int KB = TK ? p3m_tk_region(RS1, mv.tk_u1t, NEG) : p3m_kbytes(RS1, NEG);
     const int XR = p3m_xregion(nzp), SB = KB + 4 * XR;  // stage bytes
     const int lg4 = mv.lgt4;
     const int nt4 = (nkx + (1 << lg4) - 1) >> lg4;
@@ -171,7 +181,7 @@ __global__ void __launch_bounds__(kMmaT * kMmaSplit * 32, 1)
             if (item < mv.tk_items) {
                 const int b = item / mv.tk_nc, ncc = item - b * mv.tk_nc;
                 v = make_int4(mv.tk_u1o[b], mv.tk_wo[b] + ncc * mv.tk_nkc[b] * 32, b * mv.ZU + 8 * ncc,
-                              mv.ZU - 8 * ncc);
+                              (mv.ZU - 8 * ncc) | ((mv.p3m_oddmask >> b & 1) << 16));
             }
             tki[e] = v;
         }
@@ -315,8 +325,13 @@ __global__ void __launch_bounds__(kMmaT * kMmaSplit * 32, 1)
             for (int k = 0; k < kTkItems; ++k) {
                 if (k < nit) {
                     const int4 d = it4[k * NW];
-                    if (uo < d.w) kw[d.z + ko] = cr[k][0];
-                    if (uo + 1 < d.w) kw[d.z + ko + 1] = cr[k][1];
+                    const int rem = d.w & 0xffff;
+                    if (uo < rem) kw[d.z + ko] = cr[k][0];
+                    if (uo + 1 < rem) kw[d.z + ko + 1] = cr[k][1];
+                    if (d.w >> 16) {  // odd block: the negated copy too
+                        if (uo < rem) kw[8 * KS1 + d.z + ko] = -cr[k][0];
+                        if (uo + 1 < rem) kw[8 * KS1 + d.z + ko + 1] = -cr[k][1];
+                    }
                 }
             }
             if (threadIdx.x < T) kw[threadIdx.x * KS1 + RS1 - 1] = 0.0;  // the zero row
@@ -343,7 +358,7 @@ __global__ void __launch_bounds__(kMmaT * kMmaSplit * 32, 1)
 #pragma unroll
                     for (int m = 0; m < MC; ++m)
                         if (mc0 + m < mhi)
-                            dmma884(c[m][0], c[m][1], p3m_aval(kt_, (ar[k][m / 2] >> (16 * (m & 1))) & 0xffff), bv);
+                            dmma884(c[m][0], c[m][1], p3m_aval<TK>(kt_, (ar[k][m / 2] >> (16 * (m & 1))) & 0xffff), bv);
                 }
             } else {
                 for (int kc = klo; kc < khi; ++kc) {
@@ -351,7 +366,7 @@ __global__ void __launch_bounds__(kMmaT * kMmaSplit * 32, 1)
                     const uint16_t* at = atab + (kc * MCT + mc0) * 32 + lane;
 #pragma unroll
                     for (int m = 0; m < MC; ++m)
-                        if (mc0 + m < mhi) dmma884(c[m][0], c[m][1], p3m_aval(kt_, at[m * 32]), bv);
+                        if (mc0 + m < mhi) dmma884(c[m][0], c[m][1], p3m_aval<TK>(kt_, at[m * 32]), bv);
                 }
             }
             if (mc0 + MC >= mhi) {  // last read of this stage: release it to the producer
@@ -428,8 +443,9 @@ cudaError_t launch_p3m(const MV& mv, cudaStream_t st) {
     if (ntiles == 0 || mv.p3m_mct == 0) return cudaSuccess;
     const bool tk = mv.tk != 0;
     const int nst = mv.p3m_nst;
-    const size_t smem = tk ? p3m_tk_smem(mv.rs1, mv.p3m_nzt, mv.p3m_kc, mv.p3m_mct, mv.tk_u1t, mv.tk_wq, nst)
-                           : p3m_smem(mv.rs1, mv.p3m_nzt, mv.p3m_kc, mv.p3m_mct, nst);
+    const size_t smem = tk ? p3m_tk_smem(mv.rs1, mv.p3m_nzt, mv.p3m_kc, mv.p3m_mct, mv.tk_u1t, mv.tk_wq, nst,
+                                         mv.p3m_nneg > 0)
+                           : p3m_smem(mv.rs1, mv.p3m_nzt, mv.p3m_kc, mv.p3m_mct, nst, false);
     if (nst < 2 || smem > 227 * 1024) return cudaErrorInvalidConfiguration;
     // X2 of each column as a 2-D tensor of 128-byte rows, boxes of nzp + 4 rows.  The maps depend
     // only on the buffers and the shape, so they are encoded once and cached (per host thread:

@@ -438,7 +438,7 @@ static vc_status tk_tables(vc_ctx* c) {
     T.wq = w;
     if (nb * T.nc > kMmaT * kMmaSplit * kTkItems)
         return set_err(c, VC_ERR_UNSUPPORTED, "Tucker P3: too many (block, u chunk) items per tile");
-    if (p3m_tk_stages(c->rs1, c->p3m_nzt, c->p3m_kc, c->p3m_mct, T.u1t, T.wq) < 2)
+    if (p3m_tk_stages(c->rs1, c->p3m_nzt, c->p3m_kc, c->p3m_mct, T.u1t, T.wq, c->p3m_nneg > 0) < 2)
         return set_err(c, VC_ERR_UNSUPPORTED, "Tucker P3: the ranks need more shared memory than a CTA has "
                                               "(use fewer digits)");
     TkFrag f{};

@@ -91,6 +91,7 @@ struct Cols2 {
     const double* w[2];
     double* out[2];  // dots: outputs; axpy: the updated vectors
     const double* h[2];
+    double* d[2];    // k_gs_fused: the dots of the updated vectors
 };
 __global__ void __launch_bounds__(kRedNT) k_multidot2(Cols2 cc, int64_t ldv, int nv, int64_t n,
                                                       double* __restrict__ partial,
@@ -159,6 +160,96 @@ __global__ void k_multiaxpy2(Cols2 cc, int64_t ldv, int nv, int64_t n, double sg
         for (int i = 0; i < nv; ++i) acc = fma(hs[i], V[i * ldv + k], acc);
         w[k] = fma(sgn, acc, w[k]);
     }
+}
+
+// CGS2's middle passes in one basis pass (blockIdx.z = column): w <- w - V h (in place, the
+// arithmetic of k_multiaxpy / k_multiaxpy2: ascending fma chain, then fma(-1, acc, w)) and the
+// second projection's dots d = V^T w from the same V values, held in registers (NVB >= nv
+// vectors per thread), reduced per block and then in a fixed order by the last block (ticket),
+// as k_multidot2 does.  Replaces a multi-axpy + multi-dot pair: one read of V and w instead of
+// two (measured in DESIGN.md §7 "GMRES").
+template <int NVB, int NT>
+__global__ void __launch_bounds__(NT) k_gs_fused(Cols2 cc, int64_t ldv, int nv, int64_t n,
+                                                     double* __restrict__ partial,
+                                                     unsigned* __restrict__ ticket) {
+    const int z = blockIdx.z;
+    __shared__ double hs[NVB];
+    if (threadIdx.x < NVB) hs[threadIdx.x] = threadIdx.x < nv ? cc.h[z][threadIdx.x] : 0.0;
+    __syncthreads();
+    const double* __restrict__ V = cc.V[z];
+    double* __restrict__ w = cc.out[z];
+    double* __restrict__ part = partial + (size_t)z * kRedBlocks * kMaxBasis;
+    double acc[NVB];
+#pragma unroll
+    for (int i = 0; i < NVB; ++i) acc[i] = 0.0;
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        double v[NVB];  // the row's V values stay in registers
+#pragma unroll
+        for (int i = 0; i < NVB; ++i) v[i] = i < nv ? V[i * ldv + k] : 0.0;
+        double a = 0.0;
+#pragma unroll
+        for (int i = 0; i < NVB; ++i)
+            if (i < nv) a = fma(hs[i], v[i], a);
+        const double w1 = fma(-1.0, a, w[k]);
+        w[k] = w1;
+#pragma unroll
+        for (int i = 0; i < NVB; ++i) acc[i] = fma(v[i], w1, acc[i]);
+    }
+    __shared__ double s[NT / 32][NVB];
+    const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+#pragma unroll
+    for (int i = 0; i < NVB; ++i) {
+        if (i >= nv) break;
+        double v = acc[i];
+        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) s[wp][i] = v;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < nv; i += NT) {
+        double v = 0.0;
+        for (int q = 0; q < NT / 32; ++q) v += s[q][i];
+        part[(int64_t)blockIdx.x * nv + i] = v;
+    }
+    __threadfence();
+    __shared__ bool last;
+    if (threadIdx.x == 0) last = atomicAdd(ticket + z, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    for (int i = wp; i < nv; i += NT / 32) {
+        double v = 0.0;
+        for (int b = lane; b < (int)gridDim.x; b += 32) v += __ldcg(part + (int64_t)b * nv + i);
+        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) cc.d[z][i] = v;
+    }
+    if (threadIdx.x == 0) ticket[z] = 0u;
+}
+// nv above this: the separate multi-axpy + multi-dot kernels (VC_GS_FUSED=<max nv> overrides for
+// A/B runs; 0 = never fused)
+constexpr int kGsFusedMaxNV = 32;
+inline int gs_fused_max() {
+    static const int v = getenv("VC_GS_FUSED") ? std::min(kGsFusedMaxNV, atoi(getenv("VC_GS_FUSED"))) : kGsFusedMaxNV;
+    return v;
+}
+
+// w_z <- w_z - V_z h_z and d_z = V_z^T w_z for nc <= 2 columns (k_gs_fused)
+cudaError_t launch_gs_fused(const Cols2& cc, int64_t n, int nv, int nc, double* partial, unsigned* ticket,
+                            cudaStream_t st) {
+    // registers sized to the basis in steps of 4 vectors; from 28 vectors on (> 140 registers)
+    // 128-thread blocks, twice as many (the partials of <= 32 vectors x 592 blocks still fit)
+    const dim3 g(kRedBlocks, 1, nc), g2(2 * kRedBlocks, 1, nc);
+    switch ((nv + 3) / 4) {
+#define VC_GSF(K)                                                                              \
+    case K:                                                                                    \
+        if (4 * K >= 28) k_gs_fused<4 * K, 128><<<g2, 128, 0, st>>>(cc, n, nv, n, partial, ticket); \
+        else k_gs_fused<4 * K, kRedNT><<<g, kRedNT, 0, st>>>(cc, n, nv, n, partial, ticket);   \
+        break;
+        VC_GSF(1) VC_GSF(2) VC_GSF(3) VC_GSF(4) VC_GSF(5) VC_GSF(6) VC_GSF(7) VC_GSF(8)
+#undef VC_GSF
+        default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
 }
 
 // out[z] = w[z] / sqrt(*h[z])
@@ -281,6 +372,22 @@ struct Krylov {
         count_launch(c, 1);
         return comm_allreduce(c, out, nv);
     }
+    // CGS2 middle passes: t -= V[0..nv) h (device), then d = V[0..nv) . t, summed over ranks
+    vc_status fused(int nv, const double* h, double* d) {
+        if (nv > gs_fused_max()) {
+            k_multiaxpy<<<grid_for(n), 256, 0, c->stream>>>(t, V, n, nv, h, n, -1.0);
+            count_launch(c, 1);
+            return dots(V, nv, t, d);
+        }
+        Cols2 cc{};
+        cc.V[0] = V;
+        cc.out[0] = t;
+        cc.h[0] = h;
+        cc.d[0] = d;
+        VC_CUDA(c, launch_gs_fused(cc, n, nv, 1, c->partial.p, c->ticket.p, c->stream));
+        count_launch(c, 1);
+        return comm_allreduce(c, d, nv);
+    }
     vc_status norm2_host(const double* vec, double* out) {
         vc_status s = dots(vec, 1, vec, c->dvec.p);
         if (s) return s;
@@ -359,12 +466,11 @@ vc_status solve_dev(vc_ctx* c, const double* d_b, double* d_x, const vc_solve_op
             if ((e = K.op(vj, K.t, K.w))) return e;
             double* dh = c->dvec.p + (size_t)(j & 1) * 3 * kMaxBasis;
             if ((e = K.dots(K.V, j + 1, K.t, dh))) return e;
-            k_multiaxpy<<<gn, 256, 0, st>>>(K.t, K.V, n, j + 1, dh, n, -1.0);
-            if ((e = K.dots(K.V, j + 1, K.t, dh + kMaxBasis))) return e;
+            if ((e = K.fused(j + 1, dh, dh + kMaxBasis))) return e;
             k_multiaxpy<<<gn, 256, 0, st>>>(K.t, K.V, n, j + 1, dh + kMaxBasis, n, -1.0);
             if ((e = K.dots(K.t, 1, K.t, dh + 2 * kMaxBasis))) return e;
             k_scale_by_norm<<<gn, 256, 0, st>>>(vn, K.t, dh + 2 * kMaxBasis, n);
-            count_launch(c, 3);
+            count_launch(c, 2);
             VC_CUDA(c, cudaMemcpyAsync(c->h_pinned + (size_t)(j & 1) * 3 * kMaxBasis, dh,
                                        8 * 3 * kMaxBasis, cudaMemcpyDeviceToHost, st));
             VC_CUDA(c, cudaEventRecord(c->arn_ev[j & 1], st));
@@ -601,11 +707,18 @@ vc_status solve_multi_dev(vc_ctx* c, int ncol, const double* const* d_b, double*
             k_multidot2<<<gd, kRedNT, 0, st>>>(cc(A.K.V, B.K.V, A.K.t, B.K.t, ha, hb, nullptr, nullptr),
                                                n, nv, n, c->partial.p, c->ticket.p);
             if ((e = sum_ranks(0, nv))) return e;
-            k_multiaxpy2<<<ga, 256, 0, st>>>(cc(A.K.V, B.K.V, nullptr, nullptr, A.K.t, B.K.t, ha, hb),
-                                             n, nv, n, -1.0);
-            k_multidot2<<<gd, kRedNT, 0, st>>>(cc(A.K.V, B.K.V, A.K.t, B.K.t, ha + kMaxBasis,
-                                                  hb + kMaxBasis, nullptr, nullptr),
-                                               n, nv, n, c->partial.p, c->ticket.p);
+            if (nv <= gs_fused_max()) {  // t -= V h1 and h2 = V^T t in one basis pass
+                Cols2 f = cc(A.K.V, B.K.V, nullptr, nullptr, A.K.t, B.K.t, ha, hb);
+                f.d[0] = ha + kMaxBasis;
+                f.d[1] = hb + kMaxBasis;
+                VC_CUDA(c, launch_gs_fused(f, n, nv, 2, c->partial.p, c->ticket.p, st));
+            } else {
+                k_multiaxpy2<<<ga, 256, 0, st>>>(cc(A.K.V, B.K.V, nullptr, nullptr, A.K.t, B.K.t, ha, hb),
+                                                 n, nv, n, -1.0);
+                k_multidot2<<<gd, kRedNT, 0, st>>>(cc(A.K.V, B.K.V, A.K.t, B.K.t, ha + kMaxBasis,
+                                                      hb + kMaxBasis, nullptr, nullptr),
+                                                   n, nv, n, c->partial.p, c->ticket.p);
+            }
             if ((e = sum_ranks(kMaxBasis, nv))) return e;
             k_multiaxpy2<<<ga, 256, 0, st>>>(cc(A.K.V, B.K.V, nullptr, nullptr, A.K.t, B.K.t,
                                                 ha + kMaxBasis, hb + kMaxBasis),
@@ -618,7 +731,7 @@ vc_status solve_multi_dev(vc_ctx* c, int ncol, const double* const* d_b, double*
                                                     A.K.V + (size_t)nv * n, B.K.V + (size_t)nv * n,
                                                     ha + 2 * kMaxBasis, hb + 2 * kMaxBasis),
                                                  n);
-            count_launch(c, 6);
+            count_launch(c, nv <= gs_fused_max() ? 5 : 6);
         } else {
             for (const Ent& en : S.ent) {
                 Col& C = col[en.col];
@@ -627,12 +740,11 @@ vc_status solve_multi_dev(vc_ctx* c, int ncol, const double* const* d_b, double*
                 if (en.phase == 1) {  // CGS2 of w' = R A v_j against v_0..v_j, as in solve_dev
                     const int j = en.j;
                     if ((e = K.dots(K.V, j + 1, K.t, dh))) return e;
-                    k_multiaxpy<<<gn, 256, 0, st>>>(K.t, K.V, n, j + 1, dh, n, -1.0);
-                    if ((e = K.dots(K.V, j + 1, K.t, dh + kMaxBasis))) return e;
+                    if ((e = K.fused(j + 1, dh, dh + kMaxBasis))) return e;
                     k_multiaxpy<<<gn, 256, 0, st>>>(K.t, K.V, n, j + 1, dh + kMaxBasis, n, -1.0);
                     if ((e = K.dots(K.t, 1, K.t, dh + 2 * kMaxBasis))) return e;
                     k_scale_by_norm<<<gn, 256, 0, st>>>(K.V + (size_t)(j + 1) * n, K.t, dh + 2 * kMaxBasis, n);
-                    count_launch(c, 3);
+                    count_launch(c, 2);
                 } else {  // restart residual r = R (b - A x)
                     k_axpby<<<gn, 256, 0, st>>>(K.w, K.b, 1.0, -1.0, n);
                     count_launch(c);

@@ -89,7 +89,9 @@ class Stats(ctypes.Structure):
 
 
 def lib_path():
-    return os.path.join(_HERE, _LIB_NAME)
+    # VOXCAP_LIB: an alternative in-tree build of the same library (A/B timing of build
+    # variants; tools/ only)
+    return os.environ.get("VOXCAP_LIB") or os.path.join(_HERE, _LIB_NAME)
 
 
 _lib = None

@@ -241,6 +241,68 @@ __device__ __forceinline__ void fft_stage(LD&& ld, ST&& st, const double2* __res
     }
 }
 
+// Stage 0 of a PF = false transform whose input sits in (and may alias) the shared buffer:
+// every point of the thread's butterfly is read through ld(t, p) into registers, then a CTA
+// barrier (the caller's input region may overlap the FFT layout), then the DFT, inter-stage
+// twiddles and stores of fft_stage into the smi layout.  One butterfly per thread.
+template <int L, int T, int NT, bool INV, bool PF = false, bool SWZ = false, class LD>
+__device__ __forceinline__ void fft_stage0_aliased(double2* sm, LD&& ld, const double2* __restrict__ tw) {
+    constexpr int R = Plan<L>::radix(0);
+    constexpr int S = L / R;
+    constexpr int TW = kTabN / L;
+    static_assert(T * (L / R) == NT, "one stage-0 butterfly per thread");
+    // (as fft_stage: PF -> consecutive lanes on consecutive pencils)
+    const int t = PF ? threadIdx.x % T : threadIdx.x / S, b = PF ? threadIdx.x / T : threadIdx.x % S;
+    double2 v[R];
+#pragma unroll
+    for (int j = 0; j < R; ++j) v[j] = ld(t, b + j * S);
+    __syncthreads();
+    reg_dft<R, INV>(v);
+    using A = SmAcc<L, T, PF, SWZ>;
+    const int i0 = A::idx(t, b);
+    if constexpr (S > 1) {
+        double2 wp[R];
+        wp[0] = make_double2(1.0, 0.0);
+        wp[1] = twiddle<INV>(tw, b * TW);
+#pragma unroll
+        for (int m = 2; m < R; ++m) {
+            const int hb = hipow2(m);
+            wp[m] = (m == hb) ? cmul(wp[m / 2], wp[m / 2]) : cmul(wp[hb], wp[m - hb]);
+        }
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+            const int m = bitrev<R>(i);
+            sm[A::at(i0, m * S)] = m == 0 ? v[i] : cmul(v[i], wp[m]);
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < R; ++i) sm[A::at(i0, bitrev<R>(i) * S)] = v[i];
+    }
+}
+
+// Stages 1 .. NS-1 of a PF = false transform (after fft_stage0_aliased; leading barrier
+// included), the last writing through stN.
+template <int L, int T, int NT, bool INV, bool PF = false, bool SWZ = false, class ST>
+__device__ __forceinline__ void fft_run_from1(double2* sm, ST&& stN, const double2* __restrict__ tw) {
+    constexpr int NS = Plan<L>::NS;
+    const SmAcc<L, T, PF, SWZ> lds{sm}, sts{sm};
+    __syncthreads();
+    if constexpr (NS == 2) {
+        fft_stage<L, T, NT, INV, PF, 1>(lds, stN, tw);
+    } else if constexpr (NS == 3) {
+        fft_stage<L, T, NT, INV, PF, 1>(lds, sts, tw);
+        __syncthreads();
+        fft_stage<L, T, NT, INV, PF, 2>(lds, stN, tw);
+    } else {
+        static_assert(NS == 4, "2 <= NS <= 4");
+        fft_stage<L, T, NT, INV, PF, 1>(lds, sts, tw);
+        __syncthreads();
+        fft_stage<L, T, NT, INV, PF, 2>(lds, sts, tw);
+        __syncthreads();
+        fft_stage<L, T, NT, INV, PF, 3>(lds, stN, tw);
+    }
+}
+
 // Full transform: stage 0 reads through `ld0`, the last stage writes through `stN`, and the
 // intermediate stages use shared memory `sm` (layout smi<L,T,PF>).  If NS == 1 the single
 // stage goes ld0 -> stN.  No trailing __syncthreads().

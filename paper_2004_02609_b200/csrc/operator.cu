@@ -35,16 +35,24 @@ template <int L> struct FX {
     static constexpr int NT = clampi(T * L / 16, 64, 256);
     // register caps (measured on C4): P1 best at <= 96 (5 CTAs/SM), P5 at <= 128 (no spills)
     static constexpr int MINB = 65536 / (NT * 96) < 1 ? 1 : 65536 / (NT * 96);
-    static constexpr int MINB5 = 65536 / (NT * 128) < 1 ? 1 : 65536 / (NT * 128);
+#ifndef VC_P5_REGS
+#define VC_P5_REGS 128
+#endif
+    static constexpr int MINB5 = 65536 / (NT * VC_P5_REGS) < 1 ? 1 : 65536 / (NT * VC_P5_REGS);
 };
 // Tile widths the host layout code must agree with (X1 is tiled by P2's width, X3 by P4's):
 // operator_build sizes and indexes those arrays through these two functions only.
 constexpr int p2_tile(int L) { return clampi(4096 / L, 2, 32); }  // FY<L>::T
 constexpr int kP4KB = 32;                                          // P4's shared KB per stage
 constexpr int p4_tile(int L) { return clampi(kP4KB * 64 / L, 1, 32); }  // FYS<L, kP4KB>::T
+#ifndef VC_P2_MINB
+#define VC_P2_MINB 0  // 0: no minimum-blocks bound (nvcc then caps P2 at 120 registers; an
+                      // explicit 1 lets it take 142 and halves the CTAs per SM: 0.32 -> 0.48 ms)
+#endif
 template <int L> struct FY {
     static constexpr int T = p2_tile(L);  // >= 2 adjacent kx: 32-byte row segments
     static constexpr int NT = 256;
+    static constexpr int MINB2 = VC_P2_MINB;  // P2's register cap (launch bounds)
 };
 template <int L> struct TX { static constexpr int T = FX<L>::T; };
 template <int L> struct TY { static constexpr int T = FY<L>::T; };
@@ -137,7 +145,11 @@ __global__ void __launch_bounds__(FX<L>::NT, FX<L>::MINB) k_p1(MV mv) {
 // P2: forward C2C along y (zero-padded input), times conj(phi_beta,y)
 // ---------------------------------------------------------------------------------------
 template <int L, bool D>
+#if VC_P2_MINB > 0
+__global__ void __launch_bounds__(FY<L>::NT, FY<L>::MINB2) k_p2(MV mv) {
+#else
 __global__ void __launch_bounds__(FY<L>::NT) k_p2(MV mv) {
+#endif
     constexpr int T = TY<L>::T;
     extern __shared__ double2 sm[];
     const int beta = blockIdx.y;
@@ -182,7 +194,31 @@ __global__ void __launch_bounds__(FY<L>::NT) k_p2(MV mv) {
             for (int e = 1; e <= pad; ++e) o[e << mv.lgT3] = czero();
         }
     };
-    fft_run<L, T, FY<L>::NT, false, true, 0, true>(sm, ld0, stN, mv.tw);
+    // one rank (BULK): the tile's rows are one contiguous block of X1 ([row][t], P2's tile layout),
+    // fetched with a single bulk copy into the FFT buffer; stage 0 reads it from there (all loads,
+    // a barrier, then the stores: fft_stage0_aliased), so no global load waits in registers
+    constexpr bool BULK = !D && Plan<L>::NS >= 2 && T * (L / Plan<L>::radix(0)) == FY<L>::NT;
+    if constexpr (BULK) {
+        __shared__ uint64_t p2bar;
+        const unsigned bytes = (unsigned)(16 * T * ey);
+        if (threadIdx.x == 0) {
+            mbar_init(&p2bar, 1);
+            fence_mbar_init();
+            mbar_arrive_expect_tx(&p2bar, bytes);
+            bulk_g2s(sm, in0 + (int64_t)tile * ey * T, bytes, &p2bar);
+        }
+        __syncthreads();  // (the barrier is initialised before anyone waits on it)
+        mbar_wait(&p2bar, 0);
+        const double2* __restrict__ inb = sm;
+        auto lds0 = [&](int t, int n) -> double2 {
+            const int kx = tile * T + t;
+            return (n < ey && kx < nkx) ? inb[n * T + t] : czero();
+        };
+        fft_stage0_aliased<L, T, FY<L>::NT, false, true, true>(sm, lds0, mv.tw);
+        fft_run_from1<L, T, FY<L>::NT, false, true, true>(sm, stN, mv.tw);
+    } else {
+        fft_run<L, T, FY<L>::NT, false, true, 0, true>(sm, ld0, stN, mv.tw);
+    }
 }
 
 // ---------------------------------------------------------------------------------------
@@ -458,6 +494,10 @@ __global__ void __launch_bounds__(kNT3) k_p3(MV mv) {
 // ---------------------------------------------------------------------------------------
 // P5: times phi_f,x, C2R along x (two lines per complex FFT), gather + dielectric terms
 // ---------------------------------------------------------------------------------------
+// bytes of P5's staged input block (T row pairs x nk kx x 2 rows, complex), 128-byte rounded
+__host__ __device__ constexpr size_t p5_inbytes(int L, int T, int nk) {
+    return ((size_t)32 * T * nk > (size_t)16 * L * T ? ((size_t)32 * T * nk + 127) & ~(size_t)127 : (size_t)16 * L * T);
+}
 template <int L, bool D>
 __global__ void __launch_bounds__(FX<L>::NT, FX<L>::MINB5) k_p5(MV mv) {
     constexpr int T = TX<L>::T;
@@ -514,7 +554,27 @@ __global__ void __launch_bounds__(FX<L>::NT, FX<L>::MINB5) k_p5(MV mv) {
     const int Gx = mv.G[alpha][0], Gy = mv.G[alpha][1];
     const int64_t zrow =
         ((int64_t)(z + mv.lo[2]) * Gy + mv.lo[1] + mv.ya[mv.rank]) * Gx + mv.lo[0];
-    int32_t* const ss = reinterpret_cast<int32_t*>(sm + L * T);  // [2T][L]
+    // one rank (BULK): the CTA's T row pairs of X4 are one contiguous block ([pair][kx][2], P4's
+    // row-pair interleaved layout), fetched with a single bulk copy into the FFT buffer itself;
+    // stage 0 reads it from there (fft_stage0_aliased: all loads, a barrier, then the stores), so
+    // no global load sits in a thread's registers while the transform waits on it
+    constexpr bool BULK = !D && Plan<L>::NS >= 2 && T * (L / Plan<L>::radix(0)) == FX<L>::NT;
+    const int nk1 = mv.nkx;
+    int32_t* const ss = reinterpret_cast<int32_t*>(
+        reinterpret_cast<uint8_t*>(sm) + (BULK ? p5_inbytes(L, T, nk1) : sizeof(double2) * L * T));  // [2T][L]
+    __shared__ uint64_t p5bar;
+    if (BULK) {
+        const int nqc = min(T, nyp - ch * T);
+        const unsigned bytes = (unsigned)(32 * nk1 * nqc);
+        if (threadIdx.x == 0) {
+            mbar_init(&p5bar, 1);
+            fence_mbar_init();
+            mbar_arrive_expect_tx(&p5bar, bytes);
+            bulk_g2s(sm, mv.R2[0][f] + blockIdx.z * mv.colA + (((int64_t)j * nyp + ch * T) * nk1 << 1), bytes,
+                     &p5bar);
+        }
+        __syncthreads();  // (the barrier is initialised before anyone waits on it)
+    }
     for (int r = 0; r < 2 * T; ++r) {
         const int q = ch * T + (r >> 1), l = 2 * q - s + (r & 1);
         if (q >= nyp || l < 0 || l >= nrow) continue;
@@ -523,7 +583,35 @@ __global__ void __launch_bounds__(FX<L>::NT, FX<L>::MINB5) k_p5(MV mv) {
     }
     cp_async_commit();
     auto sts = [&](int t, int p, double2 v) { sm[smi<L, T, false>(t, p)] = v; };
-    fft_run<L, T, FX<L>::NT, true, false>(sm, ld0, sts, mv.tw);
+    if constexpr (BULK) {
+        // the same values as ld0 / At, read from the staged block [pair t][kx][row]
+        const double2* __restrict__ inb = sm;
+        auto As = [&](int t, int row, int k, bool v) -> double2 {
+            double2 w = v ? inb[((int64_t)t * nk1 + k) * 2 + row] : czero();
+            if (ph) w = cmul(w, half_phase(mv.tw, k, L, +1));
+            if (k == 0 || 2 * k == L) w.y = 0.0;
+            return w;
+        };
+        auto lds0 = [&](int t, int n) -> double2 {
+            const int q = ch * T + t;
+            const int l0 = 2 * q - s;
+            const bool ok = q < nyp;
+            const bool has0 = ok && l0 >= 0, has1 = ok && l0 + 1 < nrow;
+            const bool lo = 2 * n <= L;
+            const int k = lo ? n : L - n;
+            double2 A = As(t, 0, k, has0), B = As(t, 1, k, has1);
+            if (!lo) {
+                A.y = -A.y;
+                B.y = -B.y;
+            }
+            return make_double2(A.x - B.y, A.y + B.x);
+        };
+        mbar_wait(&p5bar, 0);
+        fft_stage0_aliased<L, T, FX<L>::NT, true>(sm, lds0, mv.tw);
+        fft_run_from1<L, T, FX<L>::NT, true>(sm, sts, mv.tw);
+    } else {
+        fft_run<L, T, FX<L>::NT, true, false>(sm, ld0, sts, mv.tw);
+    }
     cp_async_wait<0>();
     __syncthreads();
     const int32_t want = kind ? kSlotDiel : 0;
@@ -1080,7 +1168,9 @@ static cudaError_t launch_p5(const MV& mv, cudaStream_t st) {
     VC_DISPATCH_L(mv.Mx, {
         constexpr int T = TX<LL>::T;
         for (int f = 0; f < mv.nf; ++f) maxch = std::max(maxch, ((mv.nr[mv.rank][3 + f] + 2) / 2 + T - 1) / T);
-        const size_t smem = sizeof(double2) * LL * T + sizeof(int32_t) * 2 * T * LL;  // + slot lines
+        // FFT buffer (one rank: the staged input block, which may be a little larger) + slot lines
+        const size_t smem = (mv.W > 1 ? sizeof(double2) * LL * T : p5_inbytes(LL, T, mv.nkx)) +
+                            sizeof(int32_t) * 2 * T * LL;
         auto kern = mv.W > 1 ? k_p5<LL, true> : k_p5<LL, false>;
         cudaError_t e = prep(kern, smem);
         if (e) return e;

@@ -4,6 +4,9 @@
 
 #include <cuda.h>
 
+#include <cmath>
+#include <cstdlib>
+
 #include "common.cuh"
 #include "ctx.h"
 
@@ -105,6 +108,33 @@ inline cudaError_t prep(K kern, size_t smem) {
     // thread group) launch with different sizes, so always grant the device maximum (a
     // per-launch value would race) -- occupancy follows the actual launch size
     if (smem > 48 * 1024) return grant_max_dyn_smem(kern, max_dyn_smem());
+    return cudaSuccess;
+}
+
+// prep() plus an L1-friendly carveout: the shared-memory share of the unified L1 / shared array
+// is set to what the kernel's resident CTAs need (register / thread limits included), not the
+// maximum, so that the rest stays L1 for the twiddle table and the other cached loads (the FFT
+// passes read twiddles through L1; with an all-shared carveout they came from L2).  Falls back to
+// the all-shared carveout if the smaller one would lose a CTA per SM.  VC_CARVE=0 disables it.
+template <class K>
+inline cudaError_t prep_fit(K kern, int nthr, size_t smem) {
+    cudaError_t e = prep(kern, smem);
+    if (e) return e;
+    static const bool on = !(getenv("VC_CARVE") && !atoi(getenv("VC_CARVE")));
+    if (!on) return cudaSuccess;
+    int nb_max = 0, dev = 0, smsm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb_max, kern, nthr, smem);
+    if (e || nb_max <= 0) return e;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&smsm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+    cudaFuncAttributes fa;
+    if ((e = cudaFuncGetAttributes(&fa, kern))) return e;
+    const double need = (double)nb_max * ((double)smem + fa.sharedSizeBytes + 1024.0);
+    const int pct = std::min(100, (int)std::ceil(100.0 * need / std::max(1, smsm)) + 1);
+    if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, pct))) return e;
+    int nb2 = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb2, kern, nthr, smem);
+    if (e || nb2 < nb_max) return cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     return cudaSuccess;
 }
 

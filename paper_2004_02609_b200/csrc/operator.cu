@@ -1048,7 +1048,7 @@ static cudaError_t launch_p1(const MV& mv, cudaStream_t st) {
         for (int b = 0; b < 3; ++b) maxch = std::max(maxch, ((mv.nr[mv.rank][b] + 2) / 2 + T - 1) / T);
         const size_t smem = sizeof(double2) * LL * T;
         auto kern = mv.W > 1 ? k_p1<LL, true> : k_p1<LL, false>;
-        cudaError_t e = prep(kern, smem);
+        cudaError_t e = prep_fit(kern, FX<LL>::NT, smem);
         if (e) return e;
         dim3 grid(std::max(1, maxch * maxz), 3, mv.nb);
         kern<<<grid, FX<LL>::NT, smem, st>>>(mv);
@@ -1063,7 +1063,7 @@ static cudaError_t launch_p4s_t(const MV& mv, cudaStream_t st) {
     for (int f = 0; f < mv.nf; ++f) G += mv.nzout[f];
     const size_t smem = sizeof(double2) * 2 * LL * T;
     auto kern = mv.W > 1 ? k_p4s<LL, KB, true> : k_p4s<LL, KB, false>;
-    cudaError_t e = prep(kern, smem);
+    cudaError_t e = prep_fit(kern, NT, smem);
     if (e) return e;
     const int ntiles = G * ((mv.nkx + T - 1) / T) * mv.nb;
     if (ntiles == 0) return cudaSuccess;
@@ -1082,7 +1082,7 @@ static cudaError_t launch_p2(const MV& mv, cudaStream_t st) {
         constexpr int T = TY<LL>::T;
         const size_t smem = sizeof(double2) * LL * T;
         auto kern = mv.W > 1 ? k_p2<LL, true> : k_p2<LL, false>;
-        cudaError_t e = prep(kern, smem);
+        cudaError_t e = prep_fit(kern, FY<LL>::NT, smem);
         if (e) return e;
         dim3 grid(std::max(1, ((mv.nkx + T - 1) / T) * maxz), 3, mv.nb);
         kern<<<grid, FY<LL>::NT, smem, st>>>(mv);
@@ -1172,7 +1172,7 @@ static cudaError_t launch_p5(const MV& mv, cudaStream_t st) {
         const size_t smem = (mv.W > 1 ? sizeof(double2) * LL * T : p5_inbytes(LL, T, mv.nkx)) +
                             sizeof(int32_t) * 2 * T * LL;
         auto kern = mv.W > 1 ? k_p5<LL, true> : k_p5<LL, false>;
-        cudaError_t e = prep(kern, smem);
+        cudaError_t e = prep_fit(kern, FX<LL>::NT, smem);
         if (e) return e;
         dim3 grid(std::max(1, maxch * maxz), mv.nf, mv.nb);
         kern<<<grid, FX<LL>::NT, smem, st>>>(mv);

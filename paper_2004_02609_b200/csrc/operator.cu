@@ -253,12 +253,32 @@ __global__ void __launch_bounds__(FYS<L, KB>::NT) k_p4s(MV mv) {
         while (g >= mv.nzout[f]) g -= mv.nzout[f++];
         j = g;
     };
+    // BULK: the tile's block arrives by one cp.async.bulk (mbarrier per stage) in its plain
+    // [ky][t] layout, and stage 0 reads it from there (fft_stage0_aliased), instead of L T / NT
+    // swizzled 16-byte cp.async copies per thread
+    constexpr bool BULK = Plan<L>::NS >= 2 && T * (L / Plan<L>::radix(0)) == NT;
+    __shared__ uint64_t p4bar[2];
+    if (BULK) {
+        if (threadIdx.x == 0) {
+            mbar_init(&p4bar[0], 1);
+            mbar_init(&p4bar[1], 1);
+            fence_mbar_init();
+        }
+        __syncthreads();
+    }
     auto prefetch = [&](int tl, int stg) {
         int f, j, xt;
         decode(tl, f, j, xt);
         // kx-tile-major X3: the tile's T kx x L ky are one contiguous block
         const double2* in = mv.X3[f] + (tl / nt1) * mv.colC + ((int64_t)j * ntx + xt) * L * T;
         double2* dst = sm + stg * L * T;
+        if constexpr (BULK) {
+            if (threadIdx.x == 0) {
+                mbar_arrive_expect_tx(&p4bar[stg], (unsigned)(16 * L * T));
+                bulk_g2s(dst, in, (unsigned)(16 * L * T), &p4bar[stg]);
+            }
+            return;
+        }
         for (int e = threadIdx.x; e < L * T; e += NT) {
             const int n = e / T, t = e % T;
             const bool valid = xt * T + t < nkx;
@@ -271,9 +291,13 @@ __global__ void __launch_bounds__(FYS<L, KB>::NT) k_p4s(MV mv) {
     for (int tl = blockIdx.x; tl < ntiles; tl += gridDim.x, ++it) {
         const int stg = it & 1;
         if (tl + (int)gridDim.x < ntiles) prefetch(tl + gridDim.x, stg ^ 1);
-        else cp_async_commit();
-        cp_async_wait<1>();
-        __syncthreads();
+        else if (!BULK) cp_async_commit();
+        if constexpr (BULK) {
+            mbar_wait(&p4bar[stg], (it >> 1) & 1);
+        } else {
+            cp_async_wait<1>();
+            __syncthreads();
+        }
         int f, j, xt;
         decode(tl, f, j, xt);
         const int eyo = mv.ext_out[f][1];
@@ -301,10 +325,21 @@ __global__ void __launch_bounds__(FYS<L, KB>::NT) k_p4s(MV mv) {
                 }
             }
         };
-        fft_run<L, T, NT, true, true, 0, true>(buf, lds, stN, mv.tw);
+        if constexpr (BULK) {
+            auto lds0 = [&](int t, int n) {
+                double2 v = (xt * T + t < nkx) ? buf[n * T + t] : czero();  // plain [ky][t]
+                if (ph) v = cmul(v, half_phase(mv.tw, ktil(n, L), L, +1));
+                return v;
+            };
+            fft_stage0_aliased<L, T, NT, true, true, true>(buf, lds0, mv.tw);
+            fft_run_from1<L, T, NT, true, true, true>(buf, stN, mv.tw);
+            fence_proxy_async();  // this stage is refilled by the async proxy next
+        } else {
+            fft_run<L, T, NT, true, true, 0, true>(buf, lds, stN, mv.tw);
+        }
         __syncthreads();
     }
-    cp_async_wait<0>();
+    if (!BULK) cp_async_wait<0>();
 }
 
 // ---------------------------------------------------------------------------------------

@@ -51,7 +51,9 @@ constexpr int p4_tile(int L) { return clampi(kP4KB * 64 / L, 1, 32); }  // FYS<L
 #endif
 template <int L> struct FY {
     static constexpr int T = p2_tile(L);  // >= 2 adjacent kx: 32-byte row segments
-    static constexpr int NT = 256;
+    // 256 threads; 512 at L = 4096 (C5), where a CTA holds 2 pencils of 4096: one stage-0
+    // butterfly per thread (P2's bulk-fed stage 0) and 16 warps on the one CTA per SM
+    static constexpr int NT = L >= 4096 ? 512 : 256;
     static constexpr int MINB2 = VC_P2_MINB;  // P2's register cap (launch bounds)
 };
 template <int L> struct TX { static constexpr int T = FX<L>::T; };

@@ -56,6 +56,10 @@ def parse():
     ap.add_argument("--tol", type=float, default=1e-4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-batch", action="store_true", help="solve the m columns one at a time")
+    ap.add_argument("--tucker", type=int, default=0,
+                    help="Tucker-compressed spectra to 10^-d (NEXT-1; direct-z configs); 0 = exact (default)")
+    ap.add_argument("--tucker-cache", default=None,
+                    help="directory of the install-time Tucker cache (NEXT-4; with --tucker)")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     return ap.parse_args()
 
@@ -243,7 +247,7 @@ def main():
             ctx.set_geometry(h_label.numpy(), h_eps.numpy(), st.eps_out, st.dv)
         else:
             ctx.set_geometry(dev_label, dev_eps, st.eps_out, st.dv)
-        ctx.build_operator(batch=not args.no_batch)
+        ctx.build_operator(batch=not args.no_batch, tucker_digits=args.tucker, tucker_cache=args.tucker_cache)
         ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ea.record(ctx._tstream)
         C, info = ctx.solve_capacitance(**sopt)
@@ -322,7 +326,7 @@ def main():
         tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
         if os.path.exists(tf):
             try:
-                traffic = json.load(open(tf)).get(args.config, {}).get(f"P{dom + 1}")
+                traffic = None if args.tucker else json.load(open(tf)).get(args.config, {}).get(f"P{dom + 1}")
             except Exception:
                 traffic = None
         mv_ms = stats["ms_matvec"] / max(1, n_mv)
@@ -344,7 +348,10 @@ def main():
                        "restart": 35, "precond": "block-diagonal-diagonal, boxes 10^3",
                        "step": "set_geometry + build_operator + solve_capacitance",
                        "l2": "working set > L2 (no flush needed)",
-                       "seed": "voxgen seed 0 (one structure, all ranks)"},
+                       "seed": "voxgen seed 0 (one structure, all ranks)",
+                       "spectra": (f"Tucker-compressed, 1e-{args.tucker}" +
+                                   (" (install-time cache)" if args.tucker_cache else "")) if args.tucker
+                       else "exact"},
             "gpu_launches": stats["gpu_launches"],
             "comm_ms_per_matvec": stats["ms_comm"] / max(1, n_mv),
             "solve_s_per_column": None,

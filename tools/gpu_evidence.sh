@@ -15,5 +15,7 @@ python tools/ncu_stalls.py /tmp/prof_c4b.ncu-rep k_p3m > gpurun_out/p3_stalls.tx
 timeout 200 python tools/pass_time.py --config C4 --n 20 > gpurun_out/pass_times.txt 2>&1
 timeout 200 python tools/pass_time.py --config C3 --n 20 >> gpurun_out/pass_times.txt 2>&1
 timeout 300 python bench.py --config C3 --steps 5 --no-cpu-baseline > gpurun_out/bench_c3.log 2>&1
+timeout 300 python bench.py --tucker 10 --steps 5 --no-cpu-baseline > gpurun_out/bench_tucker.log 2>&1
+timeout 600 python bench.py --impl reference --steps 2 --warmup 3 > gpurun_out/bench_ref.log 2>&1; echo "ref rc=$?" >> gpurun_out/bench_ref.log
 echo done
 python tools/ncu_lines.py /tmp/prof_c4b.ncu-rep k_p3m 20 > gpurun_out/p3_lines.txt 2>&1; ls -la gpurun_out; du -sh gpurun_out

@@ -252,6 +252,53 @@ cudaError_t launch_gs_fused(const Cols2& cc, int64_t n, int nv, int nc, double* 
     return cudaGetLastError();
 }
 
+// CGS2's last pass with the norm: w <- w - V h (the arithmetic of k_multiaxpy / k_multiaxpy2) and
+// d[z][0] = ||w||^2 (per-block partials, then a fixed-order sum by the last block), in place of
+// a multi-axpy and a one-vector multi-dot (one read of w fewer, one launch fewer)
+__global__ void __launch_bounds__(kRedNT) k_axpy_norm(Cols2 cc, int64_t ldv, int nv, int64_t n,
+                                                      double* __restrict__ partial,
+                                                      unsigned* __restrict__ ticket) {
+    const int z = blockIdx.z;
+    __shared__ double hs[kMaxBasis];
+    if (threadIdx.x < nv) hs[threadIdx.x] = cc.h[z][threadIdx.x];
+    __syncthreads();
+    const double* __restrict__ V = cc.V[z];
+    double* __restrict__ w = cc.out[z];
+    double* __restrict__ part = partial + (size_t)z * kRedBlocks * kMaxBasis;
+    double acc2 = 0.0;
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        double acc = 0.0;
+        for (int i = 0; i < nv; ++i) acc = fma(hs[i], V[i * ldv + k], acc);
+        const double w2 = fma(-1.0, acc, w[k]);
+        w[k] = w2;
+        acc2 = fma(w2, w2, acc2);
+    }
+    __shared__ double s[kRedNT / 32];
+    const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+    for (int o = 16; o; o >>= 1) acc2 += __shfl_xor_sync(0xffffffffu, acc2, o);
+    if (lane == 0) s[wp] = acc2;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double v = 0.0;
+        for (int q = 0; q < kRedNT / 32; ++q) v += s[q];
+        part[blockIdx.x] = v;
+    }
+    __threadfence();
+    __shared__ bool last;
+    if (threadIdx.x == 0) last = atomicAdd(ticket + z, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    if (wp == 0) {
+        double v = 0.0;
+        for (int b = lane; b < (int)gridDim.x; b += 32) v += __ldcg(part + b);
+        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) cc.d[z][0] = v;
+    }
+    if (threadIdx.x == 0) ticket[z] = 0u;
+}
+
 // out[z] = w[z] / sqrt(*h[z])
 __global__ void k_scale_by_norm2(Cols2 cc, int64_t n) {
     const int z = blockIdx.z;
@@ -388,6 +435,18 @@ struct Krylov {
         count_launch(c, 1);
         return comm_allreduce(c, d, nv);
     }
+    // t -= V[0..nv) h (device), then d[0] = ||t||^2, summed over ranks
+    vc_status axpy_norm(int nv, const double* h, double* d) {
+        Cols2 cc{};
+        cc.V[0] = V;
+        cc.out[0] = t;
+        cc.h[0] = h;
+        cc.d[0] = d;
+        k_axpy_norm<<<dim3(kRedBlocks, 1, 1), kRedNT, 0, c->stream>>>(cc, n, nv, n, c->partial.p, c->ticket.p);
+        VC_CUDA(c, cudaGetLastError());
+        count_launch(c, 1);
+        return comm_allreduce(c, d, 1);
+    }
     vc_status norm2_host(const double* vec, double* out) {
         vc_status s = dots(vec, 1, vec, c->dvec.p);
         if (s) return s;
@@ -467,10 +526,9 @@ vc_status solve_dev(vc_ctx* c, const double* d_b, double* d_x, const vc_solve_op
             double* dh = c->dvec.p + (size_t)(j & 1) * 3 * kMaxBasis;
             if ((e = K.dots(K.V, j + 1, K.t, dh))) return e;
             if ((e = K.fused(j + 1, dh, dh + kMaxBasis))) return e;
-            k_multiaxpy<<<gn, 256, 0, st>>>(K.t, K.V, n, j + 1, dh + kMaxBasis, n, -1.0);
-            if ((e = K.dots(K.t, 1, K.t, dh + 2 * kMaxBasis))) return e;
+            if ((e = K.axpy_norm(j + 1, dh + kMaxBasis, dh + 2 * kMaxBasis))) return e;
             k_scale_by_norm<<<gn, 256, 0, st>>>(vn, K.t, dh + 2 * kMaxBasis, n);
-            count_launch(c, 2);
+            count_launch(c, 1);
             VC_CUDA(c, cudaMemcpyAsync(c->h_pinned + (size_t)(j & 1) * 3 * kMaxBasis, dh,
                                        8 * 3 * kMaxBasis, cudaMemcpyDeviceToHost, st));
             VC_CUDA(c, cudaEventRecord(c->arn_ev[j & 1], st));
@@ -697,7 +755,7 @@ vc_status solve_multi_dev(vc_ctx* c, int ncol, const double* const* d_b, double*
                 qq.out[0] = o0; qq.out[1] = o1; qq.h[0] = h0; qq.h[1] = h1;
                 return qq;
             };
-            const dim3 gd(kRedBlocks, (nv + kDotG - 1) / kDotG, 2), gd1(kRedBlocks, 1, 2), ga(gn, 1, 2);
+            const dim3 gd(kRedBlocks, (nv + kDotG - 1) / kDotG, 2), ga(gn, 1, 2);
             // several ranks: each column's partial dots are summed over ranks (as K.dots does)
             auto sum_ranks = [&](int off, int cnt) -> vc_status {
                 if (c->world == 1) return VC_OK;
@@ -720,18 +778,18 @@ vc_status solve_multi_dev(vc_ctx* c, int ncol, const double* const* d_b, double*
                                                    n, nv, n, c->partial.p, c->ticket.p);
             }
             if ((e = sum_ranks(kMaxBasis, nv))) return e;
-            k_multiaxpy2<<<ga, 256, 0, st>>>(cc(A.K.V, B.K.V, nullptr, nullptr, A.K.t, B.K.t,
-                                                ha + kMaxBasis, hb + kMaxBasis),
-                                             n, nv, n, -1.0);
-            k_multidot2<<<gd1, kRedNT, 0, st>>>(cc(A.K.t, B.K.t, A.K.t, B.K.t, ha + 2 * kMaxBasis,
-                                                   hb + 2 * kMaxBasis, nullptr, nullptr),
-                                                n, 1, n, c->partial.p, c->ticket.p);
+            {  // t -= V h2 and ||t||^2 in one pass
+                Cols2 f = cc(A.K.V, B.K.V, nullptr, nullptr, A.K.t, B.K.t, ha + kMaxBasis, hb + kMaxBasis);
+                f.d[0] = ha + 2 * kMaxBasis;
+                f.d[1] = hb + 2 * kMaxBasis;
+                k_axpy_norm<<<dim3(kRedBlocks, 1, 2), kRedNT, 0, st>>>(f, n, nv, n, c->partial.p, c->ticket.p);
+            }
             if ((e = sum_ranks(2 * kMaxBasis, 1))) return e;
             k_scale_by_norm2<<<ga, 256, 0, st>>>(cc(nullptr, nullptr, A.K.t, B.K.t,
                                                     A.K.V + (size_t)nv * n, B.K.V + (size_t)nv * n,
                                                     ha + 2 * kMaxBasis, hb + 2 * kMaxBasis),
                                                  n);
-            count_launch(c, nv <= gs_fused_max() ? 5 : 6);
+            count_launch(c, nv <= gs_fused_max() ? 4 : 5);
         } else {
             for (const Ent& en : S.ent) {
                 Col& C = col[en.col];
@@ -741,10 +799,9 @@ vc_status solve_multi_dev(vc_ctx* c, int ncol, const double* const* d_b, double*
                     const int j = en.j;
                     if ((e = K.dots(K.V, j + 1, K.t, dh))) return e;
                     if ((e = K.fused(j + 1, dh, dh + kMaxBasis))) return e;
-                    k_multiaxpy<<<gn, 256, 0, st>>>(K.t, K.V, n, j + 1, dh + kMaxBasis, n, -1.0);
-                    if ((e = K.dots(K.t, 1, K.t, dh + 2 * kMaxBasis))) return e;
+                    if ((e = K.axpy_norm(j + 1, dh + kMaxBasis, dh + 2 * kMaxBasis))) return e;
                     k_scale_by_norm<<<gn, 256, 0, st>>>(K.V + (size_t)(j + 1) * n, K.t, dh + 2 * kMaxBasis, n);
-                    count_launch(c, 2);
+                    count_launch(c, 1);
                 } else {  // restart residual r = R (b - A x)
                     k_axpby<<<gn, 256, 0, st>>>(K.w, K.b, 1.0, -1.0, n);
                     count_launch(c);

@@ -180,10 +180,10 @@ void comm_free(vc_ctx* c) {
 // are skipped (the producing kernel wrote the self block in place).  Stream-ordered.
 vc_status comm_alltoall(vc_ctx* c, const std::vector<const void*>& send,
                         const std::vector<size_t>& sb, const std::vector<void*>& recv,
-                        const std::vector<size_t>& rb) {
+                        const std::vector<size_t>& rb, cudaStream_t st_in) {
     Comm* m = c->comm;
     const int W = m->world, r = m->rank;
-    cudaStream_t st = c->stream;
+    cudaStream_t st = st_in ? st_in : c->stream;
     if (m->kind == 0) {
         ncclResult_t e = g_nccl.GroupStart();
         for (int q = 0; q < W && e == ncclSuccess; ++q) {

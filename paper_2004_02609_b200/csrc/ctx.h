@@ -156,6 +156,12 @@ struct vc_ctx {
     vc::Comm* comm = nullptr;
     cudaStream_t stream = nullptr;
     bool own_stream = false;
+    // several ranks: the exchanges run on their own stream, chunk by chunk, so each source's /
+    // field's all-to-all overlaps the transform of the next; events [0..8]
+    // "chunk produced" (compute stream), [9..17] "chunk exchanged" (comm stream)
+    cudaStream_t cstream = nullptr;
+    cudaEvent_t cev[18] = {};
+    bool cev_ok = false;
     std::string err;
 
     // ---- geometry (vc_set_geometry) ----
@@ -339,7 +345,8 @@ void group_destroy(void* g);
 vc_status comm_init(vc_ctx* c, int rank, int world, int transport, const void* id);
 void comm_free(vc_ctx* c);
 vc_status comm_alltoall(vc_ctx* c, const std::vector<const void*>& send, const std::vector<size_t>& sb,
-                        const std::vector<void*>& recv, const std::vector<size_t>& rb);
+                        const std::vector<void*>& recv, const std::vector<size_t>& rb,
+                        cudaStream_t st = nullptr /* nullptr: the context stream */);
 vc_status comm_allreduce(vc_ctx* c, double* d, int n);
 vc_status comm_nccl_selftest(vc_ctx* c, double* out);
 inline void count_launch(vc_ctx* c, int k = 1) { c->stats.gpu_launches += k; }

@@ -42,6 +42,9 @@ struct MV {
     // x-transformed planes travel as blocks [source][plane][own rows][dest kx] (P1 -> P2) and
     // [field][plane][dest rows][own kx] (P4 -> P5); the self block is written in place.
     int W, rank;
+    // several ranks, chunked exchange: P1 / P2 run for the sources [s0, s1),
+    // P4 / P5 for the fields [f0, f1); one launch for all: s0 = 0, s1 = 3, f0 = 0, f1 = nf
+    int s0, s1, f0, f1;
     int ya[kMaxRanks + 1], kxa[kMaxRanks + 1];
     int nr[kMaxRanks][9];  // rows of rank p within source b's (0..2) / field f's (3+f) extent
     int kx0, nkx;          // this rank's kx slab

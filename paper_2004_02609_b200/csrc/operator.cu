@@ -72,7 +72,7 @@ template <int L, bool D>
 __global__ void __launch_bounds__(FX<L>::NT, FX<L>::MINB) k_p1(MV mv) {
     constexpr int T = TX<L>::T;
     extern __shared__ double2 sm[];
-    const int beta = blockIdx.y;
+    const int beta = blockIdx.y + mv.s0;
     const int ex = mv.ext_in[beta][0];
     if (ex == 0) return;
     const int nrow = mv.nr[mv.rank][beta];  // own rows of this source grid
@@ -154,7 +154,7 @@ __global__ void __launch_bounds__(FY<L>::NT) k_p2(MV mv) {
 #endif
     constexpr int T = TY<L>::T;
     extern __shared__ double2 sm[];
-    const int beta = blockIdx.y;
+    const int beta = blockIdx.y + mv.s0;
     const int ex = mv.ext_in[beta][0], ey = mv.ext_in[beta][1], ez = mv.ext_in[beta][2];
     if (ex == 0) return;
     const int nkx = mv.nkx;  // own kx slab (local column kx)
@@ -241,17 +241,17 @@ template <int L, int KB, bool D>
 __global__ void __launch_bounds__(FYS<L, KB>::NT) k_p4s(MV mv) {
     constexpr int T = FYS<L, KB>::T, NT = FYS<L, KB>::NT;
     extern __shared__ __align__(16) double2 sm[];  // [2][L][T]
-    const int nkx = mv.nkx, nf = mv.nf;
+    const int nkx = mv.nkx;
     const int ntx = (nkx + T - 1) / T;
     int G = 0;
-    for (int f = 0; f < nf; ++f) G += mv.nzout[f];
+    for (int f = mv.f0; f < mv.f1; ++f) G += mv.nzout[f];  // fields [f0, f1)
     const int nt1 = G * ntx;  // tiles per column
     const int ntiles = nt1 * mv.nb;
     auto decode = [&](int tl, int& f, int& j, int& xt) {
         tl %= nt1;
         xt = tl % ntx;
         int g = tl / ntx;
-        f = 0;
+        f = mv.f0;
         while (g >= mv.nzout[f]) g -= mv.nzout[f++];
         j = g;
     };
@@ -539,7 +539,7 @@ template <int L, bool D>
 __global__ void __launch_bounds__(FX<L>::NT, FX<L>::MINB5) k_p5(MV mv) {
     constexpr int T = TX<L>::T;
     extern __shared__ double2 sm[];
-    const int f = blockIdx.y;
+    const int f = blockIdx.y + mv.f0;
     if (f >= mv.nf) return;
     const int kind = mv.fkind[f], alpha = mv.faxis[f];
     const int exo = mv.ext_out[f][0];
@@ -1087,7 +1087,7 @@ static cudaError_t launch_p1(const MV& mv, cudaStream_t st) {
         auto kern = mv.W > 1 ? k_p1<LL, true> : k_p1<LL, false>;
         cudaError_t e = prep_fit(kern, FX<LL>::NT, smem);
         if (e) return e;
-        dim3 grid(std::max(1, maxch * maxz), 3, mv.nb);
+        dim3 grid(std::max(1, maxch * maxz), mv.s1 - mv.s0, mv.nb);  // sources [s0, s1)
         kern<<<grid, FX<LL>::NT, smem, st>>>(mv);
     });
     return cudaGetLastError();
@@ -1097,7 +1097,7 @@ static cudaError_t launch_p4s_t(const MV& mv, cudaStream_t st) {
     constexpr int T = FYS<LL, KB>::T, NT = FYS<LL, KB>::NT;
     static_assert(T == p4_tile(LL), "X3 layout (operator_build, p4_tile) and P4's tile disagree");
     int G = 0;
-    for (int f = 0; f < mv.nf; ++f) G += mv.nzout[f];
+    for (int f = mv.f0; f < mv.f1; ++f) G += mv.nzout[f];
     const size_t smem = sizeof(double2) * 2 * LL * T;
     auto kern = mv.W > 1 ? k_p4s<LL, KB, true> : k_p4s<LL, KB, false>;
     cudaError_t e = prep_fit(kern, NT, smem);
@@ -1121,7 +1121,7 @@ static cudaError_t launch_p2(const MV& mv, cudaStream_t st) {
         auto kern = mv.W > 1 ? k_p2<LL, true> : k_p2<LL, false>;
         cudaError_t e = prep_fit(kern, FY<LL>::NT, smem);
         if (e) return e;
-        dim3 grid(std::max(1, ((mv.nkx + T - 1) / T) * maxz), 3, mv.nb);
+        dim3 grid(std::max(1, ((mv.nkx + T - 1) / T) * maxz), mv.s1 - mv.s0, mv.nb);  // sources [s0, s1)
         kern<<<grid, FY<LL>::NT, smem, st>>>(mv);
     });
     return cudaGetLastError();
@@ -1211,7 +1211,7 @@ static cudaError_t launch_p5(const MV& mv, cudaStream_t st) {
         auto kern = mv.W > 1 ? k_p5<LL, true> : k_p5<LL, false>;
         cudaError_t e = prep_fit(kern, FX<LL>::NT, smem);
         if (e) return e;
-        dim3 grid(std::max(1, maxch * maxz), mv.nf, mv.nb);
+        dim3 grid(std::max(1, maxch * maxz), mv.f1 - mv.f0, mv.nb);  // fields [f0, f1)
         kern<<<grid, FX<LL>::NT, smem, st>>>(mv);
     });
     return cudaGetLastError();
@@ -2084,6 +2084,10 @@ static MV make_mv(vc_ctx* c, const double* x, double* y) {
         mv.x2zo[b] = c->zdirect ? c->p3m_zoff[b] : 0;
     }
     mv.p3m_tab = c->p3m_tab.p;
+    mv.s0 = 0;
+    mv.s1 = 3;
+    mv.f0 = 0;
+    mv.f1 = c->nf;
     mv.p3m_nneg = c->zdirect ? c->p3m_nneg : 0;
     mv.p3m_oddmask = c->p3m_oddmask;
     mv.p3m_neg = c->p3m_tab.p + c->p3m_negoff;
@@ -2172,6 +2176,83 @@ vc_status timing_resolve(vc_ctx* c) {
     return VC_OK;
 }
 
+// Several ranks: the two all-to-alls are split by source (after P1) and by field
+// (after P4) and run on the comm stream, so each chunk's exchange overlaps the transforms of the
+// chunks after it: P1(b) -> a2a(b) || P1(b + 1); P2(b) waits for a2a(b) only; the same for
+// P4(f) -> a2a(f) -> P5(f).  The arithmetic is that of the one-launch passes (each pencil is
+// transformed by the same plan), so the partitioned matvec stays bitwise equal to one rank's.
+static vc_status a2a_chunk(vc_ctx* c, int e, int g, int col, cudaStream_t cs) {
+    const int W = c->world, rk = c->rank, nkx = c->kxa[rk + 1] - c->kxa[rk];
+    std::vector<const void*> sp(W, nullptr);
+    std::vector<void*> rp(W, nullptr);
+    std::vector<size_t> sb(W, 0), rb(W, 0);
+    for (int q = 0; q < W; ++q) {
+        if (q == rk) continue;
+        const int nkq = c->kxa[q + 1] - c->kxa[q];
+        if (e == 0) {  // source g: [sender][source][plane][rows][dest kx] blocks
+            sp[q] = c->bufS.p + c->offS1[q][g] + (size_t)col * c->colS;
+            rp[q] = c->bufA.p + c->offR1[q][g] + (size_t)col * c->colA;
+            sb[q] = 16 * (size_t)c->nzin[g] * c->nr[rk][g] * nkq;
+            rb[q] = 16 * (size_t)c->nzin[g] * c->nr[q][g] * nkx;
+        } else {  // field g: [field][plane][dest rows][own kx] blocks
+            sp[q] = c->bufS.p + c->offS2[q][g] + (size_t)col * c->colS;
+            rp[q] = c->bufA.p + c->offR2[q][g] + (size_t)col * c->colA;
+            sb[q] = 16 * (size_t)c->nzout[g] * c->nr[q][3 + g] * nkx;
+            rb[q] = 16 * (size_t)c->nzout[g] * c->nr[rk][3 + g] * nkq;
+        }
+    }
+    return comm_alltoall(c, sp, sb, rp, rb, cs);
+}
+
+static vc_status matvec_chunked(vc_ctx* c, const MV& mv, const cudaEvent_t* ev, bool det) {
+    cudaStream_t st = c->stream;
+    if (!c->cstream) VC_CUDA(c, cudaStreamCreateWithFlags(&c->cstream, cudaStreamNonBlocking));
+    if (!c->cev_ok) {
+        for (auto& e : c->cev) VC_CUDA(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        c->cev_ok = true;
+    }
+    cudaStream_t cs = c->cstream;
+    cudaEvent_t* made = c->cev;      // [0..8]: chunk produced on the compute stream
+    cudaEvent_t* moved = c->cev + 9; // [9..17]: chunk exchanged on the comm stream
+    // the comm stream starts after everything before this matvec (its buffers' previous users)
+    VC_CUDA(c, cudaEventRecord(made[8], st));
+    VC_CUDA(c, cudaStreamWaitEvent(cs, made[8], 0));
+    for (int ph = 0; ph < 2; ++ph) {  // ph 0: P1 -> a2a #1 -> P2; ph 1: P4 -> a2a #2 -> P5
+        const int ng = ph == 0 ? 3 : c->nf;
+        const int pa = ph == 0 ? 0 : 3, pb = ph == 0 ? 1 : 4;  // producing / consuming pass
+        if (ph == 1) {  // P3 between the phases
+            if (det) VC_CUDA(c, cudaEventRecord(ev[1 + 2], st));
+            VC_CUDA(c, launch_p3(mv, st));
+            if (det) VC_CUDA(c, cudaEventRecord(ev[6 + 2], st));
+        }
+        if (det) VC_CUDA(c, cudaEventRecord(ev[1 + pa], st));
+        if (det) VC_CUDA(c, cudaEventRecord(ev[12 + ph], cs));
+        for (int g = 0; g < ng; ++g) {
+            MV m = mv;
+            if (ph == 0) { m.s0 = g; m.s1 = g + 1; } else { m.f0 = g; m.f1 = g + 1; }
+            VC_CUDA(c, ph == 0 ? launch_p1(m, st) : launch_p4s(m, st));
+            VC_CUDA(c, cudaEventRecord(made[g], st));
+            VC_CUDA(c, cudaStreamWaitEvent(cs, made[g], 0));
+            for (int i = 0; i < mv.nb; ++i) {  // one exchange per batch column
+                vc_status s = a2a_chunk(c, ph, g, i, cs);
+                if (s) return s;
+            }
+            VC_CUDA(c, cudaEventRecord(moved[g], cs));
+        }
+        if (det) VC_CUDA(c, cudaEventRecord(ev[6 + pa], st));
+        if (det) VC_CUDA(c, cudaEventRecord(ev[14 + ph], cs));
+        if (det) VC_CUDA(c, cudaEventRecord(ev[1 + pb], st));
+        for (int g = 0; g < ng; ++g) {
+            MV m = mv;
+            if (ph == 0) { m.s0 = g; m.s1 = g + 1; } else { m.f0 = g; m.f1 = g + 1; }
+            VC_CUDA(c, cudaStreamWaitEvent(st, moved[g], 0));
+            VC_CUDA(c, ph == 0 ? launch_p2(m, st) : launch_p5(m, st));
+        }
+        if (det) VC_CUDA(c, cudaEventRecord(ev[6 + pb], st));
+    }
+    return VC_OK;
+}
+
 static vc_status matvec_run(vc_ctx* c, const MV& mv) {
     cudaStream_t st = c->stream;
     Timing& T = c->timing;
@@ -2197,34 +2278,18 @@ static vc_status matvec_run(vc_ctx* c, const MV& mv) {
             mv.ys[i], mv.xs[i], mv.ibar, c->NL);
     cudaError_t (*launch[5])(const MV&, cudaStream_t) = {launch_p1, launch_p2, launch_p3,
                                                          launch_p4s, launch_p5};
-    for (int p = 0; p < 5; ++p) {
-        if (c->world > 1 && (p == 1 || p == 4)) {
-            // x-transformed planes: rows -> kx slabs before P2, back before P5
-            const int e = p == 1 ? 0 : 1;
-            if (det) VC_CUDA(c, cudaEventRecord(ev[12 + e], st));
-            for (int i = 0; i < mv.nb; ++i) {  // one all-to-all per batch column
-                vc_status s;
-                if (i == 0) {
-                    s = comm_alltoall(c, c->a2a_send[e], c->a2a_sb[e], c->a2a_recv[e], c->a2a_rb[e]);
-                } else {
-                    std::vector<const void*> sp(c->a2a_send[e]);
-                    std::vector<void*> rp(c->a2a_recv[e]);
-                    for (int q = 0; q < c->world; ++q) {
-                        if (sp[q]) sp[q] = static_cast<const double2*>(sp[q]) + (size_t)i * c->colS;
-                        if (rp[q]) rp[q] = static_cast<double2*>(rp[q]) + (size_t)i * c->colA;
-                    }
-                    s = comm_alltoall(c, sp, c->a2a_sb[e], rp, c->a2a_rb[e]);
-                }
-                if (s) return s;
-            }
-            if (det) VC_CUDA(c, cudaEventRecord(ev[14 + e], st));
+    if (c->world == 1) {
+        for (int p = 0; p < 5; ++p) {
+            if (det) VC_CUDA(c, cudaEventRecord(ev[1 + p], st));
+            VC_CUDA(c, launch[p](mv, st));
+            if (det) VC_CUDA(c, cudaEventRecord(ev[6 + p], st));
         }
-        if (det) VC_CUDA(c, cudaEventRecord(ev[1 + p], st));
-        VC_CUDA(c, launch[p](mv, st));
-        if (det) VC_CUDA(c, cudaEventRecord(ev[6 + p], st));
+    } else {
+        vc_status s = matvec_chunked(c, mv, ev, det);
+        if (s) return s;
     }
     if (ev) VC_CUDA(c, cudaEventRecord(ev[11], st));
-    count_launch(c, 5 + mv.nb);
+    count_launch(c, (c->world > 1 ? 7 + 2 * c->nf : 5) + mv.nb);  // (chunked: 3 + 3 + 1 + 2 nf)
     c->stats.n_matvec += mv.nb;
     for (int p = 0; p < 5; ++p) {
         c->stats.n_pass[p] += 1;

@@ -116,6 +116,12 @@ void vc_destroy(vc_ctx* c) {
         if (c->mc_ev_ok)
             for (auto& e : c->mc_ev) cudaEventDestroy(e);
         for (auto& e : c->kev) cudaEventDestroy(e);
+        if (c->cev_ok)
+            for (auto& e : c->cev) cudaEventDestroy(e);
+        if (c->cstream) {
+            cudaStreamSynchronize(c->cstream);
+            cudaStreamDestroy(c->cstream);
+        }
         if (c->own_stream) cudaStreamDestroy(c->stream);
     }
     delete c;

@@ -163,8 +163,12 @@ __global__ void __launch_bounds__(FY<L>::NT) k_p2(MV mv) {
     // direct-z: the planes of one kx tile are adjacent blocks (their X2 elements share sectors)
     const int nzb = mv.nzin[beta];
     if (nzb == 0) return;
-    const int j = mv.zdirect ? blockIdx.x % nzb : blockIdx.x / ntile;
-    const int tile = mv.zdirect ? blockIdx.x / nzb : blockIdx.x % ntile;
+    // planes fastest in the grid when X2 elements of adjacent planes share a sector (direct-z, or
+    // a one-kx P3 tile: C5), so the CTAs writing the two halves of a sector run together and L2
+    // merges them before eviction (kx fastest otherwise)
+    const bool jfast = mv.zdirect || mv.T3 == 1;
+    const int j = jfast ? blockIdx.x % nzb : blockIdx.x / ntile;
+    const int tile = jfast ? blockIdx.x / nzb : blockIdx.x % ntile;
     if (j >= nzb || tile >= ntile) return;
     (void)ez;
     // X2 tile-major for P3, q = |ky| (ky <= L/2: side 0): [q][kx / T3][side][plane][kx % T3],
@@ -414,8 +418,13 @@ __global__ void __launch_bounds__(kNT3) k_p3(MV mv) {
         zmap[e] = (int16_t)(z < mv.ZL ? mv.planes[(9 + g) * mv.ZL + z] : -1);
     }
     __syncthreads();
-    auto issue = [&](int tl, int s) {  // one thread: fetch tile tl = q * ntile + tile into stage s
-        const size_t qt = (size_t)tl;
+    // tile order: kx tiles fastest, or (X3 one kx wide, lgt4 = 0: C5) |ky| fastest, so that the
+    // CTAs writing adjacent ky of one X3 sector run together and L2 merges the halves
+    const int nq = My / 2 + 1;
+    const bool qfast = mv.lgt4 == 0;
+    auto qt_of = [&](int tl) { return qfast ? (tl % nq) * ntile + tl / nq : tl; };  // X2 / R block
+    auto issue = [&](int tl, int s) {  // one thread: fetch tile tl (block q * ntile + tile) into stage s
+        const size_t qt = (size_t)qt_of(tl);
         mbar_arrive_expect_tx(&bar[s], (unsigned)(16 * XS + 8 * RC));
         if (nz0) bulk_g2s(xin + s * XS, mv.X2[0] + qt * T2 * nz0, 16u * T2 * nz0, &bar[s]);
         if (nz1) bulk_g2s(xin + s * XS + xo1, mv.X2[1] + qt * T2 * nz1, 16u * T2 * nz1, &bar[s]);
@@ -435,7 +444,8 @@ __global__ void __launch_bounds__(kNT3) k_p3(MV mv) {
         else { mbar_wait(&bar[1], par1); par1 ^= 1; }
         const double2* xs = xin + s * XS;
         const double* rs = rin + s * RC;
-        const int q = tl / ntile, tile = tl % ntile;
+        const int qt = qt_of(tl);
+        const int q = qt / ntile, tile = qt % ntile;
         const int nside = (q == 0 || 2 * q == My) ? 1 : 2;
         // forward z-FFT of pencils pp = beta * 2T + side * T + t (zero-padded to L)
         auto ld0 = [&](int pp, int n) -> double2 {

@@ -224,11 +224,10 @@ __global__ void __launch_bounds__(kMmaT * kMmaSplit * 32, 1)
     const int tbeg = TK ? (int)((long long)ntiles * blockIdx.x / gridDim.x) : 0;
     const int tend = TK ? (int)((long long)ntiles * (blockIdx.x + 1) / gridDim.x) : ntiles;
     auto tile_of = [&](int j) { return TK ? tbeg + j : (int)blockIdx.x + j * (int)gridDim.x; };
-    auto issue = [&](int j) {  // this CTA's j-th tile into stage j % NST
-        const int tl = tile_of(j);
-        if (tl >= tend) return;
-        const int s = j % NST;
-        if (j >= NST) mbar_wait(&empty[s], ((j / NST) - 1) & 1);
+    // producer state of the next issue (tile, stage, round): no runtime divisions per tile
+    const int tstride = TK ? 1 : (int)gridDim.x;
+    int ptl = tile_of(0), ps = 0, pround = 0;
+    auto load = [&](int tl, int s) {  // tile tl into stage s (the stage is free)
         uint8_t* st = sm + (size_t)s * SB;
         mbar_arrive_expect_tx(&full[s], kbytes + (unsigned)(2 * nb) * xbox);
         if (TK) bulk_g2s(st, mv.tk_u1 + (size_t)(tl % nt3) * mv.tk_u1t, kbytes, &full[s]);
@@ -243,6 +242,17 @@ __global__ void __launch_bounds__(kMmaT * kMmaSplit * 32, 1)
             tma_load_2d(st + KB + 3 * XR, &tmx1, 0, row0 + nzp - 4, &full[s]);
         }
     };
+    auto issue = [&](int j) {  // this CTA's j-th tile into stage j % NST (j issued in order)
+        const int tl = ptl;
+        if (tl >= tend) return;
+        const int s = ps;
+        ptl += tstride;
+        if (++ps == NST) ps = 0;
+        if (j >= NST) mbar_wait(&empty[s], (pround - 1) & 1);
+        if (ps == 0) ++pround;
+        load(tl, s);
+    };
+
     auto wissue = [&](int j) {  // TK: W fragments of tile j's q (all blocks, one bulk copy)
         const int q = tile_of(j) / nt3;
         mbar_arrive_expect_tx(wbar, (unsigned)(8 * mv.tk_wq));
@@ -286,14 +296,15 @@ __global__ void __launch_bounds__(kMmaT * kMmaSplit * 32, 1)
     const int ocol = (lane & 3) >> 1, oside = lane & 1;  // this lane's C columns (see below)
     double2* const X3c = mv.X3[0] + ocol * mv.colC;
     int qprev = -1, nwl = 0;  // TK: q of the resident W, W loads waited for
-    for (int it = 0; tile_of(it) < tend; ++it) {
-        const int tl = tile_of(it);
-        const int s = it % NST;
+    // consumer state: tile, stage and phase, and the tile's (q, x tile) advanced without divisions
+    int tl = tile_of(0), s = 0, sph = 0;
+    int q = tl / nt3, xti = tl - q * nt3;
+    const int dq = tstride / nt3, dxt = tstride - dq * nt3;
+    for (int it = 0; tl < tend; ++it) {
         if (producer) issue(it + NST - 1);
-        mbar_wait(&full[s], (it / NST) & 1);
+        mbar_wait(&full[s], sph);
         const uint8_t* stg = sm + (size_t)s * SB;
         if constexpr (TK) {
-            const int q = tl / nt3;
             if (q != qprev) {
                 mbar_wait(wbar, nwl & 1);
                 ++nwl;
@@ -340,7 +351,6 @@ __global__ void __launch_bounds__(kMmaT * kMmaSplit * 32, 1)
         }
         const double* __restrict__ kt_ = reinterpret_cast<const double*>(stg) + t * KS1;
         const uint8_t* xb_ = stg + boff0;
-        const int q = tl / nt3, xti = tl - q * nt3;
         const int kx = xti * T + t;
         const int nside = (q == 0 || 2 * q == My) ? 1 : 2;
         const bool store = kx < nkx && ocol < nb && oside < nside;
@@ -349,7 +359,17 @@ __global__ void __launch_bounds__(kMmaT * kMmaSplit * 32, 1)
             double c[MC][2];
 #pragma unroll
             for (int m = 0; m < MC; ++m) c[m][0] = c[m][1] = 0.0;
-            if (fast) {
+            if (fast && mc0 + MC <= mhi) {  // all MC row chunks: no per-chunk guards
+#pragma unroll
+                for (int k = 0; k < KCM; ++k) {
+                    if (k >= nkw) break;
+                    const int kk = klo + k;
+                    const double bv = *reinterpret_cast<const double*>(xb_ + kk * 512 + ((kk & 1) ? bsw1 : bsw0));
+#pragma unroll
+                    for (int m = 0; m < MC; ++m)
+                        dmma884(c[m][0], c[m][1], p3m_aval<TK>(kt_, (ar[k][m / 2] >> (16 * (m & 1))) & 0xffff), bv);
+                }
+            } else if (fast) {
 #pragma unroll
                 for (int k = 0; k < KCM; ++k) {
                     if (k >= nkw) break;
@@ -410,6 +430,17 @@ __global__ void __launch_bounds__(kMmaT * kMmaSplit * 32, 1)
             if (TK) fence_proxy_async();
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[s]);
+        }
+        tl += tstride;
+        q += dq;
+        xti += dxt;
+        if (xti >= nt3) {
+            xti -= nt3;
+            ++q;
+        }
+        if (++s == NST) {
+            s = 0;
+            sph ^= 1;
         }
     }
 }

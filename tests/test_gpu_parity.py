@@ -166,6 +166,27 @@ def test_matvec_padding_invariance(ctx):
     assert _rel(y1, y0) < 1e-13
 
 
+@pytest.mark.parametrize("nb", [1, 2])
+def test_matvec_dense_parity_c5_layout(ctx, nb):
+    """z-FFT mode on a grid with M_y = 2048 and M_z = 256 and a dielectric (n_f = 6): the one-kx
+    X2 / X3 layouts of C5 (P3 tile width 1, P4 tile width 1), where P2 runs planes fastest and
+    P3 walks |k_y| fastest.  A few small boxes at the ends of a thin 4 x 1000 x 120 domain keep
+    N small enough for the dense oracle."""
+    label, eps = np.zeros((120, 1000, 4), np.int32), np.ones((120, 1000, 4))
+    label[0:2, 0:3, 0:2] = 1
+    label[117:120, 996:1000, 1:3] = 2
+    eps[0:3, 995:1000, :] = 3.5    # dielectric block at the far y end, bottom
+    eps[116:120, 0:4, 2:4] = 2.0    # and at the near y end, top
+    st = voxgen.Structure(label, eps, 1.0, 1e-6, "c5layout")
+    p = _setup(ctx, st, zmode=1)
+    assert ctx.grid()[1] >= 2048 and ctx.grid()[2] >= 256, ctx.grid()
+    A = O.assemble(p)
+    X = np.stack([voxgen.seeded_vector(p.n, s) for s in range(nb)], axis=1)
+    Y = ctx.matvec_batch(X) if nb > 1 else ctx.matvec(X[:, 0])[:, None]
+    for c in range(nb):
+        assert _rel(Y[:, c], A @ X[:, c]) <= 1e-10, (c, ctx.grid(), _rel(Y[:, c], A @ X[:, c]))
+
+
 def test_matvec_device_tensors(ctx):
     import torch
     st = voxgen.config("R5")

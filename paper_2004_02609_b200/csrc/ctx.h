@@ -160,6 +160,10 @@ struct vc_ctx {
     // field's all-to-all overlaps the transform of the next; events [0..8]
     // "chunk produced" (compute stream), [9..17] "chunk exchanged" (comm stream)
     cudaStream_t cstream = nullptr;
+    // host mirror of the panel arrays (h_axis .. h_cid): copied on its own stream after the
+    // panel emit, so vc_set_geometry does not wait for it; readers call vc::mirror_wait
+    cudaStream_t mstream = nullptr;
+    cudaEvent_t mev = nullptr;
     cudaEvent_t cev[18] = {};
     bool cev_ok = false;
     std::string err;
@@ -350,4 +354,11 @@ vc_status comm_alltoall(vc_ctx* c, const std::vector<const void*>& send, const s
 vc_status comm_allreduce(vc_ctx* c, double* d, int n);
 vc_status comm_nccl_selftest(vc_ctx* c, double* out);
 inline void count_launch(vc_ctx* c, int k = 1) { c->stats.gpu_launches += k; }
+}  // namespace vc
+
+namespace vc {
+// the host panel mirror is complete (its copies were enqueued by geometry_build); thread-safe
+inline void mirror_wait(const vc_ctx* c) {
+    if (c->mev) cudaEventSynchronize(c->mev);
+}
 }  // namespace vc

@@ -396,8 +396,11 @@ __global__ void __launch_bounds__(kNT3) k_p3(MV mv) {
     double2* ph = buf + L * W;                      // [L] exp(-i pi kt / L)
     double2* xin = ph + L;                          // [NS][XS] staged X2 tiles
     double* rin = reinterpret_cast<double*>(xin + NS * XS);  // [NS][RC] staged R tiles
-    int16_t* zmap = reinterpret_cast<int16_t*>(rin + NS * RC);  // [9][L] plane -> index / -1
-    uint64_t* bar = reinterpret_cast<uint64_t*>(zmap + ((9 * L + 3) & ~3));  // [2]
+    // [9][ZS] plane -> index / -1; rows padded to L + 2 so that the three sources' (fields') rows
+    // start in different banks (lanes of one warp read several rows at the same z)
+    constexpr int ZS = L + 2;
+    int16_t* zmap = reinterpret_cast<int16_t*>(rin + NS * RC);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(zmap + ((9 * ZS + 3) & ~3));  // [2]
     __shared__ int fmeta[NF][4];                    // kind | alpha << 1, R offsets of b0..b2
     const int xo1 = T2 * nz0, xo2 = T2 * (nz0 + nz1);
     const int ntile = (Kx + T - 1) / T;
@@ -415,7 +418,7 @@ __global__ void __launch_bounds__(kNT3) k_p3(MV mv) {
     for (int k = threadIdx.x; k < L; k += kNT3) ph[k] = half_phase(mv.tw, ktil(k, L), L, -1);
     for (int e = threadIdx.x; e < 9 * L; e += kNT3) {
         const int g = e / L, z = e % L;
-        zmap[e] = (int16_t)(z < mv.ZL ? mv.planes[(9 + g) * mv.ZL + z] : -1);
+        zmap[g * ZS + z] = (int16_t)(z < mv.ZL ? mv.planes[(9 + g) * mv.ZL + z] : -1);
     }
     __syncthreads();
     // tile order: kx tiles fastest, or (X3 one kx wide, lgt4 = 0: C5) |ky| fastest, so that the
@@ -450,7 +453,7 @@ __global__ void __launch_bounds__(kNT3) k_p3(MV mv) {
         // forward z-FFT of pencils pp = beta * 2T + side * T + t (zero-padded to L)
         auto ld0 = [&](int pp, int n) -> double2 {
             const int t = pp % T, side = (pp / T) & 1, beta = pp / T2;
-            const int jz = zmap[beta * L + n];
+            const int jz = zmap[beta * ZS + n];
             if (side >= nside || tile * T + t >= Kx || jz < 0) return czero();
             const int nzb = beta == 0 ? nz0 : (beta == 1 ? nz1 : nz2);
             const int xo = beta == 0 ? 0 : (beta == 1 ? xo1 : xo2);
@@ -528,7 +531,7 @@ __global__ void __launch_bounds__(kNT3) k_p3(MV mv) {
             const int f = pp / T2, c = pp % T2;
             const int side = c / T, t = c % T;
             const int kx = tile * T + t;
-            const int jz = zmap[(3 + f) * L + Plan<L>::freq(p)];
+            const int jz = zmap[(3 + f) * ZS + Plan<L>::freq(p)];
             if (side < nside && kx < Kx && jz >= 0)
                 mv.X3[f][((((int64_t)jz * ((Kx + (1 << mv.lgt4) - 1) >> mv.lgt4) + (kx >> mv.lgt4)) * My +
                            (side ? My - q : q)) << mv.lgt4) | (kx & ((1 << mv.lgt4) - 1))] = v;
@@ -1141,7 +1144,7 @@ static size_t p3_smem(const MV& mv, int ns) {
     constexpr int W = P3T<L, NF>::W, T = P3T<L, NF>::T;
     const size_t XS = (size_t)2 * T * (mv.nzin[0] + mv.nzin[1] + mv.nzin[2]);
     return sizeof(double2) * ((size_t)L * W + L + ns * XS) + sizeof(double) * ns * (size_t)mv.rchunk +
-           sizeof(int16_t) * ((9 * L + 3) & ~3) + 2 * sizeof(uint64_t);
+           sizeof(int16_t) * ((9 * (L + 2) + 3) & ~3) + 2 * sizeof(uint64_t);
 }
 template <int L, int NF, int NS>
 static cudaError_t launch_p3_ns(const MV& mv, cudaStream_t st, size_t smem) {
@@ -1327,6 +1330,7 @@ static int next_pow2(int v) {
 }
 
 vc_status operator_build(vc_ctx* c, const vc_build_opts* o) {
+    if (c->world > 1) mirror_wait(c);  // the slab bookkeeping reads the host panel mirror
     cudaStream_t st = c->stream;
     HostTrace tr("operator");
     // window origin and per-orientation extents
@@ -1990,6 +1994,7 @@ __global__ void k_local_panels(int64_t nl, const int64_t* __restrict__ gidx,
 // This rank's panels: canonical order restricted to the panels whose slot row it owns, and
 // slot maps to local indices (world = 1: the global arrays are used as they are).
 vc_status partition_build(vc_ctx* c) {
+    mirror_wait(c);
     c->h_gidx.clear();
     if (c->world == 1) {
         c->NL = c->N;

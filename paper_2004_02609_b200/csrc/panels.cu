@@ -17,8 +17,25 @@ namespace {
 constexpr int kTile = 2048;  // faces per CTA
 constexpr int kNT = 256;
 
+// exact division of 32-bit unsigned values by a fixed divisor (round-up multiplier, shift =
+// ceil(log2 d)): the face-index decomposition is 3-4 divisions per face, and 64-bit division is a
+// long software sequence (k_count / k_emit were division-bound)
+struct FDiv {
+    uint32_t d, m, s;
+    __device__ __forceinline__ uint32_t div(uint32_t n) const {
+        return (uint32_t)(((uint64_t)__umulhi(n, m) + n) >> s);
+    }
+};
+static FDiv fdiv_make(uint32_t d) {
+    uint32_t s = 0;
+    while ((1ull << s) < d) ++s;
+    return {d, (uint32_t)((((1ull << 32) * ((1ull << s) - d)) / d) + 1), s};
+}
+
 struct Geo {
     int nx, ny, nz;
+    bool fast;        // every axis grid has < 2^32 faces: 32-bit FDiv decomposition
+    FDiv gx[3], gy[3];
     int64_t F[3];     // faces per axis grid
     int64_t Foff[3];  // offset of each axis grid in the face space
     double eps_out;
@@ -36,6 +53,16 @@ struct FaceInfo {
 __device__ __forceinline__ void face_coords(const Geo& g, int64_t f, int& a, int& i, int& j,
                                             int& k) {
     a = f < g.Foff[1] ? 0 : (f < g.Foff[2] ? 1 : 2);
+    if (g.fast) {  // (selects, not g.gx[a]: a dynamic index would copy the parameters to local memory)
+        const uint32_t r = (uint32_t)(f - (a == 0 ? 0 : (a == 1 ? g.Foff[1] : g.Foff[2])));
+        const FDiv dx = a == 0 ? g.gx[0] : (a == 1 ? g.gx[1] : g.gx[2]);
+        const FDiv dy = a == 0 ? g.gy[0] : (a == 1 ? g.gy[1] : g.gy[2]);
+        const uint32_t r1 = dx.div(r), r2 = dy.div(r1);
+        i = (int)(r - r1 * dx.d);
+        j = (int)(r1 - r2 * dy.d);
+        k = (int)r2;
+        return;
+    }
     int64_t r = f - g.Foff[a];
     const int gx = g.nx + (a == 0), gy = g.ny + (a == 1);
     i = (int)(r % gx);
@@ -199,23 +226,22 @@ __global__ void k_emit(Geo g, int64_t Ftot, const int64_t* __restrict__ tile_off
     __shared__ int sext[37];
     if (threadIdx.x < 36) sext[threadIdx.x] = (threadIdx.x % 6) < 3 ? INT32_MAX : INT32_MIN;
     if (threadIdx.x == 36) sext[36] = 0;
-    int flag[PER];
-    FaceInfo fi[PER];
-    int a0 = 0, ii[PER], jj[PER], kk[PER], aa[PER];
-    int local = 0;
+    // pass 1: one panel bit per face (the face info is recomputed for the panels in pass 2, so
+    // no per-face state stays live across the scan: 131 -> fewer registers, more CTAs per SM)
+    unsigned bits = 0;
+    int a_t = 2;  // axis of the thread's first face (faces past the end: a valid axis)
 #pragma unroll
     for (int q = 0; q < PER; ++q) {
         const int64_t f = base + (int64_t)threadIdx.x * PER + q;
-        flag[q] = 0;
-        aa[q] = 2;  // (faces past the end: no panel; a valid axis for the extent bookkeeping)
         if (f < Ftot) {
-            face_coords(g, f, aa[q], ii[q], jj[q], kk[q]);
-            fi[q] = classify(g, aa[q], ii[q], jj[q], kk[q]);
-            flag[q] = (fi[q].type == 1 || fi[q].type == 2);
+            int a, i, j, k;
+            face_coords(g, f, a, i, j, k);
+            if (q == 0) a_t = a;
+            const FaceInfo fq = classify(g, a, i, j, k);
+            bits |= (unsigned)(fq.type == 1 || fq.type == 2) << q;
         }
-        local += flag[q];
     }
-    (void)a0;
+    const int local = __popc(bits);
     // block exclusive scan of per-thread counts
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     int incl = local;
@@ -231,7 +257,6 @@ __global__ void k_emit(Geo g, int64_t Ftot, const int64_t* __restrict__ tile_off
     // panel extents of the thread's axis grid (a_t = axis of its first face) in registers;
     // one warp reduction (redux.sync) and a few shared atomics per warp instead of seven
     // shared atomics per panel on 36 addresses (contended: 0.93 ms for C4's 766k panels)
-    const int a_t = aa[0];
     int emin[2][3], emax[2][3], ncond = 0;
 #pragma unroll
     for (int d = 0; d < 2; ++d)
@@ -244,44 +269,50 @@ __global__ void k_emit(Geo g, int64_t Ftot, const int64_t* __restrict__ tile_off
     for (int q = 0; q < PER; ++q) {
         const int64_t f = base + (int64_t)threadIdx.x * PER + q;
         if (f >= Ftot) break;
-        const int a = aa[q];
-        const int64_t r = f - g.Foff[a];
-        if (flag[q]) {
-            const bool diel = fi[q].type == 2;
+        int a, iq, jq, kq;
+        face_coords(g, f, a, iq, jq, kq);
+        const int64_t r = f - (a == 0 ? 0 : (a == 1 ? g.Foff[1] : g.Foff[2]));
+        int32_t* const sm_a = a == 0 ? o.slotmap[0] : (a == 1 ? o.slotmap[1] : o.slotmap[2]);
+        if (bits >> q & 1) {
+            const FaceInfo fq = classify(g, a, iq, jq, kq);
+            const bool diel = fq.type == 2;
             ncond += diel ? 0 : 1;
             o.axis[p] = (int8_t)a;
-            o.sign[p] = (int8_t)fi[q].sign;
-            o.info[p] = (int8_t)((diel ? 1 : 0) | (fi[q].sign < 0 ? 2 : 0));
-            o.si[p] = ii[q];
-            o.sj[p] = jj[q];
-            o.sk[p] = kk[q];
-            o.cid[p] = diel ? 0 : fi[q].cid;
-            o.ed[p] = fi[q].ed;
-            o.eb[p] = fi[q].eb;
+            o.sign[p] = (int8_t)fq.sign;
+            o.info[p] = (int8_t)((diel ? 1 : 0) | (fq.sign < 0 ? 2 : 0));
+            o.si[p] = iq;
+            o.sj[p] = jq;
+            o.sk[p] = kq;
+            o.cid[p] = diel ? 0 : fq.cid;
+            o.ed[p] = fq.ed;
+            o.eb[p] = fq.eb;
             // Eq. (7): Ī = A (eps_d + eps_b) / (2 eps0 (eps_d - eps_b)); conductor rows 0
-            o.ibar[p] = diel ? o.area_over_2eps0 * (fi[q].ed + fi[q].eb) / (fi[q].ed - fi[q].eb) : 0.0;
-            o.fc[p] = diel ? 0.0 : fi[q].eb;
-            o.slotmap[a][r] = (int32_t)p | (diel ? kSlotDiel : 0) | (diel && fi[q].sign < 0 ? kSlotNeg : 0);
+            o.ibar[p] = diel ? o.area_over_2eps0 * (fq.ed + fq.eb) / (fq.ed - fq.eb) : 0.0;
+            o.fc[p] = diel ? 0.0 : fq.eb;
+            sm_a[r] = (int32_t)p | (diel ? kSlotDiel : 0) | (diel && fq.sign < 0 ? kSlotNeg : 0);
             if (a == a_t) {  // the thread's axis: extents in registers, reduced per warp below
-                const int d = diel ? 1 : 0;
-                emin[d][0] = min(emin[d][0], ii[q]);
-                emin[d][1] = min(emin[d][1], jj[q]);
-                emin[d][2] = min(emin[d][2], kk[q]);
-                emax[d][0] = max(emax[d][0], ii[q]);
-                emax[d][1] = max(emax[d][1], jj[q]);
-                emax[d][2] = max(emax[d][2], kk[q]);
+#pragma unroll
+                for (int d = 0; d < 2; ++d)  // (static indices: the arrays stay in registers)
+                    if ((d == 1) == diel) {
+                        emin[d][0] = min(emin[d][0], iq);
+                        emin[d][1] = min(emin[d][1], jq);
+                        emin[d][2] = min(emin[d][2], kq);
+                        emax[d][0] = max(emax[d][0], iq);
+                        emax[d][1] = max(emax[d][1], jq);
+                        emax[d][2] = max(emax[d][2], kq);
+                    }
             } else {  // a thread straddling two axis grids (at most two per grid boundary)
                 int* e = sext + ((diel ? 1 : 0) * 3 + a) * 6;
-                atomicMin(e + 0, ii[q]);
-                atomicMin(e + 1, jj[q]);
-                atomicMin(e + 2, kk[q]);
-                atomicMax(e + 3, ii[q]);
-                atomicMax(e + 4, jj[q]);
-                atomicMax(e + 5, kk[q]);
+                atomicMin(e + 0, iq);
+                atomicMin(e + 1, jq);
+                atomicMin(e + 2, kq);
+                atomicMax(e + 3, iq);
+                atomicMax(e + 4, jq);
+                atomicMax(e + 5, kq);
             }
             ++p;
         } else {
-            o.slotmap[a][r] = -1;
+            sm_a[r] = -1;
         }
     }
     {
@@ -324,6 +355,7 @@ __global__ void k_emit(Geo g, int64_t Ftot, const int64_t* __restrict__ tile_off
 }  // namespace
 
 vc_status geometry_build(vc_ctx* c, const int32_t* d_label, const double* d_eps) {
+    mirror_wait(c);  // the previous geometry's mirror copies are done before anything is reused
     const int64_t nvox = (int64_t)c->nx * c->ny * c->nz;
     cudaStream_t st = c->stream;
     HostTrace tr("geometry");
@@ -367,6 +399,12 @@ vc_status geometry_build(vc_ctx* c, const int32_t* d_label, const double* d_eps)
     g.Foff[1] = g.F[0];
     g.Foff[2] = g.F[0] + g.F[1];
     const int64_t Ftot = g.F[0] + g.F[1] + g.F[2];
+    g.fast = true;
+    for (int a = 0; a < 3; ++a) {
+        g.fast = g.fast && g.F[a] < (int64_t(1) << 32);
+        g.gx[a] = fdiv_make((uint32_t)(c->nx + (a == 0)));
+        g.gy[a] = fdiv_make((uint32_t)(c->ny + (a == 1)));
+    }
     g.eps_out = c->eps_out;
     g.label = d_label;
     g.eps = d_eps;
@@ -423,17 +461,26 @@ vc_status geometry_build(vc_ctx* c, const int32_t* d_label, const double* d_eps)
     k_emit<<<(unsigned)ntiles, kNT, 0, st>>>(g, Ftot, tiles.p, o);
     count_launch(c);
     VC_CUDA(c, cudaMemcpyAsync(hext.data(), ext.p, 37 * sizeof(int), cudaMemcpyDeviceToHost, st));
-    // host mirror of the structural fields
+    // host mirror of the structural fields, on the mirror stream: only its readers (the
+    // preconditioner plan, vc_get_panels, the slab partition) wait for it (vc::mirror_wait)
+    if (!c->mstream) {
+        VC_CUDA(c, cudaStreamCreateWithFlags(&c->mstream, cudaStreamNonBlocking));
+        VC_CUDA(c, cudaEventCreateWithFlags(&c->mev, cudaEventDisableTiming));
+    }
+    VC_CUDA(c, cudaEventRecord(c->mev, st));
+    VC_CUDA(c, cudaStreamWaitEvent(c->mstream, c->mev, 0));
     VC_CUDA(c, c->h_axis.resize(N));
     VC_CUDA(c, c->h_si.resize(N));
     VC_CUDA(c, c->h_sj.resize(N));
     VC_CUDA(c, c->h_sk.resize(N));
     VC_CUDA(c, c->h_cid.resize(N));
-    VC_CUDA(c, cudaMemcpyAsync(c->h_axis.data(), P.axis.p, N, cudaMemcpyDeviceToHost, st));
-    VC_CUDA(c, cudaMemcpyAsync(c->h_si.data(), P.si.p, N * 4, cudaMemcpyDeviceToHost, st));
-    VC_CUDA(c, cudaMemcpyAsync(c->h_sj.data(), P.sj.p, N * 4, cudaMemcpyDeviceToHost, st));
-    VC_CUDA(c, cudaMemcpyAsync(c->h_sk.data(), P.sk.p, N * 4, cudaMemcpyDeviceToHost, st));
-    VC_CUDA(c, cudaMemcpyAsync(c->h_cid.data(), P.cid.p, N * 4, cudaMemcpyDeviceToHost, st));
+    cudaStream_t ms = c->mstream;
+    VC_CUDA(c, cudaMemcpyAsync(c->h_axis.data(), P.axis.p, N, cudaMemcpyDeviceToHost, ms));
+    VC_CUDA(c, cudaMemcpyAsync(c->h_si.data(), P.si.p, N * 4, cudaMemcpyDeviceToHost, ms));
+    VC_CUDA(c, cudaMemcpyAsync(c->h_sj.data(), P.sj.p, N * 4, cudaMemcpyDeviceToHost, ms));
+    VC_CUDA(c, cudaMemcpyAsync(c->h_sk.data(), P.sk.p, N * 4, cudaMemcpyDeviceToHost, ms));
+    VC_CUDA(c, cudaMemcpyAsync(c->h_cid.data(), P.cid.p, N * 4, cudaMemcpyDeviceToHost, ms));
+    VC_CUDA(c, cudaEventRecord(c->mev, ms));
     VC_CUDA(c, cudaStreamSynchronize(st));
     VC_CUDA(c, cudaGetLastError());
     for (int kind = 0; kind < 2; ++kind)

@@ -379,6 +379,7 @@ struct PcPlan {
 };
 
 void pc_plan_compute(const vc_ctx* c, const int32_t box_in[3], int64_t N, PcPlan& P, bool all_panels) {
+    mirror_wait(c);  // reads the host panel mirror
     auto G = [&](int64_t i) { return c->world > 1 ? c->h_gidx[i] : i; };  // local -> global
     int nv[3], nb[3];
     const int dims[3] = {c->nx, c->ny, c->nz};

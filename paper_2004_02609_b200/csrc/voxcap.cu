@@ -102,6 +102,7 @@ void vc_destroy(vc_ctx* c) {
     {
         DeviceGuard g(c->device);
         cudaStreamSynchronize(c->stream);
+        mirror_wait(c);
         drop_geometry(c);
         precond_free(c);
         comm_free(c);
@@ -121,6 +122,10 @@ void vc_destroy(vc_ctx* c) {
         if (c->cstream) {
             cudaStreamSynchronize(c->cstream);
             cudaStreamDestroy(c->cstream);
+        }
+        if (c->mstream) {
+            cudaEventDestroy(c->mev);
+            cudaStreamDestroy(c->mstream);
         }
         if (c->own_stream) cudaStreamDestroy(c->stream);
     }
@@ -212,6 +217,7 @@ vc_status vc_get_panels(const vc_ctx* cc, int8_t* axis, int32_t* slot, int8_t* s
     if (eps_d) VC_CUDA(c, cudaMemcpyAsync(eps_d, c->pan.eps_d.p, 8 * n, cudaMemcpyDeviceToHost, st));
     if (eps_b) VC_CUDA(c, cudaMemcpyAsync(eps_b, c->pan.eps_b.p, 8 * n, cudaMemcpyDeviceToHost, st));
     VC_CUDA(c, cudaStreamSynchronize(st));
+    mirror_wait(c);
     if (slot)
         for (int64_t p = 0; p < n; ++p) {
             slot[3 * p] = c->h_si[p];

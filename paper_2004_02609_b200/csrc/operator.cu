@@ -323,11 +323,11 @@ __global__ void __launch_bounds__(FYS<L, KB>::NT) k_p4s(MV mv) {
                 if (D) {
                     mv.S2[pr][f][(tl / nt1) * (pr == mv.rank ? mv.colA : mv.colS) +
                                  ((int64_t)j * mv.nr[pr][3 + f] + (yy - y0)) * nkx + kx] = v;
-                } else {  // one rank: X4 row-pair interleaved [plane][row pair][kx][2] (P5's pairs)
+                } else {  // one rank: X4 row-pair blocked [plane][row pair][2][kx] (P5's pairs)
                     const int s5 = mv.lo[1] & 1, rr = yy + s5;
                     const int np = (mv.nr[0][3 + f] + s5 + 1) >> 1;
                     mv.S2[0][f][(tl / nt1) * mv.colA +
-                                ((((int64_t)j * np + (rr >> 1)) * nkx + kx) << 1 | (rr & 1))] = v;
+                                (((int64_t)j * np + (rr >> 1)) * 2 + (rr & 1)) * nkx + kx] = v;
                 }
             }
         };
@@ -572,10 +572,10 @@ __global__ void __launch_bounds__(FX<L>::NT, FX<L>::MINB5) k_p5(MV mv) {
             k0 = mv.kxa[qd];
             nk = mv.kxa[qd + 1] - k0;
         }
-        const int rr = yrow + s;  // one rank: row-pair interleaved X4 (see P4)
+        const int rr = yrow + s;  // one rank: row-pair blocked X4 (see P4)
         const double2* src =
             D ? mv.R2[qd][f] + blockIdx.z * mv.colA + ((int64_t)j * nrow + yrow) * nk + (k - k0)
-              : mv.R2[0][f] + blockIdx.z * mv.colA + ((((int64_t)j * nyp + (rr >> 1)) * nk + k) << 1 | (rr & 1));
+              : mv.R2[0][f] + blockIdx.z * mv.colA + (((int64_t)j * nyp + (rr >> 1)) * 2 + (rr & 1)) * nk + k;
         double2 w = v ? __ldg(src) : czero();
         if (ph) w = cmul(w, half_phase(mv.tw, k, L, +1));
         if (k == 0 || 2 * k == L) w.y = 0.0;
@@ -604,8 +604,9 @@ __global__ void __launch_bounds__(FX<L>::NT, FX<L>::MINB5) k_p5(MV mv) {
     const int Gx = mv.G[alpha][0], Gy = mv.G[alpha][1];
     const int64_t zrow =
         ((int64_t)(z + mv.lo[2]) * Gy + mv.lo[1] + mv.ya[mv.rank]) * Gx + mv.lo[0];
-    // one rank (BULK): the CTA's T row pairs of X4 are one contiguous block ([pair][kx][2], P4's
-    // row-pair interleaved layout), fetched with a single bulk copy into the FFT buffer itself;
+    // one rank (BULK): the CTA's T row pairs of X4 are one contiguous block ([pair][2][kx], P4's
+    // row-pair blocked layout: consecutive kx of a row are adjacent, so stage 0's reads are
+    // conflict-free), fetched with a single bulk copy into the FFT buffer itself;
     // stage 0 reads it from there (fft_stage0_aliased: all loads, a barrier, then the stores), so
     // no global load sits in a thread's registers while the transform waits on it
     constexpr bool BULK = !D && Plan<L>::NS >= 2 && T * (L / Plan<L>::radix(0)) == FX<L>::NT;
@@ -634,10 +635,10 @@ __global__ void __launch_bounds__(FX<L>::NT, FX<L>::MINB5) k_p5(MV mv) {
     cp_async_commit();
     auto sts = [&](int t, int p, double2 v) { sm[smi<L, T, false>(t, p)] = v; };
     if constexpr (BULK) {
-        // the same values as ld0 / At, read from the staged block [pair t][kx][row]
+        // the same values as ld0 / At, read from the staged block [pair t][row][kx]
         const double2* __restrict__ inb = sm;
         auto As = [&](int t, int row, int k, bool v) -> double2 {
-            double2 w = v ? inb[((int64_t)t * nk1 + k) * 2 + row] : czero();
+            double2 w = v ? inb[(t * 2 + row) * nk1 + k] : czero();
             if (ph) w = cmul(w, half_phase(mv.tw, k, L, +1));
             if (k == 0 || 2 * k == L) w.y = 0.0;
             return w;

@@ -548,6 +548,33 @@ __global__ void __launch_bounds__(kNT3) k_p3(MV mv) {
 __host__ __device__ constexpr size_t p5_inbytes(int L, int T, int nk) {
     return ((size_t)32 * T * nk > (size_t)16 * L * T ? ((size_t)32 * T * nk + 127) & ~(size_t)127 : (size_t)16 * L * T);
 }
+// P5's stage-0 input at line position n from the two rows' spectra A, B at kx = k (k = n, or
+// L - n with the conjugates: the rows are real): Z = A' + i B' with A' = A phi (phi the half
+// phase, ph) and Im A' dropped at the self-conjugate k.  Both rows share phi, so off those two k
+// Z = (A + i B) phi, or (conj A + i conj B) conj phi: one complex product instead of two.
+template <int L>
+__device__ __forceinline__ double2 p5_combine(double2 A, double2 B, int k, bool lo, bool ph,
+                                              const double2* __restrict__ tw) {
+    if (k == 0 || 2 * k == L) {
+        if (ph) {
+            const double2 w = half_phase(tw, k, L, +1);
+            A = cmul(A, w);
+            B = cmul(B, w);
+        }
+        return make_double2(A.x, B.x);
+    }
+    if (!lo) {
+        A.y = -A.y;
+        B.y = -B.y;
+    }
+    double2 Z = make_double2(A.x - B.y, A.y + B.x);
+    if (ph) {
+        double2 w = half_phase(tw, k, L, +1);
+        if (!lo) w.y = -w.y;
+        Z = cmul(Z, w);
+    }
+    return Z;
+}
 template <int L, bool D>
 __global__ void __launch_bounds__(FX<L>::NT, FX<L>::MINB5) k_p5(MV mv) {
     constexpr int T = TX<L>::T;
@@ -576,10 +603,7 @@ __global__ void __launch_bounds__(FX<L>::NT, FX<L>::MINB5) k_p5(MV mv) {
         const double2* src =
             D ? mv.R2[qd][f] + blockIdx.z * mv.colA + ((int64_t)j * nrow + yrow) * nk + (k - k0)
               : mv.R2[0][f] + blockIdx.z * mv.colA + (((int64_t)j * nyp + (rr >> 1)) * 2 + (rr & 1)) * nk + k;
-        double2 w = v ? __ldg(src) : czero();
-        if (ph) w = cmul(w, half_phase(mv.tw, k, L, +1));
-        if (k == 0 || 2 * k == L) w.y = 0.0;
-        return w;
+        return v ? __ldg(src) : czero();
     };
     auto ld0 = [&](int t, int n) -> double2 {
         const int q = ch * T + t;
@@ -588,12 +612,8 @@ __global__ void __launch_bounds__(FX<L>::NT, FX<L>::MINB5) k_p5(MV mv) {
         const bool has0 = ok && l0 >= 0, has1 = ok && l0 + 1 < nrow;
         const bool lo = 2 * n <= L;
         const int k = lo ? n : L - n;
-        double2 A = At(has0 ? l0 : 0, k, has0), B = At(has1 ? l0 + 1 : 0, k, has1);
-        if (!lo) {
-            A.y = -A.y;
-            B.y = -B.y;
-        }
-        return make_double2(A.x - B.y, A.y + B.x);
+        const double2 A = At(has0 ? l0 : 0, k, has0), B = At(has1 ? l0 + 1 : 0, k, has1);
+        return p5_combine<L>(A, B, k, lo, ph, mv.tw);
     };
     // the last stage goes to shared memory; the gather then walks each output line with
     // consecutive lanes on consecutive slots (coalesced slot-map reads and y writes; the panel
@@ -638,10 +658,7 @@ __global__ void __launch_bounds__(FX<L>::NT, FX<L>::MINB5) k_p5(MV mv) {
         // the same values as ld0 / At, read from the staged block [pair t][row][kx]
         const double2* __restrict__ inb = sm;
         auto As = [&](int t, int row, int k, bool v) -> double2 {
-            double2 w = v ? inb[(t * 2 + row) * nk1 + k] : czero();
-            if (ph) w = cmul(w, half_phase(mv.tw, k, L, +1));
-            if (k == 0 || 2 * k == L) w.y = 0.0;
-            return w;
+            return v ? inb[(t * 2 + row) * nk1 + k] : czero();
         };
         auto lds0 = [&](int t, int n) -> double2 {
             const int q = ch * T + t;
@@ -650,12 +667,8 @@ __global__ void __launch_bounds__(FX<L>::NT, FX<L>::MINB5) k_p5(MV mv) {
             const bool has0 = ok && l0 >= 0, has1 = ok && l0 + 1 < nrow;
             const bool lo = 2 * n <= L;
             const int k = lo ? n : L - n;
-            double2 A = As(t, 0, k, has0), B = As(t, 1, k, has1);
-            if (!lo) {
-                A.y = -A.y;
-                B.y = -B.y;
-            }
-            return make_double2(A.x - B.y, A.y + B.x);
+            const double2 A = As(t, 0, k, has0), B = As(t, 1, k, has1);
+            return p5_combine<L>(A, B, k, lo, ph, mv.tw);
         };
         mbar_wait(&p5bar, 0);
         fft_stage0_aliased<L, T, FX<L>::NT, true>(sm, lds0, mv.tw);

@@ -273,16 +273,15 @@ __global__ void __launch_bounds__(FYS<L, KB>::NT) k_p4s(MV mv) {
         __syncthreads();
     }
     auto prefetch = [&](int tl, int stg) {
+        if (BULK && threadIdx.x != 0) return;  // (one thread issues the bulk copy: only it decodes)
         int f, j, xt;
         decode(tl, f, j, xt);
         // kx-tile-major X3: the tile's T kx x L ky are one contiguous block
         const double2* in = mv.X3[f] + (tl / nt1) * mv.colC + ((int64_t)j * ntx + xt) * L * T;
         double2* dst = sm + stg * L * T;
         if constexpr (BULK) {
-            if (threadIdx.x == 0) {
-                mbar_arrive_expect_tx(&p4bar[stg], (unsigned)(16 * L * T));
-                bulk_g2s(dst, in, (unsigned)(16 * L * T), &p4bar[stg]);
-            }
+            mbar_arrive_expect_tx(&p4bar[stg], (unsigned)(16 * L * T));
+            bulk_g2s(dst, in, (unsigned)(16 * L * T), &p4bar[stg]);
             return;
         }
         for (int e = threadIdx.x; e < L * T; e += NT) {
@@ -314,20 +313,23 @@ __global__ void __launch_bounds__(FYS<L, KB>::NT) k_p4s(MV mv) {
             if (ph) v = cmul(v, half_phase(mv.tw, ktil(n, L), L, +1));
             return v;
         };
+        // one rank: X4 row-pair blocked [plane][row pair][2][kx] (P5's pairs at absolute rows
+        // (2m, 2m + 1)): row yy sits at row yy + s5 of the plane's 2 np rows
+        const int s5 = mv.lo[1] & 1;
+        double2* const o4 =
+            D ? nullptr
+              : mv.S2[0][f] + (tl / nt1) * mv.colA + ((int64_t)j * (((mv.nr[0][3 + f] + s5 + 1) >> 1) * 2) + s5) * nkx;
         auto stN = [&](int t, int p, double2 v) {
             const int kx = xt * T + t;
             const int yy = Plan<L>::freq(p);
             if (kx < nkx && yy < eyo) {
-                const int pr = D ? row_owner(mv, yy) : 0;  // row yy goes to rank pr for P5
-                const int y0 = D ? mv.ya[pr] : 0;
                 if (D) {
+                    const int pr = row_owner(mv, yy);  // row yy goes to rank pr for P5
+                    const int y0 = mv.ya[pr];
                     mv.S2[pr][f][(tl / nt1) * (pr == mv.rank ? mv.colA : mv.colS) +
                                  ((int64_t)j * mv.nr[pr][3 + f] + (yy - y0)) * nkx + kx] = v;
-                } else {  // one rank: X4 row-pair blocked [plane][row pair][2][kx] (P5's pairs)
-                    const int s5 = mv.lo[1] & 1, rr = yy + s5;
-                    const int np = (mv.nr[0][3 + f] + s5 + 1) >> 1;
-                    mv.S2[0][f][(tl / nt1) * mv.colA +
-                                (((int64_t)j * np + (rr >> 1)) * 2 + (rr & 1)) * nkx + kx] = v;
+                } else {
+                    o4[(int64_t)yy * nkx + kx] = v;
                 }
             }
         };
@@ -602,7 +604,7 @@ __global__ void __launch_bounds__(FX<L>::NT, FX<L>::MINB5) k_p5(MV mv) {
         const int rr = yrow + s;  // one rank: row-pair blocked X4 (see P4)
         const double2* src =
             D ? mv.R2[qd][f] + blockIdx.z * mv.colA + ((int64_t)j * nrow + yrow) * nk + (k - k0)
-              : mv.R2[0][f] + blockIdx.z * mv.colA + (((int64_t)j * nyp + (rr >> 1)) * 2 + (rr & 1)) * nk + k;
+              : mv.R2[0][f] + blockIdx.z * mv.colA + ((int64_t)j * nyp * 2 + rr) * nk + k;
         return v ? __ldg(src) : czero();
     };
     auto ld0 = [&](int t, int n) -> double2 {

@@ -136,7 +136,8 @@ __global__ void __launch_bounds__(FX<L>::NT, FX<L>::MINB) k_p1(MV mv) {
             if (l0 + 1 < nrow) o[nk] = B;
         } else {  // one rank: [plane][kx tile][row][kx % tk], so P2 reads each tile contiguously
             const int tk = 1 << mv.lgtk, ntk = (nk + tk - 1) >> mv.lgtk;
-            double2* o = S1self + (((int64_t)j * ntk + (k >> mv.lgtk)) * nrow + l0) * tk + (k & (tk - 1));
+            const int rowtk = nrow << mv.lgtk;  // elements of one kx tile of the plane
+            double2* o = S1self + (int64_t)j * ntk * rowtk + ((k >> mv.lgtk) * rowtk + l0 * tk + (k & (tk - 1)));
             if (l0 >= 0) o[0] = A;
             if (l0 + 1 < nrow) o[tk] = B;
         }
@@ -186,14 +187,17 @@ __global__ void __launch_bounds__(FY<L>::NT) k_p2(MV mv) {
         const int p = row_owner(mv, n);  // row n arrived from rank p
         return mv.R1[p][beta][blockIdx.z * mv.colA + ((int64_t)j * mv.nr[p][beta] + (n - mv.ya[p])) * nkx + kx];
     };
+    // element (q, kx tile, side, plane, kx % T3): the side and q strides are CTA constants and the
+    // kx / plane part is fixed per butterfly, so a store costs one 64-bit multiply-add
+    const int64_t x2ss = (int64_t)mv.x2nz[beta] << mv.lgT3, x2sq = 2 * nt3 * x2ss;
+    double2* const outj = out + ((int64_t)(mv.x2zo[beta] + j) << mv.lgT3);
     auto stN = [&](int t, int p, double2 v) {
         const int kx = tile * T + t;
         if (kx >= nkx) return;
         const int k = Plan<L>::freq(p);
         if (ph) v = cmul(v, half_phase(mv.tw, ktil(k, L), L, -1));
         const int side = k > L / 2, qq = side ? L - k : k;
-        const int64_t ts = ((int64_t)qq * nt3 + (kx >> mv.lgT3)) * 2 + side;
-        double2* o = out + ((ts * mv.x2nz[beta] + mv.x2zo[beta] + j) << mv.lgT3) + (kx & (mv.T3 - 1));
+        double2* o = outj + ((kx >> mv.lgT3) * 2 * x2ss + (kx & (mv.T3 - 1))) + qq * x2sq + (side ? x2ss : 0);
         o[0] = v;
         if (mv.zdirect && j == nzb - 1) {  // zero the padding planes up to the next source's
             const int pad = (beta < 2 ? mv.x2zo[beta + 1] : mv.x2nz[beta]) - mv.x2zo[beta] - nzb;

@@ -43,6 +43,7 @@ template <int L> struct FX {
 // Tile widths the host layout code must agree with (X1 is tiled by P2's width, X3 by P4's):
 // operator_build sizes and indexes those arrays through these two functions only.
 constexpr int p2_tile(int L) { return clampi(4096 / L, 2, 32); }  // FY<L>::T
+constexpr int kP2Ahead = 2 * 148;  // P2's L2 prefetch distance in blocks (two resident CTAs per SM)
 constexpr int kP4KB = 32;                                          // P4's shared KB per stage
 constexpr int p4_tile(int L) { return clampi(kP4KB * 64 / L, 1, 32); }  // FYS<L, kP4KB>::T
 #ifndef VC_P2_MINB
@@ -216,6 +217,12 @@ __global__ void __launch_bounds__(FY<L>::NT) k_p2(MV mv) {
             fence_mbar_init();
             mbar_arrive_expect_tx(&p2bar, bytes);
             bulk_g2s(sm, in0 + (int64_t)tile * ey * T, bytes, &p2bar);
+            // the block that takes this CTA's slot next (launch order, kP2Ahead blocks on) finds
+            // its input in L2: X1 is read once, so the prefetch adds no traffic
+            const int bn = blockIdx.x + kP2Ahead;
+            const int jn = jfast ? bn % nzb : bn / ntile, tn = jfast ? bn / nzb : bn % ntile;
+            if (jn < nzb && tn < ntile)
+                bulk_prefetch_l2(mv.R1[0][beta] + blockIdx.z * mv.colA + ((int64_t)jn * ntile + tn) * ey * T, bytes);
         }
         __syncthreads();  // (the barrier is initialised before anyone waits on it)
         mbar_wait(&p2bar, 0);

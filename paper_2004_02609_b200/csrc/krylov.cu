@@ -266,13 +266,26 @@ __global__ void __launch_bounds__(kRedNT) k_axpy_norm(Cols2 cc, int64_t ldv, int
     double* __restrict__ w = cc.out[z];
     double* __restrict__ part = partial + (size_t)z * kRedBlocks * kMaxBasis;
     double acc2 = 0.0;
-    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
-         k += (int64_t)gridDim.x * blockDim.x) {
-        double acc = 0.0;
-        for (int i = 0; i < nv; ++i) acc = fma(hs[i], V[i * ldv + k], acc);
-        const double w2 = fma(-1.0, acc, w[k]);
-        w[k] = w2;
-        acc2 = fma(w2, w2, acc2);
+    // two grid-stride elements per trip (their basis loads interleaved: twice the loads in
+    // flight), each with the one-element arithmetic in the same order, so the result is unchanged
+    const int64_t gs = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += 2 * gs) {
+        const int64_t k2 = k + gs < n ? k + gs : k;
+        double accA = 0.0, accB = 0.0;
+#pragma unroll 4
+        for (int i = 0; i < nv; ++i) {
+            const double va = V[i * ldv + k], vb = V[i * ldv + k2];
+            accA = fma(hs[i], va, accA);
+            accB = fma(hs[i], vb, accB);
+        }
+        const double wA = fma(-1.0, accA, w[k]);
+        w[k] = wA;
+        acc2 = fma(wA, wA, acc2);
+        if (k2 != k) {
+            const double wB = fma(-1.0, accB, w[k2]);
+            w[k2] = wB;
+            acc2 = fma(wB, wB, acc2);
+        }
     }
     __shared__ double s[kRedNT / 32];
     const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;

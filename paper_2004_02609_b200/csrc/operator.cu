@@ -1859,7 +1859,7 @@ vc_status operator_build(vc_ctx* c, const vc_build_opts* o) {
     for (int q = 0; q < W; ++q)
         for (int f = 0; f < c->nf; ++f) {
             c->offR2[q][f] = nR2;
-            // one rank: row-pair interleaved (P5 pairs rows at absolute (2m, 2m+1))
+            // one rank: row-pair blocked (P5 pairs rows at absolute (2m, 2m+1))
             const int s5 = c->lo[1] & 1;
             nR2 += (size_t)c->nzout[f] * nkxq(q) *
                    (W == 1 ? (size_t)2 * ((c->nr[rk][3 + f] + s5 + 1) >> 1) : (size_t)c->nr[rk][3 + f]);

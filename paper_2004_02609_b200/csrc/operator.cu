@@ -325,7 +325,10 @@ __global__ void __launch_bounds__(FYS<L, KB>::NT) k_p4s(MV mv) {
             return v;
         };
         // one rank: X4 row-pair blocked [plane][row pair][2][kx] (P5's pairs at absolute rows
-        // (2m, 2m + 1)): row yy sits at row yy + s5 of the plane's 2 np rows
+        // (2m, 2m + 1)): row yy sits at row yy + s5 of the plane's 2 np rows. A tile one kx wide
+        // (T = 1, M_y >= 2048: C5) would write 16-byte half sectors there, so it keeps the
+        // row-pair interleaved [plane][row pair][kx][2] (a pair's two rows fill one sector)
+        constexpr bool IL = T == 1;
         const int s5 = mv.lo[1] & 1;
         double2* const o4 =
             D ? nullptr
@@ -339,6 +342,8 @@ __global__ void __launch_bounds__(FYS<L, KB>::NT) k_p4s(MV mv) {
                     const int y0 = mv.ya[pr];
                     mv.S2[pr][f][(tl / nt1) * (pr == mv.rank ? mv.colA : mv.colS) +
                                  ((int64_t)j * mv.nr[pr][3 + f] + (yy - y0)) * nkx + kx] = v;
+                } else if (IL) {
+                    o4[(((int64_t)((yy + s5) >> 1) * nkx + kx) << 1 | ((yy + s5) & 1)) - (int64_t)s5 * nkx] = v;
                 } else {
                     o4[(int64_t)yy * nkx + kx] = v;
                 }
@@ -605,6 +610,7 @@ __global__ void __launch_bounds__(FX<L>::NT, FX<L>::MINB5) k_p5(MV mv) {
     if (j >= mv.nzout[f]) return;
     const int z = zlist(mv, 3 + f, j);
     const bool ph = alpha != 0;
+    const bool x4il = !D && mv.lgt4 == 0;  // P4's tile one kx wide: X4 row-pair interleaved
     auto At = [&](int yrow, int k, bool v) -> double2 {
         int qd = 0, nk = mv.nkx, k0 = 0;
         if (D) {
@@ -612,10 +618,12 @@ __global__ void __launch_bounds__(FX<L>::NT, FX<L>::MINB5) k_p5(MV mv) {
             k0 = mv.kxa[qd];
             nk = mv.kxa[qd + 1] - k0;
         }
-        const int rr = yrow + s;  // one rank: row-pair blocked X4 (see P4)
+        const int rr = yrow + s;  // one rank: row-pair blocked (interleaved: x4il) X4 (see P4)
         const double2* src =
             D ? mv.R2[qd][f] + blockIdx.z * mv.colA + ((int64_t)j * nrow + yrow) * nk + (k - k0)
-              : mv.R2[0][f] + blockIdx.z * mv.colA + ((int64_t)j * nyp * 2 + rr) * nk + k;
+              : mv.R2[0][f] + blockIdx.z * mv.colA +
+                    (x4il ? (((int64_t)j * nyp + (rr >> 1)) * nk + k) << 1 | (rr & 1)
+                          : ((int64_t)j * nyp * 2 + rr) * nk + k);
         return v ? __ldg(src) : czero();
     };
     auto ld0 = [&](int t, int n) -> double2 {
@@ -671,7 +679,7 @@ __global__ void __launch_bounds__(FX<L>::NT, FX<L>::MINB5) k_p5(MV mv) {
         // the same values as ld0 / At, read from the staged block [pair t][row][kx]
         const double2* __restrict__ inb = sm;
         auto As = [&](int t, int row, int k, bool v) -> double2 {
-            return v ? inb[(t * 2 + row) * nk1 + k] : czero();
+            return v ? inb[x4il ? (t * nk1 + k) * 2 + row : (t * 2 + row) * nk1 + k] : czero();
         };
         auto lds0 = [&](int t, int n) -> double2 {
             const int q = ch * T + t;

@@ -593,7 +593,7 @@ __device__ __forceinline__ double2 p5_combine(double2 A, double2 B, int k, bool 
     }
     return Z;
 }
-template <int L, bool D>
+template <int L, bool D, bool IL = false>  // IL: X4 row-pair interleaved (one rank, lgt4 = 0)
 __global__ void __launch_bounds__(FX<L>::NT, FX<L>::MINB5) k_p5(MV mv) {
     constexpr int T = TX<L>::T;
     extern __shared__ double2 sm[];
@@ -610,7 +610,7 @@ __global__ void __launch_bounds__(FX<L>::NT, FX<L>::MINB5) k_p5(MV mv) {
     if (j >= mv.nzout[f]) return;
     const int z = zlist(mv, 3 + f, j);
     const bool ph = alpha != 0;
-    const bool x4il = !D && mv.lgt4 == 0;  // P4's tile one kx wide: X4 row-pair interleaved
+    constexpr bool x4il = !D && IL;  // P4's tile one kx wide: X4 row-pair interleaved
     auto At = [&](int yrow, int k, bool v) -> double2 {
         int qd = 0, nk = mv.nkx, k0 = 0;
         if (D) {
@@ -1256,7 +1256,7 @@ static cudaError_t launch_p5(const MV& mv, cudaStream_t st) {
         // FFT buffer (one rank: the staged input block, which may be a little larger) + slot lines
         const size_t smem = (mv.W > 1 ? sizeof(double2) * LL * T : p5_inbytes(LL, T, mv.nkx)) +
                             sizeof(int32_t) * 2 * T * LL;
-        auto kern = mv.W > 1 ? k_p5<LL, true> : k_p5<LL, false>;
+        auto kern = mv.W > 1 ? k_p5<LL, true> : mv.lgt4 == 0 ? k_p5<LL, false, true> : k_p5<LL, false>;
         cudaError_t e = prep_fit(kern, FX<LL>::NT, smem);
         if (e) return e;
         dim3 grid(std::max(1, maxch * maxz), mv.f1 - mv.f0, mv.nb);  // fields [f0, f1)
